@@ -1,0 +1,451 @@
+#!/usr/bin/env python
+"""Benchmark: the MCAP-routed decode-linear stack of Llama-3.2-1B (BASELINE.json
+configs[1]) on B200, through the C ABI (libmcapq.so).
+
+A "step" = one pass of the whole hot path over one batch-1 decode token: 16
+layers x {q, k, v, o, gate, up, down} routed by the MCAP profile (layer 15 ->
+W4A16, the other 15 -> W4A8 with their 4 activation quantisations each), the
+step replayed as one CUDA graph.  Synthetic seeded bf16
+weights/activations (synth_inputs), random-init, no checkpoints.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+N > 1 (torchrun): every rank runs its own replica of the stack (independent
+decode streams; "scaling": "weak"); the column-sharded lm_head/MLP with its
+NCCL all-gather is measured by `--workload lmhead`.  One JSON line on rank 0.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import sys
+import threading
+import time
+
+import torch
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import synth_inputs as si  # noqa: E402
+
+METRIC = json.load(open(os.path.join(ROOT, "BASELINE.json")))["metric"]
+GOLDEN_PROFILE = os.path.join(ROOT, "tests", "golden", "llama32_1b_profile.json")
+SLOTS = ["q", "k", "v", "o", "gate", "up", "down"]
+INPUT_ID = {"q": 0, "k": 0, "v": 0, "o": 1, "gate": 2, "up": 2, "down": 3}
+MODEL = "llama-3.2-1b"
+CONFIG_ID = 2
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy read+write)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+# ---------------------------------------------------------------- clocks
+class ClockSampler:
+    """NVML sampling of SM clock + throttle reasons during the timed region."""
+
+    REASONS = {0x4: "sw_power_cap", 0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown",
+               0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown"}
+
+    def __init__(self, index: int):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self._stop = threading.Event()
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:  # noqa: BLE001 - clocks are reported as unavailable
+            self.nv = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if r & bit:
+                        self.reasons.add(name)
+            except Exception:  # noqa: BLE001
+                pass
+            time.sleep(0.005)
+
+    def __enter__(self):
+        if self.nv:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self.nv:
+            self.t.join()
+
+    def report(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons), "samples": 0}
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+# ---------------------------------------------------------------- workload
+def build_stack(mq, dev, routes, m=1):
+    """Pack the 16-layer Llama-3.2-1B linear stack; returns (stack, weights, xs, ys)."""
+    L = si.MODELS[MODEL]["layers"]
+    st = mq.Stack(routes, max_m=m)
+    weights, xs, ys = {}, {}, {}
+    for l in range(L):
+        for s_id, slot in enumerate(SLOTS):
+            n, k = si.linear_shape(MODEL, slot)
+            w = si.weight(n, k, si.seed_for(CONFIG_ID, l, slot)).to(dev)
+            pw = mq.pack_w4(w)
+            del w
+            key = (l, INPUT_ID[slot])
+            if key not in xs:
+                xs[key] = si.activation(m, k, si.seed_for(CONFIG_ID, l, slot, True), si.activation_kind(slot)).to(dev)
+            y = torch.empty(m, n, dtype=torch.bfloat16, device=dev)
+            st.set(l, s_id, INPUT_ID[slot], pw, xs[key], y)
+            weights[(l, slot)] = pw
+            ys[(l, slot)] = y
+    return st, weights, xs, ys
+
+
+def stack_with_routes(mq, routes, weights, xs, ys, m=1):
+    st = mq.Stack(routes, max_m=m)
+    L = len(routes)
+    for l in range(L):
+        for s_id, slot in enumerate(SLOTS):
+            st.set(l, s_id, INPUT_ID[slot], weights[(l, slot)], xs[(l, INPUT_ID[slot])], ys[(l, slot)])
+    return st
+
+
+def time_graph(st, stream, steps, warmup, dist=None):
+    for _ in range(warmup):
+        st.replay(stream=stream)
+    stream.synchronize()
+    if dist is not None:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(steps):
+        st.replay(stream=stream)
+    e1.record(stream)
+    e1.synchronize()
+    torch.cuda.synchronize()
+    if dist is not None:
+        dist.barrier()
+    return e0.elapsed_time(e1) / steps
+
+
+def time_dominant_kernel(mq, weights, xs, stream, reps_per_layer=4):
+    """The W4A8 GEMV of gate/up (8192x2048, the stack's largest W4A8 launch),
+    pre-quantised activations (mcapq_w4a8 launches exactly that kernel), rotating
+    over the 16 layers' weights (16 x 9.4 MB x2 > L2) so every launch streams
+    from HBM.  CUDA events on the launching stream."""
+    L = si.MODELS[MODEL]["layers"]
+    qs = {}
+    with torch.cuda.stream(stream):
+        for l in range(L):
+            qs[l] = mq.quant_a8(xs[(l, INPUT_ID["gate"])], stream=stream)
+        ys = torch.empty(1, weights[(0, "gate")].n, dtype=torch.bfloat16, device=xs[(0, 0)].device)
+        seq = [(l, s) for _ in range(reps_per_layer) for l in range(L) for s in ("gate", "up")]
+        for (l, s) in seq[:8]:
+            mq.w4a8(weights[(l, s)], *qs[l], out=ys, stream=stream)
+        stream.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for (l, s) in seq:
+            mq.w4a8(weights[(l, s)], *qs[l], out=ys, stream=stream)
+        e1.record(stream)
+        e1.synchronize()
+    per_launch_ms = e0.elapsed_time(e1) / len(seq)
+    w = weights[(0, "gate")]
+    alg_bytes = w.n * w.k // 2 + w.n * (w.k // 32) * 2 + (w.k + 8 * (w.k // 32)) + 2 * w.n
+    return per_launch_ms, alg_bytes, len(seq)
+
+
+def time_single_linears(mq, dev, stream):
+    """Single-linear rows of the metric at the other configs (cfg1 q_proj, cfg4 8B MLP,
+    cfg5 lm_head), both routes, M = 1, rotating weight copies so each launch reads HBM."""
+    out = []
+    l2 = torch.cuda.get_device_properties(dev).L2_cache_size
+    for cfg, model, slot in ((1, "llama-3.2-1b", "q"), (4, "llama-3.1-8b", "gate"), (4, "llama-3.1-8b", "down"),
+                             (5, "llama-3.1-8b", "lm_head")):
+        n, k = si.linear_shape(model, slot)
+        wbytes = n * k // 2 + n * (k // 32) * 2
+        copies = max(2, min(32, math.ceil(4 * l2 / wbytes)))
+        ws = []
+        base = si.weight(n, k, si.seed_for(cfg, 0, slot)).to(dev)
+        pw0 = mq.pack_w4(base)
+        del base
+        for c in range(copies):
+            ws.append(mq.PackedW4(pw0.nib.clone(), pw0.scale.clone()))
+        x = si.activation(1, k, si.seed_for(cfg, 0, slot, True), si.activation_kind(slot)).to(dev)
+        y = torch.empty(1, n, dtype=torch.bfloat16, device=dev)
+        row = {"config": cfg, "model": model, "slot": slot, "N": n, "K": k, "M": 1, "weight_bytes": wbytes}
+        with torch.cuda.stream(stream):
+            q, sx, sq = mq.quant_a8(x, stream=stream)
+            wsp = torch.empty(mq.workspace_bytes(0, 1, n, k), dtype=torch.uint8, device=dev)
+            for route, name in ((0, "w4a8"), (1, "w4a16")):
+                def call(pw):
+                    if route == 0:
+                        mq.linear(0, pw, x, out=y, ws=wsp, stream=stream)
+                    else:
+                        mq.w4a16(pw, x, out=y, stream=stream)
+                for pw in ws[:2]:
+                    call(pw)
+                reps = max(copies, 20)
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                stream.synchronize()
+                e0.record(stream)
+                for i in range(reps):
+                    call(ws[i % copies])
+                e1.record(stream)
+                e1.synchronize()
+                us = e0.elapsed_time(e1) * 1000 / reps
+                row[f"{name}_us"] = round(us, 3)
+                row[f"{name}_gbs"] = round(wbytes / us / 1e3, 1)
+        row["w4a8_over_w4a16"] = round(row["w4a16_us"] / row["w4a8_us"], 3)
+        out.append(row)
+        del ws, pw0
+        torch.cuda.empty_cache()
+    return out
+
+
+# ---------------------------------------------------------------- CPU oracle
+def oracle_prepare(layers=(0, 15)):
+    """Pack (outside any timing) the sample layers of the stack for the oracle:
+    layer 0 (a W4A8 layer, like 15 of the 16) and layer 15 (the W4A16 layer)."""
+    import oracle
+    oracle.build()
+    _, _, routes = oracle.routes_from_profile(open(GOLDEN_PROFILE).read())
+    prep = []
+    for l in layers:
+        packed, xin = {}, {}
+        for slot in SLOTS:
+            n, k = si.linear_shape(MODEL, slot)
+            w = si.weight(n, k, si.seed_for(CONFIG_ID, l, slot)).float().numpy()
+            packed[slot] = oracle.pack_w4(w)
+            key = INPUT_ID[slot]
+            if key not in xin:
+                xin[key] = si.activation(1, k, si.seed_for(CONFIG_ID, l, slot, True),
+                                         si.activation_kind(slot)).float().numpy()
+        prep.append((l, routes[l], packed, xin))
+    return routes, prep
+
+
+def oracle_step(routes, prep):
+    """One bounded sample: the oracle (as it stands) runs every sample layer in full
+    (quantise once per distinct input + 7 linears); the stack's GB/s is extrapolated
+    from the per-route layer times with the mask's route counts (15 W4A8 + 1 W4A16)."""
+    import oracle
+    t_route, b_layer = {}, {}
+    for (l, route, packed, xin) in prep:
+        t0 = time.perf_counter()
+        qcache, nbytes = {}, 0
+        for slot in SLOTS:
+            nib, sc = packed[slot]
+            x = xin[INPUT_ID[slot]]
+            if route == oracle.W4A8:
+                if INPUT_ID[slot] not in qcache:
+                    qcache[INPUT_ID[slot]] = oracle.quant_a8(x)
+                oracle.w4a8(nib, sc, *qcache[INPUT_ID[slot]])
+            else:
+                oracle.w4a16(nib, sc, x)
+            nbytes += nib.nbytes + sc.nbytes
+        t_route[route] = time.perf_counter() - t0
+        b_layer[route] = nbytes
+    total_t = sum(t_route[r] for r in routes)
+    total_b = sum(b_layer[r] for r in routes)
+    return total_b / total_t / 1e9, sum(t_route.values())
+
+
+def oracle_baseline(steps=3):
+    routes, prep = oracle_prepare()
+    vals, secs = [], 0.0
+    for _ in range(steps):
+        v, t = oracle_step(routes, prep)
+        vals.append(v)
+        secs += t
+    return statistics.median(vals), len(os.sched_getaffinity(0)), secs
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    routes, prep = oracle_prepare()
+    for _ in range(args.warmup):
+        oracle_step(routes, prep)
+    vals, secs = [], 0.0
+    for _ in range(args.steps):
+        v, t = oracle_step(routes, prep)
+        vals.append(v)
+        secs += t
+    v = statistics.median(vals)
+    cores = len(os.sched_getaffinity(0))
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(v, 4), "unit": "GB/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "s8xu4->s32,f32 (W4A8) | f32 (W4A16)", "data": "synthetic",
+        "config": {"workload": "llama-3.2-1b 16-layer decode linear stack, MCAP mask (L15 W4A16), batch 1"},
+        "cpu_baseline": {"value": round(v, 4), "unit": "GB/s", "cores": cores, "kind": "oracle",
+                         "sample": "per step: layer 0 (W4A8) and layer 15 (W4A16) of the stack run in full by the "
+                                   f"C oracle, extrapolated to the 15+1 mask; {secs:.1f} s of CPU work in total"},
+        "e2e": {"value": round(v, 4), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------- main
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-extras", action="store_true", help="skip per-config single-linear rows")
+    args = ap.parse_args()
+    args.warmup = max(3, args.warmup)
+    if args.impl == "reference":
+        return run_reference(args)
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    dist = None
+    if world > 1:
+        import torch.distributed as tdist
+        torch.cuda.set_device(local)
+        tdist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        dist = tdist
+    dev = torch.device(f"cuda:{local}")
+    torch.cuda.set_device(dev)
+
+    import paper_2604_21026_b200 as mq
+    mq.load()
+
+    prof = mq.profile_parse(open(GOLDEN_PROFILE).read())
+    routes = prof.routes()
+    st, weights, xs, ys = build_stack(mq, dev, routes)
+    stream = torch.cuda.Stream(device=dev)
+    with torch.cuda.stream(stream):
+        st.capture(1, stream=stream)
+    wbytes = st.weight_bytes
+    act_bytes = sum(v.numel() * 2 for v in xs.values()) + sum(v.numel() * 2 for v in ys.values())
+    l2 = torch.cuda.get_device_properties(dev).L2_cache_size
+
+    with ClockSampler(local) as clk:
+        ms = time_graph(st, stream, args.steps, args.warmup, dist)
+    # max over ranks
+    t = torch.tensor([ms], device=dev)
+    if dist is not None:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    value = world * wbytes / (ms_max * 1e-3) / 1e9
+    L = len(routes)
+
+    # route endpoints (tab:threshold all-W4A8 / all-W4A16), same weights
+    st8 = stack_with_routes(mq, [0] * L, weights, xs, ys)
+    st16 = stack_with_routes(mq, [1] * L, weights, xs, ys)
+    with torch.cuda.stream(stream):
+        st8.capture(1, stream=stream)
+        st16.capture(1, stream=stream)
+    ms8 = time_graph(st8, stream, args.steps, args.warmup)
+    ms16 = time_graph(st16, stream, args.steps, args.warmup)
+
+    # e2e: pinned host inputs -> H2D -> graph -> D2H, through mcapq_stack_step_host
+    bi, bo = st.host_bytes(1)
+    xh = torch.empty(bi, dtype=torch.uint8).pin_memory()
+    yh = torch.empty(bo, dtype=torch.uint8).pin_memory()
+    off = 0
+    for key in sorted(xs):
+        b = xs[key].cpu().view(torch.uint8).flatten()
+        xh[off:off + b.numel()] = b
+        off += b.numel()
+    for _ in range(args.warmup):
+        st.step_host(xh, yh, 1, stream=stream)
+    stream.synchronize()
+    if dist is not None:
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        st.step_host(xh, yh, 1, stream=stream)
+    e1.record(stream)
+    e1.synchronize()
+    e2e_ms = e0.elapsed_time(e1) / args.steps
+    te = torch.tensor([e2e_ms], device=dev)
+    if dist is not None:
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    e2e_value = world * wbytes / (float(te.item()) * 1e-3) / 1e9
+
+    # dominant kernel roofline
+    k_ms, k_bytes, k_reps = time_dominant_kernel(mq, weights, xs, stream)
+    peak, peak_src = peaks()
+    achieved = k_bytes / (k_ms * 1e-3) / 1e9
+
+    extras = [] if args.no_extras or rank != 0 else time_single_linears(mq, dev, stream)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        gbs, cores, secs = oracle_baseline()
+        cpu = {"value": round(gbs, 4), "unit": "GB/s", "cores": cores, "kind": "oracle",
+               "sample": "layer 0 (W4A8) + layer 15 (W4A16) of the same stack, each run in full by the C oracle "
+                         f"(3 repeats, {secs:.1f} s), extrapolated to the 15+1 mask"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(value, 1), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(ms_max, 5), "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "s8xu4->s32,f32 (W4A8) | bf16->f32 (W4A16)",
+            "data": "synthetic (seeded bf16 weights/activations, random init)",
+            "config": {"workload": "llama-3.2-1b 16-layer decode linear stack (q,k,v,o,gate,up,down), MCAP mask "
+                                   "from tab:per_layer_scores (L15 W4A16, 15 layers W4A8), batch 1, one CUDA graph",
+                       "m": 1, "layers": L, "routes": "".join(str(r) for r in routes),
+                       "weight_bytes_per_step": wbytes, "activation_bytes_per_step": act_bytes,
+                       "l2_policy": f"no flush: {wbytes / 1e6:.0f} MB of weights per step > {l2 / 1e6:.0f} MB L2",
+                       "parallelism": f"replicas x{world}" if world > 1 else "1 GPU"},
+            "us_per_layer": round(ms_max * 1000 / L, 3),
+            "us_per_linear": round(ms_max * 1000 / (L * len(SLOTS)), 3),
+            "routes_endpoints": {"all_w4a8_gbs": round(wbytes / (ms8 * 1e-3) / 1e9, 1),
+                                 "all_w4a16_gbs": round(wbytes / (ms16 * 1e-3) / 1e9, 1),
+                                 "all_w4a8_us_per_layer": round(ms8 * 1000 / L, 3),
+                                 "all_w4a16_us_per_layer": round(ms16 * 1000 / L, 3),
+                                 "w4a8_over_w4a16": round(ms16 / ms8, 3)},
+            "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                         "frac": round(achieved / peak, 4), "traffic": None,
+                         "kernel": "w4a8_gemv_dp4a (gate/up 8192x2048, M=1)",
+                         "alg_bytes_per_launch": k_bytes, "us_per_launch": round(k_ms * 1000, 3),
+                         "launches_timed": k_reps, "peak_source": peak_src,
+                         "step_frac": round(value / world / peak, 4)},
+            "e2e": {"value": round(e2e_value, 1), "unit": "GB/s", "h2d_bytes_per_step": bi, "d2h_bytes_per_step": bo,
+                    "ms_per_step": round(float(te.item()), 5), "api": "mcapq_stack_step_host"},
+            "gpu_launches": st.launches(1) * args.steps,
+            "kernels_per_step": st.launches(1),
+            "clocks": clk.report(),
+            "single_linears": extras,
+        }
+        if cpu is not None:
+            line["cpu_baseline"] = cpu
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,275 @@
+/*
+ * mcapq.h -- C ABI of the B200-native MCAP/NVE mixed-precision decode linear
+ * (arXiv 2604.21026).  Library: paper_2604_21026_b200/lib/libmcapq.so (sm_100a).
+ *
+ * The hot path: per layer i, route(i) = W4A16 if s^_i >= tau else W4A8
+ * (Alg. 1 line 13 P:557, tau = 0.7 P:643-645), where
+ *   W4A8  = Q4_0 int4 weights x per-token, per-32-group int8 activations, exact
+ *           int32 group dot products, fp32 scale-and-accumulate (P:925-943,
+ *           Appendix A);
+ *   W4A16 = the same Q4_0 weights dequantised in register against bf16
+ *           activations, fp32 accumulation.
+ * Citations: "P:n" = PAPER.md line n, "S:n" = SPEC.md line n; "A<n>" = reading
+ * n in DESIGN.md ("Readings of the paper").
+ *
+ * CONVENTIONS (apply to every call unless a call says otherwise)
+ *  - Pointers: caller-owned DEVICE memory, except where a parameter says "host".
+ *    The library never allocates device memory on a hot-path call and never
+ *    frees caller memory.  Opaque objects (mcapq_profile, mcapq_comm,
+ *    mcapq_stack) are library-owned and released by their *_free / *_destroy.
+ *  - Streams: `stream` is a cudaStream_t passed as void* (NULL = legacy default
+ *    stream).  Every device call is stream-ordered, asynchronous, never
+ *    synchronises and is CUDA-graph capturable (exceptions are marked).
+ *  - Status: every call returns mcapq_status; nothing aborts or throws across
+ *    the ABI.  Arguments are validated before anything is launched; on a non-OK
+ *    status nothing was launched.  mcapq_last_error() gives a thread-local
+ *    message for the last non-OK status on the calling thread.  Asynchronous
+ *    device faults surface at the caller's next synchronisation.
+ *  - Shapes: N = output features, K = input features (nn.Linear.weight is
+ *    [N, K], row-major), M = tokens.  K % 32 == 0 (one Q4_0 block / activation
+ *    group = 32 consecutive k, reading A1).  N >= 1, M >= 1.
+ *  - Alignment: weights / activations / outputs 16-byte aligned; leading
+ *    dimensions (ld*) in elements, multiples of 8, >= the row length.
+ *  - Dtypes: activations are bf16 (uint16 bit patterns); outputs are bf16
+ *    (RNE from fp32) or fp32, selected by mcapq_dtype (reading A11).
+ *  - Hot-path calls do NOT check for non-finite inputs: outputs are then
+ *    unspecified (never a fault).  mcapq_pack_w4 does check (dev_err).
+ *
+ * DATA LAYOUT of a packed weight ("Q4_0 SoA", reading A1/A2/A18):
+ *    nib   : uint8  [N][K/2]; block g of row n = bytes 16g..16g+15 of the row,
+ *            byte t = c[32g+t] | c[32g+t+16] << 4 (llama.cpp split nibble
+ *            format); codes c in [0,15], value = d (c - 8)
+ *            (zero point 8).
+ *    scale : uint16 [N][K/32]: the block's d as IEEE binary16 bits (P:932:
+ *            18 bytes per 32 elements = 16 nibble bytes + 2-byte fp16 d).
+ *  The nibble bytes are byte-identical to the Q4_0 block's nibble field; only
+ *  the d's are split into their own plane (structure-of-arrays).
+ */
+#ifndef MCAPQ_H
+#define MCAPQ_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MCAPQ_ABI_VERSION 1
+
+typedef enum {
+    MCAPQ_OK = 0,
+    MCAPQ_EINVAL = 1,  /* null pointer, bad shape (K % 32, M/N < 1), alignment, ld */
+    MCAPQ_EDTYPE = 2,  /* unsupported dtype value */
+    MCAPQ_ERANGE = 3,  /* value out of range (tau, world/rank, ...) */
+    MCAPQ_EPARSE = 4,  /* malformed profile JSON */
+    MCAPQ_ECUDA = 5,   /* CUDA runtime error (message in mcapq_last_error) */
+    MCAPQ_ENCCL = 6,   /* NCCL error */
+    MCAPQ_EUNSUP = 7,  /* valid request this build does not support */
+    MCAPQ_ENOSPACE = 8 /* caller-provided workspace too small */
+} mcapq_status;
+
+typedef enum { MCAPQ_BF16 = 0, MCAPQ_F32 = 1 } mcapq_dtype;
+typedef enum { MCAPQ_W4A8 = 0, MCAPQ_W4A16 = 1 } mcapq_route;
+
+/* dev_err bits written by mcapq_pack_w4 (atomic OR into a caller uint32). */
+#define MCAPQ_PACK_NONFINITE 0x1u /* a block contained inf/nan: stored as a zero block */
+#define MCAPQ_PACK_OVERFLOW 0x2u  /* |m|/8 rounds to fp16 inf (A4): d stored as inf, codes 8 */
+
+/* ---------------------------------------------------------------- library */
+int mcapq_abi_version(void);
+/* Thread-local text for the last non-OK status of this thread ("" if none). */
+const char *mcapq_last_error(void);
+const char *mcapq_status_string(int status);
+/* Number of streaming multiprocessors of the current device (0 on error). */
+int mcapq_device_sms(void);
+
+/* --------------------------------------------------------- packed weights */
+/* Bytes of the nibble plane (N*K/2) and of the scale plane (N*(K/32)*2). */
+size_t mcapq_w4_nib_bytes(int64_t n, int64_t k);
+size_t mcapq_w4_scale_bytes(int64_t n, int64_t k);
+
+/*
+ * a1. Q4_0 weight pack (load time).  P:932-933; S:283-299;
+ * readings A2-A5, A21.  Per row n, per 32-block g:
+ *   m = x[argmax_j |x_j|] (first index on ties, A3); d = fp16_rne(m / -8) (A2);
+ *   c_j = clamp(round_half_away(x_j / f32(d)), -8, 7) + 8 with IEEE division on
+ *   the stored fp16 d (A4, A5); d == 0 -> all codes 8 and d stored +0 (A21).
+ * w       : [n][ldw] of dtype wdt (MCAPQ_BF16 or MCAPQ_F32), ldw >= k.
+ * nib     : out, [n][k/2] uint8.   scale: out, [n][k/32] fp16 bits.
+ * dev_err : nullable device uint32; MCAPQ_PACK_* bits are OR-ed in (never
+ *           cleared).  A non-finite block is stored as a zero block; an fp16
+ *           overflow stores d = +-inf with all codes 8.
+ * Bit-exact with the oracle (tests/test_gpu_parity.py).
+ */
+mcapq_status mcapq_pack_w4(const void *w, int wdt, int64_t n, int64_t k, int64_t ldw, uint8_t *nib,
+                           uint16_t *scale, uint32_t *dev_err, void *stream);
+
+/*
+ * a2. Per-token, per-32-group int8 activation quantisation.  P:929-931,
+ * Appendix A.1; readings A6-A8, A21.  Per row i, group g:
+ *   a = max |x|; s = a / 127.0f (IEEE); q = clamp(round_half_away(x / s), -127,
+ *   127); sq = sum q (int32, the paper's sum_x).  a == 0 (or s == 0) -> s = +0,
+ *   q = 0.
+ * x : [m][ldx] bf16.  q: out [m][k] int8.  sx: out [m][k/32] fp32.
+ * sq: out [m][k/32] int32.  Bit-exact with the oracle.
+ */
+mcapq_status mcapq_quant_a8(const uint16_t *x, int64_t m, int64_t k, int64_t ldx, int8_t *q, float *sx,
+                            int32_t *sq, void *stream);
+
+/*
+ * a3/a5. W4A8 linear on pre-quantised activations.
+ * (deferred bias correction), reading A9:
+ *   D[i][n][g] = sum_j c_{n,32g+j} q_{i,32g+j} - 8 sq[i][g]   (exact int32)
+ *   y[i][n]    = sum_g (f32(d_{n,g}) * sx[i][g]) * f32(D)      (fp32 accumulate)
+ * nib/scale: packed weight [n, k].  q/sx/sq: as written by mcapq_quant_a8 for m
+ * tokens (row strides k, k/32, k/32).  y: out [m][ldy] of dtype ydt.
+ * m == 1 runs the batch-1 GEMV (dp4a), m > 1 the int8 tensor-core kernel.
+ * The fp32 summation order depends on K only (never on N, M or the grid), so a
+ * column shard of the weight gives bit-identical rows (A22).
+ */
+mcapq_status mcapq_w4a8(const uint8_t *nib, const uint16_t *scale, int64_t n, int64_t k, const int8_t *q,
+                        const float *sx, const int32_t *sq, int64_t m, void *y, int ydt, int64_t ldy,
+                        void *stream);
+
+/*
+ * Workspace (device bytes) a fused-quantise call needs for m tokens of k:
+ * q + sx + sq, 256-byte aligned pieces.  Route W4A16 needs 0.
+ */
+size_t mcapq_workspace_bytes(int route, int64_t m, int64_t n, int64_t k);
+
+/*
+ * a2+a3/a5. W4A8 from bf16 activations: quantise x into the workspace
+ * (mcapq_quant_a8), then mcapq_w4a8; the two launches are chained with
+ * programmatic dependent launch so the GEMV's weight stream starts while the
+ * quantiser runs.  ws: device workspace of >= mcapq_workspace_bytes(W4A8,...).
+ */
+mcapq_status mcapq_w4a8_x(const uint8_t *nib, const uint16_t *scale, int64_t n, int64_t k, const uint16_t *x,
+                          int64_t m, int64_t ldx, void *y, int ydt, int64_t ldy, void *ws, size_t ws_bytes,
+                          void *stream);
+
+/*
+ * a4/a6. W4A16 linear: exact dequantisation (reading A10/A13):
+ *   y[i][n] = sum_k (f32(d_{n,k/32}) (c_{n,k} - 8)) x_{i,k}, fp32 accumulation.
+ * Each term is exact in fp32; the inner per-group sums run on bf16 tensor cores
+ * (c - 8 is exact in bf16) with fp32 accumulation, the scale d is applied per
+ * group in fp32.  x: [m][ldx] bf16.  y: out [m][ldy].
+ */
+mcapq_status mcapq_w4a16(const uint8_t *nib, const uint16_t *scale, int64_t n, int64_t k, const uint16_t *x,
+                         int64_t m, int64_t ldx, void *y, int ydt, int64_t ldy, void *stream);
+
+/* Routed linear: route MCAPQ_W4A8 -> mcapq_w4a8_x, MCAPQ_W4A16 -> mcapq_w4a16. */
+mcapq_status mcapq_linear(int route, const uint8_t *nib, const uint16_t *scale, int64_t n, int64_t k,
+                          const uint16_t *x, int64_t m, int64_t ldx, void *y, int ydt, int64_t ldy, void *ws,
+                          size_t ws_bytes, void *stream);
+
+/*
+ * End-to-end routed linear from HOST activations: copies x_host (pinned host,
+ * [m][k] bf16) into the workspace, runs mcapq_linear, copies y back into y_host
+ * (pinned host, [m][n] of ydt); all on `stream`, asynchronous (the caller
+ * synchronises before reading y_host).  ws must hold
+ * mcapq_host_workspace_bytes(route, m, n, k) bytes.
+ */
+size_t mcapq_host_workspace_bytes(int route, int64_t m, int64_t n, int64_t k);
+mcapq_status mcapq_linear_host(int route, const uint8_t *nib, const uint16_t *scale, int64_t n, int64_t k,
+                               const uint16_t *x_host, int64_t m, void *y_host, int ydt, void *ws,
+                               size_t ws_bytes, void *stream);
+
+/*
+ * TEST ENTRY: the bit-exact integer stage of W4A8, D[i][n][g] (int32,
+ * [m][n][k/32]) computed by the same fragment code as the tensor-core kernel
+ * (mode 1) or the dp4a GEMV (mode 0).  P:937-942.
+ */
+mcapq_status mcapq_w4a8_group_dots(const uint8_t *nib, int64_t n, int64_t k, const int8_t *q, const int32_t *sq,
+                                   int64_t m, int32_t *D, int mode, void *stream);
+
+/* ------------------------------------------------------ dispatch table (a7) */
+/*
+ * MCAP profile -> per-layer routes.  Alg. 1 lines 8-13, P:840-846,
+ * the 338-byte JSON profile.  Host-only, not graph-related.
+ * JSON object (<= 64 KiB): "scores" (alias "normalized_scores") numeric array in
+ * [0, 1], or "raw_scores" (min-max normalised; max - min < epsilon -> all 0,
+ * P:550-552); optional "tau" (alias "threshold", default 0.7), "epsilon"
+ * (default 1e-9, A14), "num_layers" (alias "layers", must equal the array
+ * length); other keys ignored.  tau_override: NaN = use the file's / default.
+ * route[i] = MCAPQ_W4A16 iff s^_i >= tau (ties -> W4A16).
+ * Errors: MCAPQ_EPARSE (syntax, missing array, value outside [0,1], length
+ * mismatch), MCAPQ_ERANGE (tau < 0 or non-finite).
+ */
+typedef struct mcapq_profile mcapq_profile;
+mcapq_status mcapq_profile_parse(const char *json, size_t len, double tau_override, mcapq_profile **out);
+int mcapq_profile_layers(const mcapq_profile *p);
+double mcapq_profile_tau(const mcapq_profile *p);
+mcapq_status mcapq_profile_scores(const mcapq_profile *p, double *scores_host, int n);
+mcapq_status mcapq_profile_routes(const mcapq_profile *p, uint8_t *routes_host, int n);
+void mcapq_profile_free(mcapq_profile *p);
+
+/* ------------------------------------------------ decode linear stack (a9) */
+/*
+ * A routed stack of decode linears: L layers x S slots, each slot a packed
+ * weight, executed in (layer, slot) order with each layer's route from the
+ * dispatch table (all slots of layer i share route[i], A12).  Slots that share
+ * an input (same `input_id` within a layer, e.g. q/k/v) quantise it once
+ * (A15).  The library owns a workspace and, after mcapq_stack_capture, a CUDA
+ * graph that replays the whole step.
+ *
+ * mcapq_stack_create   : L layers, routes_host[L] (0/1), max_m tokens.
+ * mcapq_stack_set      : register slot s of layer l: weight (device), the
+ *                        device input x [m][k] bf16 and output y [m][n] (ydt),
+ *                        input_id groups slots sharing x within the layer.
+ * mcapq_stack_run      : launch every linear in order on `stream` (m tokens).
+ * mcapq_stack_capture  : capture mcapq_stack_run into a graph (m tokens).
+ * mcapq_stack_replay   : launch the captured graph on `stream`.
+ * mcapq_stack_weight_bytes : total packed weight bytes (nib + scale).
+ * mcapq_stack_launches : kernels one run launches.
+ * mcapq_stack_host_bytes : bytes of one step's inputs (which = 0: every distinct
+ *                        (layer, input_id) x, in that order, [m][k] bf16 each)
+ *                        or outputs (which = 1: every slot's y in (layer, slot)
+ *                        order, [m][n] of its ydt), packed back to back.
+ * mcapq_stack_step_host : one end-to-end step from HOST memory: copy x_host
+ *                        (pinned, the packed inputs) into the registered device
+ *                        inputs, replay the captured graph (or run, if none was
+ *                        captured for m), copy every output into y_host (pinned,
+ *                        packed).  Asynchronous on `stream`.
+ */
+typedef struct mcapq_stack mcapq_stack;
+mcapq_status mcapq_stack_create(int layers, const uint8_t *routes_host, int64_t max_m, mcapq_stack **out);
+mcapq_status mcapq_stack_set(mcapq_stack *st, int layer, int slot, int input_id, const uint8_t *nib,
+                             const uint16_t *scale, int64_t n, int64_t k, const uint16_t *x, void *y, int ydt);
+mcapq_status mcapq_stack_run(mcapq_stack *st, int64_t m, void *stream);
+mcapq_status mcapq_stack_capture(mcapq_stack *st, int64_t m, void *stream);
+mcapq_status mcapq_stack_replay(mcapq_stack *st, void *stream);
+size_t mcapq_stack_weight_bytes(const mcapq_stack *st);
+int mcapq_stack_launches(const mcapq_stack *st, int64_t m);
+size_t mcapq_stack_host_bytes(const mcapq_stack *st, int64_t m, int which);
+mcapq_status mcapq_stack_step_host(mcapq_stack *st, int64_t m, const void *x_host, void *y_host, void *stream);
+void mcapq_stack_destroy(mcapq_stack *st);
+
+/* ------------------------------------------- multi-GPU column shard (a8) */
+/*
+ * Column (output-feature) sharded linear across P GPUs of one node (north_star;
+ * the paper is single-GPU).  Rank r owns rows [r N/P, (r+1) N/P)
+ * of the packed weight (A22), computes its slice with the routed linear on the
+ * replicated x, and all-gathers over NCCL (NVLink/NVSwitch) into y_full
+ * [m][n_full] (bf16 or fp32), row-major.  Per-row arithmetic is identical to
+ * the unsharded call, so y_full is bit-identical to a 1-GPU run.
+ * mcapq_comm_unique_id (host): id[128] to broadcast (the caller uses a torch
+ * process group); mcapq_comm_init: collective over the `world` ranks, binds the
+ * communicator to the current CUDA device.  Not graph-capturable: init/destroy.
+ * ws: >= mcapq_colshard_workspace_bytes(route, m, n_full, k, world).
+ */
+typedef struct mcapq_comm mcapq_comm;
+mcapq_status mcapq_comm_unique_id(uint8_t *id_host_128);
+mcapq_status mcapq_comm_init(const uint8_t *id_host_128, int world, int rank, mcapq_comm **out);
+int mcapq_comm_world(const mcapq_comm *c);
+int mcapq_comm_rank(const mcapq_comm *c);
+size_t mcapq_colshard_workspace_bytes(int route, int64_t m, int64_t n_full, int64_t k, int world);
+mcapq_status mcapq_linear_colshard(const mcapq_comm *c, int route, const uint8_t *nib_shard,
+                                   const uint16_t *scale_shard, int64_t n_full, int64_t k, const uint16_t *x,
+                                   int64_t m, void *y_full, int ydt, void *ws, size_t ws_bytes, void *stream);
+void mcapq_comm_destroy(mcapq_comm *c);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MCAPQ_H */

@@ -1,0 +1,319 @@
+"""B200-native MCAP/NVE mixed-precision decode linear (arXiv 2604.21026).
+
+A thin binding over the C ABI (include/mcapq.h, libmcapq.so): the functions
+below only marshal torch tensors (device memory, the current CUDA stream) into
+pointers and sizes.  Every step of the hot path runs in the library's sm_100a
+kernels; there is no CPU fallback (a missing library raises ImportError on
+first use).
+
+    route(i) = W4A16 if s^_i >= tau else W4A8
+    W4A8   : Q4_0 int4 x per-token/per-32-group int8, int32 group dots
+    W4A16  : Q4_0 int4 dequantised against bf16 activations
+"""
+from __future__ import annotations
+
+import ctypes
+import math
+
+import torch
+
+from . import _lib
+from ._lib import McapqError, check, load
+
+W4A8, W4A16 = 0, 1
+BF16, F32 = 0, 1
+
+__all__ = [
+    "W4A8", "W4A16", "BF16", "F32", "McapqError", "load", "pack_w4", "quant_a8", "w4a8", "w4a8_x", "w4a16",
+    "linear", "linear_host", "w4a8_group_dots", "workspace_bytes", "host_workspace_bytes", "Profile",
+    "profile_parse", "Stack", "Comm", "linear_colshard", "PackedW4", "device_sms",
+]
+
+
+def _ptr(t: torch.Tensor | None):
+    return ctypes.c_void_p(t.data_ptr()) if t is not None else ctypes.c_void_p(0)
+
+
+def _stream(stream=None):
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def _dt(dtype) -> int:
+    if dtype == torch.bfloat16:
+        return BF16
+    if dtype == torch.float32:
+        return F32
+    raise McapqError(2, "dtype", f"unsupported dtype {dtype}")
+
+
+def _need_cuda(*ts):
+    for t in ts:
+        if t is not None and not t.is_cuda:
+            raise McapqError(1, "binding", "tensor is not on a CUDA device (no CPU path exists)")
+
+
+def device_sms() -> int:
+    return load().mcapq_device_sms()
+
+
+class PackedW4:
+    """A packed Q4_0 weight: nib uint8 [N, K/2] + scale (fp16 bits as int16) [N, K/32]."""
+
+    __slots__ = ("nib", "scale", "n", "k")
+
+    def __init__(self, nib: torch.Tensor, scale: torch.Tensor):
+        self.nib, self.scale = nib, scale
+        self.n, self.k = nib.shape[0], nib.shape[1] * 2
+
+    def shard(self, world: int, rank: int) -> "PackedW4":
+        per = self.n // world
+        return PackedW4(self.nib[rank * per:(rank + 1) * per], self.scale[rank * per:(rank + 1) * per])
+
+    @property
+    def nbytes(self) -> int:
+        return self.nib.numel() + 2 * self.scale.numel()
+
+
+def pack_w4(w: torch.Tensor, dev_err: torch.Tensor | None = None, stream=None) -> PackedW4:
+    """a1: W [N, K] bf16/fp32 (CUDA) -> PackedW4.  dev_err: optional int32[1] flag word."""
+    _need_cuda(w)
+    assert w.dim() == 2 and w.stride(1) == 1
+    n, k = w.shape
+    nib = torch.empty((n, k // 2), dtype=torch.uint8, device=w.device)
+    scale = torch.empty((n, k // 32), dtype=torch.int16, device=w.device)
+    check(load().mcapq_pack_w4(_ptr(w), _dt(w.dtype), n, k, w.stride(0), _ptr(nib), _ptr(scale), _ptr(dev_err),
+                               _stream(stream)), "mcapq_pack_w4")
+    return PackedW4(nib, scale)
+
+
+def quant_a8(x: torch.Tensor, stream=None):
+    """a2: x [M, K] bf16 -> (q int8 [M, K], sx fp32 [M, K/32], sq int32 [M, K/32])."""
+    _need_cuda(x)
+    x2 = x if x.dim() == 2 else x.view(1, -1)
+    m, k = x2.shape
+    q = torch.empty((m, k), dtype=torch.int8, device=x.device)
+    sx = torch.empty((m, k // 32), dtype=torch.float32, device=x.device)
+    sq = torch.empty((m, k // 32), dtype=torch.int32, device=x.device)
+    check(load().mcapq_quant_a8(_ptr(x2), m, k, x2.stride(0), _ptr(q), _ptr(sx), _ptr(sq), _stream(stream)),
+          "mcapq_quant_a8")
+    return q, sx, sq
+
+
+def _out(m, n, dtype, device, out):
+    if out is not None:
+        return out
+    return torch.empty((m, n), dtype=dtype, device=device)
+
+
+def w4a8(w: PackedW4, q, sx, sq, out_dtype=torch.float32, out=None, stream=None):
+    """a3/a5 on pre-quantised activations."""
+    _need_cuda(w.nib, q)
+    m = q.shape[0]
+    y = _out(m, w.n, out_dtype, q.device, out)
+    check(load().mcapq_w4a8(_ptr(w.nib), _ptr(w.scale), w.n, w.k, _ptr(q), _ptr(sx), _ptr(sq), m, _ptr(y),
+                            _dt(y.dtype), y.stride(0), _stream(stream)), "mcapq_w4a8")
+    return y
+
+
+def workspace_bytes(route: int, m: int, n: int, k: int) -> int:
+    return load().mcapq_workspace_bytes(route, m, n, k)
+
+
+def host_workspace_bytes(route: int, m: int, n: int, k: int) -> int:
+    return load().mcapq_host_workspace_bytes(route, m, n, k)
+
+
+def _ws(route, m, n, k, device, ws):
+    need = workspace_bytes(route, m, n, k)
+    if ws is not None:
+        return ws
+    return torch.empty(max(need, 256), dtype=torch.uint8, device=device)
+
+
+def w4a8_x(w: PackedW4, x: torch.Tensor, out_dtype=torch.float32, out=None, ws=None, stream=None):
+    """a2+a3/a5: quantise x then W4A8 (two PDL-chained launches)."""
+    _need_cuda(w.nib, x)
+    x2 = x if x.dim() == 2 else x.view(1, -1)
+    m = x2.shape[0]
+    y = _out(m, w.n, out_dtype, x.device, out)
+    ws = _ws(W4A8, m, w.n, w.k, x.device, ws)
+    check(load().mcapq_w4a8_x(_ptr(w.nib), _ptr(w.scale), w.n, w.k, _ptr(x2), m, x2.stride(0), _ptr(y),
+                              _dt(y.dtype), y.stride(0), _ptr(ws), ws.numel(), _stream(stream)), "mcapq_w4a8_x")
+    return y
+
+
+def w4a16(w: PackedW4, x: torch.Tensor, out_dtype=torch.float32, out=None, stream=None):
+    """a4/a6: exact-dequant W4A16 on bf16 tensor cores."""
+    _need_cuda(w.nib, x)
+    x2 = x if x.dim() == 2 else x.view(1, -1)
+    m = x2.shape[0]
+    y = _out(m, w.n, out_dtype, x.device, out)
+    check(load().mcapq_w4a16(_ptr(w.nib), _ptr(w.scale), w.n, w.k, _ptr(x2), m, x2.stride(0), _ptr(y),
+                             _dt(y.dtype), y.stride(0), _stream(stream)), "mcapq_w4a16")
+    return y
+
+
+def linear(route: int, w: PackedW4, x: torch.Tensor, out_dtype=torch.float32, out=None, ws=None, stream=None):
+    """Routed linear (a3-a6 by route)."""
+    _need_cuda(w.nib, x)
+    x2 = x if x.dim() == 2 else x.view(1, -1)
+    m = x2.shape[0]
+    y = _out(m, w.n, out_dtype, x.device, out)
+    ws = _ws(route, m, w.n, w.k, x.device, ws)
+    check(load().mcapq_linear(route, _ptr(w.nib), _ptr(w.scale), w.n, w.k, _ptr(x2), m, x2.stride(0), _ptr(y),
+                              _dt(y.dtype), y.stride(0), _ptr(ws), ws.numel(), _stream(stream)), "mcapq_linear")
+    return y
+
+
+def linear_host(route: int, w: PackedW4, x_host: torch.Tensor, y_host: torch.Tensor, ws: torch.Tensor,
+                stream=None):
+    """End-to-end routed linear from pinned host x into pinned host y (asynchronous)."""
+    m, k = x_host.shape
+    check(load().mcapq_linear_host(route, _ptr(w.nib), _ptr(w.scale), w.n, w.k, _ptr(x_host), m, _ptr(y_host),
+                                   _dt(y_host.dtype), _ptr(ws), ws.numel(), _stream(stream)), "mcapq_linear_host")
+    return y_host
+
+
+def w4a8_group_dots(w: PackedW4, q, sq, mode: int = 1, stream=None):
+    """Test entry: exact int32 D [M, N, K/32] through the dp4a (0) or IMMA (1) code."""
+    m = q.shape[0]
+    D = torch.empty((m, w.n, w.k // 32), dtype=torch.int32, device=q.device)
+    check(load().mcapq_w4a8_group_dots(_ptr(w.nib), w.n, w.k, _ptr(q), _ptr(sq), m, _ptr(D), mode,
+                                       _stream(stream)), "mcapq_w4a8_group_dots")
+    return D
+
+
+# ------------------------------------------------------------------ profile
+class Profile:
+    """Dispatch table parsed by the library (a7)."""
+
+    def __init__(self, handle):
+        self._h = handle
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            load().mcapq_profile_free(self._h)
+            self._h = None
+
+    @property
+    def layers(self) -> int:
+        return load().mcapq_profile_layers(self._h)
+
+    @property
+    def tau(self) -> float:
+        return load().mcapq_profile_tau(self._h)
+
+    def scores(self):
+        n = self.layers
+        buf = (ctypes.c_double * n)()
+        check(load().mcapq_profile_scores(self._h, ctypes.cast(buf, ctypes.c_void_p), n), "mcapq_profile_scores")
+        return list(buf)
+
+    def routes(self):
+        n = self.layers
+        buf = (ctypes.c_uint8 * n)()
+        check(load().mcapq_profile_routes(self._h, ctypes.cast(buf, ctypes.c_void_p), n), "mcapq_profile_routes")
+        return list(buf)
+
+
+def profile_parse(text: str | bytes, tau: float | None = None) -> Profile:
+    b = text.encode() if isinstance(text, str) else bytes(text)
+    h = ctypes.c_void_p()
+    check(load().mcapq_profile_parse(b, len(b), float("nan") if tau is None else float(tau), ctypes.byref(h)),
+          "mcapq_profile_parse")
+    return Profile(h)
+
+
+# ------------------------------------------------------------------ stack
+class Stack:
+    """Routed decode-linear stack (a9); the library owns its workspace and graph."""
+
+    def __init__(self, routes, max_m: int = 1):
+        self.routes = [int(r) for r in routes]
+        buf = (ctypes.c_uint8 * len(self.routes))(*self.routes)
+        h = ctypes.c_void_p()
+        check(load().mcapq_stack_create(len(self.routes), ctypes.cast(buf, ctypes.c_void_p), max_m, ctypes.byref(h)),
+              "mcapq_stack_create")
+        self._h = h
+        self._keep = []
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            load().mcapq_stack_destroy(self._h)
+            self._h = None
+
+    def set(self, layer: int, slot: int, input_id: int, w: PackedW4, x: torch.Tensor, y: torch.Tensor):
+        self._keep.append((w, x, y))
+        check(load().mcapq_stack_set(self._h, layer, slot, input_id, _ptr(w.nib), _ptr(w.scale), w.n, w.k, _ptr(x),
+                                     _ptr(y), _dt(y.dtype)), "mcapq_stack_set")
+
+    def run(self, m: int = 1, stream=None):
+        check(load().mcapq_stack_run(self._h, m, _stream(stream)), "mcapq_stack_run")
+
+    def capture(self, m: int = 1, stream=None):
+        check(load().mcapq_stack_capture(self._h, m, _stream(stream)), "mcapq_stack_capture")
+
+    def replay(self, stream=None):
+        check(load().mcapq_stack_replay(self._h, _stream(stream)), "mcapq_stack_replay")
+
+    @property
+    def weight_bytes(self) -> int:
+        return load().mcapq_stack_weight_bytes(self._h)
+
+    def launches(self, m: int = 1) -> int:
+        return load().mcapq_stack_launches(self._h, m)
+
+    def host_bytes(self, m: int = 1):
+        """(input bytes, output bytes) of one end-to-end step."""
+        return load().mcapq_stack_host_bytes(self._h, m, 0), load().mcapq_stack_host_bytes(self._h, m, 1)
+
+    def step_host(self, x_host: torch.Tensor, y_host: torch.Tensor, m: int = 1, stream=None):
+        """One end-to-end step: pinned host inputs -> graph replay -> pinned host outputs (async)."""
+        bi, bo = self.host_bytes(m)
+        assert x_host.numel() * x_host.element_size() >= bi and y_host.numel() * y_host.element_size() >= bo
+        check(load().mcapq_stack_step_host(self._h, m, _ptr(x_host), _ptr(y_host), _stream(stream)),
+              "mcapq_stack_step_host")
+
+
+# ------------------------------------------------------------------ multi-GPU
+class Comm:
+    """Library-owned NCCL communicator; the unique id travels over a torch process group."""
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+        world, rank = dist.get_world_size(group), dist.get_rank(group)
+        idbuf = torch.zeros(128, dtype=torch.uint8)
+        if rank == 0:
+            raw = (ctypes.c_uint8 * 128)()
+            check(load().mcapq_comm_unique_id(ctypes.cast(raw, ctypes.c_void_p)), "mcapq_comm_unique_id")
+            idbuf = torch.tensor(list(raw), dtype=torch.uint8)
+        obj = [idbuf.tolist()]
+        dist.broadcast_object_list(obj, src=0, group=group)
+        raw = (ctypes.c_uint8 * 128)(*obj[0])
+        h = ctypes.c_void_p()
+        check(load().mcapq_comm_init(ctypes.cast(raw, ctypes.c_void_p), world, rank, ctypes.byref(h)),
+              "mcapq_comm_init")
+        self._h, self.world, self.rank = h, world, rank
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            load().mcapq_comm_destroy(self._h)
+            self._h = None
+
+    def workspace_bytes(self, route, m, n_full, k):
+        return load().mcapq_colshard_workspace_bytes(route, m, n_full, k, self.world)
+
+
+def linear_colshard(comm: Comm, route: int, w_shard: PackedW4, n_full: int, x: torch.Tensor,
+                    out_dtype=torch.bfloat16, out=None, ws=None, stream=None):
+    """a8: column-sharded routed linear + NCCL all-gather into y_full [M, n_full]."""
+    x2 = x if x.dim() == 2 else x.view(1, -1)
+    m = x2.shape[0]
+    y = _out(m, n_full, out_dtype, x.device, out)
+    need = comm.workspace_bytes(route, m, n_full, w_shard.k)
+    ws = ws if ws is not None else torch.empty(max(need, 256), dtype=torch.uint8, device=x.device)
+    check(load().mcapq_linear_colshard(comm._h, route, _ptr(w_shard.nib), _ptr(w_shard.scale), n_full, w_shard.k,
+                                       _ptr(x2), m, _ptr(y), _dt(y.dtype), _ptr(ws), ws.numel(), _stream(stream)),
+          "mcapq_linear_colshard")
+    return y

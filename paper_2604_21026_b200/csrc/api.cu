@@ -1,0 +1,274 @@
+// api.cu -- the extern "C" boundary of libmcapq (include/mcapq.h): argument
+// validation, status codes, workspace carve-up and route dispatch.  Every
+// arithmetic step runs in the kernels of kernels_*.cu.
+#include <cmath>
+#include <cstring>
+
+#include "internal.h"
+
+namespace mcapq {
+
+static thread_local char g_err[512] = "";
+
+void set_error(const char *fmt, ...)
+{
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_err, sizeof(g_err), fmt, ap);
+    va_end(ap);
+}
+void clear_error() { g_err[0] = '\0'; }
+
+int device_sms()
+{
+    int dev = 0, sms = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return 0;
+    if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return 0;
+    return sms;
+}
+
+static size_t align256(size_t b) { return (b + 255) & ~(size_t)255; }
+
+size_t a8_workspace_bytes(int64_t m, int64_t k)
+{
+    const int64_t G = k / 32;
+    return align256((size_t)(m * k)) + align256((size_t)(m * G) * 4) + align256((size_t)(m * G) * 4);
+}
+
+A8Workspace a8_workspace(void *ws, int64_t m, int64_t k)
+{
+    const int64_t G = k / 32;
+    uint8_t *p = reinterpret_cast<uint8_t *>(ws);
+    A8Workspace w;
+    w.q = reinterpret_cast<int8_t *>(p);
+    p += align256((size_t)(m * k));
+    w.sx = reinterpret_cast<float *>(p);
+    p += align256((size_t)(m * G) * 4);
+    w.sq = reinterpret_cast<int32_t *>(p);
+    return w;
+}
+
+}  // namespace mcapq
+
+using namespace mcapq;
+
+#define CHECK_SHAPE(n, k, m)                                                                                  \
+    MCAPQ_REQUIRE((n) >= 1 && (k) >= 32 && (k) % 32 == 0 && (m) >= 1, MCAPQ_EINVAL,                          \
+                  "bad shape n=%lld k=%lld m=%lld (need n>=1, m>=1, k>=32, k%%32==0)", (long long)(n),      \
+                  (long long)(k), (long long)(m))
+#define CHECK_PTR(p, name) MCAPQ_REQUIRE((p) != nullptr, MCAPQ_EINVAL, "%s is NULL", name)
+#define CHECK_AL16(p, name) MCAPQ_REQUIRE(aligned16(p), MCAPQ_EINVAL, "%s is not 16-byte aligned", name)
+#define CHECK_LD(ld, minv, name)                                                                              \
+    MCAPQ_REQUIRE((ld) >= (minv) && (ld) % 8 == 0, MCAPQ_EINVAL, "%s=%lld must be >= %lld and a multiple of 8", \
+                  name, (long long)(ld), (long long)(minv))
+#define CHECK_YDT(d) MCAPQ_REQUIRE((d) == MCAPQ_BF16 || (d) == MCAPQ_F32, MCAPQ_EDTYPE, "bad output dtype %d", (d))
+#define LAUNCH_TRY(expr)                                                                                      \
+    do {                                                                                                      \
+        cudaError_t e_ = (expr);                                                                              \
+        if (e_ != cudaSuccess) {                                                                              \
+            set_error("kernel launch failed: %s", cudaGetErrorString(e_));                                  \
+            return MCAPQ_ECUDA;                                                                               \
+        }                                                                                                     \
+    } while (0)
+
+static mcapq_status check_weight(const uint8_t *nib, const uint16_t *scale, int64_t n, int64_t k)
+{
+    CHECK_PTR(nib, "nib");
+    CHECK_PTR(scale, "scale");
+    CHECK_AL16(nib, "nib");
+    MCAPQ_REQUIRE((reinterpret_cast<uintptr_t>(scale) & 1u) == 0, MCAPQ_EINVAL, "scale is not 2-byte aligned");
+    (void)n;
+    (void)k;
+    return MCAPQ_OK;
+}
+
+extern "C" {
+
+int mcapq_abi_version(void) { return MCAPQ_ABI_VERSION; }
+const char *mcapq_last_error(void) { return g_err; }
+
+const char *mcapq_status_string(int s)
+{
+    switch (s) {
+    case MCAPQ_OK: return "ok";
+    case MCAPQ_EINVAL: return "invalid argument";
+    case MCAPQ_EDTYPE: return "unsupported dtype";
+    case MCAPQ_ERANGE: return "value out of range";
+    case MCAPQ_EPARSE: return "profile parse error";
+    case MCAPQ_ECUDA: return "CUDA error";
+    case MCAPQ_ENCCL: return "NCCL error";
+    case MCAPQ_EUNSUP: return "unsupported";
+    case MCAPQ_ENOSPACE: return "workspace too small";
+    default: return "unknown status";
+    }
+}
+
+int mcapq_device_sms(void) { return device_sms(); }
+
+size_t mcapq_w4_nib_bytes(int64_t n, int64_t k) { return (n > 0 && k > 0) ? (size_t)(n * (k / 2)) : 0; }
+size_t mcapq_w4_scale_bytes(int64_t n, int64_t k) { return (n > 0 && k > 0) ? (size_t)(n * (k / 32) * 2) : 0; }
+
+mcapq_status mcapq_pack_w4(const void *w, int wdt, int64_t n, int64_t k, int64_t ldw, uint8_t *nib,
+                           uint16_t *scale, uint32_t *dev_err, void *stream)
+{
+    clear_error();
+    CHECK_SHAPE(n, k, 1);
+    CHECK_PTR(w, "w");
+    CHECK_PTR(nib, "nib");
+    CHECK_PTR(scale, "scale");
+    MCAPQ_REQUIRE(wdt == MCAPQ_BF16 || wdt == MCAPQ_F32, MCAPQ_EDTYPE, "bad weight dtype %d", wdt);
+    MCAPQ_REQUIRE(ldw >= k, MCAPQ_EINVAL, "ldw=%lld < k=%lld", (long long)ldw, (long long)k);
+    MCAPQ_REQUIRE((reinterpret_cast<uintptr_t>(w) & 3u) == 0 && (reinterpret_cast<uintptr_t>(scale) & 1u) == 0,
+                  MCAPQ_EINVAL, "misaligned w/scale");
+    LAUNCH_TRY(launch_pack_w4(w, wdt, n, k, ldw, nib, scale, dev_err, as_stream(stream)));
+    return MCAPQ_OK;
+}
+
+mcapq_status mcapq_quant_a8(const uint16_t *x, int64_t m, int64_t k, int64_t ldx, int8_t *q, float *sx,
+                            int32_t *sq, void *stream)
+{
+    clear_error();
+    CHECK_SHAPE(1, k, m);
+    CHECK_PTR(x, "x");
+    CHECK_PTR(q, "q");
+    CHECK_PTR(sx, "sx");
+    CHECK_PTR(sq, "sq");
+    MCAPQ_REQUIRE(ldx >= k, MCAPQ_EINVAL, "ldx=%lld < k", (long long)ldx);
+    MCAPQ_REQUIRE((reinterpret_cast<uintptr_t>(x) & 1u) == 0, MCAPQ_EINVAL, "x misaligned");
+    LAUNCH_TRY(launch_quant_a8(x, m, k, ldx, q, sx, sq, as_stream(stream), false));
+    return MCAPQ_OK;
+}
+
+mcapq_status mcapq_w4a8(const uint8_t *nib, const uint16_t *scale, int64_t n, int64_t k, const int8_t *q,
+                        const float *sx, const int32_t *sq, int64_t m, void *y, int ydt, int64_t ldy, void *stream)
+{
+    clear_error();
+    CHECK_SHAPE(n, k, m);
+    mcapq_status st = check_weight(nib, scale, n, k);
+    if (st != MCAPQ_OK) return st;
+    CHECK_PTR(q, "q");
+    CHECK_PTR(sx, "sx");
+    CHECK_PTR(sq, "sq");
+    CHECK_PTR(y, "y");
+    CHECK_AL16(q, "q");
+    CHECK_AL16(y, "y");
+    CHECK_YDT(ydt);
+    CHECK_LD(ldy, n, "ldy");
+    LAUNCH_TRY(launch_w4a8(nib, scale, n, k, q, sx, sq, m, y, ydt, ldy, as_stream(stream), false));
+    return MCAPQ_OK;
+}
+
+size_t mcapq_workspace_bytes(int route, int64_t m, int64_t n, int64_t k)
+{
+    (void)n;
+    if (route != MCAPQ_W4A8 || m < 1 || k < 32) return 0;
+    return a8_workspace_bytes(m, k);
+}
+
+mcapq_status mcapq_w4a8_x(const uint8_t *nib, const uint16_t *scale, int64_t n, int64_t k, const uint16_t *x,
+                          int64_t m, int64_t ldx, void *y, int ydt, int64_t ldy, void *ws, size_t ws_bytes,
+                          void *stream)
+{
+    clear_error();
+    CHECK_SHAPE(n, k, m);
+    mcapq_status st = check_weight(nib, scale, n, k);
+    if (st != MCAPQ_OK) return st;
+    CHECK_PTR(x, "x");
+    CHECK_PTR(y, "y");
+    CHECK_PTR(ws, "ws");
+    CHECK_AL16(x, "x");
+    CHECK_AL16(y, "y");
+    CHECK_AL16(ws, "ws");
+    CHECK_YDT(ydt);
+    CHECK_LD(ldx, k, "ldx");
+    CHECK_LD(ldy, n, "ldy");
+    MCAPQ_REQUIRE(ws_bytes >= a8_workspace_bytes(m, k), MCAPQ_ENOSPACE, "workspace %zu < %zu", ws_bytes,
+                  a8_workspace_bytes(m, k));
+    const A8Workspace w = a8_workspace(ws, m, k);
+    cudaStream_t s = as_stream(stream);
+    LAUNCH_TRY(launch_quant_a8(x, m, k, ldx, w.q, w.sx, w.sq, s, false));
+    LAUNCH_TRY(launch_w4a8(nib, scale, n, k, w.q, w.sx, w.sq, m, y, ydt, ldy, s, true));
+    return MCAPQ_OK;
+}
+
+mcapq_status mcapq_w4a16(const uint8_t *nib, const uint16_t *scale, int64_t n, int64_t k, const uint16_t *x,
+                         int64_t m, int64_t ldx, void *y, int ydt, int64_t ldy, void *stream)
+{
+    clear_error();
+    CHECK_SHAPE(n, k, m);
+    mcapq_status st = check_weight(nib, scale, n, k);
+    if (st != MCAPQ_OK) return st;
+    CHECK_PTR(x, "x");
+    CHECK_PTR(y, "y");
+    CHECK_AL16(x, "x");
+    CHECK_AL16(y, "y");
+    CHECK_YDT(ydt);
+    CHECK_LD(ldx, k, "ldx");
+    CHECK_LD(ldy, n, "ldy");
+    LAUNCH_TRY(launch_w4a16(nib, scale, n, k, x, m, ldx, y, ydt, ldy, as_stream(stream), false));
+    return MCAPQ_OK;
+}
+
+mcapq_status mcapq_linear(int route, const uint8_t *nib, const uint16_t *scale, int64_t n, int64_t k,
+                          const uint16_t *x, int64_t m, int64_t ldx, void *y, int ydt, int64_t ldy, void *ws,
+                          size_t ws_bytes, void *stream)
+{
+    if (route == MCAPQ_W4A8) return mcapq_w4a8_x(nib, scale, n, k, x, m, ldx, y, ydt, ldy, ws, ws_bytes, stream);
+    if (route == MCAPQ_W4A16) return mcapq_w4a16(nib, scale, n, k, x, m, ldx, y, ydt, ldy, stream);
+    clear_error();
+    set_error("bad route %d", route);
+    return MCAPQ_EINVAL;
+}
+
+size_t mcapq_host_workspace_bytes(int route, int64_t m, int64_t n, int64_t k)
+{
+    if (m < 1 || n < 1 || k < 32) return 0;
+    const size_t xb = align256((size_t)(m * k) * 2), yb = align256((size_t)(m * n) * 4);
+    return xb + yb + mcapq_workspace_bytes(route, m, n, k);
+}
+
+mcapq_status mcapq_linear_host(int route, const uint8_t *nib, const uint16_t *scale, int64_t n, int64_t k,
+                               const uint16_t *x_host, int64_t m, void *y_host, int ydt, void *ws, size_t ws_bytes,
+                               void *stream)
+{
+    clear_error();
+    CHECK_SHAPE(n, k, m);
+    CHECK_PTR(x_host, "x_host");
+    CHECK_PTR(y_host, "y_host");
+    CHECK_PTR(ws, "ws");
+    CHECK_AL16(ws, "ws");
+    CHECK_YDT(ydt);
+    MCAPQ_REQUIRE(route == MCAPQ_W4A8 || route == MCAPQ_W4A16, MCAPQ_EINVAL, "bad route %d", route);
+    MCAPQ_REQUIRE(ws_bytes >= mcapq_host_workspace_bytes(route, m, n, k), MCAPQ_ENOSPACE, "workspace too small");
+    const size_t xb = align256((size_t)(m * k) * 2), yb = align256((size_t)(m * n) * 4);
+    uint8_t *p = reinterpret_cast<uint8_t *>(ws);
+    uint16_t *xd = reinterpret_cast<uint16_t *>(p);
+    void *yd = p + xb;
+    void *rest = p + xb + yb;
+    cudaStream_t s = as_stream(stream);
+    MCAPQ_CUDA_TRY(cudaMemcpyAsync(xd, x_host, (size_t)(m * k) * 2, cudaMemcpyHostToDevice, s));
+    mcapq_status st = mcapq_linear(route, nib, scale, n, k, xd, m, k, yd, ydt, n, rest,
+                                   ws_bytes - xb - yb, stream);
+    if (st != MCAPQ_OK) return st;
+    MCAPQ_CUDA_TRY(cudaMemcpyAsync(y_host, yd, (size_t)(m * n) * (ydt == MCAPQ_F32 ? 4 : 2),
+                                   cudaMemcpyDeviceToHost, s));
+    return MCAPQ_OK;
+}
+
+mcapq_status mcapq_w4a8_group_dots(const uint8_t *nib, int64_t n, int64_t k, const int8_t *q, const int32_t *sq,
+                                   int64_t m, int32_t *D, int mode, void *stream)
+{
+    clear_error();
+    CHECK_SHAPE(n, k, m);
+    CHECK_PTR(nib, "nib");
+    CHECK_PTR(q, "q");
+    CHECK_PTR(sq, "sq");
+    CHECK_PTR(D, "D");
+    CHECK_AL16(nib, "nib");
+    CHECK_AL16(q, "q");
+    MCAPQ_REQUIRE(mode == 0 || mode == 1, MCAPQ_EINVAL, "mode must be 0 (dp4a) or 1 (imma)");
+    LAUNCH_TRY(launch_w4a8_group_dots(nib, n, k, q, sq, m, D, mode, as_stream(stream)));
+    return MCAPQ_OK;
+}
+
+}  // extern "C"

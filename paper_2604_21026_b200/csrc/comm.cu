@@ -1,0 +1,154 @@
+// comm.cu -- column (output-feature) sharded decode linear over NCCL (row a8).
+//
+// north_star: large linears (MLP, lm_head) are column-sharded across the GPUs
+// of one 8xB200 node with an NCCL all-gather over NVLink/NVSwitch.  The paper
+// itself is single-GPU.  Rank r owns rows [r N/P, (r+1) N/P) of
+// the packed weight (reading A22); every rank holds the full x.  Each rank runs
+// the routed linear on its shard; the per-row arithmetic depends on K only, so
+// the gathered y is bit-identical to the single-GPU result.
+//   M == 1 : the rank-major gather is already the row order of y -> gather in
+//            place into y_full.
+//   M  > 1 : gather [P][M][N/P] into the workspace, then one permute kernel
+//            writes y_full[m][r N/P + j].
+#include <nccl.h>
+
+#include "internal.h"
+
+struct mcapq_comm {
+    ncclComm_t comm = nullptr;
+    int world = 1, rank = 0;
+};
+
+using namespace mcapq;
+
+namespace {
+
+__global__ void permute_rank_major(const uint8_t *__restrict__ src, uint8_t *__restrict__ dst, int64_t m,
+                                   int64_t n_full, int world, int es)
+{
+    const int64_t per = n_full / world;
+    const int64_t total = m * n_full;
+    for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+         idx += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = idx / n_full, c = idx % n_full;
+        const int64_t r = c / per, j = c % per;
+        const int64_t s = (r * m + i) * per + j;
+        if (es == 4)
+            reinterpret_cast<float *>(dst)[idx] = reinterpret_cast<const float *>(src)[s];
+        else
+            reinterpret_cast<uint16_t *>(dst)[idx] = reinterpret_cast<const uint16_t *>(src)[s];
+    }
+}
+
+size_t align256(size_t b) { return (b + 255) & ~(size_t)255; }
+
+}  // namespace
+
+#define NCCL_TRY(expr)                                                                                        \
+    do {                                                                                                      \
+        ncclResult_t r_ = (expr);                                                                             \
+        if (r_ != ncclSuccess) {                                                                              \
+            set_error("%s: %s", #expr, ncclGetErrorString(r_));                                              \
+            return MCAPQ_ENCCL;                                                                               \
+        }                                                                                                     \
+    } while (0)
+
+extern "C" {
+
+mcapq_status mcapq_comm_unique_id(uint8_t *id_host_128)
+{
+    clear_error();
+    MCAPQ_REQUIRE(id_host_128, MCAPQ_EINVAL, "id is NULL");
+    static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId must be 128 bytes");
+    ncclUniqueId id;
+    NCCL_TRY(ncclGetUniqueId(&id));
+    memcpy(id_host_128, &id, 128);
+    return MCAPQ_OK;
+}
+
+mcapq_status mcapq_comm_init(const uint8_t *id_host_128, int world, int rank, mcapq_comm **out)
+{
+    clear_error();
+    MCAPQ_REQUIRE(id_host_128 && out, MCAPQ_EINVAL, "NULL argument");
+    MCAPQ_REQUIRE(world >= 1 && rank >= 0 && rank < world, MCAPQ_ERANGE, "bad world=%d rank=%d", world, rank);
+    ncclUniqueId id;
+    memcpy(&id, id_host_128, 128);
+    mcapq_comm *c = new (std::nothrow) mcapq_comm;
+    MCAPQ_REQUIRE(c, MCAPQ_ECUDA, "out of host memory");
+    ncclResult_t r = ncclCommInitRank(&c->comm, world, id, rank);
+    if (r != ncclSuccess) {
+        set_error("ncclCommInitRank: %s", ncclGetErrorString(r));
+        delete c;
+        return MCAPQ_ENCCL;
+    }
+    c->world = world;
+    c->rank = rank;
+    *out = c;
+    return MCAPQ_OK;
+}
+
+int mcapq_comm_world(const mcapq_comm *c) { return c ? c->world : 0; }
+int mcapq_comm_rank(const mcapq_comm *c) { return c ? c->rank : -1; }
+
+size_t mcapq_colshard_workspace_bytes(int route, int64_t m, int64_t n_full, int64_t k, int world)
+{
+    if (world < 1 || m < 1 || n_full < 1 || k < 32 || n_full % world) return 0;
+    const int64_t per = n_full / world;
+    size_t b = align256((size_t)(m * per) * 4);               // local slice (fp32 worst case)
+    if (m > 1) b += align256((size_t)(m * n_full) * 4);        // rank-major gather
+    if (route == MCAPQ_W4A8) b += a8_workspace_bytes(m, k);
+    return b;
+}
+
+mcapq_status mcapq_linear_colshard(const mcapq_comm *c, int route, const uint8_t *nib_shard,
+                                   const uint16_t *scale_shard, int64_t n_full, int64_t k, const uint16_t *x,
+                                   int64_t m, void *y_full, int ydt, void *ws, size_t ws_bytes, void *stream)
+{
+    clear_error();
+    MCAPQ_REQUIRE(c && c->comm, MCAPQ_EINVAL, "communicator is NULL");
+    MCAPQ_REQUIRE(n_full % c->world == 0, MCAPQ_EINVAL, "N=%lld not divisible by P=%d", (long long)n_full, c->world);
+    MCAPQ_REQUIRE(ydt == MCAPQ_BF16 || ydt == MCAPQ_F32, MCAPQ_EDTYPE, "bad ydt");
+    MCAPQ_REQUIRE(route == MCAPQ_W4A8 || route == MCAPQ_W4A16, MCAPQ_EINVAL, "bad route");
+    MCAPQ_REQUIRE(ws && aligned16(ws) && y_full && aligned16(y_full), MCAPQ_EINVAL, "NULL/misaligned ws or y");
+    MCAPQ_REQUIRE(ws_bytes >= mcapq_colshard_workspace_bytes(route, m, n_full, k, c->world), MCAPQ_ENOSPACE,
+                  "workspace too small");
+    const int64_t per = n_full / c->world;
+    MCAPQ_REQUIRE(per % 8 == 0, MCAPQ_EINVAL, "N/P=%lld must be a multiple of 8", (long long)per);
+    const int es = ydt == MCAPQ_F32 ? 4 : 2;
+    uint8_t *p = reinterpret_cast<uint8_t *>(ws);
+    uint8_t *local = p;
+    p += align256((size_t)(m * per) * 4);
+    uint8_t *gathered = nullptr;
+    if (m > 1) {
+        gathered = p;
+        p += align256((size_t)(m * n_full) * 4);
+    }
+    void *rest = p;
+    const size_t rest_bytes = ws_bytes - (size_t)(p - reinterpret_cast<uint8_t *>(ws));
+    cudaStream_t s = as_stream(stream);
+
+    mcapq_status st = mcapq_linear(route, nib_shard, scale_shard, per, k, x, m, k, local, ydt, per, rest, rest_bytes,
+                                   stream);
+    if (st != MCAPQ_OK) return st;
+    const ncclDataType_t dt = ydt == MCAPQ_F32 ? ncclFloat32 : ncclBfloat16;
+    if (m == 1) {
+        NCCL_TRY(ncclAllGather(local, y_full, (size_t)per, dt, c->comm, s));
+    } else {
+        NCCL_TRY(ncclAllGather(local, gathered, (size_t)(m * per), dt, c->comm, s));
+        const int64_t total = m * n_full;
+        const int grid = (int)((total + 255) / 256 < 4096 ? (total + 255) / 256 : 4096);
+        permute_rank_major<<<grid, 256, 0, s>>>(gathered, reinterpret_cast<uint8_t *>(y_full), m, n_full, c->world,
+                                                es);
+        MCAPQ_CUDA_TRY(cudaGetLastError());
+    }
+    return MCAPQ_OK;
+}
+
+void mcapq_comm_destroy(mcapq_comm *c)
+{
+    if (!c) return;
+    if (c->comm) ncclCommDestroy(c->comm);
+    delete c;
+}
+
+}  // extern "C"

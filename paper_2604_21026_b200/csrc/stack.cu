@@ -1,0 +1,258 @@
+// stack.cu -- the routed decode-linear stack (row a9): L layers x S slots under
+// the MCAP dispatch table, replayed as one CUDA graph per decode step
+// ("CUDA graph capture for decode"; routing P:840-846).
+//
+// Each layer follows route[i] (all its slots, reading A12).  W4A8 layers
+// quantise each distinct input once (slots with the same input_id, e.g. q/k/v,
+// share it: reading A15) into one library-owned workspace.  Every
+// kernel is launched with programmatic dependent launch: a GEMV starts
+// streaming its weights while its predecessor drains and waits
+// (griddepcontrol.wait) only before reading activations, so the step's
+// 100+ launches overlap their ramps.  Data order stays total: each kernel waits
+// for its predecessor's completion before touching activations.
+#include <vector>
+
+#include "internal.h"
+
+namespace {
+constexpr int kMaxSlots = 16;
+struct Slot {
+    bool set = false;
+    int input_id = 0;
+    const uint8_t *nib = nullptr;
+    const uint16_t *scale = nullptr;
+    int64_t n = 0, k = 0;
+    const uint16_t *x = nullptr;
+    void *y = nullptr;
+    int ydt = 0;
+};
+}  // namespace
+
+struct mcapq_stack {
+    int layers = 0;
+    std::vector<uint8_t> routes;
+    int64_t max_m = 1;
+    std::vector<Slot> slots;   // [layers][kMaxSlots]
+    void *ws = nullptr;
+    size_t ws_bytes = 0;
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    int64_t graph_m = 0;
+};
+
+using namespace mcapq;
+
+static mcapq_status ensure_ws(mcapq_stack *st, int64_t k)
+{
+    const size_t need = a8_workspace_bytes(st->max_m, k);
+    if (need <= st->ws_bytes) return MCAPQ_OK;
+    if (st->ws) cudaFree(st->ws);
+    st->ws = nullptr;
+    st->ws_bytes = 0;
+    MCAPQ_CUDA_TRY(cudaMalloc(&st->ws, need));
+    st->ws_bytes = need;
+    return MCAPQ_OK;
+}
+
+extern "C" {
+
+mcapq_status mcapq_stack_create(int layers, const uint8_t *routes_host, int64_t max_m, mcapq_stack **out)
+{
+    clear_error();
+    MCAPQ_REQUIRE(out && routes_host && layers >= 1 && max_m >= 1, MCAPQ_EINVAL, "bad stack_create arguments");
+    for (int i = 0; i < layers; ++i)
+        MCAPQ_REQUIRE(routes_host[i] <= 1, MCAPQ_EINVAL, "route[%d]=%d is not 0/1", i, routes_host[i]);
+    mcapq_stack *st = new (std::nothrow) mcapq_stack;
+    MCAPQ_REQUIRE(st, MCAPQ_ECUDA, "out of host memory");
+    st->layers = layers;
+    st->routes.assign(routes_host, routes_host + layers);
+    st->max_m = max_m;
+    st->slots.resize((size_t)layers * kMaxSlots);
+    *out = st;
+    return MCAPQ_OK;
+}
+
+mcapq_status mcapq_stack_set(mcapq_stack *st, int layer, int slot, int input_id, const uint8_t *nib,
+                             const uint16_t *scale, int64_t n, int64_t k, const uint16_t *x, void *y, int ydt)
+{
+    clear_error();
+    MCAPQ_REQUIRE(st, MCAPQ_EINVAL, "stack is NULL");
+    MCAPQ_REQUIRE(layer >= 0 && layer < st->layers && slot >= 0 && slot < kMaxSlots, MCAPQ_EINVAL,
+                  "layer/slot out of range");
+    MCAPQ_REQUIRE(nib && scale && x && y && aligned16(nib) && aligned16(x) && aligned16(y), MCAPQ_EINVAL,
+                  "NULL or misaligned pointer");
+    MCAPQ_REQUIRE(n >= 1 && k >= 32 && k % 32 == 0 && n % 8 == 0, MCAPQ_EINVAL, "bad shape n=%lld k=%lld",
+                  (long long)n, (long long)k);
+    MCAPQ_REQUIRE(ydt == MCAPQ_BF16 || ydt == MCAPQ_F32, MCAPQ_EDTYPE, "bad ydt");
+    Slot &s = st->slots[(size_t)layer * kMaxSlots + slot];
+    s.set = true;
+    s.input_id = input_id;
+    s.nib = nib;
+    s.scale = scale;
+    s.n = n;
+    s.k = k;
+    s.x = x;
+    s.y = y;
+    s.ydt = ydt;
+    if (st->routes[layer] == MCAPQ_W4A8) return ensure_ws(st, k);
+    return MCAPQ_OK;
+}
+
+mcapq_status mcapq_stack_run(mcapq_stack *st, int64_t m, void *stream)
+{
+    clear_error();
+    MCAPQ_REQUIRE(st && m >= 1 && m <= st->max_m, MCAPQ_EINVAL, "bad stack_run arguments");
+    cudaStream_t s = as_stream(stream);
+    for (int l = 0; l < st->layers; ++l) {
+        const bool a8 = st->routes[l] == MCAPQ_W4A8;
+        int last_input = -1 << 30;
+        const int64_t *dummy = nullptr;
+        (void)dummy;
+        A8Workspace w = {};
+        for (int sl = 0; sl < kMaxSlots; ++sl) {
+            const Slot &s_ = st->slots[(size_t)l * kMaxSlots + sl];
+            if (!s_.set) continue;
+            if (a8) {
+                if (s_.input_id != last_input) {
+                    w = a8_workspace(st->ws, m, s_.k);
+                    cudaError_t e = launch_quant_a8(s_.x, m, s_.k, s_.k, w.q, w.sx, w.sq, s, true);
+                    MCAPQ_REQUIRE(e == cudaSuccess, MCAPQ_ECUDA, "quant launch: %s", cudaGetErrorString(e));
+                    last_input = s_.input_id;
+                }
+                cudaError_t e = launch_w4a8(s_.nib, s_.scale, s_.n, s_.k, w.q, w.sx, w.sq, m, s_.y, s_.ydt, s_.n, s, true);
+                MCAPQ_REQUIRE(e == cudaSuccess, MCAPQ_ECUDA, "w4a8 launch: %s", cudaGetErrorString(e));
+            } else {
+                cudaError_t e = launch_w4a16(s_.nib, s_.scale, s_.n, s_.k, s_.x, m, s_.k, s_.y, s_.ydt, s_.n, s, true);
+                MCAPQ_REQUIRE(e == cudaSuccess, MCAPQ_ECUDA, "w4a16 launch: %s", cudaGetErrorString(e));
+            }
+        }
+    }
+    return MCAPQ_OK;
+}
+
+mcapq_status mcapq_stack_capture(mcapq_stack *st, int64_t m, void *stream)
+{
+    clear_error();
+    MCAPQ_REQUIRE(st, MCAPQ_EINVAL, "stack is NULL");
+    cudaStream_t s = as_stream(stream);
+    MCAPQ_REQUIRE(s != nullptr, MCAPQ_EINVAL, "graph capture needs a non-default stream");
+    if (st->exec) cudaGraphExecDestroy(st->exec);
+    if (st->graph) cudaGraphDestroy(st->graph);
+    st->exec = nullptr;
+    st->graph = nullptr;
+    MCAPQ_CUDA_TRY(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+    mcapq_status r = mcapq_stack_run(st, m, stream);
+    cudaGraph_t g = nullptr;
+    cudaError_t e = cudaStreamEndCapture(s, &g);
+    if (r != MCAPQ_OK) {
+        if (g) cudaGraphDestroy(g);
+        return r;
+    }
+    MCAPQ_CUDA_TRY(e);
+    st->graph = g;
+    MCAPQ_CUDA_TRY(cudaGraphInstantiate(&st->exec, g, 0));
+    st->graph_m = m;
+    return MCAPQ_OK;
+}
+
+mcapq_status mcapq_stack_replay(mcapq_stack *st, void *stream)
+{
+    clear_error();
+    MCAPQ_REQUIRE(st && st->exec, MCAPQ_EINVAL, "no captured graph");
+    MCAPQ_CUDA_TRY(cudaGraphLaunch(st->exec, as_stream(stream)));
+    return MCAPQ_OK;
+}
+
+size_t mcapq_stack_weight_bytes(const mcapq_stack *st)
+{
+    if (!st) return 0;
+    size_t b = 0;
+    for (const Slot &s : st->slots)
+        if (s.set) b += (size_t)(s.n * (s.k / 2)) + (size_t)(s.n * (s.k / 32) * 2);
+    return b;
+}
+
+int mcapq_stack_launches(const mcapq_stack *st, int64_t m)
+{
+    (void)m;
+    if (!st) return 0;
+    int c = 0;
+    for (int l = 0; l < st->layers; ++l) {
+        int last = -1 << 30;
+        for (int sl = 0; sl < kMaxSlots; ++sl) {
+            const Slot &s = st->slots[(size_t)l * kMaxSlots + sl];
+            if (!s.set) continue;
+            if (st->routes[l] == MCAPQ_W4A8 && s.input_id != last) {
+                ++c;
+                last = s.input_id;
+            }
+            ++c;
+        }
+    }
+    return c;
+}
+
+size_t mcapq_stack_host_bytes(const mcapq_stack *st, int64_t m, int which)
+{
+    if (!st || m < 1) return 0;
+    size_t b = 0;
+    for (int l = 0; l < st->layers; ++l) {
+        int last = -1 << 30;
+        for (int sl = 0; sl < kMaxSlots; ++sl) {
+            const Slot &s = st->slots[(size_t)l * kMaxSlots + sl];
+            if (!s.set) continue;
+            if (which == 0) {
+                if (s.input_id != last) b += (size_t)(m * s.k) * 2;
+                last = s.input_id;
+            } else {
+                b += (size_t)(m * s.n) * (s.ydt == MCAPQ_F32 ? 4 : 2);
+            }
+        }
+    }
+    return b;
+}
+
+mcapq_status mcapq_stack_step_host(mcapq_stack *st, int64_t m, const void *x_host, void *y_host, void *stream)
+{
+    clear_error();
+    MCAPQ_REQUIRE(st && x_host && y_host && m >= 1 && m <= st->max_m, MCAPQ_EINVAL, "bad stack_step_host arguments");
+    cudaStream_t s = as_stream(stream);
+    const uint8_t *xp = reinterpret_cast<const uint8_t *>(x_host);
+    for (int l = 0; l < st->layers; ++l) {
+        int last = -1 << 30;
+        for (int sl = 0; sl < kMaxSlots; ++sl) {
+            const Slot &s_ = st->slots[(size_t)l * kMaxSlots + sl];
+            if (!s_.set || s_.input_id == last) continue;
+            last = s_.input_id;
+            const size_t b = (size_t)(m * s_.k) * 2;
+            MCAPQ_CUDA_TRY(cudaMemcpyAsync(const_cast<uint16_t *>(s_.x), xp, b, cudaMemcpyHostToDevice, s));
+            xp += b;
+        }
+    }
+    if (st->exec && st->graph_m == m) {
+        MCAPQ_CUDA_TRY(cudaGraphLaunch(st->exec, s));
+    } else {
+        mcapq_status r = mcapq_stack_run(st, m, stream);
+        if (r != MCAPQ_OK) return r;
+    }
+    uint8_t *yp = reinterpret_cast<uint8_t *>(y_host);
+    for (size_t i = 0; i < st->slots.size(); ++i) {
+        const Slot &s_ = st->slots[i];
+        if (!s_.set) continue;
+        const size_t b = (size_t)(m * s_.n) * (s_.ydt == MCAPQ_F32 ? 4 : 2);
+        MCAPQ_CUDA_TRY(cudaMemcpyAsync(yp, s_.y, b, cudaMemcpyDeviceToHost, s));
+        yp += b;
+    }
+    return MCAPQ_OK;
+}
+
+void mcapq_stack_destroy(mcapq_stack *st)
+{
+    if (!st) return;
+    if (st->exec) cudaGraphExecDestroy(st->exec);
+    if (st->graph) cudaGraphDestroy(st->graph);
+    if (st->ws) cudaFree(st->ws);
+    delete st;
+}
+
+}  // extern "C"

@@ -1,0 +1,280 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the CPU oracle on identical
+seeded inputs (synth_inputs).  Integer stages bit-exact; outputs within the
+north-star tolerance (reading T):
+    |y - y*| <= rtol * max(|y*_n|, rms(y*)),  y* = oracle fp64 reference,
+    rtol = 1e-3 (fp32 output), 2e-3 (bf16 output).
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+import torch
+
+import synth_inputs as si
+
+pytestmark = pytest.mark.gpu
+
+GOLD = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+
+
+@pytest.fixture(scope="module")
+def mq():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2604_21026_b200 as mq
+    mq.load()
+    return mq
+
+
+DEV = "cuda:0"
+
+
+def _f32(t):
+    return t.float().cpu().numpy()
+
+
+def _pack_both(mq, orc, w_bf16):
+    pw = mq.pack_w4(w_bf16.to(DEV))
+    nib, sc = orc.pack_w4(_f32(w_bf16))
+    return pw, nib, sc
+
+
+def _assert_close(y_gpu, y64, rtol):
+    y = y_gpu.float().cpu().numpy().astype(np.float64)
+    ref = np.asarray(y64, np.float64).reshape(y.shape)
+    rms = np.sqrt(np.mean(ref ** 2)) if ref.size else 0.0
+    tol = rtol * np.maximum(np.abs(ref), rms)
+    bad = np.abs(y - ref) > tol
+    assert not bad.any(), (f"{bad.sum()} of {bad.size} outside tolerance; worst rel "
+                           f"{(np.abs(y - ref) / np.maximum(np.abs(ref), rms + 1e-300)).max():.3e}")
+
+
+# ---------------------------------------------------------------- a1 pack
+@pytest.mark.parametrize("n,k,kind", [(64, 256, "synth"), (37, 4096, "synth"), (1, 32, "synth"),
+                                      (48, 512, "adv"), (200, 2048, "adv")])
+def test_pack_bit_exact(mq, orc, n, k, kind):
+    w = si.weight(n, k, 11 + n) if kind == "synth" else si.adversarial_weight(n, k, 12 + n)
+    pw, nib, sc = _pack_both(mq, orc, w)
+    torch.cuda.synchronize()
+    assert np.array_equal(pw.nib.cpu().numpy(), nib)
+    assert np.array_equal(pw.scale.cpu().numpy().view(np.uint16), sc)
+
+
+def test_pack_f32_input_and_ldw(mq, orc):
+    w = (torch.randn(33, 96 + 32, generator=torch.Generator().manual_seed(3)) * 0.05)
+    w[5, 40] = 0.0
+    wd = w.to(DEV)
+    sub = wd[:, :96]                    # ldw = 128 > k = 96
+    pw = mq.pack_w4(sub)
+    nib, sc = orc.pack_w4(w[:, :96].numpy())
+    assert np.array_equal(pw.nib.cpu().numpy(), nib)
+    assert np.array_equal(pw.scale.cpu().numpy().view(np.uint16), sc)
+
+
+def test_pack_dev_err_flags(mq, orc):
+    w = torch.zeros(2, 64, dtype=torch.float32)
+    w[0, 3] = float("inf")
+    w[1, 40] = 6e5                      # |m|/8 > 65504 -> fp16 overflow (A4)
+    err = torch.zeros(1, dtype=torch.int32, device=DEV)
+    pw = mq.pack_w4(w.to(DEV), dev_err=err)
+    torch.cuda.synchronize()
+    assert int(err.item()) == 0x3
+    st, nib, sc = orc.pack_w4_status(w.numpy())
+    assert st == 3
+    assert np.array_equal(pw.nib.cpu().numpy(), nib)
+    assert np.array_equal(pw.scale.cpu().numpy().view(np.uint16), sc)
+
+
+# ---------------------------------------------------------------- a2 quant
+@pytest.mark.parametrize("m,k,kind", [(1, 2048, "synth"), (3, 4096, "swiglu"), (16, 1024, "adv"), (64, 3072, "synth")])
+def test_quant_a8_bit_exact(mq, orc, m, k, kind):
+    if kind == "adv":
+        x = si.adversarial_activation(m, k, 21)
+    else:
+        x = si.activation(m, k, 22 + m, "swiglu" if kind == "swiglu" else "rmsnorm")
+    q, s, sq = mq.quant_a8(x.to(DEV))
+    oq, os_, osq = orc.quant_a8(_f32(x))
+    torch.cuda.synchronize()
+    assert np.array_equal(q.cpu().numpy(), oq)
+    assert np.array_equal(s.cpu().numpy().view(np.uint32), os_.view(np.uint32))
+    assert np.array_equal(sq.cpu().numpy(), osq)
+
+
+# ---------------------------------------------------------------- integer stage
+@pytest.mark.parametrize("mode", [0, 1])
+@pytest.mark.parametrize("n,k,m", [(40, 512, 1), (33, 1024, 5), (16, 2048, 16)])
+def test_group_dots_bit_exact(mq, orc, mode, n, k, m):
+    w = si.adversarial_weight(n, k, 31 + n)
+    x = si.activation(m, k, 32 + m)
+    pw, nib, sc = _pack_both(mq, orc, w)
+    q, s, sq = mq.quant_a8(x.to(DEV))
+    D = mq.w4a8_group_dots(pw, q, sq, mode=mode)
+    oq, os_, osq = orc.quant_a8(_f32(x))
+    oD = orc.w4a8_group_dots(nib, oq, osq)
+    assert np.array_equal(D.cpu().numpy(), oD)
+
+
+# ---------------------------------------------------------------- a3-a6 outputs
+SHAPES = [(200, 2048), (3072, 1024), (48, 14336), (512, 3072)]
+
+
+@pytest.mark.parametrize("n,k", SHAPES)
+@pytest.mark.parametrize("m", [1, 2, 5, 8, 16, 64])
+@pytest.mark.parametrize("route", [0, 1])
+def test_linear_vs_oracle(mq, orc, route, m, n, k):
+    if m == 64 and n * k > 3072 * 1024:
+        pytest.skip("oracle time")
+    w = si.weight(n, k, 41 + n + k)
+    x = si.activation(m, k, 42 + m + k, "swiglu" if k >= 8192 else "rmsnorm")
+    pw, nib, sc = _pack_both(mq, orc, w)
+    xd = x.to(DEV)
+    for out_dtype, rtol in ((torch.float32, 1e-3), (torch.bfloat16, 2e-3)):
+        y = mq.linear(route, pw, xd, out_dtype=out_dtype)
+        if route == 0:
+            _, y64 = orc.w4a8_from_x(nib, sc, _f32(x))
+        else:
+            _, y64 = orc.w4a16(nib, sc, _f32(x))
+        _assert_close(y, y64, rtol)
+
+
+@pytest.mark.parametrize("m", [1, 8, 16])
+def test_w4a8_prequantised_matches_fused(mq, orc, m):
+    n, k = 96, 2048
+    pw, nib, sc = _pack_both(mq, orc, si.weight(n, k, 51))
+    xd = si.activation(m, k, 52).to(DEV)
+    q, s, sq = mq.quant_a8(xd)
+    y1 = mq.w4a8(pw, q, s, sq)
+    y2 = mq.w4a8_x(pw, xd)
+    torch.cuda.synchronize()
+    assert torch.equal(y1, y2)
+
+
+def test_zero_activation_and_impulse_rows(mq, orc):
+    # S:315 / S:324-325 special cases through the GPU path
+    k = 256
+    w = torch.zeros(16, k)
+    picks = [(r, (r * 13) % k, float(r - 8) or 1.0) for r in range(16)]
+    for r, col, v in picks:
+        w[r, col] = v
+    pw = mq.pack_w4(w.to(torch.bfloat16).to(DEV))
+    z = torch.zeros(1, k, dtype=torch.bfloat16, device=DEV)
+    assert torch.count_nonzero(mq.w4a8_x(pw, z)) == 0
+    assert torch.count_nonzero(mq.w4a16(pw, z)) == 0
+    x = si.activation(1, k, 61)
+    y = mq.w4a16(pw, x.to(DEV)).cpu()
+    for r, col, v in picks:
+        assert y[0, r].item() == np.float32(v) * np.float32(x[0, col].float().item())
+
+
+def test_column_shards_bit_identical(mq):
+    # A22: per-row arithmetic depends on K only -> any row slice reproduces the full result bit-for-bit
+    n, k = 1024, 4096
+    pw = mq.pack_w4(si.weight(n, k, 71).to(DEV))
+    for m in (1, 16):
+        x = si.activation(m, k, 72 + m).to(DEV)
+        for route in (0, 1):
+            full = mq.linear(route, pw, x)
+            for P in (2, 4, 8):
+                parts = [mq.linear(route, pw.shard(P, r), x) for r in range(P)]
+                assert torch.equal(torch.cat(parts, dim=1), full)
+
+
+def test_deterministic(mq):
+    n, k = 2048, 2048
+    pw = mq.pack_w4(si.weight(n, k, 81).to(DEV))
+    x = si.activation(4, k, 82).to(DEV)
+    for route in (0, 1):
+        a = mq.linear(route, pw, x)
+        b = mq.linear(route, pw, x)
+        assert torch.equal(a, b)
+
+
+def test_linear_host_e2e(mq, orc):
+    n, k, m = 512, 2048, 1
+    w = si.weight(n, k, 91)
+    x = si.activation(m, k, 92)
+    pw = mq.pack_w4(w.to(DEV))
+    xh = x.pin_memory()
+    for route in (0, 1):
+        yh = torch.empty(m, n, dtype=torch.float32).pin_memory()
+        ws = torch.empty(mq.host_workspace_bytes(route, m, n, k), dtype=torch.uint8, device=DEV)
+        mq.linear_host(route, pw, xh, yh, ws)
+        torch.cuda.synchronize()
+        yd = mq.linear(route, pw, x.to(DEV))
+        assert torch.equal(yh, yd.cpu())
+
+
+# ---------------------------------------------------------------- full-size configs, sampled rows
+FULL = [("llama-3.1-8b", "gate", 1), ("llama-3.1-8b", "down", 1), ("llama-3.1-8b", "lm_head", 1),
+        ("llama-3.1-8b", "lm_head", 64), ("llama-3.2-3b", "up", 16), ("llama-3.2-3b", "q", 64)]
+
+
+@pytest.mark.parametrize("model,slot,m", FULL)
+def test_full_size_sampled_rows(mq, orc, model, slot, m):
+    n, k = si.linear_shape(model, slot)
+    w = si.weight(n, k, si.seed_for(5, 0, slot))
+    x = si.activation(m, k, si.seed_for(5, 0, slot, True), si.activation_kind(slot))
+    pw = mq.pack_w4(w.to(DEV))
+    rows = np.sort(np.random.default_rng(n + k).choice(n, size=48, replace=False))
+    rows[-1] = n - 1
+    nib, sc = orc.pack_w4(_f32(w[rows]))
+    assert np.array_equal(pw.nib[rows].cpu().numpy(), nib)
+    assert np.array_equal(pw.scale[rows].cpu().numpy().view(np.uint16), sc)
+    xd = x.to(DEV)
+    for route in (0, 1):
+        y = mq.linear(route, pw, xd, out_dtype=torch.bfloat16)
+        if route == 0:
+            _, y64 = orc.w4a8_from_x(nib, sc, _f32(x))
+        else:
+            _, y64 = orc.w4a16(nib, sc, _f32(x))
+        _assert_close(y[:, rows], y64, 2e-3)
+
+
+# ---------------------------------------------------------------- a7 + a9 stack
+def test_stack_matches_oracle_and_graph_replay(mq, orc):
+    prof = mq.profile_parse(open(os.path.join(GOLD, "llama32_1b_profile.json")).read())
+    routes = prof.routes()
+    assert routes == [0] * 15 + [1]
+    L = 4
+    routes = [0, 1, 0, 1]
+    dims = {"q": (256, 512), "k": (64, 512), "v": (64, 512), "o": (512, 256), "gate": (1024, 512),
+            "up": (1024, 512), "down": (512, 1024)}
+    inputs = {"q": 0, "k": 0, "v": 0, "o": 1, "gate": 2, "up": 2, "down": 3}
+    st = mq.Stack(routes, max_m=2)
+    ref = []
+    xs = {}
+    for l in range(L):
+        for slot_id, (slot, (n, k)) in enumerate(dims.items()):
+            w = si.weight(n, k, si.seed_for(2, l, slot))
+            key = (l, inputs[slot])
+            if key not in xs:
+                xs[key] = si.activation(2, k, si.seed_for(2, l, slot, True), si.activation_kind(slot))
+            x = xs[key]
+            pw = mq.pack_w4(w.to(DEV))
+            xd = x.to(DEV)
+            y = torch.empty(2, n, dtype=torch.bfloat16, device=DEV)
+            st.set(l, slot_id, inputs[slot], pw, xd, y)
+            ref.append((l, y, w, x))
+    assert st.launches(2) == 2 * (7 + 4) + 2 * 7
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        st.run(2, stream=s)
+    s.synchronize()
+    first = [y.clone() for (_, y, _, _) in ref]
+    for (l, y, w, x) in ref:
+        nib, sc = orc.pack_w4(_f32(w))
+        if routes[l] == 0:
+            _, y64 = orc.w4a8_from_x(nib, sc, _f32(x))
+        else:
+            _, y64 = orc.w4a16(nib, sc, _f32(x))
+        _assert_close(y, y64, 2e-3)
+    for (_, y, _, _) in ref:
+        y.zero_()
+    torch.cuda.synchronize()
+    st.capture(2, stream=s)
+    st.replay(stream=s)
+    s.synchronize()
+    for a, (_, y, _, _) in zip(first, ref):
+        assert torch.equal(a, y)
+    assert st.weight_bytes == sum(pw_n * k // 2 + pw_n * k // 32 * 2 for pw_n, k in dims.values()) * L
