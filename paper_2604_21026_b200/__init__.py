@@ -280,17 +280,24 @@ class Stack:
 class Comm:
     """Library-owned NCCL communicator; the unique id travels over a torch process group."""
 
+    @staticmethod
+    def bootstrap_id(group=None) -> bytes:
+        """Rank 0 draws the NCCL unique id through the library; every rank of the
+        torch process group receives the same 128 bytes."""
+        import torch.distributed as dist
+        obj = [None]
+        if dist.get_rank(group) == 0:
+            raw = (ctypes.c_uint8 * 128)()
+            check(load().mcapq_comm_unique_id(ctypes.cast(raw, ctypes.c_void_p)), "mcapq_comm_unique_id")
+            obj = [bytes(raw)]
+        src = dist.get_global_rank(group, 0) if group is not None else 0
+        dist.broadcast_object_list(obj, src=src, group=group)
+        return obj[0]
+
     def __init__(self, group=None):
         import torch.distributed as dist
         world, rank = dist.get_world_size(group), dist.get_rank(group)
-        idbuf = torch.zeros(128, dtype=torch.uint8)
-        if rank == 0:
-            raw = (ctypes.c_uint8 * 128)()
-            check(load().mcapq_comm_unique_id(ctypes.cast(raw, ctypes.c_void_p)), "mcapq_comm_unique_id")
-            idbuf = torch.tensor(list(raw), dtype=torch.uint8)
-        obj = [idbuf.tolist()]
-        dist.broadcast_object_list(obj, src=0, group=group)
-        raw = (ctypes.c_uint8 * 128)(*obj[0])
+        raw = (ctypes.c_uint8 * 128)(*self.bootstrap_id(group))
         h = ctypes.c_void_p()
         check(load().mcapq_comm_init(ctypes.cast(raw, ctypes.c_void_p), world, rank, ctypes.byref(h)),
               "mcapq_comm_init")
