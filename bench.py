@@ -148,29 +148,31 @@ def time_graph(st, stream, steps, warmup, dist=None):
 
 
 def time_dominant_kernel(mq, weights, xs, stream, reps_per_layer=4):
-    """The W4A8 GEMV of gate/up (8192x2048, the stack's largest W4A8 launch),
-    pre-quantised activations (mcapq_w4a8 launches exactly that kernel), rotating
-    over the 16 layers' weights (16 x 9.4 MB x2 > L2) so every launch streams
-    from HBM.  CUDA events on the launching stream."""
+    """The stack's dominant kernel: the grouped W4A8 gate+up launch (2 x 8192x2048,
+    stream_linear<DP4A> with the quantiser fused), exactly as the stack launches it
+    (mcapq_linear_group), rotating over the 16 layers' weights (16 x 18.9 MB > L2)
+    so every launch streams from HBM.  CUDA events on the launching stream."""
     L = si.MODELS[MODEL]["layers"]
-    qs = {}
+    dev = xs[(0, 0)].device
+    n = weights[(0, "gate")].n
+    outs = [torch.empty(1, n, dtype=torch.bfloat16, device=dev) for _ in range(2)]
+    seq = [l for _ in range(reps_per_layer) for l in range(L)]
     with torch.cuda.stream(stream):
-        for l in range(L):
-            qs[l] = mq.quant_a8(xs[(l, INPUT_ID["gate"])], stream=stream)
-        ys = torch.empty(1, weights[(0, "gate")].n, dtype=torch.bfloat16, device=xs[(0, 0)].device)
-        seq = [(l, s) for _ in range(reps_per_layer) for l in range(L) for s in ("gate", "up")]
-        for (l, s) in seq[:8]:
-            mq.w4a8(weights[(l, s)], *qs[l], out=ys, stream=stream)
+        def call(l):
+            mq.linear_group(0, [weights[(l, "gate")], weights[(l, "up")]], xs[(l, INPUT_ID["gate"])], outs=outs,
+                            stream=stream)
+        for l in seq[:4]:
+            call(l)
         stream.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        for (l, s) in seq:
-            mq.w4a8(weights[(l, s)], *qs[l], out=ys, stream=stream)
+        for l in seq:
+            call(l)
         e1.record(stream)
         e1.synchronize()
     per_launch_ms = e0.elapsed_time(e1) / len(seq)
     w = weights[(0, "gate")]
-    alg_bytes = w.n * w.k // 2 + w.n * (w.k // 32) * 2 + (w.k + 8 * (w.k // 32)) + 2 * w.n
+    alg_bytes = 2 * (w.n * w.k // 2 + w.n * (w.k // 32) * 2) + 2 * w.k + 2 * 2 * w.n
     return per_launch_ms, alg_bytes, len(seq)
 
 
@@ -427,7 +429,7 @@ def main():
                                  "w4a8_over_w4a16": round(ms16 / ms8, 3)},
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                          "frac": round(achieved / peak, 4), "traffic": None,
-                         "kernel": "w4a8_gemv_dp4a (gate/up 8192x2048, M=1)",
+                         "kernel": "stream_linear<DP4A> grouped gate+up (2 x 8192x2048, M=1, fused quantiser)",
                          "alg_bytes_per_launch": k_bytes, "us_per_launch": round(k_ms * 1000, 3),
                          "launches_timed": k_reps, "peak_source": peak_src,
                          "step_frac": round(value / world / peak, 4)},

@@ -164,6 +164,19 @@ mcapq_status mcapq_linear(int route, const uint8_t *nib, const uint16_t *scale, 
                           size_t ws_bytes, void *stream);
 
 /*
+ * Grouped routed linear: `count` (1..4) linears that share the same input x
+ * (q/k/v, gate/up; the paper's fused QKV kernel P:977) in ONE launch.  Host
+ * arrays nibs/scales/ns/ys/ldys give each linear's packed weight, N, output and
+ * its leading dimension; k, x, m, ldx, ydt are shared.  Results are identical
+ * to `count` separate mcapq_linear calls (bit-for-bit).  ws: as mcapq_linear
+ * (used only when a linear falls off the K % 256 == 0 fast path).
+ */
+mcapq_status mcapq_linear_group(int route, int count, const uint8_t *const *nibs, const uint16_t *const *scales,
+                                const int64_t *ns, int64_t k, const uint16_t *x, int64_t m, int64_t ldx,
+                                void *const *ys, int ydt, const int64_t *ldys, void *ws, size_t ws_bytes,
+                                void *stream);
+
+/*
  * End-to-end routed linear from HOST activations: copies x_host (pinned host,
  * [m][k] bf16) into the workspace, runs mcapq_linear, copies y back into y_host
  * (pinned host, [m][n] of ydt); all on `stream`, asynchronous (the caller

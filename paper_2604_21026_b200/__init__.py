@@ -25,7 +25,7 @@ BF16, F32 = 0, 1
 
 __all__ = [
     "W4A8", "W4A16", "BF16", "F32", "McapqError", "load", "pack_w4", "quant_a8", "w4a8", "w4a8_x", "w4a16",
-    "linear", "linear_host", "w4a8_group_dots", "workspace_bytes", "host_workspace_bytes", "Profile",
+    "linear", "linear_group", "linear_host", "w4a8_group_dots", "workspace_bytes", "host_workspace_bytes", "Profile",
     "profile_parse", "Stack", "Comm", "linear_colshard", "PackedW4", "device_sms",
 ]
 
@@ -164,6 +164,28 @@ def linear(route: int, w: PackedW4, x: torch.Tensor, out_dtype=torch.float32, ou
     check(load().mcapq_linear(route, _ptr(w.nib), _ptr(w.scale), w.n, w.k, _ptr(x2), m, x2.stride(0), _ptr(y),
                               _dt(y.dtype), y.stride(0), _ptr(ws), ws.numel(), _stream(stream)), "mcapq_linear")
     return y
+
+
+def linear_group(route: int, ws_list, x: torch.Tensor, out_dtype=torch.float32, outs=None, ws=None, stream=None):
+    """Grouped routed linear: several PackedW4 sharing the same input x in one launch."""
+    ws_list = list(ws_list)
+    x2 = x if x.dim() == 2 else x.view(1, -1)
+    m, k = x2.shape
+    cnt = len(ws_list)
+    outs = outs if outs is not None else [torch.empty((m, w.n), dtype=out_dtype, device=x.device) for w in ws_list]
+    arr = lambda T, vals: (T * cnt)(*vals)  # noqa: E731
+    nibs = arr(ctypes.c_void_p, [w.nib.data_ptr() for w in ws_list])
+    scs = arr(ctypes.c_void_p, [w.scale.data_ptr() for w in ws_list])
+    ns = arr(ctypes.c_int64, [w.n for w in ws_list])
+    ys = arr(ctypes.c_void_p, [y.data_ptr() for y in outs])
+    lds = arr(ctypes.c_int64, [y.stride(0) for y in outs])
+    ws = _ws(route, m, max(w.n for w in ws_list), k, x.device, ws)
+    check(load().mcapq_linear_group(route, cnt, ctypes.cast(nibs, ctypes.c_void_p), ctypes.cast(scs, ctypes.c_void_p),
+                                    ctypes.cast(ns, ctypes.c_void_p), k, _ptr(x2), m, x2.stride(0),
+                                    ctypes.cast(ys, ctypes.c_void_p), _dt(outs[0].dtype),
+                                    ctypes.cast(lds, ctypes.c_void_p), _ptr(ws), ws.numel(), _stream(stream)),
+          "mcapq_linear_group")
+    return outs
 
 
 def linear_host(route: int, w: PackedW4, x_host: torch.Tensor, y_host: torch.Tensor, ws: torch.Tensor,

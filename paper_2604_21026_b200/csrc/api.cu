@@ -5,6 +5,7 @@
 #include <cstring>
 
 #include "internal.h"
+#include "stream.h"
 
 namespace mcapq {
 
@@ -184,8 +185,21 @@ mcapq_status mcapq_w4a8_x(const uint8_t *nib, const uint16_t *scale, int64_t n, 
     CHECK_LD(ldy, n, "ldy");
     MCAPQ_REQUIRE(ws_bytes >= a8_workspace_bytes(m, k), MCAPQ_ENOSPACE, "workspace %zu < %zu", ws_bytes,
                   a8_workspace_bytes(m, k));
-    const A8Workspace w = a8_workspace(ws, m, k);
     cudaStream_t s = as_stream(stream);
+    if (stream_supported(k) && aligned16(scale)) {
+        // persistent TMA-fed kernel with the quantiser fused into its prologue
+        StreamGroup g = {};
+        g.count = 1;
+        g.k = k;
+        g.nib[0] = nib;
+        g.scale[0] = scale;
+        g.n[0] = n;
+        g.y[0] = y;
+        g.ldy[0] = ldy;
+        LAUNCH_TRY(launch_stream_group(MCAPQ_W4A8, g, x, m, ldx, ydt, s, false));
+        return MCAPQ_OK;
+    }
+    const A8Workspace w = a8_workspace(ws, m, k);
     LAUNCH_TRY(launch_quant_a8(x, m, k, ldx, w.q, w.sx, w.sq, s, false));
     LAUNCH_TRY(launch_w4a8(nib, scale, n, k, w.q, w.sx, w.sq, m, y, ydt, ldy, s, true));
     return MCAPQ_OK;
@@ -205,6 +219,18 @@ mcapq_status mcapq_w4a16(const uint8_t *nib, const uint16_t *scale, int64_t n, i
     CHECK_YDT(ydt);
     CHECK_LD(ldx, k, "ldx");
     CHECK_LD(ldy, n, "ldy");
+    if (stream_supported(k) && aligned16(scale)) {
+        StreamGroup g = {};
+        g.count = 1;
+        g.k = k;
+        g.nib[0] = nib;
+        g.scale[0] = scale;
+        g.n[0] = n;
+        g.y[0] = y;
+        g.ldy[0] = ldy;
+        LAUNCH_TRY(launch_stream_group(MCAPQ_W4A16, g, x, m, ldx, ydt, as_stream(stream), false));
+        return MCAPQ_OK;
+    }
     LAUNCH_TRY(launch_w4a16(nib, scale, n, k, x, m, ldx, y, ydt, ldy, as_stream(stream), false));
     return MCAPQ_OK;
 }
@@ -218,6 +244,51 @@ mcapq_status mcapq_linear(int route, const uint8_t *nib, const uint16_t *scale, 
     clear_error();
     set_error("bad route %d", route);
     return MCAPQ_EINVAL;
+}
+
+mcapq_status mcapq_linear_group(int route, int count, const uint8_t *const *nibs, const uint16_t *const *scales,
+                                const int64_t *ns, int64_t k, const uint16_t *x, int64_t m, int64_t ldx,
+                                void *const *ys, int ydt, const int64_t *ldys, void *ws, size_t ws_bytes,
+                                void *stream)
+{
+    clear_error();
+    MCAPQ_REQUIRE(count >= 1 && count <= kMaxGroup, MCAPQ_EINVAL, "group count %d not in [1, %d]", count, kMaxGroup);
+    MCAPQ_REQUIRE(nibs && scales && ns && ys && ldys, MCAPQ_EINVAL, "NULL host array");
+    MCAPQ_REQUIRE(route == MCAPQ_W4A8 || route == MCAPQ_W4A16, MCAPQ_EINVAL, "bad route %d", route);
+    bool fast = stream_supported(k);
+    for (int i = 0; i < count; ++i) {
+        CHECK_SHAPE(ns[i], k, m);
+        mcapq_status st = check_weight(nibs[i], scales[i], ns[i], k);
+        if (st != MCAPQ_OK) return st;
+        CHECK_PTR(ys[i], "y");
+        CHECK_AL16(ys[i], "y");
+        CHECK_LD(ldys[i], ns[i], "ldy");
+        fast = fast && aligned16(scales[i]);
+    }
+    CHECK_PTR(x, "x");
+    CHECK_AL16(x, "x");
+    CHECK_YDT(ydt);
+    CHECK_LD(ldx, k, "ldx");
+    if (fast) {
+        StreamGroup g = {};
+        g.count = count;
+        g.k = k;
+        for (int i = 0; i < count; ++i) {
+            g.nib[i] = nibs[i];
+            g.scale[i] = scales[i];
+            g.n[i] = ns[i];
+            g.y[i] = ys[i];
+            g.ldy[i] = ldys[i];
+        }
+        LAUNCH_TRY(launch_stream_group(route, g, x, m, ldx, ydt, as_stream(stream), false));
+        return MCAPQ_OK;
+    }
+    for (int i = 0; i < count; ++i) {
+        mcapq_status st = mcapq_linear(route, nibs[i], scales[i], ns[i], k, x, m, ldx, ys[i], ydt, ldys[i], ws,
+                                       ws_bytes, stream);
+        if (st != MCAPQ_OK) return st;
+    }
+    return MCAPQ_OK;
 }
 
 size_t mcapq_host_workspace_bytes(int route, int64_t m, int64_t n, int64_t k)

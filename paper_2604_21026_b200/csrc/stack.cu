@@ -13,6 +13,7 @@
 #include <vector>
 
 #include "internal.h"
+#include "stream.h"
 
 namespace {
 constexpr int kMaxSlots = 16;
@@ -98,34 +99,79 @@ mcapq_status mcapq_stack_set(mcapq_stack *st, int layer, int slot, int input_id,
     return MCAPQ_OK;
 }
 
+}  // extern "C"
+
+// Consecutive set slots of a layer with the same input_id form a launch group
+// (<= kMaxGroup linears, same K, fast-path eligible).  Calls f(first, count).
+template <typename F>
+static mcapq_status for_each_group(const mcapq_stack *st, int l, F f)
+{
+    int sl = 0;
+    while (sl < kMaxSlots) {
+        const Slot &a = st->slots[(size_t)l * kMaxSlots + sl];
+        if (!a.set) { ++sl; continue; }
+        int cnt = 1;
+        const bool fast = stream_supported(a.k) && aligned16(a.scale);
+        while (fast && sl + cnt < kMaxSlots && cnt < kMaxGroup) {
+            const Slot &b = st->slots[(size_t)l * kMaxSlots + sl + cnt];
+            if (!b.set || b.input_id != a.input_id || b.k != a.k || b.x != a.x || b.ydt != a.ydt ||
+                !aligned16(b.scale))
+                break;
+            ++cnt;
+        }
+        mcapq_status r = f(sl, cnt, fast);
+        if (r != MCAPQ_OK) return r;
+        sl += cnt;
+    }
+    return MCAPQ_OK;
+}
+
+extern "C" {
+
 mcapq_status mcapq_stack_run(mcapq_stack *st, int64_t m, void *stream)
 {
     clear_error();
     MCAPQ_REQUIRE(st && m >= 1 && m <= st->max_m, MCAPQ_EINVAL, "bad stack_run arguments");
     cudaStream_t s = as_stream(stream);
     for (int l = 0; l < st->layers; ++l) {
-        const bool a8 = st->routes[l] == MCAPQ_W4A8;
+        const int route = st->routes[l];
         int last_input = -1 << 30;
-        const int64_t *dummy = nullptr;
-        (void)dummy;
         A8Workspace w = {};
-        for (int sl = 0; sl < kMaxSlots; ++sl) {
-            const Slot &s_ = st->slots[(size_t)l * kMaxSlots + sl];
-            if (!s_.set) continue;
-            if (a8) {
-                if (s_.input_id != last_input) {
-                    w = a8_workspace(st->ws, m, s_.k);
-                    cudaError_t e = launch_quant_a8(s_.x, m, s_.k, s_.k, w.q, w.sx, w.sq, s, true);
-                    MCAPQ_REQUIRE(e == cudaSuccess, MCAPQ_ECUDA, "quant launch: %s", cudaGetErrorString(e));
-                    last_input = s_.input_id;
+        mcapq_status r = for_each_group(st, l, [&](int first, int cnt, bool fast) -> mcapq_status {
+            const Slot &a = st->slots[(size_t)l * kMaxSlots + first];
+            if (fast) {
+                StreamGroup g = {};
+                g.count = cnt;
+                g.k = a.k;
+                for (int i = 0; i < cnt; ++i) {
+                    const Slot &b = st->slots[(size_t)l * kMaxSlots + first + i];
+                    g.nib[i] = b.nib;
+                    g.scale[i] = b.scale;
+                    g.n[i] = b.n;
+                    g.y[i] = b.y;
+                    g.ldy[i] = b.n;
                 }
-                cudaError_t e = launch_w4a8(s_.nib, s_.scale, s_.n, s_.k, w.q, w.sx, w.sq, m, s_.y, s_.ydt, s_.n, s, true);
+                cudaError_t e = launch_stream_group(route, g, a.x, m, a.k, a.ydt, s, true);
+                MCAPQ_REQUIRE(e == cudaSuccess, MCAPQ_ECUDA, "stream launch: %s", cudaGetErrorString(e));
+                return MCAPQ_OK;
+            }
+            // generic path (K % 256 != 0): separate quantiser + GEMV
+            if (route == MCAPQ_W4A8) {
+                if (a.input_id != last_input) {
+                    w = a8_workspace(st->ws, m, a.k);
+                    cudaError_t e = launch_quant_a8(a.x, m, a.k, a.k, w.q, w.sx, w.sq, s, true);
+                    MCAPQ_REQUIRE(e == cudaSuccess, MCAPQ_ECUDA, "quant launch: %s", cudaGetErrorString(e));
+                    last_input = a.input_id;
+                }
+                cudaError_t e = launch_w4a8(a.nib, a.scale, a.n, a.k, w.q, w.sx, w.sq, m, a.y, a.ydt, a.n, s, true);
                 MCAPQ_REQUIRE(e == cudaSuccess, MCAPQ_ECUDA, "w4a8 launch: %s", cudaGetErrorString(e));
             } else {
-                cudaError_t e = launch_w4a16(s_.nib, s_.scale, s_.n, s_.k, s_.x, m, s_.k, s_.y, s_.ydt, s_.n, s, true);
+                cudaError_t e = launch_w4a16(a.nib, a.scale, a.n, a.k, a.x, m, a.k, a.y, a.ydt, a.n, s, true);
                 MCAPQ_REQUIRE(e == cudaSuccess, MCAPQ_ECUDA, "w4a16 launch: %s", cudaGetErrorString(e));
             }
-        }
+            return MCAPQ_OK;
+        });
+        if (r != MCAPQ_OK) return r;
     }
     return MCAPQ_OK;
 }
@@ -174,20 +220,25 @@ size_t mcapq_stack_weight_bytes(const mcapq_stack *st)
 
 int mcapq_stack_launches(const mcapq_stack *st, int64_t m)
 {
-    (void)m;
-    if (!st) return 0;
+    if (!st || m < 1) return 0;
     int c = 0;
     for (int l = 0; l < st->layers; ++l) {
         int last = -1 << 30;
-        for (int sl = 0; sl < kMaxSlots; ++sl) {
-            const Slot &s = st->slots[(size_t)l * kMaxSlots + sl];
-            if (!s.set) continue;
-            if (st->routes[l] == MCAPQ_W4A8 && s.input_id != last) {
-                ++c;
-                last = s.input_id;
+        for_each_group(st, l, [&](int first, int cnt, bool fast) -> mcapq_status {
+            const Slot &a = st->slots[(size_t)l * kMaxSlots + first];
+            if (fast) {
+                const int tp = stream_tokens_per_pass(st->routes[l], a.k);
+                c += (int)((m + tp - 1) / tp);
+            } else {
+                if (st->routes[l] == MCAPQ_W4A8 && a.input_id != last) {
+                    ++c;
+                    last = a.input_id;
+                }
+                c += 1;
             }
-            ++c;
-        }
+            (void)cnt;
+            return MCAPQ_OK;
+        });
     }
     return c;
 }

@@ -131,7 +131,20 @@ def test_group_dots_bit_exact(mq, orc, mode, n, k, m):
 
 
 # ---------------------------------------------------------------- a3-a6 outputs
-SHAPES = [(200, 2048), (3072, 1024), (48, 14336), (512, 3072)]
+# K % 256 == 0 takes the persistent TMA stream path; K = 800 the generic kernels
+SHAPES = [(200, 2048), (3072, 1024), (48, 14336), (512, 3072), (72, 800)]
+
+
+@pytest.mark.parametrize("m", [1, 3, 8, 11])
+@pytest.mark.parametrize("route", [0, 1])
+def test_grouped_launch_bit_identical_to_separate(mq, route, m):
+    # fused QKV / gate-up launch: same bits as one launch per linear
+    k = 2048
+    ws = [mq.pack_w4(si.weight(n, k, 300 + n).to(DEV)) for n in (2048, 512, 512)]
+    x = si.activation(m, k, 301 + m).to(DEV)
+    outs = mq.linear_group(route, ws, x)
+    for w, y in zip(ws, outs):
+        assert torch.equal(y, mq.linear(route, w, x))
 
 
 @pytest.mark.parametrize("n,k", SHAPES)
@@ -271,7 +284,7 @@ def test_stack_matches_oracle_and_graph_replay(mq, orc):
             y = torch.empty(2, n, dtype=torch.bfloat16, device=DEV)
             st.set(l, slot_id, inputs[slot], pw, xd, y)
             ref.append((l, y, w, x))
-    assert st.launches(2) == 2 * (7 + 4) + 2 * 7
+    assert st.launches(2) == 4 * L          # qkv, o, gate/up, down: one grouped launch each
     s = torch.cuda.Stream()
     with torch.cuda.stream(s):
         st.run(2, stream=s)
