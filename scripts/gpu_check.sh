@@ -12,9 +12,9 @@ timeout 900 python bench.py > $OUT/bench.json 2> $OUT/bench.err; echo "bench exi
 if [ "${NCU:-1}" = "1" ]; then
   timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:'gemv|tc_linear|quant_a8|stream_linear' -c 300 --csv \
      --log-file $OUT/launches.csv python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-extras > $OUT/ncu_launch.log 2>&1
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:stream_linear -s 40 -c 2 \
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:stream_linear -s 42 -c 1 \
      -o $OUT/prof_w4a8 python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-extras > $OUT/ncu_full.log 2>&1
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:stream_linear -s 189 -c 1 \
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:stream_linear -s 62 -c 1 \
      -o $OUT/prof_w4a16 python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-extras > $OUT/ncu_full16.log 2>&1
 fi
 echo done > $OUT/DONE
