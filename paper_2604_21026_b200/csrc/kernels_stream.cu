@@ -1,36 +1,38 @@
-// kernels_stream.cu -- persistent, TMA-bulk-fed decode linears for sm_100a
-// (rows a3-a6 at M <= 8 tokens per pass; the "stream" path).
+// kernels_stream.cu -- persistent, TMA-fed decode linears for sm_100a
+// (rows a3-a6 at <= 8 tokens per pass; the "stream" path, K % 256 == 0, K >= 2048).
 //
 // One CTA per SM (grid <= #SMs), warp-specialised:
 //   warp 8 (producer, one elected lane): walks the CTA's work items (16-row
-//     tile x 1 KiB K-chunk) and moves each into a shared-memory ring with
-//     cp.async.bulk (the 1-D TMA engine, SASS UBLKCP) -- 16 row copies of the
-//     nibble chunk + 16 row copies of its fp16 scales, completion counted on the
-//     stage's mbarrier (complete_tx).  It reads only weights, so it never waits
-//     on the predecessor kernel: under programmatic dependent launch the weight
-//     stream of linear i+1 starts while linear i drains.
-//   warps 0-7 (consumers): griddepcontrol.wait, then stage this pass's
-//     activations in shared memory -- for W4A8 they QUANTISE x themselves (the
-//     same warp-per-group code as quant_a8_kernel, so q/s/sum_q are bit-identical;
-//     no separate launch), for W4A16 they stage x in MMA-fragment order -- and
-//     then consume the ring.
-// Engines (one template parameter):
+//     tile x 1 KiB K-chunk = 2048 weights per row) and moves each into a
+//     shared-memory ring with 2-D TMA (cp.async.bulk.tensor, 128-B swizzle):
+//     8 boxes of {128 B x 16 rows} of nibbles + 1 box of {64 fp16 x 16 rows} of
+//     scales per stage, completion counted on the stage's mbarrier.  It reads
+//     only weights and never waits on the predecessor kernel, so under
+//     programmatic dependent launch the weight stream of linear i+1 starts
+//     while linear i drains.  Rows past N are zero-filled by TMA (never stored).
+//   warps 0-7 (consumers): griddepcontrol.wait, one bulk copy of this pass's x
+//     into shared memory, then W4A8 consumers QUANTISE it themselves (the same
+//     warp-per-group arithmetic as quant_a8_kernel -> bit-identical q / s / sum q,
+//     no separate launch) and W4A16 consumers re-stage it in MMA-fragment order;
+//     then they consume the ring.
+// Engines (template parameter):
 //   DP4A : W4A8, 1 token.  warp w owns rows 2w, 2w+1 of the tile, lane l the
-//          blocks l, l+32 of the chunk: LDS.128 nibbles, 8 IDP.4A per block,
-//          deferred correction D = sumi - 8 sum_x, fp32 (d s) D.
+//          blocks l, l+32 of the chunk: one conflict-free LDS.128 per block,
+//          8 IDP.4A, deferred correction D = sumi - 8 sum_x,
+//          fp32 (d s) D.
 //   IMMA : W4A8, 2..8 tokens.  warp w owns blocks w, w+8, .. of the chunk for all
-//          16 rows: ldmatrix.x4 hands each lane (gid, t) word t of rows gid /
-//          gid+8 of two blocks -- exactly the m16n8k32 s8 A fragment of the split
-//          nibble layout -- one mma.sync per block (exact int32 D per block).
+//          16 rows; ldmatrix.x4 hands lane (gid, t) word t of rows gid / gid+8 of
+//          two blocks -- exactly the m16n8k32.s8 A fragment of the split nibble
+//          layout; one mma.sync per block gives the exact int32 D.
 //   HMMA : W4A16, 1..8 tokens.  Same fragments; nibbles -> exact bf16 (c - 8)
-//          (magic 0x4300 + packed FMA), two m16n8k16 bf16 MMAs per block, fp32
-//          per-block scale (exact products, fp32 accumulation).
-// Work: a "group" of up to 4 linears sharing the same input x (fused QKV,
-// fused gate/up; P:977 nve_qkv_matvec_w4a16) -- their 16-row tiles are numbered
-// consecutively and split into contiguous, balanced ranges per CTA.
-// Determinism: chunk size and the block->lane/warp maps depend on K only, the
-// cross-lane/cross-warp reductions have a fixed order: every output row is
-// bit-identical whatever N, the group, the grid or the shard (reading A22).
+//          (OR into the 0x4300 mantissa + one packed FMA), two m16n8k16 bf16
+//          MMAs per block, fp32 per-block scale (exact products, fp32 sums).
+// Work: a group of up to 4 linears sharing x (fused QKV / gate-up):
+// their 16-row tiles are numbered consecutively and split into contiguous,
+// balanced ranges per CTA.
+// Determinism: the chunking and the block->lane/warp maps depend on K only and
+// all reductions have a fixed order, so an output row is bit-identical whatever
+// N, the group, the grid or the column shard (reading A22).
 #include "internal.h"
 #include "stream.h"
 
@@ -40,10 +42,10 @@ namespace {
 constexpr int kConsumerWarps = 8;
 constexpr int kThreads = (kConsumerWarps + 1) * 32;
 constexpr int kTileRows = 16;
-constexpr int kChunkBytes = 1024;              // nibble bytes per row per stage (2048 weights)
-constexpr int kNibStride = kChunkBytes + 16;    // padded smem row: ldmatrix rows hit distinct banks
-constexpr int kScaleStride = 144;               // 64 fp16 scales + pad (16-B multiple, 4-bank skew)
-constexpr int kStageBytes = kTileRows * (kNibStride + kScaleStride);
+constexpr int kChunkBytes = 1024;                  // nibble bytes per row per stage
+constexpr int kChunkBlocks = kChunkBytes / 16;     // 64 Q4_0 blocks
+constexpr int kBox = 128 * kTileRows;              // one {128 B x 16 rows} TMA box
+constexpr int kStageBytes = 8 * kBox + kBox;       // 8 nibble boxes + 1 scale box (18 KiB)
 constexpr int kRedBytes = kConsumerWarps * kTileRows * 8 * 4;
 
 enum Engine { DP4A = 0, IMMA = 1, HMMA = 2 };
@@ -74,14 +76,21 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity)
         "r"(parity)
         : "memory");
 }
-__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar,
-                                         uint64_t policy)
+__device__ __forceinline__ void tma_2d(void *dst, const CUtensorMap *map, int x, int y, uint64_t *bar,
+                                       uint64_t policy)
 {
     asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
-            smem_addr(dst)),
-        "l"(src), "r"(bytes), "r"(smem_addr(bar)), "l"(policy)
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint"
+        " [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(smem_addr(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(smem_addr(bar)), "l"(policy)
         : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar)
+{
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_addr(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_addr(bar))
+                 : "memory");
 }
 __device__ __forceinline__ uint64_t evict_first_policy()
 {
@@ -95,13 +104,22 @@ __device__ __forceinline__ void ldmatrix_x4(uint32_t addr, uint32_t &r0, uint32_
                  : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
                  : "r"(addr));
 }
-__host__ __device__ __forceinline__ int64_t imin64(int64_t a, int64_t b) { return a < b ? a : b; }
-
 __device__ __forceinline__ float h2f(uint16_t h)
 {
     float f;
     asm("cvt.f32.f16 %0, %1;" : "=f"(f) : "h"(h));
     return f;
+}
+__device__ __forceinline__ void bar_consumers() { asm volatile("bar.sync 1, %0;" ::"n"(kConsumerWarps * 32) : "memory"); }
+
+// 128-B swizzle of a {128 B x 16 rows} box: 16-B chunk c of row r sits at c ^ (r & 7).
+__device__ __forceinline__ int nib_off(int r, int b)          // block b (0..63) of the chunk, row r
+{
+    return (b >> 3) * kBox + r * 128 + (((b & 7) ^ (r & 7)) << 4);
+}
+__device__ __forceinline__ int scale_off(int r, int b)
+{
+    return 8 * kBox + r * 128 + ((((b >> 3) ^ (r & 7))) << 4) + ((b & 7) << 1);
 }
 
 // ------------------------------------------------------------------ fragments
@@ -154,78 +172,69 @@ __device__ __forceinline__ void hmma(uint32_t a0, uint32_t a1, uint32_t a2, uint
 }
 
 // ------------------------------------------------------------------ the kernel
-struct Smem {
-    // layout (dynamic shared memory, 128-B aligned pieces)
-    uint8_t *ring;          // stages x kStageBytes
-    uint64_t *full, *empty; // stages each
-    uint8_t *act;           // activations of this pass
-    float *red;             // kRedBytes
-};
-
-__device__ __forceinline__ int linear_of_tile(const StreamArgs &a, int tile)
-{
-    int l = 0;
-#pragma unroll
-    for (int i = 1; i < kMaxGroup; ++i)
-        if (i < a.count && tile >= a.tile_start[i]) l = i;
-    return l;
-}
-
+// Activation layouts (per token, tsz bytes apart):
+//  W4A8 : q_lo [G][16] | q_hi [G][16] | 16 B pad  (q_lo = elements 0..15 of each group,
+//         q_hi = 16..31: lane-per-block LDS.128 reads are consecutive -> conflict-free),
+//         then sx [ntok][G] fp32, sq [ntok][G] int32 after all tokens.
+//  W4A16: [G][4 t][8 bf16] in fragment order (4t,4t+2,4t+1,4t+3,4t+16,4t+18,4t+17,4t+19) | 64 B pad.
 template <int E>
-__global__ void __launch_bounds__(kThreads, 1) stream_linear(const StreamArgs a)
+__global__ void __launch_bounds__(kThreads, 1) stream_linear(const __grid_constant__ StreamArgs a)
 {
-    extern __shared__ __align__(128) uint8_t smem_raw[];
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t *base = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t k = a.k;
     const int G = (int)(k / 32);
-    const int nchunks = (int)((k / 2 + kChunkBytes - 1) / kChunkBytes);
+    const int K2 = (int)(k / 2);
+    const int nchunks = (K2 + kChunkBytes - 1) / kChunkBytes;
     const int S = a.stages;
 
-    uint8_t *ring = smem_raw;
-    uint64_t *full = reinterpret_cast<uint64_t *>(smem_raw + (size_t)S * kStageBytes);
+    uint8_t *ring = base;
+    uint64_t *full = reinterpret_cast<uint64_t *>(base + (size_t)S * kStageBytes);
     uint64_t *empty = full + S;
-    uint8_t *act = reinterpret_cast<uint8_t *>(empty + S) + 0;
-    act = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(act) + 127) & ~(uintptr_t)127);
-    float *red = reinterpret_cast<float *>(act + a.act_bytes);
+    uint64_t *xbar = empty + S;
+    uint8_t *xraw = base + a.xraw_off;
+    uint8_t *act = base + a.act_off;
+    float *red = reinterpret_cast<float *>(base + a.red_off);
 
-    // this CTA's contiguous tile range
     const int T = a.tile_start[a.count];
     const int t0 = (int)(((int64_t)T * blockIdx.x) / gridDim.x);
     const int t1 = (int)(((int64_t)T * (blockIdx.x + 1)) / gridDim.x);
-    const int items = (t1 - t0) * nchunks;
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < S; ++s) {
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], kConsumerWarps);
         }
+        mbar_init(xbar, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
-    dev::griddep_launch();   // the next linear may launch now; it only touches weights until its own wait
+    dev::griddep_launch();   // the next linear may launch: it only touches weights until its own wait
 
     if (warp == kConsumerWarps) {
         // ================= producer =================
         if (lane == 0) {
             const uint64_t pol = evict_first_policy();
-            for (int it = 0; it < items; ++it) {
-                const int s = it % S;
-                const uint32_t ph = (uint32_t)(it / S) & 1u;
-                mbar_wait(&empty[s], ph ^ 1u);
-                const int tile = t0 + it / nchunks, ch = it % nchunks;
-                const int li = linear_of_tile(a, tile);
-                const int64_t row0 = (int64_t)(tile - a.tile_start[li]) * kTileRows;
-                const int rows = (int)imin64(kTileRows, a.n[li] - row0);
-                const int64_t off = (int64_t)ch * kChunkBytes;
-                const uint32_t cb = (uint32_t)imin64(kChunkBytes, k / 2 - off);
-                const uint32_t sb = cb / 8;   // fp16 scale bytes: cb/16 blocks x 2 B
-                uint8_t *st = ring + (size_t)s * kStageBytes;
-                mbar_expect_tx(&full[s], (uint32_t)rows * (cb + sb));
-                const uint8_t *nsrc = a.nib[li] + row0 * (k / 2) + off;
-                const uint8_t *ssrc = reinterpret_cast<const uint8_t *>(a.scale[li]) + row0 * (k / 16) + off / 8;
-                for (int r = 0; r < rows; ++r) {
-                    bulk_g2s(st + r * kNibStride, nsrc + r * (k / 2), cb, &full[s], pol);
-                    bulk_g2s(st + kTileRows * kNibStride + r * kScaleStride, ssrc + r * (k / 16), sb, &full[s], pol);
+            int s = 0;
+            uint32_t ph = 0;
+            int li = 0;
+            for (int tile = t0; tile < t1; ++tile) {
+                while (li + 1 < a.count && tile >= a.tile_start[li + 1]) ++li;
+                const int row0 = (tile - a.tile_start[li]) * kTileRows;
+                for (int ch = 0; ch < nchunks; ++ch) {
+                    mbar_wait(&empty[s], ph ^ 1u);
+                    const int rem = K2 - ch * kChunkBytes;
+                    const int nbox = (rem < kChunkBytes ? rem : kChunkBytes) / 128;
+                    uint8_t *st = ring + (size_t)s * kStageBytes;
+                    mbar_expect_tx(&full[s], (uint32_t)(nbox + 1) * kBox);
+                    for (int b = 0; b < nbox; ++b)
+                        tma_2d(st + b * kBox, &a.tm_nib[li], ch * kChunkBytes + b * 128, row0, &full[s], pol);
+                    tma_2d(st + 8 * kBox, &a.tm_scale[li], ch * kChunkBlocks, row0, &full[s], pol);
+                    if (++s == S) {
+                        s = 0;
+                        ph ^= 1u;
+                    }
                 }
             }
         }
@@ -235,53 +244,42 @@ __global__ void __launch_bounds__(kThreads, 1) stream_linear(const StreamArgs a)
     // ================= consumers: stage activations =================
     dev::griddep_wait();
     const int ntok = a.ntok;
+    if (threadIdx.x == 0) {
+        mbar_expect_tx(xbar, (uint32_t)(ntok * 2 * k));
+        for (int i = 0; i < ntok; ++i) bulk_g2s(xraw + (size_t)i * 2 * k, a.x + (a.tok0 + i) * a.ldx, (uint32_t)(2 * k), xbar);
+    }
+    mbar_wait(xbar, 0);
+    const uint16_t *xs = reinterpret_cast<const uint16_t *>(xraw);
+    const int tsz = (E == HMMA) ? (int)(2 * k + 64) : (int)(k + 16);
+    float *sx_s = reinterpret_cast<float *>(act + (size_t)ntok * tsz);
+    int32_t *sq_s = reinterpret_cast<int32_t *>(act + (size_t)ntok * tsz + 4 * (size_t)ntok * G);
     if constexpr (E == DP4A || E == IMMA) {
-        // fused per-token, per-32-group quantisation (identical arithmetic to quant_a8_kernel)
-        const int64_t qs = k + 16;
-        int8_t *q_s = reinterpret_cast<int8_t *>(act);
-        float *sx_s = reinterpret_cast<float *>(act + a.ntok_cap * qs);
-        int32_t *sq_s = reinterpret_cast<int32_t *>(act + a.ntok_cap * qs + 4 * a.ntok_cap * G);
-        // 4 groups per warp in flight (independent chains), lane j = element j of a group
-        for (int base = warp; base < ntok * G; base += 4 * kConsumerWarps) {
-            float v[4];
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                const int grp = base + u * kConsumerWarps;
-                v[u] = 0.f;
-                if (grp < ntok * G) {
-                    const int i = grp / G, g = grp % G;
-                    v[u] = dev::bf16_bits_to_float(a.x[(a.tok0 + i) * a.ldx + 32 * g + lane]);
-                }
+        // per-token, per-32-group quantisation: identical arithmetic to quant_a8_kernel
+        for (int grp = warp; grp < ntok * G; grp += kConsumerWarps) {
+            const int i = grp / G, g = grp - i * G;
+            const float v = dev::bf16_bits_to_float(xs[(size_t)i * k + 32 * g + lane]);
+            const bool finite = __all_sync(0xffffffffu, isfinite(v));
+            const float amax = __uint_as_float(__reduce_max_sync(0xffffffffu, __float_as_uint(fabsf(v))));
+            const float s = __fdiv_rn(amax, 127.0f);
+            int code = 0;
+            const bool live = finite && s != 0.0f;
+            if (live) {
+                float r = roundf(__fdiv_rn(v, s));
+                r = fminf(fmaxf(r, -127.0f), 127.0f);
+                code = (int)r;
             }
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                const int grp = base + u * kConsumerWarps;
-                if (grp >= ntok * G) break;
-                const int i = grp / G, g = grp % G;
-                const bool finite = __all_sync(0xffffffffu, isfinite(v[u]));
-                const float amax = __uint_as_float(__reduce_max_sync(0xffffffffu, __float_as_uint(fabsf(v[u]))));
-                const float s = __fdiv_rn(amax, 127.0f);
-                int code = 0;
-                const bool live = finite && s != 0.0f;
-                if (live) {
-                    float r = roundf(__fdiv_rn(v[u], s));
-                    r = fminf(fmaxf(r, -127.0f), 127.0f);
-                    code = (int)r;
-                }
-                q_s[i * qs + 32 * g + lane] = (int8_t)code;
-                const int sum = __reduce_add_sync(0xffffffffu, code);
-                if (lane == 0) {
-                    sx_s[i * G + g] = live ? s : 0.0f;
-                    sq_s[i * G + g] = sum;
-                }
+            int8_t *qt = reinterpret_cast<int8_t *>(act + (size_t)i * tsz);
+            qt[(lane < 16 ? 16 * g : K2 + 16 * g - 16) + lane] = (int8_t)code;
+            const int sum = __reduce_add_sync(0xffffffffu, code);
+            if (lane == 0) {
+                sx_s[i * G + g] = live ? s : 0.0f;
+                sq_s[i * G + g] = sum;
             }
         }
     } else {
-        // x in fragment order per (token, block, t): (4t,4t+2) (4t+1,4t+3) (4t+16,4t+18) (4t+17,4t+19)
-        const int64_t xs = 2 * k + 64;
         for (int idx = threadIdx.x; idx < ntok * G * 4; idx += kConsumerWarps * 32) {
-            const int tk = idx / (G * 4), rem = idx % (G * 4), g = rem >> 2, tt = rem & 3;
-            const uint16_t *src = a.x + (a.tok0 + tk) * a.ldx + 32 * g + 4 * tt;
+            const int tk = idx / (G * 4), rem = idx - tk * G * 4, g = rem >> 2, tt = rem & 3;
+            const uint16_t *src = xs + (size_t)tk * k + 32 * g + 4 * tt;
             const uint2 lo = *reinterpret_cast<const uint2 *>(src);
             const uint2 hi = *reinterpret_cast<const uint2 *>(src + 16);
             uint4 o;
@@ -289,182 +287,211 @@ __global__ void __launch_bounds__(kThreads, 1) stream_linear(const StreamArgs a)
             o.y = __byte_perm(lo.x, lo.y, 0x7632);
             o.z = __byte_perm(hi.x, hi.y, 0x5410);
             o.w = __byte_perm(hi.x, hi.y, 0x7632);
-            *reinterpret_cast<uint4 *>(act + tk * xs + 64 * g + 16 * tt) = o;
+            *reinterpret_cast<uint4 *>(act + (size_t)tk * tsz + 64 * g + 16 * tt) = o;
         }
     }
-    asm volatile("bar.sync 1, %0;" ::"n"(kConsumerWarps * 32) : "memory");   // consumers only
+    bar_consumers();
 
     // ================= consumers: main loop =================
     const int gid = lane >> 2, t = lane & 3;
-    float acc[4] = {0.f, 0.f, 0.f, 0.f};
-    for (int it = 0; it < items; ++it) {
-        const int s = it % S;
-        const uint32_t ph = (uint32_t)(it / S) & 1u;
-        const int tile = t0 + it / nchunks, ch = it % nchunks;
-        const int nblk = (int)(imin64(kChunkBytes, k / 2 - (int64_t)ch * kChunkBytes) / 16);
-        const int blk0 = ch * (kChunkBytes / 16);   // first block of the chunk within the row
-        if (ch == 0) acc[0] = acc[1] = acc[2] = acc[3] = 0.f;
-        mbar_wait(&full[s], ph);
-        const uint8_t *st = ring + (size_t)s * kStageBytes;
-        const uint8_t *sc = st + kTileRows * kNibStride;
+    int s = 0;
+    uint32_t ph = 0;
+    int li = 0;
+    for (int tile = t0; tile < t1; ++tile) {
+        while (li + 1 < a.count && tile >= a.tile_start[li + 1]) ++li;
+        float acc[4] = {0.f, 0.f, 0.f, 0.f};
+        for (int ch = 0; ch < nchunks; ++ch) {
+            const int rem = K2 - ch * kChunkBytes;
+            const int nblk = (rem < kChunkBytes ? rem : kChunkBytes) / 16;
+            const int blk0 = ch * kChunkBlocks;
+            mbar_wait(&full[s], ph);
+            const uint8_t *st = ring + (size_t)s * kStageBytes;
 
-        if constexpr (E == DP4A) {
-            const int8_t *q_s = reinterpret_cast<const int8_t *>(act);
-            const float *sx_s = reinterpret_cast<const float *>(act + a.ntok_cap * (k + 16));
-            const int32_t *sq_s = reinterpret_cast<const int32_t *>(act + a.ntok_cap * (k + 16) + 4 * a.ntok_cap * G);
-#pragma unroll
-            for (int rr = 0; rr < 2; ++rr) {
-                const int r = 2 * warp + rr;
-#pragma unroll
-                for (int h = 0; h < 2; ++h) {
-                    const int b = lane + 32 * h;
-                    if (b < nblk) {
-                        const uint4 w = *reinterpret_cast<const uint4 *>(st + r * kNibStride + 16 * b);
-                        const uint16_t d16 = *reinterpret_cast<const uint16_t *>(sc + r * kScaleStride + 2 * b);
-                        const int g = blk0 + b;
-                        const int4 qa = *reinterpret_cast<const int4 *>(q_s + 32 * g);
-                        const int4 qb = *reinterpret_cast<const int4 *>(q_s + 32 * g + 16);
-                        const int D = block_sumi_dp4a(w, qa, qb) - 8 * sq_s[g];
-                        acc[rr] = fmaf(h2f(d16) * sx_s[g], (float)D, acc[rr]);
-                    }
-                }
-            }
-        } else {
-            // warp w: blocks w, w+8, ... of the chunk, two per ldmatrix.x4
-            const uint32_t st_a = smem_addr(st);
-            for (int b = warp; b < nblk; b += 2 * kConsumerWarps) {
-                const int b2 = b + kConsumerWarps;
-                const bool two = b2 < nblk;
-                // lanes 0-7: rows 0-7 @ b, 8-15: rows 8-15 @ b, 16-23: rows 0-7 @ b2, 24-31: rows 8-15 @ b2
-                const int mrow = (lane & 7) + ((lane >> 3) & 1) * 8;
-                const int mblk = (lane >> 4) ? (two ? b2 : b) : b;
-                uint32_t wa0, wb0, wa1, wb1;
-                ldmatrix_x4(st_a + mrow * kNibStride + 16 * mblk, wa0, wb0, wa1, wb1);
-#pragma unroll
-                for (int u = 0; u < 2; ++u) {
-                    if (u == 1 && !two) break;
-                    const int bb = u ? b2 : b;
-                    const uint32_t wa = u ? wa1 : wa0, wb = u ? wb1 : wb0;
-                    const float da = h2f(*reinterpret_cast<const uint16_t *>(sc + gid * kScaleStride + 2 * bb));
-                    const float db = h2f(*reinterpret_cast<const uint16_t *>(sc + (gid + 8) * kScaleStride + 2 * bb));
-                    const int g = blk0 + bb;
-                    if constexpr (E == IMMA) {
-                        const int64_t qs = k + 16;
-                        const int8_t *q_s = reinterpret_cast<const int8_t *>(act);
-                        const float *sx_s = reinterpret_cast<const float *>(act + a.ntok_cap * qs);
-                        const int32_t *sq_s =
-                            reinterpret_cast<const int32_t *>(act + a.ntok_cap * qs + 4 * a.ntok_cap * G);
-                        uint32_t b0 = 0, b1 = 0;
-                        if (gid < ntok) {
-                            b0 = *reinterpret_cast<const uint32_t *>(q_s + gid * qs + 32 * g + 4 * t);
-                            b1 = *reinterpret_cast<const uint32_t *>(q_s + gid * qs + 32 * g + 16 + 4 * t);
-                        }
-                        int c[4];
-                        imma(wa, wb, b0, b1, c);
-                        const int c0 = 2 * t, c1 = 2 * t + 1;
-                        const float s0 = c0 < ntok ? sx_s[c0 * G + g] : 0.f;
-                        const float s1 = c1 < ntok ? sx_s[c1 * G + g] : 0.f;
-                        const int q0 = c0 < ntok ? sq_s[c0 * G + g] : 0;
-                        const int q1 = c1 < ntok ? sq_s[c1 * G + g] : 0;
-                        acc[0] = fmaf(da * s0, (float)(c[0] - 8 * q0), acc[0]);
-                        acc[1] = fmaf(da * s1, (float)(c[1] - 8 * q1), acc[1]);
-                        acc[2] = fmaf(db * s0, (float)(c[2] - 8 * q0), acc[2]);
-                        acc[3] = fmaf(db * s1, (float)(c[3] - 8 * q1), acc[3]);
-                    } else {
-                        uint4 bx = make_uint4(0, 0, 0, 0);
-                        if (gid < ntok) bx = *reinterpret_cast<const uint4 *>(act + gid * (2 * k + 64) + 64 * g + 16 * t);
-                        uint32_t pa[4], pb[4];
-                        dequant_bf16(wa, pa);
-                        dequant_bf16(wb, pb);
-                        float c[4] = {0.f, 0.f, 0.f, 0.f};
-                        hmma(pa[0], pb[0], pa[2], pb[2], bx.x, bx.y, c);
-                        hmma(pa[1], pb[1], pa[3], pb[3], bx.z, bx.w, c);
-                        acc[0] = fmaf(da, c[0], acc[0]);
-                        acc[1] = fmaf(da, c[1], acc[1]);
-                        acc[2] = fmaf(db, c[2], acc[2]);
-                        acc[3] = fmaf(db, c[3], acc[3]);
-                    }
-                }
-            }
-        }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[s]);
-
-        if (ch == nchunks - 1) {
-            // ---- tile epilogue: fixed-order reductions, store
-            const int li = linear_of_tile(a, tile);
-            const int64_t row0 = (int64_t)(tile - a.tile_start[li]) * kTileRows;
-            const int64_t n = a.n[li];
             if constexpr (E == DP4A) {
+                const uint8_t *q_lo = act, *q_hi = act + K2;
 #pragma unroll
-                for (int rr = 0; rr < 2; ++rr)
+                for (int rr = 0; rr < 2; ++rr) {
+                    const int r = 2 * warp + rr;
 #pragma unroll
-                    for (int off = 16; off > 0; off >>= 1) acc[rr] += __shfl_xor_sync(0xffffffffu, acc[rr], off);
-                if (lane < 2) {
-                    const int64_t row = row0 + 2 * warp + lane;
-                    if (row < n) dev::store_out(a.y[li], a.ydt, a.tok0 * a.ldy[li] + row, lane ? acc[1] : acc[0]);
+                    for (int h = 0; h < 2; ++h) {
+                        const int b = lane + 32 * h;
+                        if (b < nblk) {
+                            const uint4 w = *reinterpret_cast<const uint4 *>(st + nib_off(r, b));
+                            const uint16_t d16 = *reinterpret_cast<const uint16_t *>(st + scale_off(r, b));
+                            const int g = blk0 + b;
+                            const int4 qa = *reinterpret_cast<const int4 *>(q_lo + 16 * g);
+                            const int4 qb = *reinterpret_cast<const int4 *>(q_hi + 16 * g);
+                            const int D = block_sumi_dp4a(w, qa, qb) - 8 * sq_s[g];
+                            acc[rr] = fmaf(h2f(d16) * sx_s[g], (float)D, acc[rr]);
+                        }
+                    }
                 }
             } else {
-                float *rw = red + warp * 128;
-                const int c0 = 2 * t, c1 = 2 * t + 1;
-                rw[gid * 8 + c0] = acc[0];
-                rw[gid * 8 + c1] = acc[1];
-                rw[(gid + 8) * 8 + c0] = acc[2];
-                rw[(gid + 8) * 8 + c1] = acc[3];
-                asm volatile("bar.sync 1, %0;" ::"n"(kConsumerWarps * 32) : "memory");
-                if (threadIdx.x < 128) {
-                    const int r = threadIdx.x >> 3, tk = threadIdx.x & 7;
-                    float sum = red[threadIdx.x];
+                const uint32_t st_a = smem_addr(st);
+                const int mrow = (lane & 7) + ((lane >> 3) & 1) * 8;
+                for (int b = warp; b < nblk; b += 2 * kConsumerWarps) {
+                    const int b2 = b + kConsumerWarps;
+                    const bool two = b2 < nblk;
+                    const int mblk = (lane >> 4) && two ? b2 : b;
+                    uint32_t wa0, wb0, wa1, wb1;
+                    ldmatrix_x4(st_a + nib_off(mrow, mblk), wa0, wb0, wa1, wb1);
 #pragma unroll
-                    for (int w = 1; w < kConsumerWarps; ++w) sum += red[w * 128 + threadIdx.x];
-                    const int64_t row = row0 + r;
-                    if (row < n && tk < ntok) dev::store_out(a.y[li], a.ydt, (a.tok0 + tk) * a.ldy[li] + row, sum);
+                    for (int u = 0; u < 2; ++u) {
+                        if (u == 1 && !two) break;
+                        const int bb = u ? b2 : b;
+                        const uint32_t wa = u ? wa1 : wa0, wb = u ? wb1 : wb0;
+                        const float da = h2f(*reinterpret_cast<const uint16_t *>(st + scale_off(gid, bb)));
+                        const float db = h2f(*reinterpret_cast<const uint16_t *>(st + scale_off(gid + 8, bb)));
+                        const int g = blk0 + bb;
+                        if constexpr (E == IMMA) {
+                            uint32_t b0 = 0, b1 = 0;
+                            if (gid < ntok) {
+                                const uint8_t *qt = act + (size_t)gid * tsz;
+                                b0 = *reinterpret_cast<const uint32_t *>(qt + 16 * g + 4 * t);
+                                b1 = *reinterpret_cast<const uint32_t *>(qt + K2 + 16 * g + 4 * t);
+                            }
+                            int c[4];
+                            imma(wa, wb, b0, b1, c);
+                            const int c0 = 2 * t, c1 = 2 * t + 1;
+                            const float s0 = c0 < ntok ? sx_s[c0 * G + g] : 0.f;
+                            const float s1 = c1 < ntok ? sx_s[c1 * G + g] : 0.f;
+                            const int q0 = c0 < ntok ? sq_s[c0 * G + g] : 0;
+                            const int q1 = c1 < ntok ? sq_s[c1 * G + g] : 0;
+                            acc[0] = fmaf(da * s0, (float)(c[0] - 8 * q0), acc[0]);
+                            acc[1] = fmaf(da * s1, (float)(c[1] - 8 * q1), acc[1]);
+                            acc[2] = fmaf(db * s0, (float)(c[2] - 8 * q0), acc[2]);
+                            acc[3] = fmaf(db * s1, (float)(c[3] - 8 * q1), acc[3]);
+                        } else {
+                            uint4 bx = make_uint4(0, 0, 0, 0);
+                            if (gid < ntok) bx = *reinterpret_cast<const uint4 *>(act + (size_t)gid * tsz + 64 * g + 16 * t);
+                            uint32_t pa[4], pb[4];
+                            dequant_bf16(wa, pa);
+                            dequant_bf16(wb, pb);
+                            float c[4] = {0.f, 0.f, 0.f, 0.f};
+                            hmma(pa[0], pb[0], pa[2], pb[2], bx.x, bx.y, c);
+                            hmma(pa[1], pb[1], pa[3], pb[3], bx.z, bx.w, c);
+                            acc[0] = fmaf(da, c[0], acc[0]);
+                            acc[1] = fmaf(da, c[1], acc[1]);
+                            acc[2] = fmaf(db, c[2], acc[2]);
+                            acc[3] = fmaf(db, c[3], acc[3]);
+                        }
+                    }
                 }
-                asm volatile("bar.sync 1, %0;" ::"n"(kConsumerWarps * 32) : "memory");
             }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[s]);
+            if (++s == S) {
+                s = 0;
+                ph ^= 1u;
+            }
+        }
+        // ---- tile epilogue: fixed-order reductions, store
+        const int64_t row0 = (int64_t)(tile - a.tile_start[li]) * kTileRows;
+        const int64_t n = a.n[li];
+        if constexpr (E == DP4A) {
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) {
+                acc[0] += __shfl_xor_sync(0xffffffffu, acc[0], off);
+                acc[1] += __shfl_xor_sync(0xffffffffu, acc[1], off);
+            }
+            if (lane < 2) {
+                const int64_t row = row0 + 2 * warp + lane;
+                if (row < n) dev::store_out(a.y[li], a.ydt, a.tok0 * a.ldy[li] + row, lane ? acc[1] : acc[0]);
+            }
+        } else {
+            float *rw = red + warp * 128;
+            const int c0 = 2 * t, c1 = 2 * t + 1;
+            rw[gid * 8 + c0] = acc[0];
+            rw[gid * 8 + c1] = acc[1];
+            rw[(gid + 8) * 8 + c0] = acc[2];
+            rw[(gid + 8) * 8 + c1] = acc[3];
+            bar_consumers();
+            if (threadIdx.x < 128) {
+                const int r = threadIdx.x >> 3, tk = threadIdx.x & 7;
+                float sum = red[threadIdx.x];
+#pragma unroll
+                for (int w = 1; w < kConsumerWarps; ++w) sum += red[w * 128 + threadIdx.x];
+                const int64_t row = row0 + r;
+                if (row < n && tk < ntok) dev::store_out(a.y[li], a.ydt, (a.tok0 + tk) * a.ldy[li] + row, sum);
+            }
+            bar_consumers();
         }
     }
 }
 
-}  // namespace
+// ------------------------------------------------------------------ host side
+typedef CUresult (*EncodeTiledFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
+                                  const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 
-// activation bytes of one pass of `ntok` tokens
-static size_t act_bytes(int engine, int64_t k, int ntok)
+EncodeTiledFn encode_fn()
+{
+    static EncodeTiledFn fn = nullptr;
+    if (!fn) {
+        void *p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<EncodeTiledFn>(p);
+    }
+    return fn;
+}
+
+bool encode_maps(CUtensorMap *tn, CUtensorMap *ts, const uint8_t *nib, const uint16_t *scale, int64_t n, int64_t k)
+{
+    EncodeTiledFn fn = encode_fn();
+    if (!fn) return false;
+    const cuuint64_t nd[2] = {(cuuint64_t)(k / 2), (cuuint64_t)n};
+    const cuuint64_t ns[1] = {(cuuint64_t)(k / 2)};
+    const cuuint32_t nbox[2] = {128, kTileRows};
+    const cuuint32_t es[2] = {1, 1};
+    if (fn(tn, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<uint8_t *>(nib), nd, ns, nbox, es,
+           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+        return false;
+    const cuuint64_t sd[2] = {(cuuint64_t)(k / 32), (cuuint64_t)n};
+    const cuuint64_t ss[1] = {(cuuint64_t)(k / 16)};
+    const cuuint32_t sbox[2] = {kChunkBlocks, kTileRows};
+    return fn(ts, CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, const_cast<uint16_t *>(scale), sd, ss, sbox, es,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+size_t act_bytes(int engine, int64_t k, int ntok)
 {
     const int64_t G = k / 32;
     if (engine == HMMA) return (size_t)ntok * (size_t)(2 * k + 64);
     return (size_t)ntok * (size_t)(k + 16) + (size_t)ntok * 8 * (size_t)G;
 }
 
-bool stream_supported(int64_t k) { return k >= 256 && k % 256 == 0; }
+size_t round_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
-int stream_tokens_per_pass(int route, int64_t k)
+// Shared-memory plan: ring (S stages) | barriers | x raw | activations | reduction.
+// Aim at <= ~113 KB so that this linear and the next (PDL) fit on one SM together.
+size_t plan_smem(int engine, int64_t k, int ntok, StreamArgs &a)
 {
-    // keep activations + 3 ring stages within ~110 KB so two CTAs (this linear and the
-    // next, PDL-overlapped) can share an SM
-    const int engine = route == MCAPQ_W4A16 ? HMMA : IMMA;
-    const size_t budget = 110 * 1024 - 3 * (size_t)kStageBytes - kRedBytes - 256;
-    int tp = 8;
-    while (tp > 1 && act_bytes(engine, k, tp) > budget) --tp;
-    return tp;
+    const size_t xraw = round_up((size_t)ntok * 2 * (size_t)k, 128);
+    const size_t act = round_up(act_bytes(engine, k, ntok), 128);
+    const size_t fixed = 128 + xraw + act + kRedBytes;
+    const size_t budget = 112 * 1024;
+    int S = (int)(((long)budget - (long)fixed - 1024) / kStageBytes);
+    S = S < 2 ? 2 : (S > 6 ? 6 : S);
+    a.stages = S;
+    a.xraw_off = (int)((size_t)S * kStageBytes + 128);
+    a.act_off = (int)(a.xraw_off + xraw);
+    a.red_off = (int)(a.act_off + act);
+    return 1024 + (size_t)a.red_off + kRedBytes;
 }
 
 template <int E>
-static cudaError_t launch_one(StreamArgs a, cudaStream_t s, bool pdl, int sms)
+cudaError_t launch_one(StreamArgs &a, cudaStream_t s, bool pdl, int sms)
 {
-    const size_t ab = (act_bytes(E, a.k, a.ntok_cap) + 127) & ~(size_t)127;
-    a.act_bytes = (int)ab;
-    // stages: as many as fit in ~110 KB (>= 2)
-    const size_t fixed = ab + kRedBytes + 256;
-    int S = (int)((110 * 1024 - (long)fixed) / (kStageBytes + 16));
-    S = S < 2 ? 2 : (S > 6 ? 6 : S);
-    a.stages = S;
-    const size_t smem = (size_t)S * kStageBytes + 16 * (size_t)S + 128 + fixed;
-    static int attr_done[3] = {0, 0, 0};
-    if (!attr_done[E]) {
+    const size_t smem = plan_smem(E, a.k, a.ntok, a);
+    static int attr_done = 0;
+    if (!attr_done) {
         cudaError_t e = cudaFuncSetAttribute(stream_linear<E>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
         if (e != cudaSuccess) return e;
-        attr_done[E] = 1;
+        attr_done = 1;
     }
     const int T = a.tile_start[a.count];
     const int grid = T < sms ? T : sms;
@@ -472,15 +499,34 @@ static cudaError_t launch_one(StreamArgs a, cudaStream_t s, bool pdl, int sms)
     return launch_pdl(stream_linear<E>, dim3(grid), dim3(kThreads), smem, s, pdl, a);
 }
 
+}  // namespace
+
+bool stream_supported(int64_t k) { return k >= 2048 && k % 256 == 0 && encode_fn() != nullptr; }
+
+int stream_tokens_per_pass(int route, int64_t k)
+{
+    // activations of up to 8 tokens, as long as >= 2 ring stages fit the ~112 KB plan
+    const int engine = route == MCAPQ_W4A16 ? HMMA : IMMA;
+    int tp = 8;
+    while (tp > 1) {
+        const size_t need = 1024 + 128 + round_up((size_t)tp * 2 * (size_t)k, 128) +
+                            round_up(act_bytes(engine, k, tp), 128) + kRedBytes + 2 * (size_t)kStageBytes;
+        if (need <= 112 * 1024) break;
+        --tp;
+    }
+    return tp;
+}
+
 cudaError_t launch_stream_group(int route, const StreamGroup &g, const uint16_t *x, int64_t m, int64_t ldx, int ydt,
                                 cudaStream_t s, bool pdl)
 {
-    StreamArgs a = {};
+    StreamArgs a;
+    memset(&a, 0, sizeof(a));
     a.count = g.count;
     int tiles = 0;
     for (int i = 0; i < g.count; ++i) {
-        a.nib[i] = g.nib[i];
-        a.scale[i] = g.scale[i];
+        if (!encode_maps(&a.tm_nib[i], &a.tm_scale[i], g.nib[i], g.scale[i], g.n[i], g.k))
+            return cudaErrorInvalidValue;
         a.n[i] = g.n[i];
         a.y[i] = g.y[i];
         a.ldy[i] = g.ldy[i];
@@ -497,7 +543,6 @@ cudaError_t launch_stream_group(int route, const StreamGroup &g, const uint16_t 
     for (int64_t tok0 = 0; tok0 < m; tok0 += tp) {
         a.tok0 = tok0;
         a.ntok = (int)((m - tok0) < tp ? (m - tok0) : tp);
-        a.ntok_cap = a.ntok;
         cudaError_t e;
         if (route == MCAPQ_W4A16)
             e = launch_one<HMMA>(a, s, pdl, sms);

@@ -1,5 +1,7 @@
-// stream.h -- the persistent TMA-bulk-fed decode-linear path (kernels_stream.cu).
+// stream.h -- the persistent TMA-fed decode-linear path (kernels_stream.cu).
 #pragma once
+#include <cuda.h>
+
 #include "internal.h"
 
 namespace mcapq {
@@ -17,26 +19,29 @@ struct StreamGroup {
     int64_t ldy[kMaxGroup];
 };
 
-// Kernel parameters (by value).
-struct StreamArgs {
-    int count;
-    const uint8_t *nib[kMaxGroup];
-    const uint16_t *scale[kMaxGroup];
-    int64_t n[kMaxGroup];
+// Kernel parameters (passed by value as a __grid_constant__: the TMA unit reads
+// the tensor maps straight from parameter space).
+struct alignas(64) StreamArgs {
+    CUtensorMap tm_nib[kMaxGroup];     // uint8 [N][K/2], box {128 B, 16 rows}, 128B swizzle
+    CUtensorMap tm_scale[kMaxGroup];   // uint16 [N][K/32], box {64, 16 rows}, 128B swizzle
     void *y[kMaxGroup];
+    int64_t n[kMaxGroup];
     int64_t ldy[kMaxGroup];
     int tile_start[kMaxGroup + 1];
+    int count;
     int64_t k;
     const uint16_t *x;
     int64_t ldx;
     int64_t tok0;
-    int ntok, ntok_cap;
+    int ntok;
     int ydt;
     int stages;
-    int act_bytes;
+    int act_off;     // byte offset of the activation area in dynamic smem
+    int red_off;     // byte offset of the reduction area
+    int xraw_off;    // byte offset of the raw x staging area
 };
 
-// K % 256 == 0 (16-B aligned scale rows for the bulk copies) and 16-B aligned planes.
+// K % 256 == 0 (16-B aligned scale rows for the tensor maps) and 16-B aligned planes.
 bool stream_supported(int64_t k);
 int stream_tokens_per_pass(int route, int64_t k);
 cudaError_t launch_stream_group(int route, const StreamGroup &g, const uint16_t *x, int64_t m, int64_t ldx,

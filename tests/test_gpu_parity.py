@@ -55,7 +55,7 @@ def _assert_close(y_gpu, y64, rtol):
     rms = np.sqrt(np.mean(ref ** 2)) if ref.size else 0.0
     if y_gpu.dtype == torch.bfloat16:
         tol = 1e-3 * np.maximum(np.abs(ref), rms) + _half_ulp_bf16(ref)
-        if ref.size:
+        if ref.size >= 512:       # a statistic of RNE rounding (~1.7e-3): noisy on short vectors
             nrm = np.linalg.norm(y - ref) / max(np.linalg.norm(ref), 1e-300)
             assert nrm <= rtol, f"normwise rel err {nrm:.3e} > {rtol}"
     else:
