@@ -51,45 +51,46 @@ constexpr int kRedBytes = kConsumerWarps * kTileRows * 8 * 4;
 enum Engine { DP4A = 0, IMMA = 1, HMMA = 2 };
 
 // ------------------------------------------------------------------ PTX helpers
+// All shared-memory traffic uses explicit 32-bit shared-window addresses
+// (ld.shared / st.shared): the 1024-B alignment of the dynamic smem base would
+// otherwise turn the pointers generic (LD.E with 64-bit address math).
 __device__ __forceinline__ uint32_t smem_addr(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
-__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count)
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count)
 {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count) : "memory");
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
 }
-__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes)
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes)
 {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes)
-                 : "memory");
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
 }
-__device__ __forceinline__ void mbar_arrive(uint64_t *bar)
+__device__ __forceinline__ void mbar_arrive(uint32_t bar)
 {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
 }
-__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity)
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity)
 {
     asm volatile(
         "{\n\t.reg .pred p;\n\t"
         "WAIT_%=:\n\t"
         "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
-        "@!p bra WAIT_%=;\n\t}" ::"r"(smem_addr(bar)),
+        "@!p bra WAIT_%=;\n\t}" ::"r"(bar),
         "r"(parity)
         : "memory");
 }
-__device__ __forceinline__ void tma_2d(void *dst, const CUtensorMap *map, int x, int y, uint64_t *bar,
+__device__ __forceinline__ void tma_2d(uint32_t dst, const CUtensorMap *map, int x, int y, uint32_t bar,
                                        uint64_t policy)
 {
     asm volatile(
         "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint"
-        " [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(smem_addr(dst)),
-        "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(smem_addr(bar)), "l"(policy)
+        " [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(bar), "l"(policy)
         : "memory");
 }
-__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar)
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void *src, uint32_t bytes, uint32_t bar)
 {
-    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                     smem_addr(dst)),
-                 "l"(src), "r"(bytes), "r"(smem_addr(bar))
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+                 "l"(src), "r"(bytes), "r"(bar)
                  : "memory");
 }
 __device__ __forceinline__ uint64_t evict_first_policy()
@@ -104,6 +105,42 @@ __device__ __forceinline__ void ldmatrix_x4(uint32_t addr, uint32_t &r0, uint32_
                  : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
                  : "r"(addr));
 }
+__device__ __forceinline__ uint4 lds128(uint32_t a)
+{
+    uint4 v;
+    asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ uint2 lds64(uint32_t a)
+{
+    uint2 v;
+    asm volatile("ld.shared.v2.u32 {%0,%1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ uint32_t lds32(uint32_t a)
+{
+    uint32_t v;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ uint16_t lds16(uint32_t a)
+{
+    uint16_t v;
+    asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ void sts128(uint32_t a, uint4 v)
+{
+    asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(a), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w) : "memory");
+}
+__device__ __forceinline__ void sts32(uint32_t a, uint32_t v)
+{
+    asm volatile("st.shared.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+__device__ __forceinline__ void sts8(uint32_t a, uint32_t v)
+{
+    asm volatile("st.shared.u8 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
 __device__ __forceinline__ float h2f(uint16_t h)
 {
     float f;
@@ -113,13 +150,13 @@ __device__ __forceinline__ float h2f(uint16_t h)
 __device__ __forceinline__ void bar_consumers() { asm volatile("bar.sync 1, %0;" ::"n"(kConsumerWarps * 32) : "memory"); }
 
 // 128-B swizzle of a {128 B x 16 rows} box: 16-B chunk c of row r sits at c ^ (r & 7).
-__device__ __forceinline__ int nib_off(int r, int b)          // block b (0..63) of the chunk, row r
+__device__ __forceinline__ uint32_t nib_off(int r, int b)          // block b (0..63) of the chunk, row r
 {
-    return (b >> 3) * kBox + r * 128 + (((b & 7) ^ (r & 7)) << 4);
+    return (uint32_t)((b >> 3) * kBox + r * 128 + (((b & 7) ^ (r & 7)) << 4));
 }
-__device__ __forceinline__ int scale_off(int r, int b)
+__device__ __forceinline__ uint32_t scale_off(int r, int b)
 {
-    return 8 * kBox + r * 128 + ((((b >> 3) ^ (r & 7))) << 4) + ((b & 7) << 1);
+    return (uint32_t)(8 * kBox + r * 128 + ((((b >> 3) ^ (r & 7))) << 4) + ((b & 7) << 1));
 }
 
 // ------------------------------------------------------------------ fragments
@@ -172,252 +209,7 @@ __device__ __forceinline__ void hmma(uint32_t a0, uint32_t a1, uint32_t a2, uint
 }
 
 // ------------------------------------------------------------------ the kernel
-// Activation layouts (per token, tsz bytes apart):
-//  W4A8 : q_lo [G][16] | q_hi [G][16] | 16 B pad  (q_lo = elements 0..15 of each group,
-//         q_hi = 16..31: lane-per-block LDS.128 reads are consecutive -> conflict-free),
-//         then sx [ntok][G] fp32, sq [ntok][G] int32 after all tokens.
-//  W4A16: [G][4 t][8 bf16] in fragment order (4t,4t+2,4t+1,4t+3,4t+16,4t+18,4t+17,4t+19) | 64 B pad.
-template <int E>
-__global__ void __launch_bounds__(kThreads, 1) stream_linear(const __grid_constant__ StreamArgs a)
-{
-    extern __shared__ uint8_t smem_raw[];
-    uint8_t *base = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int64_t k = a.k;
-    const int G = (int)(k / 32);
-    const int K2 = (int)(k / 2);
-    const int nchunks = (K2 + kChunkBytes - 1) / kChunkBytes;
-    const int S = a.stages;
-
-    uint8_t *ring = base;
-    uint64_t *full = reinterpret_cast<uint64_t *>(base + (size_t)S * kStageBytes);
-    uint64_t *empty = full + S;
-    uint64_t *xbar = empty + S;
-    uint8_t *xraw = base + a.xraw_off;
-    uint8_t *act = base + a.act_off;
-    float *red = reinterpret_cast<float *>(base + a.red_off);
-
-    const int T = a.tile_start[a.count];
-    const int t0 = (int)(((int64_t)T * blockIdx.x) / gridDim.x);
-    const int t1 = (int)(((int64_t)T * (blockIdx.x + 1)) / gridDim.x);
-
-    if (threadIdx.x == 0) {
-        for (int s = 0; s < S; ++s) {
-            mbar_init(&full[s], 1);
-            mbar_init(&empty[s], kConsumerWarps);
-        }
-        mbar_init(xbar, 1);
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    __syncthreads();
-    dev::griddep_launch();   // the next linear may launch: it only touches weights until its own wait
-
-    if (warp == kConsumerWarps) {
-        // ================= producer =================
-        if (lane == 0) {
-            const uint64_t pol = evict_first_policy();
-            int s = 0;
-            uint32_t ph = 0;
-            int li = 0;
-            for (int tile = t0; tile < t1; ++tile) {
-                while (li + 1 < a.count && tile >= a.tile_start[li + 1]) ++li;
-                const int row0 = (tile - a.tile_start[li]) * kTileRows;
-                for (int ch = 0; ch < nchunks; ++ch) {
-                    mbar_wait(&empty[s], ph ^ 1u);
-                    const int rem = K2 - ch * kChunkBytes;
-                    const int nbox = (rem < kChunkBytes ? rem : kChunkBytes) / 128;
-                    uint8_t *st = ring + (size_t)s * kStageBytes;
-                    mbar_expect_tx(&full[s], (uint32_t)(nbox + 1) * kBox);
-                    for (int b = 0; b < nbox; ++b)
-                        tma_2d(st + b * kBox, &a.tm_nib[li], ch * kChunkBytes + b * 128, row0, &full[s], pol);
-                    tma_2d(st + 8 * kBox, &a.tm_scale[li], ch * kChunkBlocks, row0, &full[s], pol);
-                    if (++s == S) {
-                        s = 0;
-                        ph ^= 1u;
-                    }
-                }
-            }
-        }
-        return;
-    }
-
-    // ================= consumers: stage activations =================
-    dev::griddep_wait();
-    const int ntok = a.ntok;
-    if (threadIdx.x == 0) {
-        mbar_expect_tx(xbar, (uint32_t)(ntok * 2 * k));
-        for (int i = 0; i < ntok; ++i) bulk_g2s(xraw + (size_t)i * 2 * k, a.x + (a.tok0 + i) * a.ldx, (uint32_t)(2 * k), xbar);
-    }
-    mbar_wait(xbar, 0);
-    const uint16_t *xs = reinterpret_cast<const uint16_t *>(xraw);
-    const int tsz = (E == HMMA) ? (int)(2 * k + 64) : (int)(k + 16);
-    float *sx_s = reinterpret_cast<float *>(act + (size_t)ntok * tsz);
-    int32_t *sq_s = reinterpret_cast<int32_t *>(act + (size_t)ntok * tsz + 4 * (size_t)ntok * G);
-    if constexpr (E == DP4A || E == IMMA) {
-        // per-token, per-32-group quantisation: identical arithmetic to quant_a8_kernel
-        for (int grp = warp; grp < ntok * G; grp += kConsumerWarps) {
-            const int i = grp / G, g = grp - i * G;
-            const float v = dev::bf16_bits_to_float(xs[(size_t)i * k + 32 * g + lane]);
-            const bool finite = __all_sync(0xffffffffu, isfinite(v));
-            const float amax = __uint_as_float(__reduce_max_sync(0xffffffffu, __float_as_uint(fabsf(v))));
-            const float s = __fdiv_rn(amax, 127.0f);
-            int code = 0;
-            const bool live = finite && s != 0.0f;
-            if (live) {
-                float r = roundf(__fdiv_rn(v, s));
-                r = fminf(fmaxf(r, -127.0f), 127.0f);
-                code = (int)r;
-            }
-            int8_t *qt = reinterpret_cast<int8_t *>(act + (size_t)i * tsz);
-            qt[(lane < 16 ? 16 * g : K2 + 16 * g - 16) + lane] = (int8_t)code;
-            const int sum = __reduce_add_sync(0xffffffffu, code);
-            if (lane == 0) {
-                sx_s[i * G + g] = live ? s : 0.0f;
-                sq_s[i * G + g] = sum;
-            }
-        }
-    } else {
-        for (int idx = threadIdx.x; idx < ntok * G * 4; idx += kConsumerWarps * 32) {
-            const int tk = idx / (G * 4), rem = idx - tk * G * 4, g = rem >> 2, tt = rem & 3;
-            const uint16_t *src = xs + (size_t)tk * k + 32 * g + 4 * tt;
-            const uint2 lo = *reinterpret_cast<const uint2 *>(src);
-            const uint2 hi = *reinterpret_cast<const uint2 *>(src + 16);
-            uint4 o;
-            o.x = __byte_perm(lo.x, lo.y, 0x5410);
-            o.y = __byte_perm(lo.x, lo.y, 0x7632);
-            o.z = __byte_perm(hi.x, hi.y, 0x5410);
-            o.w = __byte_perm(hi.x, hi.y, 0x7632);
-            *reinterpret_cast<uint4 *>(act + (size_t)tk * tsz + 64 * g + 16 * tt) = o;
-        }
-    }
-    bar_consumers();
-
-    // ================= consumers: main loop =================
-    const int gid = lane >> 2, t = lane & 3;
-    int s = 0;
-    uint32_t ph = 0;
-    int li = 0;
-    for (int tile = t0; tile < t1; ++tile) {
-        while (li + 1 < a.count && tile >= a.tile_start[li + 1]) ++li;
-        float acc[4] = {0.f, 0.f, 0.f, 0.f};
-        for (int ch = 0; ch < nchunks; ++ch) {
-            const int rem = K2 - ch * kChunkBytes;
-            const int nblk = (rem < kChunkBytes ? rem : kChunkBytes) / 16;
-            const int blk0 = ch * kChunkBlocks;
-            mbar_wait(&full[s], ph);
-            const uint8_t *st = ring + (size_t)s * kStageBytes;
-
-            if constexpr (E == DP4A) {
-                const uint8_t *q_lo = act, *q_hi = act + K2;
-#pragma unroll
-                for (int rr = 0; rr < 2; ++rr) {
-                    const int r = 2 * warp + rr;
-#pragma unroll
-                    for (int h = 0; h < 2; ++h) {
-                        const int b = lane + 32 * h;
-                        if (b < nblk) {
-                            const uint4 w = *reinterpret_cast<const uint4 *>(st + nib_off(r, b));
-                            const uint16_t d16 = *reinterpret_cast<const uint16_t *>(st + scale_off(r, b));
-                            const int g = blk0 + b;
-                            const int4 qa = *reinterpret_cast<const int4 *>(q_lo + 16 * g);
-                            const int4 qb = *reinterpret_cast<const int4 *>(q_hi + 16 * g);
-                            const int D = block_sumi_dp4a(w, qa, qb) - 8 * sq_s[g];
-                            acc[rr] = fmaf(h2f(d16) * sx_s[g], (float)D, acc[rr]);
-                        }
-                    }
-                }
-            } else {
-                const uint32_t st_a = smem_addr(st);
-                const int mrow = (lane & 7) + ((lane >> 3) & 1) * 8;
-                for (int b = warp; b < nblk; b += 2 * kConsumerWarps) {
-                    const int b2 = b + kConsumerWarps;
-                    const bool two = b2 < nblk;
-                    const int mblk = (lane >> 4) && two ? b2 : b;
-                    uint32_t wa0, wb0, wa1, wb1;
-                    ldmatrix_x4(st_a + nib_off(mrow, mblk), wa0, wb0, wa1, wb1);
-#pragma unroll
-                    for (int u = 0; u < 2; ++u) {
-                        if (u == 1 && !two) break;
-                        const int bb = u ? b2 : b;
-                        const uint32_t wa = u ? wa1 : wa0, wb = u ? wb1 : wb0;
-                        const float da = h2f(*reinterpret_cast<const uint16_t *>(st + scale_off(gid, bb)));
-                        const float db = h2f(*reinterpret_cast<const uint16_t *>(st + scale_off(gid + 8, bb)));
-                        const int g = blk0 + bb;
-                        if constexpr (E == IMMA) {
-                            uint32_t b0 = 0, b1 = 0;
-                            if (gid < ntok) {
-                                const uint8_t *qt = act + (size_t)gid * tsz;
-                                b0 = *reinterpret_cast<const uint32_t *>(qt + 16 * g + 4 * t);
-                                b1 = *reinterpret_cast<const uint32_t *>(qt + K2 + 16 * g + 4 * t);
-                            }
-                            int c[4];
-                            imma(wa, wb, b0, b1, c);
-                            const int c0 = 2 * t, c1 = 2 * t + 1;
-                            const float s0 = c0 < ntok ? sx_s[c0 * G + g] : 0.f;
-                            const float s1 = c1 < ntok ? sx_s[c1 * G + g] : 0.f;
-                            const int q0 = c0 < ntok ? sq_s[c0 * G + g] : 0;
-                            const int q1 = c1 < ntok ? sq_s[c1 * G + g] : 0;
-                            acc[0] = fmaf(da * s0, (float)(c[0] - 8 * q0), acc[0]);
-                            acc[1] = fmaf(da * s1, (float)(c[1] - 8 * q1), acc[1]);
-                            acc[2] = fmaf(db * s0, (float)(c[2] - 8 * q0), acc[2]);
-                            acc[3] = fmaf(db * s1, (float)(c[3] - 8 * q1), acc[3]);
-                        } else {
-                            uint4 bx = make_uint4(0, 0, 0, 0);
-                            if (gid < ntok) bx = *reinterpret_cast<const uint4 *>(act + (size_t)gid * tsz + 64 * g + 16 * t);
-                            uint32_t pa[4], pb[4];
-                            dequant_bf16(wa, pa);
-                            dequant_bf16(wb, pb);
-                            float c[4] = {0.f, 0.f, 0.f, 0.f};
-                            hmma(pa[0], pb[0], pa[2], pb[2], bx.x, bx.y, c);
-                            hmma(pa[1], pb[1], pa[3], pb[3], bx.z, bx.w, c);
-                            acc[0] = fmaf(da, c[0], acc[0]);
-                            acc[1] = fmaf(da, c[1], acc[1]);
-                            acc[2] = fmaf(db, c[2], acc[2]);
-                            acc[3] = fmaf(db, c[3], acc[3]);
-                        }
-                    }
-                }
-            }
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&empty[s]);
-            if (++s == S) {
-                s = 0;
-                ph ^= 1u;
-            }
-        }
-        // ---- tile epilogue: fixed-order reductions, store
-        const int64_t row0 = (int64_t)(tile - a.tile_start[li]) * kTileRows;
-        const int64_t n = a.n[li];
-        if constexpr (E == DP4A) {
-#pragma unroll
-            for (int off = 16; off > 0; off >>= 1) {
-                acc[0] += __shfl_xor_sync(0xffffffffu, acc[0], off);
-                acc[1] += __shfl_xor_sync(0xffffffffu, acc[1], off);
-            }
-            if (lane < 2) {
-                const int64_t row = row0 + 2 * warp + lane;
-                if (row < n) dev::store_out(a.y[li], a.ydt, a.tok0 * a.ldy[li] + row, lane ? acc[1] : acc[0]);
-            }
-        } else {
-            float *rw = red + warp * 128;
-            const int c0 = 2 * t, c1 = 2 * t + 1;
-            rw[gid * 8 + c0] = acc[0];
-            rw[gid * 8 + c1] = acc[1];
-            rw[(gid + 8) * 8 + c0] = acc[2];
-            rw[(gid + 8) * 8 + c1] = acc[3];
-            bar_consumers();
-            if (threadIdx.x < 128) {
-                const int r = threadIdx.x >> 3, tk = threadIdx.x & 7;
-                float sum = red[threadIdx.x];
-#pragma unroll
-                for (int w = 1; w < kConsumerWarps; ++w) sum += red[w * 128 + threadIdx.x];
-                const int64_t row = row0 + r;
-                if (row < n && tk < ntok) dev::store_out(a.y[li], a.ydt, (a.tok0 + tk) * a.ldy[li] + row, sum);
-            }
-            bar_consumers();
-        }
-    }
-}
+#include "stream_kernel.cuh"
 
 // ------------------------------------------------------------------ host side
 typedef CUresult (*EncodeTiledFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,

@@ -1,0 +1,260 @@
+// stream_kernel.cuh -- the persistent TMA-fed decode-linear kernel (included by
+// kernels_stream.cu, which holds the PTX helpers, fragments and host launch).
+//
+// Shared memory (dynamic, 1024-B aligned base sb; all offsets 32-bit shared
+// addresses):  ring [S x 18 KiB] | full[S] empty[S] xbar | x raw | activations | reduction
+// Activation layouts (per token, tsz bytes apart):
+//  W4A8 : q_lo [G][16] | q_hi [G][16] | 16 B pad   (q_lo = elements 0..15 of each
+//         32-group, q_hi = 16..31: lane-per-block LDS.128 are consecutive), then
+//         sx [ntok][G] fp32 and sq [ntok][G] int32 after all tokens.
+//  W4A16: [G][4 t][8 bf16] in fragment order (4t,4t+2,4t+1,4t+3,4t+16,4t+18,4t+17,4t+19) | 64 B pad.
+#pragma once
+
+template <int E>
+__global__ void __launch_bounds__(kThreads, 1) stream_linear(const __grid_constant__ StreamArgs a)
+{
+    extern __shared__ __align__(16) uint8_t smem_raw[];
+    const uint32_t sraw = smem_addr(smem_raw);
+    const uint32_t sb = (sraw + 1023u) & ~1023u;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t k = a.k;
+    const int G = (int)(k / 32);
+    const int K2 = (int)(k / 2);
+    const int nchunks = (K2 + kChunkBytes - 1) / kChunkBytes;
+    const int S = a.stages;
+
+    const uint32_t ring = sb;
+    const uint32_t full = sb + (uint32_t)S * kStageBytes;       // S x 8 B
+    const uint32_t empty = full + 8u * S;                        // S x 8 B
+    const uint32_t xbar = empty + 8u * S;
+    const uint32_t xraw = sb + a.xraw_off;
+    const uint32_t act = sb + a.act_off;
+    const uint32_t red = sb + a.red_off;
+
+    const int T = a.tile_start[a.count];
+    const int t0 = (int)(((int64_t)T * blockIdx.x) / gridDim.x);
+    const int t1 = (int)(((int64_t)T * (blockIdx.x + 1)) / gridDim.x);
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < S; ++s) {
+            mbar_init(full + 8u * s, 1);
+            mbar_init(empty + 8u * s, kConsumerWarps);
+        }
+        mbar_init(xbar, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    dev::griddep_launch();   // the next linear may launch: it only touches weights until its own wait
+
+    if (warp == kConsumerWarps) {
+        // ================= producer =================
+        if (lane == 0) {
+            const uint64_t pol = evict_first_policy();
+            int s = 0;
+            uint32_t ph = 0;
+            int li = 0;
+            for (int tile = t0; tile < t1; ++tile) {
+                while (li + 1 < a.count && tile >= a.tile_start[li + 1]) ++li;
+                const int row0 = (tile - a.tile_start[li]) * kTileRows;
+                for (int ch = 0; ch < nchunks; ++ch) {
+                    mbar_wait(empty + 8u * s, ph ^ 1u);
+                    const int rem = K2 - ch * kChunkBytes;
+                    const int nbox = (rem < kChunkBytes ? rem : kChunkBytes) / 128;
+                    const uint32_t st = ring + (uint32_t)s * kStageBytes;
+                    const uint32_t fb = full + 8u * s;
+                    mbar_expect_tx(fb, (uint32_t)(nbox + 1) * kBox);
+                    for (int b = 0; b < nbox; ++b)
+                        tma_2d(st + b * kBox, &a.tm_nib[li], ch * kChunkBytes + b * 128, row0, fb, pol);
+                    tma_2d(st + 8 * kBox, &a.tm_scale[li], ch * kChunkBlocks, row0, fb, pol);
+                    if (++s == S) {
+                        s = 0;
+                        ph ^= 1u;
+                    }
+                }
+            }
+        }
+        return;
+    }
+
+    // ================= consumers: stage activations =================
+    dev::griddep_wait();
+    const int ntok = a.ntok;
+    if (threadIdx.x == 0) {
+        mbar_expect_tx(xbar, (uint32_t)(ntok * 2 * k));
+        for (int i = 0; i < ntok; ++i)
+            bulk_g2s(xraw + (uint32_t)(i * 2 * k), a.x + (a.tok0 + i) * a.ldx, (uint32_t)(2 * k), xbar);
+    }
+    mbar_wait(xbar, 0);
+    const uint32_t tsz = (E == HMMA) ? (uint32_t)(2 * k + 64) : (uint32_t)(k + 16);
+    const uint32_t sx_s = act + (uint32_t)ntok * tsz;                    // [ntok][G] fp32
+    const uint32_t sq_s = sx_s + 4u * (uint32_t)(ntok * G);              // [ntok][G] int32
+    if constexpr (E == DP4A || E == IMMA) {
+        // per-token, per-32-group quantisation: identical arithmetic to quant_a8_kernel
+        const int groups = ntok * G;
+        for (int grp = warp; grp < groups; grp += kConsumerWarps) {
+            const int i = grp / G, g = grp - i * G;
+            const float v = dev::bf16_bits_to_float(lds16(xraw + 2u * (uint32_t)(i * k + 32 * g + lane)));
+            const bool finite = __all_sync(0xffffffffu, isfinite(v));
+            const float amax = __uint_as_float(__reduce_max_sync(0xffffffffu, __float_as_uint(fabsf(v))));
+            const float s = __fdiv_rn(amax, 127.0f);
+            int code = 0;
+            const bool live = finite && s != 0.0f;
+            if (live) {
+                float r = roundf(__fdiv_rn(v, s));
+                r = fminf(fmaxf(r, -127.0f), 127.0f);
+                code = (int)r;
+            }
+            const uint32_t qt = act + (uint32_t)i * tsz;
+            sts8(qt + (lane < 16 ? 16u * g + lane : (uint32_t)K2 + 16u * g + lane - 16u), (uint32_t)code & 0xffu);
+            const int sum = __reduce_add_sync(0xffffffffu, code);
+            if (lane == 0) {
+                sts32(sx_s + 4u * (uint32_t)(i * G + g), __float_as_uint(live ? s : 0.0f));
+                sts32(sq_s + 4u * (uint32_t)(i * G + g), (uint32_t)sum);
+            }
+        }
+    } else {
+        for (int idx = threadIdx.x; idx < ntok * G * 4; idx += kConsumerWarps * 32) {
+            const int tk = idx / (G * 4), rem = idx - tk * G * 4, g = rem >> 2, tt = rem & 3;
+            const uint32_t src = xraw + 2u * (uint32_t)(tk * k + 32 * g + 4 * tt);
+            const uint2 lo = lds64(src);        // x[4t..4t+3]
+            const uint2 hi = lds64(src + 32);   // x[4t+16..4t+19]
+            uint4 o;
+            o.x = __byte_perm(lo.x, lo.y, 0x5410);
+            o.y = __byte_perm(lo.x, lo.y, 0x7632);
+            o.z = __byte_perm(hi.x, hi.y, 0x5410);
+            o.w = __byte_perm(hi.x, hi.y, 0x7632);
+            sts128(act + (uint32_t)tk * tsz + 64u * g + 16u * tt, o);
+        }
+    }
+    bar_consumers();
+
+    // ================= consumers: main loop =================
+    const int gid = lane >> 2, t = lane & 3;
+    const int mrow = (lane & 7) + ((lane >> 3) & 1) * 8;    // ldmatrix row of this lane
+    int s = 0;
+    uint32_t ph = 0;
+    int li = 0;
+    for (int tile = t0; tile < t1; ++tile) {
+        while (li + 1 < a.count && tile >= a.tile_start[li + 1]) ++li;
+        float acc[4] = {0.f, 0.f, 0.f, 0.f};
+        for (int ch = 0; ch < nchunks; ++ch) {
+            const int rem = K2 - ch * kChunkBytes;
+            const int nblk = (rem < kChunkBytes ? rem : kChunkBytes) / 16;
+            const int blk0 = ch * kChunkBlocks;
+            mbar_wait(full + 8u * s, ph);
+            const uint32_t st = ring + (uint32_t)s * kStageBytes;
+
+            if constexpr (E == DP4A) {
+                // lane l: blocks l and l+32 of rows 2w, 2w+1
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const int b = lane + 32 * h;
+                    if (h == 0 || b < nblk) {            // nblk is a multiple of 32 (K % 1024 == 0) or 16
+                        if (b < nblk) {
+                            const int g = blk0 + b;
+                            const uint4 qa = lds128(act + 16u * g);
+                            const uint4 qb = lds128(act + (uint32_t)K2 + 16u * g);
+                            const float sxg = __uint_as_float(lds32(sx_s + 4u * g));
+                            const int sqg8 = 8 * (int)lds32(sq_s + 4u * g);
+#pragma unroll
+                            for (int rr = 0; rr < 2; ++rr) {
+                                const int r = 2 * warp + rr;
+                                const uint4 w = lds128(st + nib_off(r, b));
+                                const uint16_t d16 = lds16(st + scale_off(r, b));
+                                const int D = block_sumi_dp4a(w, make_int4(qa.x, qa.y, qa.z, qa.w),
+                                                              make_int4(qb.x, qb.y, qb.z, qb.w)) - sqg8;
+                                acc[rr] = fmaf(h2f(d16) * sxg, (float)D, acc[rr]);
+                            }
+                        }
+                    }
+                }
+            } else {
+                for (int b = warp; b < nblk; b += 2 * kConsumerWarps) {
+                    const int b2 = b + kConsumerWarps;
+                    const bool two = b2 < nblk;
+                    const int mblk = ((lane >> 4) && two) ? b2 : b;
+                    uint32_t wa0, wb0, wa1, wb1;
+                    ldmatrix_x4(st + nib_off(mrow, mblk), wa0, wb0, wa1, wb1);
+#pragma unroll
+                    for (int u = 0; u < 2; ++u) {
+                        if (u == 1 && !two) break;
+                        const int bb = u ? b2 : b;
+                        const uint32_t wa = u ? wa1 : wa0, wb = u ? wb1 : wb0;
+                        const float da = h2f(lds16(st + scale_off(gid, bb)));
+                        const float db = h2f(lds16(st + scale_off(gid + 8, bb)));
+                        const int g = blk0 + bb;
+                        if constexpr (E == IMMA) {
+                            uint32_t b0 = 0, b1 = 0;
+                            if (gid < ntok) {
+                                const uint32_t qt = act + (uint32_t)gid * tsz;
+                                b0 = lds32(qt + 16u * g + 4u * t);
+                                b1 = lds32(qt + (uint32_t)K2 + 16u * g + 4u * t);
+                            }
+                            int c[4];
+                            imma(wa, wb, b0, b1, c);
+                            const int c0 = 2 * t, c1 = 2 * t + 1;
+                            const float s0 = c0 < ntok ? __uint_as_float(lds32(sx_s + 4u * (c0 * G + g))) : 0.f;
+                            const float s1 = c1 < ntok ? __uint_as_float(lds32(sx_s + 4u * (c1 * G + g))) : 0.f;
+                            const int q0 = c0 < ntok ? (int)lds32(sq_s + 4u * (c0 * G + g)) : 0;
+                            const int q1 = c1 < ntok ? (int)lds32(sq_s + 4u * (c1 * G + g)) : 0;
+                            acc[0] = fmaf(da * s0, (float)(c[0] - 8 * q0), acc[0]);
+                            acc[1] = fmaf(da * s1, (float)(c[1] - 8 * q1), acc[1]);
+                            acc[2] = fmaf(db * s0, (float)(c[2] - 8 * q0), acc[2]);
+                            acc[3] = fmaf(db * s1, (float)(c[3] - 8 * q1), acc[3]);
+                        } else {
+                            uint4 bx = make_uint4(0, 0, 0, 0);
+                            if (gid < ntok) bx = lds128(act + (uint32_t)gid * tsz + 64u * g + 16u * t);
+                            uint32_t pa[4], pb[4];
+                            dequant_bf16(wa, pa);
+                            dequant_bf16(wb, pb);
+                            float c[4] = {0.f, 0.f, 0.f, 0.f};
+                            hmma(pa[0], pb[0], pa[2], pb[2], bx.x, bx.y, c);
+                            hmma(pa[1], pb[1], pa[3], pb[3], bx.z, bx.w, c);
+                            acc[0] = fmaf(da, c[0], acc[0]);
+                            acc[1] = fmaf(da, c[1], acc[1]);
+                            acc[2] = fmaf(db, c[2], acc[2]);
+                            acc[3] = fmaf(db, c[3], acc[3]);
+                        }
+                    }
+                }
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(empty + 8u * s);
+            if (++s == S) {
+                s = 0;
+                ph ^= 1u;
+            }
+        }
+        // ---- tile epilogue: fixed-order reductions, store
+        const int64_t row0 = (int64_t)(tile - a.tile_start[li]) * kTileRows;
+        const int64_t n = a.n[li];
+        if constexpr (E == DP4A) {
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) {
+                acc[0] += __shfl_xor_sync(0xffffffffu, acc[0], off);
+                acc[1] += __shfl_xor_sync(0xffffffffu, acc[1], off);
+            }
+            if (lane < 2) {
+                const int64_t row = row0 + 2 * warp + lane;
+                if (row < n) dev::store_out(a.y[li], a.ydt, a.tok0 * a.ldy[li] + row, lane ? acc[1] : acc[0]);
+            }
+        } else {
+            const uint32_t rw = red + 512u * warp;
+            const int c0 = 2 * t, c1 = 2 * t + 1;
+            sts32(rw + 4u * (gid * 8 + c0), __float_as_uint(acc[0]));
+            sts32(rw + 4u * (gid * 8 + c1), __float_as_uint(acc[1]));
+            sts32(rw + 4u * ((gid + 8) * 8 + c0), __float_as_uint(acc[2]));
+            sts32(rw + 4u * ((gid + 8) * 8 + c1), __float_as_uint(acc[3]));
+            bar_consumers();
+            if (threadIdx.x < 128) {
+                const int r = threadIdx.x >> 3, tk = threadIdx.x & 7;
+                float sum = __uint_as_float(lds32(red + 4u * threadIdx.x));
+#pragma unroll
+                for (int w = 1; w < kConsumerWarps; ++w) sum += __uint_as_float(lds32(red + 512u * w + 4u * threadIdx.x));
+                const int64_t row = row0 + r;
+                if (row < n && tk < ntok) dev::store_out(a.y[li], a.ydt, (a.tok0 + tk) * a.ldy[li] + row, sum);
+            }
+            bar_consumers();
+        }
+    }
+}

@@ -260,14 +260,24 @@ def test_full_size_sampled_rows(mq, orc, model, slot, m):
 
 
 # ---------------------------------------------------------------- a7 + a9 stack
-def test_stack_matches_oracle_and_graph_replay(mq, orc):
+STACK_DIMS = {
+    # K < 2048: generic kernels, separate quantiser launches (4 + 7 per W4A8 layer, 7 per W4A16 layer)
+    "generic": ({"q": (256, 512), "k": (64, 512), "v": (64, 512), "o": (512, 256), "gate": (1024, 512),
+                 "up": (1024, 512), "down": (512, 1024)}, 2 * (4 + 7) + 2 * 7),
+    # K >= 2048: TMA stream kernels, grouped qkv / o / gate-up / down launches, quantiser fused
+    "stream": ({"q": (256, 2048), "k": (64, 2048), "v": (64, 2048), "o": (512, 2048), "gate": (384, 2048),
+                "up": (384, 2048), "down": (256, 2048)}, 4 * 4),
+}
+
+
+@pytest.mark.parametrize("kind", ["generic", "stream"])
+def test_stack_matches_oracle_and_graph_replay(mq, orc, kind):
     prof = mq.profile_parse(open(os.path.join(GOLD, "llama32_1b_profile.json")).read())
     routes = prof.routes()
     assert routes == [0] * 15 + [1]
     L = 4
     routes = [0, 1, 0, 1]
-    dims = {"q": (256, 512), "k": (64, 512), "v": (64, 512), "o": (512, 256), "gate": (1024, 512),
-            "up": (1024, 512), "down": (512, 1024)}
+    dims, launches = STACK_DIMS[kind]
     inputs = {"q": 0, "k": 0, "v": 0, "o": 1, "gate": 2, "up": 2, "down": 3}
     st = mq.Stack(routes, max_m=2)
     ref = []
@@ -284,7 +294,7 @@ def test_stack_matches_oracle_and_graph_replay(mq, orc):
             y = torch.empty(2, n, dtype=torch.bfloat16, device=DEV)
             st.set(l, slot_id, inputs[slot], pw, xd, y)
             ref.append((l, y, w, x))
-    assert st.launches(2) == 4 * L          # qkv, o, gate/up, down: one grouped launch each
+    assert st.launches(2) == launches
     s = torch.cuda.Stream()
     with torch.cuda.stream(s):
         st.run(2, stream=s)
