@@ -39,7 +39,7 @@
 namespace mcapq {
 namespace {
 
-constexpr int kConsumerWarps = 8;
+constexpr int kConsumerWarps = 16;   // one output row per warp per 16-row tile (DP4A); 4 warps / SMSP
 constexpr int kThreads = (kConsumerWarps + 1) * 32;
 constexpr int kTileRows = 16;
 constexpr int kChunkBytes = 1024;                  // nibble bytes per row per stage

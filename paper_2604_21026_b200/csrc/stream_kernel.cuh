@@ -145,26 +145,37 @@ __global__ void __launch_bounds__(kThreads, 1) stream_linear(const __grid_consta
             const uint32_t st = ring + (uint32_t)s * kStageBytes;
 
             if constexpr (E == DP4A) {
-                // lane l: blocks l and l+32 of rows 2w, 2w+1
+                // warp w: row w of the tile; lane l: blocks l and l+32 of the chunk (in that order)
+                const int r = warp;
+                if (nblk == kChunkBlocks) {
+                    // full chunk: no predicates, both blocks' load/dp4a chains interleave
+                    const int g0 = blk0 + lane, g1 = g0 + 32;
+                    const uint4 w0 = lds128(st + nib_off(r, lane));
+                    const uint4 w1 = lds128(st + nib_off(r, lane + 32));
+                    const uint4 qa0 = lds128(act + 16u * g0), qb0 = lds128(act + (uint32_t)K2 + 16u * g0);
+                    const uint4 qa1 = lds128(act + 16u * g1), qb1 = lds128(act + (uint32_t)K2 + 16u * g1);
+                    const float d0 = h2f(lds16(st + scale_off(r, lane)));
+                    const float d1 = h2f(lds16(st + scale_off(r, lane + 32)));
+                    const float s0 = __uint_as_float(lds32(sx_s + 4u * g0));
+                    const float s1 = __uint_as_float(lds32(sx_s + 4u * g1));
+                    const int D0 = block_sumi_dp4a(w0, make_int4(qa0.x, qa0.y, qa0.z, qa0.w),
+                                                   make_int4(qb0.x, qb0.y, qb0.z, qb0.w)) - 8 * (int)lds32(sq_s + 4u * g0);
+                    const int D1 = block_sumi_dp4a(w1, make_int4(qa1.x, qa1.y, qa1.z, qa1.w),
+                                                   make_int4(qb1.x, qb1.y, qb1.z, qb1.w)) - 8 * (int)lds32(sq_s + 4u * g1);
+                    acc[0] = fmaf(d0 * s0, (float)D0, acc[0]);
+                    acc[0] = fmaf(d1 * s1, (float)D1, acc[0]);
+                } else {
 #pragma unroll
-                for (int h = 0; h < 2; ++h) {
-                    const int b = lane + 32 * h;
-                    if (h == 0 || b < nblk) {            // nblk is a multiple of 32 (K % 1024 == 0) or 16
+                    for (int h = 0; h < 2; ++h) {
+                        const int b = lane + 32 * h;
                         if (b < nblk) {
                             const int g = blk0 + b;
-                            const uint4 qa = lds128(act + 16u * g);
-                            const uint4 qb = lds128(act + (uint32_t)K2 + 16u * g);
-                            const float sxg = __uint_as_float(lds32(sx_s + 4u * g));
-                            const int sqg8 = 8 * (int)lds32(sq_s + 4u * g);
-#pragma unroll
-                            for (int rr = 0; rr < 2; ++rr) {
-                                const int r = 2 * warp + rr;
-                                const uint4 w = lds128(st + nib_off(r, b));
-                                const uint16_t d16 = lds16(st + scale_off(r, b));
-                                const int D = block_sumi_dp4a(w, make_int4(qa.x, qa.y, qa.z, qa.w),
-                                                              make_int4(qb.x, qb.y, qb.z, qb.w)) - sqg8;
-                                acc[rr] = fmaf(h2f(d16) * sxg, (float)D, acc[rr]);
-                            }
+                            const uint4 qa = lds128(act + 16u * g), qb = lds128(act + (uint32_t)K2 + 16u * g);
+                            const uint4 w = lds128(st + nib_off(r, b));
+                            const int D = block_sumi_dp4a(w, make_int4(qa.x, qa.y, qa.z, qa.w),
+                                                          make_int4(qb.x, qb.y, qb.z, qb.w)) - 8 * (int)lds32(sq_s + 4u * g);
+                            acc[0] = fmaf(h2f(lds16(st + scale_off(r, b))) * __uint_as_float(lds32(sx_s + 4u * g)),
+                                          (float)D, acc[0]);
                         }
                     }
                 }
@@ -230,13 +241,10 @@ __global__ void __launch_bounds__(kThreads, 1) stream_linear(const __grid_consta
         const int64_t n = a.n[li];
         if constexpr (E == DP4A) {
 #pragma unroll
-            for (int off = 16; off > 0; off >>= 1) {
-                acc[0] += __shfl_xor_sync(0xffffffffu, acc[0], off);
-                acc[1] += __shfl_xor_sync(0xffffffffu, acc[1], off);
-            }
-            if (lane < 2) {
-                const int64_t row = row0 + 2 * warp + lane;
-                if (row < n) dev::store_out(a.y[li], a.ydt, a.tok0 * a.ldy[li] + row, lane ? acc[1] : acc[0]);
+            for (int off = 16; off > 0; off >>= 1) acc[0] += __shfl_xor_sync(0xffffffffu, acc[0], off);
+            if (lane == 0) {
+                const int64_t row = row0 + warp;
+                if (row < n) dev::store_out(a.y[li], a.ydt, a.tok0 * a.ldy[li] + row, acc[0]);
             }
         } else {
             const uint32_t rw = red + 512u * warp;
