@@ -33,6 +33,8 @@
 // Determinism: the chunking and the block->lane/warp maps depend on K only and
 // all reductions have a fixed order, so an output row is bit-identical whatever
 // N, the group, the grid or the column shard (reading A22).
+#include <cstdlib>
+
 #include "internal.h"
 #include "stream.h"
 
@@ -48,7 +50,7 @@ constexpr int kBox = 128 * kTileRows;              // one {128 B x 16 rows} TMA 
 constexpr int kStageBytes = 8 * kBox + kBox;       // 8 nibble boxes + 1 scale box (18 KiB)
 constexpr int kRedBytes = kConsumerWarps * kTileRows * 8 * 4;
 
-enum Engine { DP4A = 0, IMMA = 1, HMMA = 2 };
+enum Engine { DP4A = 0, IMMA = 1, HMMA = 2, NONE = 3 };   // NONE: bandwidth probe
 
 // ------------------------------------------------------------------ PTX helpers
 // All shared-memory traffic uses explicit 32-bit shared-window addresses
@@ -252,7 +254,7 @@ bool encode_maps(CUtensorMap *tn, CUtensorMap *ts, const uint8_t *nib, const uin
 size_t act_bytes(int engine, int64_t k, int ntok)
 {
     const int64_t G = k / 32;
-    if (engine == HMMA) return (size_t)ntok * (size_t)(2 * k + 64);
+    if (engine == HMMA || engine == NONE) return (size_t)ntok * (size_t)(2 * k + 64);
     return (size_t)ntok * (size_t)(k + 16) + (size_t)ntok * 8 * (size_t)G;
 }
 
@@ -260,14 +262,39 @@ size_t round_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
 // Shared-memory plan: ring (S stages) | barriers | x raw | activations | reduction.
 // Aim at <= ~113 KB so that this linear and the next (PDL) fit on one SM together.
+// Launch-shape knobs, read once from the environment (benchmarking / tuning only;
+// the defaults are the tuned values):
+//   MCAPQ_STREAM_SMEM_KB   shared-memory plan per CTA (default 112: two CTAs per SM)
+//   MCAPQ_STREAM_STAGES    max ring stages (default 12)
+//   MCAPQ_STREAM_NOCOMPUTE 1 = consumers only drain the ring (bandwidth probe; outputs garbage)
+//   MCAPQ_STREAM_PDL       1 = API calls also launch with programmatic dependent launch
+struct Tune {
+    int smem_kb = 112, max_stages = 12, nocompute = 0, pdl = 0;
+};
+const Tune &tune()
+{
+    static Tune t = [] {
+        Tune v;
+        if (const char *e = getenv("MCAPQ_STREAM_SMEM_KB")) v.smem_kb = atoi(e);
+        if (const char *e = getenv("MCAPQ_STREAM_STAGES")) v.max_stages = atoi(e);
+        if (const char *e = getenv("MCAPQ_STREAM_NOCOMPUTE")) v.nocompute = atoi(e);
+        if (const char *e = getenv("MCAPQ_STREAM_PDL")) v.pdl = atoi(e);
+        if (v.smem_kb < 40) v.smem_kb = 40;
+        if (v.smem_kb > 226) v.smem_kb = 226;
+        if (v.max_stages < 2) v.max_stages = 2;
+        return v;
+    }();
+    return t;
+}
+
 size_t plan_smem(int engine, int64_t k, int ntok, StreamArgs &a)
 {
     const size_t xraw = round_up((size_t)ntok * 2 * (size_t)k, 128);
     const size_t act = round_up(act_bytes(engine, k, ntok), 128);
     const size_t fixed = 128 + xraw + act + kRedBytes;
-    const size_t budget = 112 * 1024;
+    const size_t budget = (size_t)tune().smem_kb * 1024;
     int S = (int)(((long)budget - (long)fixed - 1024) / kStageBytes);
-    S = S < 2 ? 2 : (S > 6 ? 6 : S);
+    S = S < 2 ? 2 : (S > tune().max_stages ? tune().max_stages : S);
     a.stages = S;
     a.xraw_off = (int)((size_t)S * kStageBytes + 128);
     a.act_off = (int)(a.xraw_off + xraw);
@@ -332,11 +359,14 @@ cudaError_t launch_stream_group(int route, const StreamGroup &g, const uint16_t 
     a.ydt = ydt;
     const int sms = device_sms();
     const int tp = stream_tokens_per_pass(route, g.k);
+    pdl = pdl || tune().pdl;
     for (int64_t tok0 = 0; tok0 < m; tok0 += tp) {
         a.tok0 = tok0;
         a.ntok = (int)((m - tok0) < tp ? (m - tok0) : tp);
         cudaError_t e;
-        if (route == MCAPQ_W4A16)
+        if (tune().nocompute)
+            e = launch_one<NONE>(a, s, pdl, sms);
+        else if (route == MCAPQ_W4A16)
             e = launch_one<HMMA>(a, s, pdl, sms);
         else if (a.ntok == 1)
             e = launch_one<DP4A>(a, s, pdl, sms);

@@ -85,7 +85,7 @@ __global__ void __launch_bounds__(kThreads, 1) stream_linear(const __grid_consta
             bulk_g2s(xraw + (uint32_t)(i * 2 * k), a.x + (a.tok0 + i) * a.ldx, (uint32_t)(2 * k), xbar);
     }
     mbar_wait(xbar, 0);
-    const uint32_t tsz = (E == HMMA) ? (uint32_t)(2 * k + 64) : (uint32_t)(k + 16);
+    const uint32_t tsz = (E == HMMA || E == NONE) ? (uint32_t)(2 * k + 64) : (uint32_t)(k + 16);
     const uint32_t sx_s = act + (uint32_t)ntok * tsz;                    // [ntok][G] fp32
     const uint32_t sq_s = sx_s + 4u * (uint32_t)(ntok * G);              // [ntok][G] int32
     if constexpr (E == DP4A || E == IMMA) {
@@ -144,7 +144,9 @@ __global__ void __launch_bounds__(kThreads, 1) stream_linear(const __grid_consta
             mbar_wait(full + 8u * s, ph);
             const uint32_t st = ring + (uint32_t)s * kStageBytes;
 
-            if constexpr (E == DP4A) {
+            if constexpr (E == NONE) {
+                // bandwidth probe: drain the stage without computing
+            } else if constexpr (E == DP4A) {
                 // warp w: row w of the tile; lane l: blocks l and l+32 of the chunk (in that order)
                 const int r = warp;
                 if (nblk == kChunkBlocks) {
