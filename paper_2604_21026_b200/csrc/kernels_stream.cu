@@ -89,6 +89,15 @@ __device__ __forceinline__ void tma_2d(uint32_t dst, const CUtensorMap *map, int
         "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(bar), "l"(policy)
         : "memory");
 }
+__device__ __forceinline__ void tma_3d(uint32_t dst, const CUtensorMap *map, int x, int y, int z, uint32_t bar,
+                                       uint64_t policy)
+{
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint"
+        " [%0], [%1, {%2, %3, %4}], [%5], %6;" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(z), "r"(bar), "l"(policy)
+        : "memory");
+}
 __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void *src, uint32_t bytes, uint32_t bar)
 {
     asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
@@ -235,11 +244,14 @@ bool encode_maps(CUtensorMap *tn, CUtensorMap *ts, const uint8_t *nib, const uin
 {
     EncodeTiledFn fn = encode_fn();
     if (!fn) return false;
-    const cuuint64_t nd[2] = {(cuuint64_t)(k / 2), (cuuint64_t)n};
-    const cuuint64_t ns[1] = {(cuuint64_t)(k / 2)};
-    const cuuint32_t nbox[2] = {128, kTileRows};
-    const cuuint32_t es[2] = {1, 1};
-    if (fn(tn, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<uint8_t *>(nib), nd, ns, nbox, es,
+    // nibbles as a 3-D view {128 B column slice, row, 128-B column}: one box
+    // {128, 16 rows, 8 columns} = one 16 KiB stage, landing in smem as [column][row][128 B]
+    // with the 128-B swizzle keyed by the row (the layout nib_off() reads).
+    const cuuint64_t nd[3] = {128, (cuuint64_t)n, (cuuint64_t)(k / 256)};
+    const cuuint64_t ns[2] = {(cuuint64_t)(k / 2), 128};
+    const cuuint32_t nbox[3] = {128, kTileRows, 8};
+    const cuuint32_t es[3] = {1, 1, 1};
+    if (fn(tn, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<uint8_t *>(nib), nd, ns, nbox, es,
            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
         return false;

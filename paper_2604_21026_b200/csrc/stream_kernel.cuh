@@ -58,13 +58,11 @@ __global__ void __launch_bounds__(kThreads, 1) stream_linear(const __grid_consta
                 const int row0 = (tile - a.tile_start[li]) * kTileRows;
                 for (int ch = 0; ch < nchunks; ++ch) {
                     mbar_wait(empty + 8u * s, ph ^ 1u);
-                    const int rem = K2 - ch * kChunkBytes;
-                    const int nbox = (rem < kChunkBytes ? rem : kChunkBytes) / 128;
                     const uint32_t st = ring + (uint32_t)s * kStageBytes;
                     const uint32_t fb = full + 8u * s;
-                    mbar_expect_tx(fb, (uint32_t)(nbox + 1) * kBox);
-                    for (int b = 0; b < nbox; ++b)
-                        tma_2d(st + b * kBox, &a.tm_nib[li], ch * kChunkBytes + b * 128, row0, fb, pol);
+                    // full boxes always: TMA zero-fills rows past N / columns past K and counts them
+                    mbar_expect_tx(fb, (uint32_t)kStageBytes);
+                    tma_3d(st, &a.tm_nib[li], 0, row0, ch * 8, fb, pol);
                     tma_2d(st + 8 * kBox, &a.tm_scale[li], ch * kChunkBlocks, row0, fb, pol);
                     if (++s == S) {
                         s = 0;
