@@ -210,6 +210,29 @@ __device__ __forceinline__ void dequant_bf16(uint32_t w, uint32_t p[4])
     asm("fma.rn.bf16x2 %0, %1, %2, %3;" : "=r"(p[3]) : "r"(hi1), "r"(one), "r"(m136));
 }
 
+// W4A16 A fragment as 128 + c (exact bf16): one LOP3 (+ one shift) per pair, no
+// per-element subtract -- the -136 (= -128 offset - 8 zero point) enters through
+// the MMA accumulator init (kernel: corr = -136 * sum x).  Element order per
+// thread t: p0 = (4t, 4t+2)  p1 = (4t+16, 4t+18)  p2 = (4t+1, 4t+3)  p3 = (4t+17, 4t+19).
+__device__ __forceinline__ void magic_bf16(uint32_t w, uint32_t p[4])
+{
+    const uint32_t magic = 0x43004300u;   // bf16x2 (128, 128)
+    p[0] = (w & 0x000F000Fu) | magic;
+    p[1] = ((w >> 4) & 0x000F000Fu) | magic;
+    p[2] = ((w >> 8) & 0x000F000Fu) | magic;
+    p[3] = ((w >> 12) & 0x000F000Fu) | magic;
+}
+
+// D = A.B + C with an explicit accumulator init (C may repeat registers).
+__device__ __forceinline__ void hmma_c(uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3, uint32_t b0, uint32_t b1,
+                                       float c0, float c1, float c2, float c3, float d[4])
+{
+    asm volatile(
+        "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%10,%11,%12,%13};"
+        : "=f"(d[0]), "=f"(d[1]), "=f"(d[2]), "=f"(d[3])
+        : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1), "f"(c0), "f"(c1), "f"(c2), "f"(c3));
+}
+
 __device__ __forceinline__ void hmma(uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3, uint32_t b0, uint32_t b1,
                                      float c[4])
 {
@@ -266,7 +289,7 @@ bool encode_maps(CUtensorMap *tn, CUtensorMap *ts, const uint8_t *nib, const uin
 size_t act_bytes(int engine, int64_t k, int ntok)
 {
     const int64_t G = k / 32;
-    if (engine == HMMA || engine == NONE) return (size_t)ntok * (size_t)(2 * k + 64);
+    if (engine == HMMA || engine == NONE) return (size_t)ntok * (size_t)(2 * k + 64) + 32 * (size_t)G;
     return (size_t)ntok * (size_t)(k + 16) + (size_t)ntok * 8 * (size_t)G;
 }
 

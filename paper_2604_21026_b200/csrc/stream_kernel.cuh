@@ -1,13 +1,14 @@
 // stream_kernel.cuh -- the persistent TMA-fed decode-linear kernel (included by
 // kernels_stream.cu, which holds the PTX helpers, fragments and host launch).
 //
-// Shared memory (dynamic, 1024-B aligned base sb; all offsets 32-bit shared
+// Shared memory (dynamic, 1024-B aligned base sb; all offsets are 32-bit shared
 // addresses):  ring [S x 18 KiB] | full[S] empty[S] xbar | x raw | activations | reduction
 // Activation layouts (per token, tsz bytes apart):
 //  W4A8 : q_lo [G][16] | q_hi [G][16] | 16 B pad   (q_lo = elements 0..15 of each
 //         32-group, q_hi = 16..31: lane-per-block LDS.128 are consecutive), then
 //         sx [ntok][G] fp32 and sq [ntok][G] int32 after all tokens.
-//  W4A16: [G][4 t][8 bf16] in fragment order (4t,4t+2,4t+1,4t+3,4t+16,4t+18,4t+17,4t+19) | 64 B pad.
+//  W4A16: [G][4 t][8 bf16] in fragment order (4t,4t+2,4t+1,4t+3,4t+16,4t+18,4t+17,4t+19) | 64 B pad,
+//         then corr [G][8 tokens] fp32 = -136 * sum_j x_j of the group (see HMMA below).
 #pragma once
 
 template <int E>
@@ -83,32 +84,61 @@ __global__ void __launch_bounds__(kThreads, 1) stream_linear(const __grid_consta
             bulk_g2s(xraw + (uint32_t)(i * 2 * k), a.x + (a.tok0 + i) * a.ldx, (uint32_t)(2 * k), xbar);
     }
     mbar_wait(xbar, 0);
-    const uint32_t tsz = (E == HMMA || E == NONE) ? (uint32_t)(2 * k + 64) : (uint32_t)(k + 16);
-    const uint32_t sx_s = act + (uint32_t)ntok * tsz;                    // [ntok][G] fp32
-    const uint32_t sq_s = sx_s + 4u * (uint32_t)(ntok * G);              // [ntok][G] int32
-    if constexpr (E == DP4A || E == IMMA) {
-        // per-token, per-32-group quantisation: identical arithmetic to quant_a8_kernel
-        const int groups = ntok * G;
-        for (int grp = warp; grp < groups; grp += kConsumerWarps) {
-            const int i = grp / G, g = grp - i * G;
-            const float v = dev::bf16_bits_to_float(lds16(xraw + 2u * (uint32_t)(i * k + 32 * g + lane)));
-            const bool finite = __all_sync(0xffffffffu, isfinite(v));
-            const float amax = __uint_as_float(__reduce_max_sync(0xffffffffu, __float_as_uint(fabsf(v))));
+    constexpr bool kA16 = (E == HMMA || E == NONE);
+    const uint32_t tsz = kA16 ? (uint32_t)(2 * k + 64) : (uint32_t)(k + 16);
+    const uint32_t sx_s = act + (uint32_t)ntok * tsz;                    // W4A8: [ntok][G] fp32
+    const uint32_t sq_s = sx_s + 4u * (uint32_t)(ntok * G);              // W4A8: [ntok][G] int32
+    const uint32_t corr_s = act + (uint32_t)ntok * tsz;                  // W4A16: [G][8] fp32
+    if constexpr (!kA16) {
+        // Per-token, per-32-group quantisation, one thread per group:
+        // the same IEEE operations as quant_a8_kernel (exact max, __fdiv_rn, roundf,
+        // clamp, exact int sum), so q / s / sum q are bit-identical.
+        for (int idx = threadIdx.x; idx < ntok * G; idx += kConsumerWarps * 32) {
+            const int i = idx / G, g = idx - i * G;
+            const uint32_t src = xraw + 2u * (uint32_t)(i * k + 32 * g);
+            float v[32];
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                const uint4 u = lds128(src + 16u * c);
+                const uint32_t w4[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    v[8 * c + 2 * e] = __uint_as_float(w4[e] << 16);
+                    v[8 * c + 2 * e + 1] = __uint_as_float(w4[e] & 0xffff0000u);
+                }
+            }
+            float amax = 0.0f;
+            bool finite = true;
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+                finite = finite && isfinite(v[j]);
+                amax = fmaxf(amax, fabsf(v[j]));
+            }
             const float s = __fdiv_rn(amax, 127.0f);
-            int code = 0;
             const bool live = finite && s != 0.0f;
-            if (live) {
-                float r = roundf(__fdiv_rn(v, s));
-                r = fminf(fmaxf(r, -127.0f), 127.0f);
-                code = (int)r;
+            uint32_t pk[8];
+            int sum = 0;
+#pragma unroll
+            for (int j4 = 0; j4 < 8; ++j4) {
+                uint32_t word = 0;
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    int code = 0;
+                    if (live) {
+                        float r = roundf(__fdiv_rn(v[4 * j4 + e], s));
+                        r = fminf(fmaxf(r, -127.0f), 127.0f);
+                        code = (int)r;
+                    }
+                    sum += code;
+                    word |= ((uint32_t)code & 0xffu) << (8 * e);
+                }
+                pk[j4] = word;
             }
             const uint32_t qt = act + (uint32_t)i * tsz;
-            sts8(qt + (lane < 16 ? 16u * g + lane : (uint32_t)K2 + 16u * g + lane - 16u), (uint32_t)code & 0xffu);
-            const int sum = __reduce_add_sync(0xffffffffu, code);
-            if (lane == 0) {
-                sts32(sx_s + 4u * (uint32_t)(i * G + g), __float_as_uint(live ? s : 0.0f));
-                sts32(sq_s + 4u * (uint32_t)(i * G + g), (uint32_t)sum);
-            }
+            sts128(qt + 16u * g, make_uint4(pk[0], pk[1], pk[2], pk[3]));
+            sts128(qt + (uint32_t)K2 + 16u * g, make_uint4(pk[4], pk[5], pk[6], pk[7]));
+            sts32(sx_s + 4u * (uint32_t)(i * G + g), __float_as_uint(live ? s : 0.0f));
+            sts32(sq_s + 4u * (uint32_t)(i * G + g), (uint32_t)sum);
         }
     } else {
         for (int idx = threadIdx.x; idx < ntok * G * 4; idx += kConsumerWarps * 32) {
@@ -123,12 +153,32 @@ __global__ void __launch_bounds__(kThreads, 1) stream_linear(const __grid_consta
             o.w = __byte_perm(hi.x, hi.y, 0x7632);
             sts128(act + (uint32_t)tk * tsz + 64u * g + 16u * tt, o);
         }
+        // corr[g][tok] = -136 * sum of the group's x in fp32, fixed order (tokens >= ntok: 0)
+        for (int idx = threadIdx.x; idx < G * 8; idx += kConsumerWarps * 32) {
+            const int g = idx >> 3, tk = idx & 7;
+            float sum = 0.0f;
+            if (tk < ntok) {
+                const uint32_t src = xraw + 2u * (uint32_t)(tk * k + 32 * g);
+#pragma unroll
+                for (int c = 0; c < 4; ++c) {
+                    const uint4 u = lds128(src + 16u * c);
+                    const uint32_t w4[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        sum += __uint_as_float(w4[e] << 16);
+                        sum += __uint_as_float(w4[e] & 0xffff0000u);
+                    }
+                }
+            }
+            sts32(corr_s + 4u * (uint32_t)idx, __float_as_uint(-136.0f * sum));
+        }
     }
     bar_consumers();
 
     // ================= consumers: main loop =================
     const int gid = lane >> 2, t = lane & 3;
     const int mrow = (lane & 7) + ((lane >> 3) & 1) * 8;    // ldmatrix row of this lane
+    const int mhalf = lane >> 4;                             // ldmatrix: lanes 16-31 address the 2nd block
     int s = 0;
     uint32_t ph = 0;
     int li = 0;
@@ -180,20 +230,23 @@ __global__ void __launch_bounds__(kThreads, 1) stream_linear(const __grid_consta
                     }
                 }
             } else {
-                for (int b = warp; b < nblk; b += 2 * kConsumerWarps) {
-                    const int b2 = b + kConsumerWarps;
-                    const bool two = b2 < nblk;
-                    const int mblk = ((lane >> 4) && two) ? b2 : b;
-                    uint32_t wa0, wb0, wa1, wb1;
-                    ldmatrix_x4(st + nib_off(mrow, mblk), wa0, wb0, wa1, wb1);
+                // warp w: blocks 4w .. 4w+3 of the chunk (contiguous; in that order) for all 16 rows
+                const int bq = 4 * warp;
+                if (bq < nblk) {
+                    uint32_t wv[8];   // [block j][row half]: wa(j) = wv[2j], wb(j) = wv[2j+1]
+                    ldmatrix_x4(st + nib_off(mrow, bq + mhalf), wv[0], wv[1], wv[2], wv[3]);
+                    ldmatrix_x4(st + nib_off(mrow, bq + 2 + mhalf), wv[4], wv[5], wv[6], wv[7]);
+                    // scales of rows gid / gid+8 for the 4 blocks: one 8-byte load each
+                    const uint2 sa = lds64(st + scale_off(gid, bq));
+                    const uint2 sbb = lds64(st + scale_off(gid + 8, bq));
+                    const float dA[4] = {h2f((uint16_t)(sa.x & 0xffff)), h2f((uint16_t)(sa.x >> 16)),
+                                         h2f((uint16_t)(sa.y & 0xffff)), h2f((uint16_t)(sa.y >> 16))};
+                    const float dB[4] = {h2f((uint16_t)(sbb.x & 0xffff)), h2f((uint16_t)(sbb.x >> 16)),
+                                         h2f((uint16_t)(sbb.y & 0xffff)), h2f((uint16_t)(sbb.y >> 16))};
 #pragma unroll
-                    for (int u = 0; u < 2; ++u) {
-                        if (u == 1 && !two) break;
-                        const int bb = u ? b2 : b;
-                        const uint32_t wa = u ? wa1 : wa0, wb = u ? wb1 : wb0;
-                        const float da = h2f(lds16(st + scale_off(gid, bb)));
-                        const float db = h2f(lds16(st + scale_off(gid + 8, bb)));
-                        const int g = blk0 + bb;
+                    for (int j = 0; j < 4; ++j) {
+                        const uint32_t wa = wv[2 * j], wb = wv[2 * j + 1];
+                        const int g = blk0 + bq + j;
                         if constexpr (E == IMMA) {
                             uint32_t b0 = 0, b1 = 0;
                             if (gid < ntok) {
@@ -208,23 +261,30 @@ __global__ void __launch_bounds__(kThreads, 1) stream_linear(const __grid_consta
                             const float s1 = c1 < ntok ? __uint_as_float(lds32(sx_s + 4u * (c1 * G + g))) : 0.f;
                             const int q0 = c0 < ntok ? (int)lds32(sq_s + 4u * (c0 * G + g)) : 0;
                             const int q1 = c1 < ntok ? (int)lds32(sq_s + 4u * (c1 * G + g)) : 0;
-                            acc[0] = fmaf(da * s0, (float)(c[0] - 8 * q0), acc[0]);
-                            acc[1] = fmaf(da * s1, (float)(c[1] - 8 * q1), acc[1]);
-                            acc[2] = fmaf(db * s0, (float)(c[2] - 8 * q0), acc[2]);
-                            acc[3] = fmaf(db * s1, (float)(c[3] - 8 * q1), acc[3]);
+                            acc[0] = fmaf(dA[j] * s0, (float)(c[0] - 8 * q0), acc[0]);
+                            acc[1] = fmaf(dA[j] * s1, (float)(c[1] - 8 * q1), acc[1]);
+                            acc[2] = fmaf(dB[j] * s0, (float)(c[2] - 8 * q0), acc[2]);
+                            acc[3] = fmaf(dB[j] * s1, (float)(c[3] - 8 * q1), acc[3]);
                         } else {
+                            // A = 128 + c (exact bf16, no per-element subtract); the -8 zero point
+                            // and the +128 offset enter through the accumulator init
+                            // C = -136 * sum_j x_j, so D = sum_j (c_j - 8) x_j.
                             uint4 bx = make_uint4(0, 0, 0, 0);
                             if (gid < ntok) bx = lds128(act + (uint32_t)gid * tsz + 64u * g + 16u * t);
+                            const uint2 cru = lds64(corr_s + 32u * g + 8u * t);
+                            const float2 cr = make_float2(__uint_as_float(cru.x), __uint_as_float(cru.y));
                             uint32_t pa[4], pb[4];
-                            dequant_bf16(wa, pa);
-                            dequant_bf16(wb, pb);
-                            float c[4] = {0.f, 0.f, 0.f, 0.f};
-                            hmma(pa[0], pb[0], pa[2], pb[2], bx.x, bx.y, c);
+                            magic_bf16(wa, pa);
+                            magic_bf16(wb, pb);
+                            float c[4];
+                            hmma_c(pa[0], pb[0], pa[2], pb[2], bx.x, bx.y, cr.x, cr.y, cr.x, cr.y, c);
                             hmma(pa[1], pb[1], pa[3], pb[3], bx.z, bx.w, c);
-                            acc[0] = fmaf(da, c[0], acc[0]);
-                            acc[1] = fmaf(da, c[1], acc[1]);
-                            acc[2] = fmaf(db, c[2], acc[2]);
-                            acc[3] = fmaf(db, c[3], acc[3]);
+                            acc[0] = fmaf(dA[j], c[0], acc[0]);
+                            acc[2] = fmaf(dB[j], c[2], acc[2]);
+                            if (ntok > 1) {
+                                acc[1] = fmaf(dA[j], c[1], acc[1]);
+                                acc[3] = fmaf(dB[j], c[3], acc[3]);
+                            }
                         }
                     }
                 }

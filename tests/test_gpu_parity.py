@@ -292,10 +292,10 @@ def test_stack_matches_oracle_and_graph_replay(mq, orc, kind):
             w = si.weight(n, k, si.seed_for(2, l, slot))
             key = (l, inputs[slot])
             if key not in xs:
-                xs[key] = si.activation(2, k, si.seed_for(2, l, slot, True), si.activation_kind(slot))
-            x = xs[key]
+                xa = si.activation(2, k, si.seed_for(2, l, slot, True), si.activation_kind(slot))
+                xs[key] = (xa, xa.to(DEV))     # slots sharing an input share the device tensor
+            x, xd = xs[key]
             pw = mq.pack_w4(w.to(DEV))
-            xd = x.to(DEV)
             y = torch.empty(2, n, dtype=torch.bfloat16, device=DEV)
             st.set(l, slot_id, inputs[slot], pw, xd, y)
             ref.append((l, y, w, x))
