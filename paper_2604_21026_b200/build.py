@@ -49,7 +49,7 @@ def _sources():
 
 
 def _headers():
-    return sorted(glob.glob(str(CSRC / "*.h")) + [str(INCLUDE / "mcapq.h")])
+    return sorted(glob.glob(str(CSRC / "*.h")) + glob.glob(str(CSRC / "*.cuh")) + [str(INCLUDE / "mcapq.h")])
 
 
 def _compile(src: str, nccl_inc: str) -> tuple[str, str]:

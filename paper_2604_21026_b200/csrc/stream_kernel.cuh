@@ -90,55 +90,64 @@ __global__ void __launch_bounds__(kThreads, 1) stream_linear(const __grid_consta
     const uint32_t sq_s = sx_s + 4u * (uint32_t)(ntok * G);              // W4A8: [ntok][G] int32
     const uint32_t corr_s = act + (uint32_t)ntok * tsz;                  // W4A16: [G][8] fp32
     if constexpr (!kA16) {
-        // Per-token, per-32-group quantisation, one thread per group:
-        // the same IEEE operations as quant_a8_kernel (exact max, __fdiv_rn, roundf,
-        // clamp, exact int sum), so q / s / sum q are bit-identical.
-        for (int idx = threadIdx.x; idx < ntok * G; idx += kConsumerWarps * 32) {
-            const int i = idx / G, g = idx - i * G;
-            const uint32_t src = xraw + 2u * (uint32_t)(i * k + 32 * g);
-            float v[32];
+        // Per-token, per-32-group quantisation, a quad of threads per
+        // group (8 elements each): the same IEEE operations as quant_a8_kernel
+        // (exact max, __fdiv_rn, roundf, clamp, exact int sum), so q / s / sum q are
+        // bit-identical.  All lanes of a warp run the same trip count (quad shuffles).
+        const int nq = ntok * G * 4;
+        for (int base = 0; base < nq; base += kConsumerWarps * 32) {
+            const int idx = base + threadIdx.x;
+            const bool on = idx < nq;
+            const int grp = on ? (idx >> 2) : 0, sub = idx & 3;
+            const int i = grp / G, g = grp - i * G;
+            const uint4 u = lds128(xraw + 2u * (uint32_t)(i * k + 32 * g + 8 * sub));
+            const uint32_t w4[4] = {u.x, u.y, u.z, u.w};
+            float v[8];
 #pragma unroll
-            for (int c = 0; c < 4; ++c) {
-                const uint4 u = lds128(src + 16u * c);
-                const uint32_t w4[4] = {u.x, u.y, u.z, u.w};
-#pragma unroll
-                for (int e = 0; e < 4; ++e) {
-                    v[8 * c + 2 * e] = __uint_as_float(w4[e] << 16);
-                    v[8 * c + 2 * e + 1] = __uint_as_float(w4[e] & 0xffff0000u);
-                }
+            for (int e = 0; e < 4; ++e) {
+                v[2 * e] = __uint_as_float(w4[e] << 16);
+                v[2 * e + 1] = __uint_as_float(w4[e] & 0xffff0000u);
             }
             float amax = 0.0f;
-            bool finite = true;
+            int fin = 1;
 #pragma unroll
-            for (int j = 0; j < 32; ++j) {
-                finite = finite && isfinite(v[j]);
+            for (int j = 0; j < 8; ++j) {
+                fin &= isfinite(v[j]) ? 1 : 0;
                 amax = fmaxf(amax, fabsf(v[j]));
             }
+            amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, 1));
+            amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, 2));
+            fin &= __shfl_xor_sync(0xffffffffu, fin, 1);
+            fin &= __shfl_xor_sync(0xffffffffu, fin, 2);
             const float s = __fdiv_rn(amax, 127.0f);
-            const bool live = finite && s != 0.0f;
-            uint32_t pk[8];
+            const bool live = fin && s != 0.0f;
+            uint32_t lo = 0, hi = 0;
             int sum = 0;
 #pragma unroll
-            for (int j4 = 0; j4 < 8; ++j4) {
-                uint32_t word = 0;
-#pragma unroll
-                for (int e = 0; e < 4; ++e) {
-                    int code = 0;
-                    if (live) {
-                        float r = roundf(__fdiv_rn(v[4 * j4 + e], s));
-                        r = fminf(fmaxf(r, -127.0f), 127.0f);
-                        code = (int)r;
-                    }
-                    sum += code;
-                    word |= ((uint32_t)code & 0xffu) << (8 * e);
+            for (int j = 0; j < 8; ++j) {
+                int code = 0;
+                if (live) {
+                    float r = roundf(__fdiv_rn(v[j], s));
+                    r = fminf(fmaxf(r, -127.0f), 127.0f);
+                    code = (int)r;
                 }
-                pk[j4] = word;
+                sum += code;
+                if (j < 4)
+                    lo |= ((uint32_t)code & 0xffu) << (8 * j);
+                else
+                    hi |= ((uint32_t)code & 0xffu) << (8 * (j - 4));
             }
-            const uint32_t qt = act + (uint32_t)i * tsz;
-            sts128(qt + 16u * g, make_uint4(pk[0], pk[1], pk[2], pk[3]));
-            sts128(qt + (uint32_t)K2 + 16u * g, make_uint4(pk[4], pk[5], pk[6], pk[7]));
-            sts32(sx_s + 4u * (uint32_t)(i * G + g), __float_as_uint(live ? s : 0.0f));
-            sts32(sq_s + 4u * (uint32_t)(i * G + g), (uint32_t)sum);
+            sum += __shfl_xor_sync(0xffffffffu, sum, 1);
+            sum += __shfl_xor_sync(0xffffffffu, sum, 2);
+            if (on) {
+                // elements 8sub..8sub+7: sub 0/1 -> q_lo, sub 2/3 -> q_hi
+                const uint32_t qt = act + (uint32_t)i * tsz + (sub < 2 ? 0u : (uint32_t)K2) + 16u * g + 8u * (sub & 1);
+                asm volatile("st.shared.v2.u32 [%0], {%1,%2};" ::"r"(qt), "r"(lo), "r"(hi) : "memory");
+                if (sub == 0) {
+                    sts32(sx_s + 4u * (uint32_t)(i * G + g), __float_as_uint(live ? s : 0.0f));
+                    sts32(sq_s + 4u * (uint32_t)(i * G + g), (uint32_t)sum);
+                }
+            }
         }
     } else {
         for (int idx = threadIdx.x; idx < ntok * G * 4; idx += kConsumerWarps * 32) {
