@@ -12,7 +12,9 @@
 #pragma once
 
 template <int E>
-__global__ void __launch_bounds__(kThreads, 1) stream_linear(const __grid_constant__ StreamArgs a)
+// 2 CTAs per SM (<= 60 registers, <= ~113 KB smem): under PDL the next linear's CTA
+// becomes resident beside this one and starts its weight stream early.
+__global__ void __launch_bounds__(kThreads, 2) stream_linear(const __grid_constant__ StreamArgs a)
 {
     extern __shared__ __align__(16) uint8_t smem_raw[];
     const uint32_t sraw = smem_addr(smem_raw);
