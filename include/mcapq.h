@@ -196,6 +196,15 @@ mcapq_status mcapq_linear_host(int route, const uint8_t *nib, const uint16_t *sc
 mcapq_status mcapq_w4a8_group_dots(const uint8_t *nib, int64_t n, int64_t k, const int8_t *q, const int32_t *sq,
                                    int64_t m, int32_t *D, int mode, void *stream);
 
+/*
+ * DEBUG: per-CTA timeline of the stream kernels, recorded only when the
+ * environment has MCAPQ_STREAM_TRACE=1 at library load.  Copies up to
+ * max_records records of 8 uint64 {launch id, block, t_start, t_after_wait,
+ * t_activations_ready, t_end, 0, 0} (%globaltimer ns) into host memory;
+ * synchronises the device.  Returns the number of records.
+ */
+size_t mcapq_debug_stream_trace(uint64_t *host_out, size_t max_records);
+
 /* ------------------------------------------------------ dispatch table (a7) */
 /*
  * MCAP profile -> per-layer routes.  Alg. 1 lines 8-13, P:840-846,

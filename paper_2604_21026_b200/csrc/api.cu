@@ -106,6 +106,12 @@ const char *mcapq_status_string(int s)
 
 int mcapq_device_sms(void) { return device_sms(); }
 
+size_t mcapq_debug_stream_trace(uint64_t *host_out, size_t max_records)
+{
+    if (!host_out) return 0;
+    return stream_trace_read(reinterpret_cast<unsigned long long *>(host_out), max_records);
+}
+
 size_t mcapq_w4_nib_bytes(int64_t n, int64_t k) { return (n > 0 && k > 0) ? (size_t)(n * (k / 2)) : 0; }
 size_t mcapq_w4_scale_bytes(int64_t n, int64_t k) { return (n > 0 && k > 0) ? (size_t)(n * (k / 32) * 2) : 0; }
 

@@ -158,6 +158,12 @@ __device__ __forceinline__ float h2f(uint16_t h)
     asm("cvt.f32.f16 %0, %1;" : "=f"(f) : "h"(h));
     return f;
 }
+__device__ __forceinline__ unsigned long long globaltimer()
+{
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
 __device__ __forceinline__ void bar_consumers() { asm volatile("bar.sync 1, %0;" ::"n"(kConsumerWarps * 32) : "memory"); }
 
 // 128-B swizzle of a {128 B x 16 rows} box: 16-B chunk c of row r sits at c ^ (r & 7).
@@ -304,7 +310,7 @@ size_t round_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 //   MCAPQ_STREAM_NOCOMPUTE 1 = consumers only drain the ring (bandwidth probe; outputs garbage)
 //   MCAPQ_STREAM_PDL       1 = API calls also launch with programmatic dependent launch
 struct Tune {
-    int smem_kb = 112, max_stages = 12, nocompute = 0, pdl = 0;
+    int smem_kb = 112, max_stages = 12, nocompute = 0, pdl = 0, trace = 0;
 };
 const Tune &tune()
 {
@@ -314,6 +320,7 @@ const Tune &tune()
         if (const char *e = getenv("MCAPQ_STREAM_STAGES")) v.max_stages = atoi(e);
         if (const char *e = getenv("MCAPQ_STREAM_NOCOMPUTE")) v.nocompute = atoi(e);
         if (const char *e = getenv("MCAPQ_STREAM_PDL")) v.pdl = atoi(e);
+        if (const char *e = getenv("MCAPQ_STREAM_TRACE")) v.trace = atoi(e);
         if (v.smem_kb < 40) v.smem_kb = 40;
         if (v.smem_kb > 226) v.smem_kb = 226;
         if (v.max_stages < 2) v.max_stages = 2;
@@ -321,6 +328,10 @@ const Tune &tune()
     }();
     return t;
 }
+
+unsigned long long *g_trace = nullptr;   // debug timeline buffer (MCAPQ_STREAM_TRACE)
+size_t g_trace_used = 0;
+int g_trace_launches = 0;
 
 size_t plan_smem(int engine, int64_t k, int ntok, StreamArgs &a)
 {
@@ -350,10 +361,34 @@ cudaError_t launch_one(StreamArgs &a, cudaStream_t s, bool pdl, int sms)
     const int T = a.tile_start[a.count];
     const int grid = T < sms ? T : sms;
     if (grid == 0) return cudaSuccess;
+    a.trace = nullptr;
+    if (tune().trace) {
+        // debug timeline: one 8 x u64 record per CTA, bump-allocated per launch (wraps)
+        constexpr size_t kCap = 1u << 20;
+        if (!g_trace) {
+            if (cudaMalloc(&g_trace, kCap * 64) != cudaSuccess) g_trace = nullptr;
+            else cudaMemset(g_trace, 0, kCap * 64);
+        }
+        if (g_trace) {
+            if (g_trace_used + (size_t)grid > kCap) g_trace_used = 0;
+            a.trace = g_trace + 8 * g_trace_used;
+            a.launch_id = g_trace_launches++;
+            g_trace_used += (size_t)grid;
+        }
+    }
     return launch_pdl(stream_linear<E>, dim3(grid), dim3(kThreads), smem, s, pdl, a);
 }
 
 }  // namespace
+
+size_t stream_trace_read(unsigned long long *host_out, size_t max_records)
+{
+    if (!g_trace) return 0;
+    const size_t n = g_trace_used < max_records ? g_trace_used : max_records;
+    if (cudaDeviceSynchronize() != cudaSuccess) return 0;
+    if (cudaMemcpy(host_out, g_trace, n * 64, cudaMemcpyDeviceToHost) != cudaSuccess) return 0;
+    return n;
+}
 
 bool stream_supported(int64_t k) { return k >= 2048 && k % 256 == 0 && encode_fn() != nullptr; }
 

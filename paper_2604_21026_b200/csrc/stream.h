@@ -39,7 +39,14 @@ struct alignas(64) StreamArgs {
     int act_off;     // byte offset of the activation area in dynamic smem
     int red_off;     // byte offset of the reduction area
     int xraw_off;    // byte offset of the raw x staging area
+    unsigned long long *trace;   // debug timeline (MCAPQ_STREAM_TRACE): 8 u64 per CTA, or null
+    int launch_id;
 };
+
+// Debug timeline (MCAPQ_STREAM_TRACE=1): per CTA {launch, block, t_start, t_wait,
+// t_ready, t_end, 0, 0} from %globaltimer (ns).  Returns the number of records
+// copied into host_out (<= max_records).
+size_t stream_trace_read(unsigned long long *host_out, size_t max_records);
 
 // K % 256 == 0 (16-B aligned scale rows for the tensor maps) and 16-B aligned planes.
 bool stream_supported(int64_t k);

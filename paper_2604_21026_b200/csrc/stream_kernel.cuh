@@ -48,6 +48,8 @@ __global__ void __launch_bounds__(kThreads, 2) stream_linear(const __grid_consta
     }
     __syncthreads();
     dev::griddep_launch();   // the next linear may launch: it only touches weights until its own wait
+    unsigned long long tr_start = 0, tr_wait = 0, tr_ready = 0;
+    if (a.trace) tr_start = globaltimer();
 
     if (warp == kConsumerWarps) {
         // ================= producer =================
@@ -79,6 +81,7 @@ __global__ void __launch_bounds__(kThreads, 2) stream_linear(const __grid_consta
 
     // ================= consumers: stage activations =================
     dev::griddep_wait();
+    if (a.trace) tr_wait = globaltimer();
     const int ntok = a.ntok;
     if (threadIdx.x == 0) {
         mbar_expect_tx(xbar, (uint32_t)(ntok * 2 * k));
@@ -185,6 +188,7 @@ __global__ void __launch_bounds__(kThreads, 2) stream_linear(const __grid_consta
         }
     }
     bar_consumers();
+    if (a.trace) tr_ready = globaltimer();
 
     // ================= consumers: main loop =================
     const int gid = lane >> 2, t = lane & 3;
@@ -335,5 +339,14 @@ __global__ void __launch_bounds__(kThreads, 2) stream_linear(const __grid_consta
             }
             bar_consumers();
         }
+    }
+    if (a.trace && threadIdx.x == 0) {
+        unsigned long long *r = a.trace + 8ull * (unsigned long long)blockIdx.x;
+        r[0] = (unsigned long long)a.launch_id;
+        r[1] = blockIdx.x;
+        r[2] = tr_start;
+        r[3] = tr_wait;
+        r[4] = tr_ready;
+        r[5] = globaltimer();
     }
 }
