@@ -35,6 +35,8 @@ def main():
     st, weights, xs, ys = bench.build_stack(mq, dev, routes)
     stream = torch.cuda.Stream()
     with torch.cuda.stream(stream):
+        st.run(1, stream=stream)          # allocates the trace buffer outside the capture
+        stream.synchronize()
         st.capture(1, stream=stream)
         for _ in range(3):
             st.replay(stream=stream)
