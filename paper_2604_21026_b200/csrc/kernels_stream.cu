@@ -34,6 +34,10 @@
 // all reductions have a fixed order, so an output row is bit-identical whatever
 // N, the group, the grid or the column shard (reading A22).
 #include <cstdlib>
+#include <mutex>
+#include <unordered_map>
+#include <utility>
+#include <vector>
 
 #include "internal.h"
 #include "stream.h"
@@ -381,6 +385,64 @@ cudaError_t launch_one(StreamArgs &a, cudaStream_t s, bool pdl, int sms)
 
 }  // namespace
 
+// ------------------------------------------------------------------ descriptor table
+// Device-resident {nib, scale} tensor-map pairs, keyed by (nib, scale, n, k).
+// Entries are written once (pinned staging -> cudaMemcpyAsync, capturable) and
+// never reused, so a kernel in flight or a captured graph always sees its own.
+namespace {
+struct DescKey {
+    const void *nib, *scale;
+    int64_t n, k;
+    bool operator==(const DescKey &o) const { return nib == o.nib && scale == o.scale && n == o.n && k == o.k; }
+};
+struct DescKeyHash {
+    size_t operator()(const DescKey &d) const
+    {
+        return std::hash<const void *>()(d.nib) ^ (std::hash<const void *>()(d.scale) << 1) ^ (size_t)(d.n * 31 + d.k);
+    }
+};
+struct DescTable {
+    std::mutex mu;
+    std::unordered_map<DescKey, const CUtensorMap *, DescKeyHash> map;
+    std::vector<std::pair<CUtensorMap *, CUtensorMap *>> blocks;   // (device, pinned host)
+    int used = 0;                                                   // pairs used in the last block
+    static constexpr int kPairs = 4096;
+};
+DescTable &desc_table()
+{
+    static DescTable t;
+    return t;
+}
+}  // namespace
+
+const CUtensorMap *stream_descriptors(const uint8_t *nib, const uint16_t *scale, int64_t n, int64_t k,
+                                      cudaStream_t s)
+{
+    DescTable &t = desc_table();
+    std::lock_guard<std::mutex> lock(t.mu);
+    const DescKey key{nib, scale, n, k};
+    auto it = t.map.find(key);
+    if (it != t.map.end()) return it->second;
+    if (t.blocks.empty() || t.used == DescTable::kPairs) {
+        CUtensorMap *d = nullptr, *h = nullptr;
+        if (cudaMalloc(&d, sizeof(CUtensorMap) * 2 * DescTable::kPairs) != cudaSuccess) return nullptr;
+        if (cudaMallocHost(&h, sizeof(CUtensorMap) * 2 * DescTable::kPairs) != cudaSuccess) {
+            cudaFree(d);
+            return nullptr;
+        }
+        t.blocks.emplace_back(d, h);
+        t.used = 0;
+    }
+    CUtensorMap *dpair = t.blocks.back().first + 2 * t.used;
+    CUtensorMap *hpair = t.blocks.back().second + 2 * t.used;
+    if (!encode_maps(&hpair[0], &hpair[1], nib, scale, n, k)) return nullptr;
+    if (cudaMemcpyAsync(dpair, hpair, 2 * sizeof(CUtensorMap), cudaMemcpyHostToDevice, s) != cudaSuccess)
+        return nullptr;
+    ++t.used;
+    t.map.emplace(key, dpair);
+    return dpair;
+}
+
 size_t stream_trace_read(unsigned long long *host_out, size_t max_records)
 {
     if (!g_trace) return 0;
@@ -414,8 +476,8 @@ cudaError_t launch_stream_group(int route, const StreamGroup &g, const uint16_t 
     a.count = g.count;
     int tiles = 0;
     for (int i = 0; i < g.count; ++i) {
-        if (!encode_maps(&a.tm_nib[i], &a.tm_scale[i], g.nib[i], g.scale[i], g.n[i], g.k))
-            return cudaErrorInvalidValue;
+        a.maps[i] = stream_descriptors(g.nib[i], g.scale[i], g.n[i], g.k, s);
+        if (!a.maps[i]) return cudaErrorInvalidValue;
         a.n[i] = g.n[i];
         a.y[i] = g.y[i];
         a.ldy[i] = g.ldy[i];

@@ -95,6 +95,12 @@ mcapq_status mcapq_stack_set(mcapq_stack *st, int layer, int slot, int input_id,
     s.x = x;
     s.y = y;
     s.ydt = ydt;
+    if (stream_supported(k) && aligned16(scale)) {
+        // encode + upload this weight's TMA descriptors now, outside any graph capture
+        MCAPQ_REQUIRE(stream_descriptors(nib, scale, n, k, nullptr) != nullptr, MCAPQ_ECUDA,
+                      "TMA descriptor encode/upload failed");
+        MCAPQ_CUDA_TRY(cudaStreamSynchronize(nullptr));
+    }
     if (st->routes[layer] == MCAPQ_W4A8) return ensure_ws(st, k);
     return MCAPQ_OK;
 }

@@ -19,11 +19,13 @@ struct StreamGroup {
     int64_t ldy[kMaxGroup];
 };
 
-// Kernel parameters (passed by value as a __grid_constant__: the TMA unit reads
-// the tensor maps straight from parameter space).
-struct alignas(64) StreamArgs {
-    CUtensorMap tm_nib[kMaxGroup];     // uint8 [N][K/2], box {128 B, 16 rows}, 128B swizzle
-    CUtensorMap tm_scale[kMaxGroup];   // uint16 [N][K/32], box {64, 16 rows}, 128B swizzle
+// Kernel parameters (small: the launch rate of graph kernel nodes drops with the
+// parameter block size).  The TMA descriptors live in a device-resident table,
+// encoded once per packed weight: maps[i] -> {nib map, scale map}.
+//   nib  : uint8 3-D view {128 B, N rows, K/256 columns}, box {128, 16, 8}, 128B swizzle
+//   scale: uint16 [N][K/32], box {64, 16 rows}, 128B swizzle
+struct StreamArgs {
+    const CUtensorMap *maps[kMaxGroup];
     void *y[kMaxGroup];
     int64_t n[kMaxGroup];
     int64_t ldy[kMaxGroup];
@@ -50,6 +52,11 @@ size_t stream_trace_read(unsigned long long *host_out, size_t max_records);
 
 // K % 256 == 0 (16-B aligned scale rows for the tensor maps) and 16-B aligned planes.
 bool stream_supported(int64_t k);
+// Device pointer to the {nib, scale} tensor-map pair of a packed weight, encoding
+// and uploading it on first use (stream-ordered; capturable once the table exists).
+// Returns null on failure.
+const CUtensorMap *stream_descriptors(const uint8_t *nib, const uint16_t *scale, int64_t n, int64_t k,
+                                      cudaStream_t s);
 int stream_tokens_per_pass(int route, int64_t k);
 cudaError_t launch_stream_group(int route, const StreamGroup &g, const uint16_t *x, int64_t m, int64_t ldx,
                                 int ydt, cudaStream_t s, bool pdl);

@@ -54,6 +54,10 @@ __global__ void __launch_bounds__(kThreads, 2) stream_linear(const __grid_consta
     if (warp == kConsumerWarps) {
         // ================= producer =================
         if (lane == 0) {
+            for (int i = 0; i < a.count; ++i) {
+                asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(a.maps[i])) : "memory");
+                asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(a.maps[i] + 1)) : "memory");
+            }
             const uint64_t pol = evict_first_policy();
             int s = 0;
             uint32_t ph = 0;
@@ -67,8 +71,8 @@ __global__ void __launch_bounds__(kThreads, 2) stream_linear(const __grid_consta
                     const uint32_t fb = full + 8u * s;
                     // full boxes always: TMA zero-fills rows past N / columns past K and counts them
                     mbar_expect_tx(fb, (uint32_t)kStageBytes);
-                    tma_3d(st, &a.tm_nib[li], 0, row0, ch * 8, fb, pol);
-                    tma_2d(st + 8 * kBox, &a.tm_scale[li], ch * kChunkBlocks, row0, fb, pol);
+                    tma_3d(st, a.maps[li], 0, row0, ch * 8, fb, pol);
+                    tma_2d(st + 8 * kBox, a.maps[li] + 1, ch * kChunkBlocks, row0, fb, pol);
                     if (++s == S) {
                         s = 0;
                         ph ^= 1u;
