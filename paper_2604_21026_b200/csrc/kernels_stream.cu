@@ -162,6 +162,18 @@ __device__ __forceinline__ float h2f(uint16_t h)
     asm("cvt.f32.f16 %0, %1;" : "=f"(f) : "h"(h));
     return f;
 }
+__device__ __forceinline__ uint4 ldg_nc_128(const void *p)
+{
+    uint4 v;
+    asm volatile("ld.global.nc.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
+    return v;
+}
+__device__ __forceinline__ uint2 ldg_nc_64(const void *p)
+{
+    uint2 v;
+    asm volatile("ld.global.nc.v2.u32 {%0,%1}, [%2];" : "=r"(v.x), "=r"(v.y) : "l"(p));
+    return v;
+}
 __device__ __forceinline__ unsigned long long globaltimer()
 {
     unsigned long long t;
@@ -339,7 +351,8 @@ int g_trace_launches = 0;
 
 size_t plan_smem(int engine, int64_t k, int ntok, StreamArgs &a)
 {
-    const size_t xraw = round_up((size_t)ntok * 2 * (size_t)k, 128);
+    const size_t xraw = 0;   // x is read from global directly (no smem staging copy)
+    (void)ntok;
     const size_t act = round_up(act_bytes(engine, k, ntok), 128);
     const size_t fixed = 128 + xraw + act + kRedBytes;
     const size_t budget = (size_t)tune().smem_kb * 1024;
@@ -460,7 +473,7 @@ int stream_tokens_per_pass(int route, int64_t k)
     const int engine = route == MCAPQ_W4A16 ? HMMA : IMMA;
     int tp = 8;
     while (tp > 1) {
-        const size_t need = 1024 + 128 + round_up((size_t)tp * 2 * (size_t)k, 128) +
+        const size_t need = 1024 + 128 +
                             round_up(act_bytes(engine, k, tp), 128) + kRedBytes + 2 * (size_t)kStageBytes;
         if (need <= 112 * 1024) break;
         --tp;

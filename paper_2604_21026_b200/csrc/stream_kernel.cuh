@@ -87,12 +87,11 @@ __global__ void __launch_bounds__(kThreads, 2) stream_linear(const __grid_consta
     dev::griddep_wait();
     if (a.trace) tr_wait = globaltimer();
     const int ntok = a.ntok;
-    if (threadIdx.x == 0) {
-        mbar_expect_tx(xbar, (uint32_t)(ntok * 2 * k));
-        for (int i = 0; i < ntok; ++i)
-            bulk_g2s(xraw + (uint32_t)(i * 2 * k), a.x + (a.tok0 + i) * a.ldx, (uint32_t)(2 * k), xbar);
-    }
-    mbar_wait(xbar, 0);
+    // x is read straight from global (L2) by all consumer threads in parallel: one
+    // memory round trip, no serial copy + barrier on the dependent-kernel chain
+    const uint16_t *xg = a.x + a.tok0 * a.ldx;
+    (void)xraw;
+    (void)xbar;
     constexpr bool kA16 = (E == HMMA || E == NONE);
     const uint32_t tsz = kA16 ? (uint32_t)(2 * k + 64) : (uint32_t)(k + 16);
     const uint32_t sx_s = act + (uint32_t)ntok * tsz;                    // W4A8: [ntok][G] fp32
@@ -109,7 +108,7 @@ __global__ void __launch_bounds__(kThreads, 2) stream_linear(const __grid_consta
             const bool on = idx < nq;
             const int grp = on ? (idx >> 2) : 0, sub = idx & 3;
             const int i = grp / G, g = grp - i * G;
-            const uint4 u = lds128(xraw + 2u * (uint32_t)(i * k + 32 * g + 8 * sub));
+            const uint4 u = ldg_nc_128(xg + i * a.ldx + 32 * g + 8 * sub);
             const uint32_t w4[4] = {u.x, u.y, u.z, u.w};
             float v[8];
 #pragma unroll
@@ -159,36 +158,38 @@ __global__ void __launch_bounds__(kThreads, 2) stream_linear(const __grid_consta
             }
         }
     } else {
-        for (int idx = threadIdx.x; idx < ntok * G * 4; idx += kConsumerWarps * 32) {
-            const int tk = idx / (G * 4), rem = idx - tk * G * 4, g = rem >> 2, tt = rem & 3;
-            const uint32_t src = xraw + 2u * (uint32_t)(tk * k + 32 * g + 4 * tt);
-            const uint2 lo = lds64(src);        // x[4t..4t+3]
-            const uint2 hi = lds64(src + 32);   // x[4t+16..4t+19]
-            uint4 o;
-            o.x = __byte_perm(lo.x, lo.y, 0x5410);
-            o.y = __byte_perm(lo.x, lo.y, 0x7632);
-            o.z = __byte_perm(hi.x, hi.y, 0x5410);
-            o.w = __byte_perm(hi.x, hi.y, 0x7632);
-            sts128(act + (uint32_t)tk * tsz + 64u * g + 16u * tt, o);
-        }
-        // corr[g][tok] = -136 * sum of the group's x in fp32, fixed order (tokens >= ntok: 0)
-        for (int idx = threadIdx.x; idx < G * 8; idx += kConsumerWarps * 32) {
-            const int g = idx >> 3, tk = idx & 7;
-            float sum = 0.0f;
-            if (tk < ntok) {
-                const uint32_t src = xraw + 2u * (uint32_t)(tk * k + 32 * g);
+        // tokens >= ntok contribute a zero accumulator init
+        for (int idx = threadIdx.x; idx < G * 8; idx += kConsumerWarps * 32)
+            if ((idx & 7) >= ntok) sts32(corr_s + 4u * (uint32_t)idx, 0u);
+        const int nq = ntok * G * 4;
+        for (int base = 0; base < nq; base += kConsumerWarps * 32) {
+            const int idx = base + threadIdx.x;
+            const bool on = idx < nq;
+            const int q = on ? idx : 0;
+            const int tk = q / (G * 4), rem = q - tk * G * 4, g = rem >> 2, tt = rem & 3;
+            const uint16_t *src = xg + tk * a.ldx + 32 * g + 4 * tt;
+            const uint2 lo = ldg_nc_64(src);        // x[4t..4t+3]
+            const uint2 hi = ldg_nc_64(src + 16);   // x[4t+16..4t+19]
+            // corr[g][tok] = -136 * sum of the group's 32 x in fp32 (fixed order: this
+            // thread's 8 in sequence, then the quad butterfly)
+            float part = 0.0f;
+            const uint32_t e8[4] = {lo.x, lo.y, hi.x, hi.y};
 #pragma unroll
-                for (int c = 0; c < 4; ++c) {
-                    const uint4 u = lds128(src + 16u * c);
-                    const uint32_t w4[4] = {u.x, u.y, u.z, u.w};
-#pragma unroll
-                    for (int e = 0; e < 4; ++e) {
-                        sum += __uint_as_float(w4[e] << 16);
-                        sum += __uint_as_float(w4[e] & 0xffff0000u);
-                    }
-                }
+            for (int e = 0; e < 4; ++e) {
+                part += __uint_as_float(e8[e] << 16);
+                part += __uint_as_float(e8[e] & 0xffff0000u);
             }
-            sts32(corr_s + 4u * (uint32_t)idx, __float_as_uint(-136.0f * sum));
+            part += __shfl_xor_sync(0xffffffffu, part, 1);
+            part += __shfl_xor_sync(0xffffffffu, part, 2);
+            if (on) {
+                uint4 o;
+                o.x = __byte_perm(lo.x, lo.y, 0x5410);
+                o.y = __byte_perm(lo.x, lo.y, 0x7632);
+                o.z = __byte_perm(hi.x, hi.y, 0x5410);
+                o.w = __byte_perm(hi.x, hi.y, 0x7632);
+                sts128(act + (uint32_t)tk * tsz + 64u * g + 16u * tt, o);
+                if (tt == 0) sts32(corr_s + 4u * (uint32_t)(g * 8 + tk), __float_as_uint(-136.0f * part));
+            }
         }
     }
     bar_consumers();
