@@ -48,7 +48,7 @@ __global__ void __launch_bounds__(kThreads, 2) stream_linear(const __grid_consta
     }
     __syncthreads();
     dev::griddep_launch();   // the next linear may launch: it only touches weights until its own wait
-    unsigned long long tr_start = 0, tr_wait = 0, tr_ready = 0;
+    unsigned long long tr_start = 0, tr_wait = 0, tr_ready = 0, tr_x = 0, tr_first = 0;
     if (a.trace) tr_start = globaltimer();
 
     if (warp == kConsumerWarps) {
@@ -123,6 +123,7 @@ __global__ void __launch_bounds__(kThreads, 2) stream_linear(const __grid_consta
                 fin &= isfinite(v[j]) ? 1 : 0;
                 amax = fmaxf(amax, fabsf(v[j]));
             }
+            if (a.trace && base == 0) tr_x = globaltimer();   // x of the first pass has arrived
             amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, 1));
             amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, 2));
             fin &= __shfl_xor_sync(0xffffffffu, fin, 1);
@@ -210,6 +211,7 @@ __global__ void __launch_bounds__(kThreads, 2) stream_linear(const __grid_consta
             const int nblk = (rem < kChunkBytes ? rem : kChunkBytes) / 16;
             const int blk0 = ch * kChunkBlocks;
             mbar_wait(full + 8u * s, ph);
+            if (a.trace && tr_first == 0) tr_first = globaltimer();   // first weight stage available
             const uint32_t st = ring + (uint32_t)s * kStageBytes;
 
             if constexpr (E == NONE) {
@@ -353,5 +355,7 @@ __global__ void __launch_bounds__(kThreads, 2) stream_linear(const __grid_consta
         r[3] = tr_wait;
         r[4] = tr_ready;
         r[5] = globaltimer();
+        r[6] = tr_x;
+        r[7] = tr_first;
     }
 }

@@ -65,7 +65,7 @@ def main():
                 mq.linear_group(route, sets[i % copies], x, outs=outs, ws=ws, stream=stream)
 
             with torch.cuda.stream(stream):
-                for i in range(2):
+                for i in range(copies):     # descriptors of every copy encoded outside the capture
                     call(i)
                 stream.synchronize()
                 g = torch.cuda.CUDAGraph()

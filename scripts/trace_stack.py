@@ -46,8 +46,8 @@ def main():
     rec = buf[:n]
     launches = sorted(set(int(v) for v in rec[:, 0]))
     t0 = None
-    print(f"{'launch':>6} {'ctas':>5} {'start_min':>9} {'start_med':>9} {'wait_med':>9} {'ready_med':>9} "
-          f"{'end_med':>9} {'end_max':>9}  (us, relative to the first launch's first CTA start)")
+    print(f"{'launch':>6} {'ctas':>5} {'start_min':>9} {'start_med':>9} {'wait_med':>9} {'x_med':>9} {'ready_med':>9} "
+          f"{'stage1':>9} {'end_med':>9} {'end_max':>9}  (us, relative to the first launch's first CTA start)")
     rows = []
     for lid in launches:
         r = rec[rec[:, 0] == lid]
@@ -58,8 +58,9 @@ def main():
     t0 = min(int(r[:, 2].min()) for _, r in rows)
     for lid, r in rows[: args.launches]:
         f = lambda col: (r[:, col].astype(np.int64) - t0) / 1000.0  # noqa: E731
-        print(f"{lid:6d} {len(r):5d} {f(2).min():9.2f} {np.median(f(2)):9.2f} {np.median(f(3)):9.2f} "
-              f"{np.median(f(4)):9.2f} {np.median(f(5)):9.2f} {f(5).max():9.2f}")
+        fx = np.median(f(6)) if (r[:, 6] > 0).all() else float("nan")
+        print(f"{lid:6d} {len(r):5d} {f(2).min():9.2f} {np.median(f(2)):9.2f} {np.median(f(3)):9.2f} {fx:9.2f} "
+              f"{np.median(f(4)):9.2f} {np.median(f(7)):9.2f} {np.median(f(5)):9.2f} {f(5).max():9.2f}")
     ends = [((r[:, 5].astype(np.int64) - t0).max()) / 1000 for _, r in rows]
     print("total span us:", max(ends))
 
