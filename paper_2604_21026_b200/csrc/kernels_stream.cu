@@ -54,7 +54,8 @@ constexpr int kBox = 128 * kTileRows;              // one {128 B x 16 rows} TMA 
 constexpr int kStageBytes = 8 * kBox + kBox;       // 8 nibble boxes + 1 scale box (18 KiB)
 constexpr int kRedBytes = kConsumerWarps * kTileRows * 8 * 4;
 
-enum Engine { DP4A = 0, IMMA = 1, HMMA = 2, NONE = 3 };   // NONE: bandwidth probe
+// HMMA1: W4A16 with a single token (only MMA column 0 is computed);  NONE: bandwidth probe
+enum Engine { DP4A = 0, IMMA = 1, HMMA = 2, NONE = 3, HMMA1 = 4 };
 
 // ------------------------------------------------------------------ PTX helpers
 // All shared-memory traffic uses explicit 32-bit shared-window addresses
@@ -236,13 +237,36 @@ __device__ __forceinline__ void dequant_bf16(uint32_t w, uint32_t p[4])
 // per-element subtract -- the -136 (= -128 offset - 8 zero point) enters through
 // the MMA accumulator init (kernel: corr = -136 * sum x).  Element order per
 // thread t: p0 = (4t, 4t+2)  p1 = (4t+16, 4t+18)  p2 = (4t+1, 4t+3)  p3 = (4t+17, 4t+19).
-__device__ __forceinline__ void magic_bf16(uint32_t w, uint32_t p[4])
+__device__ __forceinline__ uint32_t lop3_and_or(uint32_t a, uint32_t mask, uint32_t magic)
 {
-    const uint32_t magic = 0x43004300u;   // bf16x2 (128, 128)
-    p[0] = (w & 0x000F000Fu) | magic;
-    p[1] = ((w >> 4) & 0x000F000Fu) | magic;
-    p[2] = ((w >> 8) & 0x000F000Fu) | magic;
-    p[3] = ((w >> 12) & 0x000F000Fu) | magic;
+    // (a & mask) | magic in ONE LOP3 (the compiler splits it in two with two immediates)
+    uint32_t d;
+    asm("lop3.b32 %0, %1, %2, %3, 0xEA;" : "=r"(d) : "r"(a), "r"(mask), "r"(magic));
+    return d;
+}
+__device__ __forceinline__ void magic_bf16(uint32_t w, uint32_t mask, uint32_t magic, uint32_t p[4])
+{
+    p[0] = lop3_and_or(w, mask, magic);
+    p[1] = lop3_and_or(w >> 4, mask, magic);
+    p[2] = lop3_and_or(w >> 8, mask, magic);
+    p[3] = lop3_and_or(w >> 12, mask, magic);
+}
+
+// Exact per-token activation code q = clamp(round_half_away(fl(v / s)), -127, 127)
+// from a per-group reciprocal: v * fl(1/s) is within 2.3e-5 of fl(v/s) for
+// |v/s| <= 127.01, so both round to the same integer unless v * inv lies within
+// 1e-4 of a half-integer; those rare cases take the IEEE division.  Bit-identical to
+// roundf(__fdiv_rn(v, s)) clamped (test_gpu_parity: quantiser bit-exact vs oracle).
+__device__ __forceinline__ int quant_code(float v, float s, float inv)
+{
+    const float qa = v * inv;
+    const float aq = fabsf(qa);
+    const float fr = aq - truncf(aq);
+    float r = roundf(qa);
+    // near a half-integer, or inv not finite (s subnormal): the IEEE division decides
+    if (fabsf(fr - 0.5f) <= 1e-4f || !(aq <= 128.0f)) r = roundf(__fdiv_rn(v, s));
+    r = fminf(fmaxf(r, -127.0f), 127.0f);
+    return (int)r;
 }
 
 // D = A.B + C with an explicit accumulator init (C may repeat registers).
@@ -311,7 +335,7 @@ bool encode_maps(CUtensorMap *tn, CUtensorMap *ts, const uint8_t *nib, const uin
 size_t act_bytes(int engine, int64_t k, int ntok)
 {
     const int64_t G = k / 32;
-    if (engine == HMMA || engine == NONE) return (size_t)ntok * (size_t)(2 * k + 64) + 32 * (size_t)G;
+    if (engine == HMMA || engine == HMMA1 || engine == NONE) return (size_t)ntok * (size_t)(2 * k + 64) + 32 * (size_t)G;
     return (size_t)ntok * (size_t)(k + 16) + (size_t)ntok * 8 * (size_t)G;
 }
 
@@ -512,7 +536,7 @@ cudaError_t launch_stream_group(int route, const StreamGroup &g, const uint16_t 
         if (tune().nocompute)
             e = launch_one<NONE>(a, s, pdl, sms);
         else if (route == MCAPQ_W4A16)
-            e = launch_one<HMMA>(a, s, pdl, sms);
+            e = a.ntok == 1 ? launch_one<HMMA1>(a, s, pdl, sms) : launch_one<HMMA>(a, s, pdl, sms);
         else if (a.ntok == 1)
             e = launch_one<DP4A>(a, s, pdl, sms);
         else

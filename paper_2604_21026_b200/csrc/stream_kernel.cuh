@@ -92,7 +92,7 @@ __global__ void __launch_bounds__(kThreads, 2) stream_linear(const __grid_consta
     const uint16_t *xg = a.x + a.tok0 * a.ldx;
     (void)xraw;
     (void)xbar;
-    constexpr bool kA16 = (E == HMMA || E == NONE);
+    constexpr bool kA16 = (E == HMMA || E == HMMA1 || E == NONE);
     const uint32_t tsz = kA16 ? (uint32_t)(2 * k + 64) : (uint32_t)(k + 16);
     const uint32_t sx_s = act + (uint32_t)ntok * tsz;                    // W4A8: [ntok][G] fp32
     const uint32_t sq_s = sx_s + 4u * (uint32_t)(ntok * G);              // W4A8: [ntok][G] int32
@@ -130,16 +130,12 @@ __global__ void __launch_bounds__(kThreads, 2) stream_linear(const __grid_consta
             fin &= __shfl_xor_sync(0xffffffffu, fin, 2);
             const float s = __fdiv_rn(amax, 127.0f);
             const bool live = fin && s != 0.0f;
+            const float inv = __frcp_rn(s);
             uint32_t lo = 0, hi = 0;
             int sum = 0;
 #pragma unroll
             for (int j = 0; j < 8; ++j) {
-                int code = 0;
-                if (live) {
-                    float r = roundf(__fdiv_rn(v[j], s));
-                    r = fminf(fmaxf(r, -127.0f), 127.0f);
-                    code = (int)r;
-                }
+                const int code = live ? quant_code(v[j], s, inv) : 0;
                 sum += code;
                 if (j < 4)
                     lo |= ((uint32_t)code & 0xffu) << (8 * j);
@@ -200,6 +196,8 @@ __global__ void __launch_bounds__(kThreads, 2) stream_linear(const __grid_consta
     const int gid = lane >> 2, t = lane & 3;
     const int mrow = (lane & 7) + ((lane >> 3) & 1) * 8;    // ldmatrix row of this lane
     const int mhalf = lane >> 4;                             // ldmatrix: lanes 16-31 address the 2nd block
+    uint32_t kNib2 = 0x000F000Fu, kMagic = 0x43004300u;      // in registers: one LOP3 per bf16 pair
+    asm volatile("" : "+r"(kNib2), "+r"(kMagic));
     int s = 0;
     uint32_t ph = 0;
     int li = 0;
@@ -288,24 +286,29 @@ __global__ void __launch_bounds__(kThreads, 2) stream_linear(const __grid_consta
                             acc[2] = fmaf(dB[j] * s0, (float)(c[2] - 8 * q0), acc[2]);
                             acc[3] = fmaf(dB[j] * s1, (float)(c[3] - 8 * q1), acc[3]);
                         } else {
-                            // A = 128 + c (exact bf16, no per-element subtract); the -8 zero point
-                            // and the +128 offset enter through the accumulator init
-                            // C = -136 * sum_j x_j, so D = sum_j (c_j - 8) x_j.
+                            // A = 128 + c (exact bf16, one LOP3 per pair, no per-element
+                            // subtract); D = sum_j (128 + c_j) x_j is exact per product, and
+                            // corr = -136 * sum_j x_j restores sum_j (c_j - 8) x_j in fp32.
                             uint4 bx = make_uint4(0, 0, 0, 0);
                             if (gid < ntok) bx = lds128(act + (uint32_t)gid * tsz + 64u * g + 16u * t);
-                            const uint2 cru = lds64(corr_s + 32u * g + 8u * t);
-                            const float2 cr = make_float2(__uint_as_float(cru.x), __uint_as_float(cru.y));
                             uint32_t pa[4], pb[4];
-                            magic_bf16(wa, pa);
-                            magic_bf16(wb, pb);
+                            magic_bf16(wa, kNib2, kMagic, pa);
+                            magic_bf16(wb, kNib2, kMagic, pb);
                             float c[4];
-                            hmma_c(pa[0], pb[0], pa[2], pb[2], bx.x, bx.y, cr.x, cr.y, cr.x, cr.y, c);
+                            hmma_c(pa[0], pb[0], pa[2], pb[2], bx.x, bx.y, 0.f, 0.f, 0.f, 0.f, c);
                             hmma(pa[1], pb[1], pa[3], pb[3], bx.z, bx.w, c);
-                            acc[0] = fmaf(dA[j], c[0], acc[0]);
-                            acc[2] = fmaf(dB[j], c[2], acc[2]);
-                            if (ntok > 1) {
-                                acc[1] = fmaf(dA[j], c[1], acc[1]);
-                                acc[3] = fmaf(dB[j], c[3], acc[3]);
+                            if constexpr (E == HMMA1) {
+                                // one token: only column 0 (lanes t == 0) is live
+                                const float crx = __uint_as_float(lds32(corr_s + 32u * g));
+                                acc[0] = fmaf(dA[j], c[0] + crx, acc[0]);
+                                acc[2] = fmaf(dB[j], c[2] + crx, acc[2]);
+                            } else {
+                                const uint2 cru = lds64(corr_s + 32u * g + 8u * t);
+                                const float crx = __uint_as_float(cru.x), cry = __uint_as_float(cru.y);
+                                acc[0] = fmaf(dA[j], c[0] + crx, acc[0]);
+                                acc[1] = fmaf(dA[j], c[1] + cry, acc[1]);
+                                acc[2] = fmaf(dB[j], c[2] + crx, acc[2]);
+                                acc[3] = fmaf(dB[j], c[3] + cry, acc[3]);
                             }
                         }
                     }
