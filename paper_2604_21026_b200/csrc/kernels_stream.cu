@@ -397,6 +397,10 @@ cudaError_t launch_one(StreamArgs &a, cudaStream_t s, bool pdl, int sms)
     if (!attr_done) {
         cudaError_t e = cudaFuncSetAttribute(stream_linear<E>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
         if (e != cudaSuccess) return e;
+        // one L1/shared carveout for every linear: consecutive (PDL-overlapped) kernels
+        // never force an SM to drain for a carveout change
+        e = cudaFuncSetAttribute(stream_linear<E>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+        if (e != cudaSuccess) return e;
         attr_done = 1;
     }
     const int T = a.tile_start[a.count];
