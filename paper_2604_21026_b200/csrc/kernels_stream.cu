@@ -289,7 +289,9 @@ __device__ __forceinline__ void hmma(uint32_t a0, uint32_t a1, uint32_t a2, uint
 }
 
 // ------------------------------------------------------------------ the kernel
+#include "stream_engines.cuh"
 #include "stream_kernel.cuh"
+#include "stack_kernel.cuh"
 
 // ------------------------------------------------------------------ host side
 typedef CUresult (*EncodeTiledFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
@@ -350,7 +352,7 @@ size_t round_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 //   MCAPQ_STREAM_NOCOMPUTE 1 = consumers only drain the ring (bandwidth probe; outputs garbage)
 //   MCAPQ_STREAM_PDL       1 = API calls also launch with programmatic dependent launch
 struct Tune {
-    int smem_kb = 112, max_stages = 12, nocompute = 0, pdl = 0, trace = 0;
+    int smem_kb = 112, max_stages = 12, nocompute = 0, pdl = 0, trace = 0, step_smem_kb = 220, step = 1;
 };
 const Tune &tune()
 {
@@ -361,6 +363,10 @@ const Tune &tune()
         if (const char *e = getenv("MCAPQ_STREAM_NOCOMPUTE")) v.nocompute = atoi(e);
         if (const char *e = getenv("MCAPQ_STREAM_PDL")) v.pdl = atoi(e);
         if (const char *e = getenv("MCAPQ_STREAM_TRACE")) v.trace = atoi(e);
+        if (const char *e = getenv("MCAPQ_STEP_SMEM_KB")) v.step_smem_kb = atoi(e);
+        if (const char *e = getenv("MCAPQ_STEP_KERNEL")) v.step = atoi(e);
+        if (v.step_smem_kb < 60) v.step_smem_kb = 60;
+        if (v.step_smem_kb > 226) v.step_smem_kb = 226;
         if (v.smem_kb < 40) v.smem_kb = 40;
         if (v.smem_kb > 226) v.smem_kb = 226;
         if (v.max_stages < 2) v.max_stages = 2;
@@ -482,6 +488,83 @@ const CUtensorMap *stream_descriptors(const uint8_t *nib, const uint16_t *scale,
     ++t.used;
     t.map.emplace(key, dpair);
     return dpair;
+}
+
+// ------------------------------------------------------------------ persistent step
+size_t stack_op_bytes() { return sizeof(StackOp); }
+bool stack_step_enabled() { return tune().step != 0 && encode_fn() != nullptr; }
+
+bool stack_fill_op(void *host_op, int route, const StreamGroup &g, const uint16_t *x, int ydt, cudaStream_t s)
+{
+    StackOp op;
+    memset(&op, 0, sizeof(op));
+    int tiles = 0;
+    for (int i = 0; i < g.count; ++i) {
+        op.maps[i] = stream_descriptors(g.nib[i], g.scale[i], g.n[i], g.k, s);
+        if (!op.maps[i]) return false;
+        op.y[i] = g.y[i];
+        op.n[i] = g.n[i];
+        op.tile_start[i] = tiles;
+        tiles += (int)((g.n[i] + kTileRows - 1) / kTileRows);
+    }
+    op.tile_start[g.count] = tiles;
+    op.count = g.count;
+    op.route = route;
+    op.ydt = ydt;
+    op.k = g.k;
+    op.x = x;
+    memcpy(host_op, &op, sizeof(op));
+    return true;
+}
+
+cudaError_t launch_stack_step(const void *ops_dev, int nops, unsigned int *counters_dev, int64_t max_k,
+                              cudaStream_t s)
+{
+    static int attr_done = 0;
+    if (!attr_done) {
+        cudaError_t e = cudaFuncSetAttribute(stack_step, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+        if (e != cudaSuccess) return e;
+        attr_done = 1;
+    }
+    cudaError_t e = cudaMemsetAsync(counters_dev, 0, sizeof(unsigned int) * (size_t)nops, s);
+    if (e != cudaSuccess) return e;
+    StackArgs a;
+    memset(&a, 0, sizeof(a));
+    a.ops = reinterpret_cast<const StackOp *>(ops_dev);
+    a.nops = nops;
+    a.counters = counters_dev;
+    // one CTA per SM: activations for the largest K under either route, the rest is ring
+    const size_t act = round_up(act_bytes(HMMA1, max_k, 1) > act_bytes(DP4A, max_k, 1) ? act_bytes(HMMA1, max_k, 1)
+                                                                                           : act_bytes(DP4A, max_k, 1),
+                                128);
+    const size_t budget = (size_t)tune().step_smem_kb * 1024;
+    int S = (int)(((long)budget - 1024 - 128 - (long)act - kRedBytes) / kStageBytes);
+    S = S < 2 ? 2 : (S > 16 ? 16 : S);
+    a.stages = S;
+    a.act_off = S * kStageBytes + 128;
+    a.red_off = (int)(a.act_off + act);
+    const size_t smem = 1024 + (size_t)a.red_off + kRedBytes;
+    const int grid = device_sms();
+    if (tune().trace) {
+        // debug timeline: [op][cta] records at the start of the trace buffer
+        constexpr size_t kCap = 1u << 20;
+        if (!g_trace && cudaMalloc(&g_trace, kCap * 64) != cudaSuccess) g_trace = nullptr;
+        if (g_trace && (size_t)nops * grid <= kCap) {
+            a.trace = g_trace;
+            g_trace_used = (size_t)nops * grid;
+        }
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeCooperative;   // all CTAs co-resident: the grid barrier is safe
+    attr[0].val.cooperative = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, stack_step, a);
 }
 
 size_t stream_trace_read(unsigned long long *host_out, size_t max_records)

@@ -39,9 +39,26 @@ struct mcapq_stack {
     cudaGraph_t graph = nullptr;
     cudaGraphExec_t exec = nullptr;
     int64_t graph_m = 0;
+    // persistent step program (M = 1): one op per launch group, executed by stack_step
+    bool prog_dirty = true, prog_ok = false;
+    void *ops_dev = nullptr, *ops_host = nullptr;
+    unsigned int *counters = nullptr;
+    int nops = 0;
+    int64_t max_k = 0;
 };
 
 using namespace mcapq;
+
+static void free_program(mcapq_stack *st)
+{
+    if (st->ops_dev) cudaFree(st->ops_dev);
+    if (st->ops_host) cudaFreeHost(st->ops_host);
+    if (st->counters) cudaFree(st->counters);
+    st->ops_dev = st->ops_host = nullptr;
+    st->counters = nullptr;
+    st->nops = 0;
+    st->prog_ok = false;
+}
 
 static mcapq_status ensure_ws(mcapq_stack *st, int64_t k)
 {
@@ -95,6 +112,7 @@ mcapq_status mcapq_stack_set(mcapq_stack *st, int layer, int slot, int input_id,
     s.x = x;
     s.y = y;
     s.ydt = ydt;
+    st->prog_dirty = true;
     if (stream_supported(k) && aligned16(scale)) {
         // encode + upload this weight's TMA descriptors now, outside any graph capture
         MCAPQ_REQUIRE(stream_descriptors(nib, scale, n, k, nullptr) != nullptr, MCAPQ_ECUDA,
@@ -132,6 +150,59 @@ static mcapq_status for_each_group(const mcapq_stack *st, int l, F f)
     return MCAPQ_OK;
 }
 
+static StreamGroup group_of(const mcapq_stack *st, int l, int first, int cnt)
+{
+    StreamGroup g = {};
+    g.count = cnt;
+    g.k = st->slots[(size_t)l * kMaxSlots + first].k;
+    for (int i = 0; i < cnt; ++i) {
+        const Slot &b = st->slots[(size_t)l * kMaxSlots + first + i];
+        g.nib[i] = b.nib;
+        g.scale[i] = b.scale;
+        g.n[i] = b.n;
+        g.y[i] = b.y;
+        g.ldy[i] = b.n;
+    }
+    return g;
+}
+
+// Build the persistent-step program (one op per launch group, in decode order) in
+// device memory.  Host-synchronous: call outside graph capture.  prog_ok stays
+// false when a group is off the TMA fast path (then the per-linear path runs).
+static mcapq_status build_program(mcapq_stack *st)
+{
+    free_program(st);
+    st->prog_dirty = false;
+    if (!stack_step_enabled()) return MCAPQ_OK;
+    std::vector<std::pair<int, std::pair<int, int>>> groups;   // (layer, (first, count))
+    bool all_fast = true;
+    for (int l = 0; l < st->layers; ++l)
+        for_each_group(st, l, [&](int first, int cnt, bool fast) -> mcapq_status {
+            all_fast = all_fast && fast;
+            groups.push_back({l, {first, cnt}});
+            return MCAPQ_OK;
+        });
+    if (!all_fast || groups.empty()) return MCAPQ_OK;
+    const size_t ob = stack_op_bytes();
+    st->nops = (int)groups.size();
+    MCAPQ_CUDA_TRY(cudaMallocHost(&st->ops_host, ob * st->nops));
+    MCAPQ_CUDA_TRY(cudaMalloc(&st->ops_dev, ob * st->nops));
+    MCAPQ_CUDA_TRY(cudaMalloc(&st->counters, sizeof(unsigned int) * st->nops));
+    st->max_k = 0;
+    for (int i = 0; i < st->nops; ++i) {
+        const int l = groups[i].first, first = groups[i].second.first, cnt = groups[i].second.second;
+        const StreamGroup g = group_of(st, l, first, cnt);
+        const Slot &a = st->slots[(size_t)l * kMaxSlots + first];
+        MCAPQ_REQUIRE(stack_fill_op(reinterpret_cast<uint8_t *>(st->ops_host) + ob * i, st->routes[l], g, a.x,
+                                    a.ydt, nullptr),
+                      MCAPQ_ECUDA, "stack op %d: TMA descriptor encode failed", i);
+        st->max_k = g.k > st->max_k ? g.k : st->max_k;
+    }
+    MCAPQ_CUDA_TRY(cudaMemcpy(st->ops_dev, st->ops_host, ob * st->nops, cudaMemcpyHostToDevice));
+    st->prog_ok = true;
+    return MCAPQ_OK;
+}
+
 extern "C" {
 
 mcapq_status mcapq_stack_run(mcapq_stack *st, int64_t m, void *stream)
@@ -139,6 +210,20 @@ mcapq_status mcapq_stack_run(mcapq_stack *st, int64_t m, void *stream)
     clear_error();
     MCAPQ_REQUIRE(st && m >= 1 && m <= st->max_m, MCAPQ_EINVAL, "bad stack_run arguments");
     cudaStream_t s = as_stream(stream);
+    if (m == 1 && st->prog_dirty) {
+        cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+        cudaStreamIsCapturing(s, &cs);
+        if (cs == cudaStreamCaptureStatusNone) {
+            mcapq_status r = build_program(st);
+            if (r != MCAPQ_OK) return r;
+        }
+    }
+    if (m == 1 && !st->prog_dirty && st->prog_ok) {
+        // the whole step in one persistent cooperative kernel
+        cudaError_t e = launch_stack_step(st->ops_dev, st->nops, st->counters, st->max_k, s);
+        MCAPQ_REQUIRE(e == cudaSuccess, MCAPQ_ECUDA, "stack_step launch: %s", cudaGetErrorString(e));
+        return MCAPQ_OK;
+    }
     for (int l = 0; l < st->layers; ++l) {
         const int route = st->routes[l];
         int last_input = -1 << 30;
@@ -188,6 +273,10 @@ mcapq_status mcapq_stack_capture(mcapq_stack *st, int64_t m, void *stream)
     MCAPQ_REQUIRE(st, MCAPQ_EINVAL, "stack is NULL");
     cudaStream_t s = as_stream(stream);
     MCAPQ_REQUIRE(s != nullptr, MCAPQ_EINVAL, "graph capture needs a non-default stream");
+    if (m == 1 && st->prog_dirty) {
+        mcapq_status r = build_program(st);   // allocations happen before the capture
+        if (r != MCAPQ_OK) return r;
+    }
     if (st->exec) cudaGraphExecDestroy(st->exec);
     if (st->graph) cudaGraphDestroy(st->graph);
     st->exec = nullptr;
@@ -227,6 +316,7 @@ size_t mcapq_stack_weight_bytes(const mcapq_stack *st)
 int mcapq_stack_launches(const mcapq_stack *st, int64_t m)
 {
     if (!st || m < 1) return 0;
+    if (m == 1 && !st->prog_dirty && st->prog_ok) return 1;   // the persistent step kernel
     int c = 0;
     for (int l = 0; l < st->layers; ++l) {
         int last = -1 << 30;
@@ -309,6 +399,7 @@ void mcapq_stack_destroy(mcapq_stack *st)
     if (st->exec) cudaGraphExecDestroy(st->exec);
     if (st->graph) cudaGraphDestroy(st->graph);
     if (st->ws) cudaFree(st->ws);
+    free_program(st);
     delete st;
 }
 

@@ -52,6 +52,18 @@ size_t stream_trace_read(unsigned long long *host_out, size_t max_records);
 
 // K % 256 == 0 (16-B aligned scale rows for the tensor maps) and 16-B aligned planes.
 bool stream_supported(int64_t k);
+// Persistent decode-step kernel (stack_kernel.cuh): a program of ops, one per
+// grouped linear, executed in order in ONE cooperative launch (M = 1 tokens).
+size_t stack_op_bytes();
+bool stack_step_enabled();   // MCAPQ_STEP_KERNEL (default 1)
+// Fill one op (host memory, stack_op_bytes() bytes) for `route` over group g with
+// input x [k] bf16 and outputs g.y (ydt); encodes/uploads descriptors on `s`.
+bool stack_fill_op(void *host_op, int route, const StreamGroup &g, const uint16_t *x, int ydt, cudaStream_t s);
+// Launch the step: ops_dev = nops filled ops in device memory; counters_dev = nops
+// uint32 (zeroed here, stream-ordered); max_k = the largest K of the program.
+cudaError_t launch_stack_step(const void *ops_dev, int nops, unsigned int *counters_dev, int64_t max_k,
+                              cudaStream_t s);
+
 // Device pointer to the {nib, scale} tensor-map pair of a packed weight, encoding
 // and uploading it on first use (stream-ordered; capturable once the table exists).
 // Returns null on failure.

@@ -1,0 +1,308 @@
+// stream_engines.cuh -- the per-stage compute of the TMA-fed decode linears,
+// shared by the per-linear kernel (stream_kernel.cuh) and the persistent
+// decode-step kernel (stack_kernel.cuh).  Included by kernels_stream.cu after
+// its PTX helpers and fragment routines.
+//
+// Activation layouts in shared memory (per token, tsz bytes apart):
+//  W4A8 : q_lo [G][16] | q_hi [G][16] | 16 B pad   (q_lo = elements 0..15 of each
+//         32-group, q_hi = 16..31: lane-per-block LDS.128 reads are consecutive),
+//         then sx [ntok][G] fp32 and sq [ntok][G] int32 after all tokens.
+//  W4A16: [G][4 t][8 bf16] in fragment order (4t,4t+2,4t+1,4t+3,4t+16,4t+18,4t+17,4t+19) | 64 B pad,
+//         then corr [G][8 tokens] fp32 = -136 * sum_j x_j of the group.
+#pragma once
+
+struct ActSmem {
+    uint32_t act, tsz, sx, sq, corr;
+};
+
+__device__ __forceinline__ ActSmem act_layout(bool a16, uint32_t act, int64_t k, int ntok)
+{
+    ActSmem L;
+    const int G = (int)(k / 32);
+    L.act = act;
+    L.tsz = a16 ? (uint32_t)(2 * k + 64) : (uint32_t)(k + 16);
+    L.sx = act + (uint32_t)ntok * L.tsz;          // W4A8: [ntok][G] fp32
+    L.sq = L.sx + 4u * (uint32_t)(ntok * G);      // W4A8: [ntok][G] int32
+    L.corr = act + (uint32_t)ntok * L.tsz;        // W4A16: [G][8] fp32
+    return L;
+}
+
+// ---------------------------------------------------------------- activation staging
+// W4A8: per-token, per-32-group quantisation, a quad of threads per
+// group (8 elements each), x read straight from global (L2): exact max,
+// s = amax / 127 (IEEE), q = clamp(round_half_away(x / s)) via quant_code (exact),
+// exact int sum -- bit-identical to quant_a8_kernel.  Warp-uniform trip counts
+// (quad shuffles).  Called by all nthreads consumer threads (tid in [0, nthreads)).
+// kCoherent: x may have been written by other CTAs of the same kernel (persistent
+// step kernel) -> ld.global.cg (L2) instead of the read-only .nc path.
+template <bool kCoherent>
+__device__ __forceinline__ uint4 ldg_x128(const void *p)
+{
+    if constexpr (kCoherent) {
+        uint4 v;
+        asm volatile("ld.global.cg.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
+        return v;
+    } else {
+        return ldg_nc_128(p);
+    }
+}
+template <bool kCoherent>
+__device__ __forceinline__ uint2 ldg_x64(const void *p)
+{
+    if constexpr (kCoherent) {
+        uint2 v;
+        asm volatile("ld.global.cg.v2.u32 {%0,%1}, [%2];" : "=r"(v.x), "=r"(v.y) : "l"(p));
+        return v;
+    } else {
+        return ldg_nc_64(p);
+    }
+}
+
+template <bool kCoherent>
+__device__ __forceinline__ void stage_a8(const uint16_t *xg, int64_t ldx, int ntok, int64_t k, const ActSmem &L,
+                                         int tid, int nthreads)
+{
+    const int G = (int)(k / 32);
+    const uint32_t K2 = (uint32_t)(k / 2);
+    const int nq = ntok * G * 4;
+    for (int base = 0; base < nq; base += nthreads) {
+        const int idx = base + tid;
+        const bool on = idx < nq;
+        const int grp = on ? (idx >> 2) : 0, sub = idx & 3;
+        const int i = grp / G, g = grp - i * G;
+        const uint4 u = ldg_x128<kCoherent>(xg + i * ldx + 32 * g + 8 * sub);
+        const uint32_t w4[4] = {u.x, u.y, u.z, u.w};
+        float v[8];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            v[2 * e] = __uint_as_float(w4[e] << 16);
+            v[2 * e + 1] = __uint_as_float(w4[e] & 0xffff0000u);
+        }
+        float amax = 0.0f;
+        int fin = 1;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            fin &= isfinite(v[j]) ? 1 : 0;
+            amax = fmaxf(amax, fabsf(v[j]));
+        }
+        amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, 1));
+        amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, 2));
+        fin &= __shfl_xor_sync(0xffffffffu, fin, 1);
+        fin &= __shfl_xor_sync(0xffffffffu, fin, 2);
+        const float s = __fdiv_rn(amax, 127.0f);
+        const bool live = fin && s != 0.0f;
+        const float inv = __frcp_rn(s);
+        uint32_t lo = 0, hi = 0;
+        int sum = 0;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            const int code = live ? quant_code(v[j], s, inv) : 0;
+            sum += code;
+            if (j < 4)
+                lo |= ((uint32_t)code & 0xffu) << (8 * j);
+            else
+                hi |= ((uint32_t)code & 0xffu) << (8 * (j - 4));
+        }
+        sum += __shfl_xor_sync(0xffffffffu, sum, 1);
+        sum += __shfl_xor_sync(0xffffffffu, sum, 2);
+        if (on) {
+            // elements 8sub..8sub+7: sub 0/1 -> q_lo, sub 2/3 -> q_hi
+            const uint32_t qt = L.act + (uint32_t)i * L.tsz + (sub < 2 ? 0u : K2) + 16u * g + 8u * (sub & 1);
+            asm volatile("st.shared.v2.u32 [%0], {%1,%2};" ::"r"(qt), "r"(lo), "r"(hi) : "memory");
+            if (sub == 0) {
+                sts32(L.sx + 4u * (uint32_t)(i * G + g), __float_as_uint(live ? s : 0.0f));
+                sts32(L.sq + 4u * (uint32_t)(i * G + g), (uint32_t)sum);
+            }
+        }
+    }
+}
+
+// W4A16: x re-staged in MMA-fragment order + corr[g][tok] = -136 * sum of the group
+// (fp32; this thread's 8 values in sequence, then the quad butterfly).
+template <bool kCoherent>
+__device__ __forceinline__ void stage_a16(const uint16_t *xg, int64_t ldx, int ntok, int64_t k, const ActSmem &L,
+                                          int tid, int nthreads)
+{
+    const int G = (int)(k / 32);
+    for (int idx = tid; idx < G * 8; idx += nthreads)     // tokens >= ntok: zero init
+        if ((idx & 7) >= ntok) sts32(L.corr + 4u * (uint32_t)idx, 0u);
+    const int nq = ntok * G * 4;
+    for (int base = 0; base < nq; base += nthreads) {
+        const int idx = base + tid;
+        const bool on = idx < nq;
+        const int q = on ? idx : 0;
+        const int tk = q / (G * 4), rem = q - tk * G * 4, g = rem >> 2, tt = rem & 3;
+        const uint16_t *src = xg + tk * ldx + 32 * g + 4 * tt;
+        const uint2 lo = ldg_x64<kCoherent>(src);        // x[4t..4t+3]
+        const uint2 hi = ldg_x64<kCoherent>(src + 16);   // x[4t+16..4t+19]
+        float part = 0.0f;
+        const uint32_t e8[4] = {lo.x, lo.y, hi.x, hi.y};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            part += __uint_as_float(e8[e] << 16);
+            part += __uint_as_float(e8[e] & 0xffff0000u);
+        }
+        part += __shfl_xor_sync(0xffffffffu, part, 1);
+        part += __shfl_xor_sync(0xffffffffu, part, 2);
+        if (on) {
+            uint4 o;
+            o.x = __byte_perm(lo.x, lo.y, 0x5410);
+            o.y = __byte_perm(lo.x, lo.y, 0x7632);
+            o.z = __byte_perm(hi.x, hi.y, 0x5410);
+            o.w = __byte_perm(hi.x, hi.y, 0x7632);
+            sts128(L.act + (uint32_t)tk * L.tsz + 64u * g + 16u * tt, o);
+            if (tt == 0) sts32(L.corr + 4u * (uint32_t)(g * 8 + tk), __float_as_uint(-136.0f * part));
+        }
+    }
+}
+
+// ---------------------------------------------------------------- per-stage compute
+// DP4A (W4A8, 1 token): warp w owns row w of the 16-row tile; lane l the blocks l and
+// l+32 of the chunk, in that order.  8 IDP.4A + deferred correction D = sumi - 8 sum_x
+// + fp32 (d s) D per block.
+__device__ __forceinline__ void chunk_dp4a(uint32_t st, int nblk, int blk0, uint32_t K2, const ActSmem &L, int warp,
+                                           int lane, float &acc)
+{
+    const int r = warp;
+    if (nblk == kChunkBlocks) {
+        // full chunk: no predicates, both blocks' load/dp4a chains interleave
+        const int g0 = blk0 + lane, g1 = g0 + 32;
+        const uint4 w0 = lds128(st + nib_off(r, lane));
+        const uint4 w1 = lds128(st + nib_off(r, lane + 32));
+        const uint4 qa0 = lds128(L.act + 16u * g0), qb0 = lds128(L.act + K2 + 16u * g0);
+        const uint4 qa1 = lds128(L.act + 16u * g1), qb1 = lds128(L.act + K2 + 16u * g1);
+        const float d0 = h2f(lds16(st + scale_off(r, lane)));
+        const float d1 = h2f(lds16(st + scale_off(r, lane + 32)));
+        const float s0 = __uint_as_float(lds32(L.sx + 4u * g0));
+        const float s1 = __uint_as_float(lds32(L.sx + 4u * g1));
+        const int D0 = block_sumi_dp4a(w0, make_int4(qa0.x, qa0.y, qa0.z, qa0.w),
+                                       make_int4(qb0.x, qb0.y, qb0.z, qb0.w)) - 8 * (int)lds32(L.sq + 4u * g0);
+        const int D1 = block_sumi_dp4a(w1, make_int4(qa1.x, qa1.y, qa1.z, qa1.w),
+                                       make_int4(qb1.x, qb1.y, qb1.z, qb1.w)) - 8 * (int)lds32(L.sq + 4u * g1);
+        acc = fmaf(d0 * s0, (float)D0, acc);
+        acc = fmaf(d1 * s1, (float)D1, acc);
+    } else {
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int b = lane + 32 * h;
+            if (b < nblk) {
+                const int g = blk0 + b;
+                const uint4 qa = lds128(L.act + 16u * g), qb = lds128(L.act + K2 + 16u * g);
+                const uint4 w = lds128(st + nib_off(r, b));
+                const int D = block_sumi_dp4a(w, make_int4(qa.x, qa.y, qa.z, qa.w),
+                                              make_int4(qb.x, qb.y, qb.z, qb.w)) - 8 * (int)lds32(L.sq + 4u * g);
+                acc = fmaf(h2f(lds16(st + scale_off(r, b))) * __uint_as_float(lds32(L.sx + 4u * g)), (float)D, acc);
+            }
+        }
+    }
+}
+
+// MMA engines: warp w owns blocks 4w..4w+3 of the chunk (contiguous, in that order)
+// for all 16 rows; ldmatrix.x4 hands lane (gid, t) word t of rows gid / gid+8 of two
+// blocks -- the m16n8k32.s8 / m16n8k16.bf16 A fragment of the split nibble layout.
+//   IMMA  (W4A8, 2..8 tokens): one mma.sync per block -> exact int32 D, fp32 d s D.
+//   HMMA  (W4A16, 2..8 tokens) / HMMA1 (1 token): A = 128 + c (exact bf16, one LOP3
+//         per pair), two MMAs per block, D + corr restores sum (c - 8) x in fp32.
+template <int E>
+__device__ __forceinline__ void chunk_mma(uint32_t st, int nblk, int blk0, uint32_t K2, const ActSmem &L, int G,
+                                          int ntok, int warp, int lane, uint32_t kNib2, uint32_t kMagic, float acc[4])
+{
+    const int gid = lane >> 2, t = lane & 3;
+    const int mrow = (lane & 7) + ((lane >> 3) & 1) * 8;    // ldmatrix row of this lane
+    const int mhalf = lane >> 4;                             // lanes 16-31 address the 2nd block
+    const int bq = 4 * warp;
+    if (bq >= nblk) return;
+    uint32_t wv[8];   // [block j][row half]: wa(j) = wv[2j], wb(j) = wv[2j+1]
+    ldmatrix_x4(st + nib_off(mrow, bq + mhalf), wv[0], wv[1], wv[2], wv[3]);
+    ldmatrix_x4(st + nib_off(mrow, bq + 2 + mhalf), wv[4], wv[5], wv[6], wv[7]);
+    // scales of rows gid / gid+8 for the 4 blocks: one 8-byte load each
+    const uint2 sa = lds64(st + scale_off(gid, bq));
+    const uint2 sbb = lds64(st + scale_off(gid + 8, bq));
+    const float dA[4] = {h2f((uint16_t)(sa.x & 0xffff)), h2f((uint16_t)(sa.x >> 16)), h2f((uint16_t)(sa.y & 0xffff)),
+                         h2f((uint16_t)(sa.y >> 16))};
+    const float dB[4] = {h2f((uint16_t)(sbb.x & 0xffff)), h2f((uint16_t)(sbb.x >> 16)),
+                         h2f((uint16_t)(sbb.y & 0xffff)), h2f((uint16_t)(sbb.y >> 16))};
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        const uint32_t wa = wv[2 * j], wb = wv[2 * j + 1];
+        const int g = blk0 + bq + j;
+        if constexpr (E == IMMA) {
+            uint32_t b0 = 0, b1 = 0;
+            if (gid < ntok) {
+                const uint32_t qt = L.act + (uint32_t)gid * L.tsz;
+                b0 = lds32(qt + 16u * g + 4u * t);
+                b1 = lds32(qt + K2 + 16u * g + 4u * t);
+            }
+            int c[4];
+            imma(wa, wb, b0, b1, c);
+            const int c0 = 2 * t, c1 = 2 * t + 1;
+            const float s0 = c0 < ntok ? __uint_as_float(lds32(L.sx + 4u * (c0 * G + g))) : 0.f;
+            const float s1 = c1 < ntok ? __uint_as_float(lds32(L.sx + 4u * (c1 * G + g))) : 0.f;
+            const int q0 = c0 < ntok ? (int)lds32(L.sq + 4u * (c0 * G + g)) : 0;
+            const int q1 = c1 < ntok ? (int)lds32(L.sq + 4u * (c1 * G + g)) : 0;
+            acc[0] = fmaf(dA[j] * s0, (float)(c[0] - 8 * q0), acc[0]);
+            acc[1] = fmaf(dA[j] * s1, (float)(c[1] - 8 * q1), acc[1]);
+            acc[2] = fmaf(dB[j] * s0, (float)(c[2] - 8 * q0), acc[2]);
+            acc[3] = fmaf(dB[j] * s1, (float)(c[3] - 8 * q1), acc[3]);
+        } else {
+            uint4 bx = make_uint4(0, 0, 0, 0);
+            if (gid < ntok) bx = lds128(L.act + (uint32_t)gid * L.tsz + 64u * g + 16u * t);
+            uint32_t pa[4], pb[4];
+            magic_bf16(wa, kNib2, kMagic, pa);
+            magic_bf16(wb, kNib2, kMagic, pb);
+            float c[4];
+            hmma_c(pa[0], pb[0], pa[2], pb[2], bx.x, bx.y, 0.f, 0.f, 0.f, 0.f, c);
+            hmma(pa[1], pb[1], pa[3], pb[3], bx.z, bx.w, c);
+            if constexpr (E == HMMA1) {
+                // one token: only column 0 (lanes t == 0) is live
+                const float crx = __uint_as_float(lds32(L.corr + 32u * g));
+                acc[0] = fmaf(dA[j], c[0] + crx, acc[0]);
+                acc[2] = fmaf(dB[j], c[2] + crx, acc[2]);
+            } else {
+                const uint2 cru = lds64(L.corr + 32u * g + 8u * t);
+                const float crx = __uint_as_float(cru.x), cry = __uint_as_float(cru.y);
+                acc[0] = fmaf(dA[j], c[0] + crx, acc[0]);
+                acc[1] = fmaf(dA[j], c[1] + cry, acc[1]);
+                acc[2] = fmaf(dB[j], c[2] + crx, acc[2]);
+                acc[3] = fmaf(dB[j], c[3] + cry, acc[3]);
+            }
+        }
+    }
+}
+
+// ---------------------------------------------------------------- tile epilogues
+// DP4A: fixed xor butterfly; lane 0 of warp w stores row row0 + w.
+__device__ __forceinline__ void epilogue_dp4a(float acc, int64_t row0, int64_t n, void *y, int ydt, int64_t off, int warp,
+                                              int lane)
+{
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) {
+        const int64_t row = row0 + warp;
+        if (row < n) dev::store_out(y, ydt, off + row, acc);
+    }
+}
+
+// MMA: fixed-order cross-warp reduction through shared memory (red: 16 warps x 512 B).
+__device__ __forceinline__ void epilogue_mma(const float acc[4], uint32_t red, int64_t row0, int64_t n, void *y,
+                                             int ydt, int64_t ldy, int64_t tok0, int ntok, int warp, int lane)
+{
+    const int gid = lane >> 2, t = lane & 3;
+    const uint32_t rw = red + 512u * warp;
+    const int c0 = 2 * t, c1 = 2 * t + 1;
+    sts32(rw + 4u * (gid * 8 + c0), __float_as_uint(acc[0]));
+    sts32(rw + 4u * (gid * 8 + c1), __float_as_uint(acc[1]));
+    sts32(rw + 4u * ((gid + 8) * 8 + c0), __float_as_uint(acc[2]));
+    sts32(rw + 4u * ((gid + 8) * 8 + c1), __float_as_uint(acc[3]));
+    bar_consumers();
+    const int tid = warp * 32 + lane;
+    if (tid < 128) {
+        const int r = tid >> 3, tk = tid & 7;
+        float sum = __uint_as_float(lds32(red + 4u * tid));
+#pragma unroll
+        for (int w = 1; w < kConsumerWarps; ++w) sum += __uint_as_float(lds32(red + 512u * w + 4u * tid));
+        const int64_t row = row0 + r;
+        if (row < n && tk < ntok) dev::store_out(y, ydt, (tok0 + tk) * ldy + row, sum);
+    }
+    bar_consumers();
+}
