@@ -81,6 +81,13 @@ __global__ void __launch_bounds__(kThreads, 1) stack_step(const __grid_constant_
                 const int T = op.tile_start[count];
                 const int t0 = (int)(((int64_t)T * blockIdx.x) / gridDim.x);
                 const int t1 = (int)(((int64_t)T * (blockIdx.x + 1)) / gridDim.x);
+                // warm this linear's input in L2 (evict_last) while its weights stream: the
+                // consumers read x on the dependent chain, an L2 hit instead of a DRAM trip
+                // queued behind the weight stream.  A prefetch only fills L2, so it is safe
+                // even when x is written by the previous linear later (L2 is coherent).
+                const int xlines = (int)((op.k * 2 + 127) / 128);
+                for (int ln = blockIdx.x; ln < xlines; ln += gridDim.x)
+                    asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(op.x + 64 * ln) : "memory");
                 int li = 0;
                 for (int tile = t0; tile < t1; ++tile) {
                     while (li + 1 < count && tile >= op.tile_start[li + 1]) ++li;

@@ -12,19 +12,43 @@
 #pragma once
 
 struct ActSmem {
-    uint32_t act, tsz, sx, sq, corr;
+    uint32_t act, tsz, ssq, corr;
 };
 
+// W4A8 per-group scalars are stored as pairs ssq[tok][g] = {s (fp32 bits), 8 * sum q}.
 __device__ __forceinline__ ActSmem act_layout(bool a16, uint32_t act, int64_t k, int ntok)
 {
     ActSmem L;
-    const int G = (int)(k / 32);
     L.act = act;
     L.tsz = a16 ? (uint32_t)(2 * k + 64) : (uint32_t)(k + 16);
-    L.sx = act + (uint32_t)ntok * L.tsz;          // W4A8: [ntok][G] fp32
-    L.sq = L.sx + 4u * (uint32_t)(ntok * G);      // W4A8: [ntok][G] int32
+    L.ssq = act + (uint32_t)ntok * L.tsz;         // W4A8: [ntok][G] x {fp32 s, int32 8 sum q}
     L.corr = act + (uint32_t)ntok * L.tsz;        // W4A16: [G][8] fp32
     return L;
+}
+
+// u8 x s8 dot of 4 bytes (the high nibbles kept in place: 16 c_hi as u8)
+__device__ __forceinline__ int dp4a_us(uint32_t a, int b, int c)
+{
+    int d;
+    asm("dp4a.u32.s32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+    return d;
+}
+
+// D = sum_j c_j q_j - 8 sum q over one block, exact int32: the low
+// nibbles (elements 4u..4u+3 of word u) against q words u, the high nibbles left in
+// place (16 c, elements 4u+16..) against q words 4+u, then >> 4 (exact: a multiple of 16).
+__device__ __forceinline__ int block_D(uint4 w, uint4 qa, uint4 qb, int sq8)
+{
+    int lo = 0, hi = 0;
+    lo = __dp4a((int)(w.x & 0x0F0F0F0Fu), (int)qa.x, lo);
+    hi = dp4a_us(w.x & 0xF0F0F0F0u, (int)qb.x, hi);
+    lo = __dp4a((int)(w.y & 0x0F0F0F0Fu), (int)qa.y, lo);
+    hi = dp4a_us(w.y & 0xF0F0F0F0u, (int)qb.y, hi);
+    lo = __dp4a((int)(w.z & 0x0F0F0F0Fu), (int)qa.z, lo);
+    hi = dp4a_us(w.z & 0xF0F0F0F0u, (int)qb.z, hi);
+    lo = __dp4a((int)(w.w & 0x0F0F0F0Fu), (int)qa.w, lo);
+    hi = dp4a_us(w.w & 0xF0F0F0F0u, (int)qb.w, hi);
+    return lo + (hi >> 4) - sq8;
 }
 
 // ---------------------------------------------------------------- activation staging
@@ -109,10 +133,10 @@ __device__ __forceinline__ void stage_a8(const uint16_t *xg, int64_t ldx, int nt
             // elements 8sub..8sub+7: sub 0/1 -> q_lo, sub 2/3 -> q_hi
             const uint32_t qt = L.act + (uint32_t)i * L.tsz + (sub < 2 ? 0u : K2) + 16u * g + 8u * (sub & 1);
             asm volatile("st.shared.v2.u32 [%0], {%1,%2};" ::"r"(qt), "r"(lo), "r"(hi) : "memory");
-            if (sub == 0) {
-                sts32(L.sx + 4u * (uint32_t)(i * G + g), __float_as_uint(live ? s : 0.0f));
-                sts32(L.sq + 4u * (uint32_t)(i * G + g), (uint32_t)sum);
-            }
+            if (sub == 0)
+                asm volatile("st.shared.v2.u32 [%0], {%1,%2};" ::"r"(L.ssq + 8u * (uint32_t)(i * G + g)),
+                             "r"(__float_as_uint(live ? s : 0.0f)), "r"((uint32_t)(8 * sum))
+                             : "memory");
         }
     }
 }
@@ -173,14 +197,11 @@ __device__ __forceinline__ void chunk_dp4a(uint32_t st, int nblk, int blk0, uint
         const uint4 qa1 = lds128(L.act + 16u * g1), qb1 = lds128(L.act + K2 + 16u * g1);
         const float d0 = h2f(lds16(st + scale_off(r, lane)));
         const float d1 = h2f(lds16(st + scale_off(r, lane + 32)));
-        const float s0 = __uint_as_float(lds32(L.sx + 4u * g0));
-        const float s1 = __uint_as_float(lds32(L.sx + 4u * g1));
-        const int D0 = block_sumi_dp4a(w0, make_int4(qa0.x, qa0.y, qa0.z, qa0.w),
-                                       make_int4(qb0.x, qb0.y, qb0.z, qb0.w)) - 8 * (int)lds32(L.sq + 4u * g0);
-        const int D1 = block_sumi_dp4a(w1, make_int4(qa1.x, qa1.y, qa1.z, qa1.w),
-                                       make_int4(qb1.x, qb1.y, qb1.z, qb1.w)) - 8 * (int)lds32(L.sq + 4u * g1);
-        acc = fmaf(d0 * s0, (float)D0, acc);
-        acc = fmaf(d1 * s1, (float)D1, acc);
+        const uint2 p0 = lds64(L.ssq + 8u * g0), p1 = lds64(L.ssq + 8u * g1);
+        const int D0 = block_D(w0, qa0, qb0, (int)p0.y);
+        const int D1 = block_D(w1, qa1, qb1, (int)p1.y);
+        acc = fmaf(d0 * __uint_as_float(p0.x), (float)D0, acc);
+        acc = fmaf(d1 * __uint_as_float(p1.x), (float)D1, acc);
     } else {
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
@@ -189,9 +210,9 @@ __device__ __forceinline__ void chunk_dp4a(uint32_t st, int nblk, int blk0, uint
                 const int g = blk0 + b;
                 const uint4 qa = lds128(L.act + 16u * g), qb = lds128(L.act + K2 + 16u * g);
                 const uint4 w = lds128(st + nib_off(r, b));
-                const int D = block_sumi_dp4a(w, make_int4(qa.x, qa.y, qa.z, qa.w),
-                                              make_int4(qb.x, qb.y, qb.z, qb.w)) - 8 * (int)lds32(L.sq + 4u * g);
-                acc = fmaf(h2f(lds16(st + scale_off(r, b))) * __uint_as_float(lds32(L.sx + 4u * g)), (float)D, acc);
+                const uint2 p = lds64(L.ssq + 8u * g);
+                const int D = block_D(w, qa, qb, (int)p.y);
+                acc = fmaf(h2f(lds16(st + scale_off(r, b))) * __uint_as_float(p.x), (float)D, acc);
             }
         }
     }
@@ -236,14 +257,13 @@ __device__ __forceinline__ void chunk_mma(uint32_t st, int nblk, int blk0, uint3
             int c[4];
             imma(wa, wb, b0, b1, c);
             const int c0 = 2 * t, c1 = 2 * t + 1;
-            const float s0 = c0 < ntok ? __uint_as_float(lds32(L.sx + 4u * (c0 * G + g))) : 0.f;
-            const float s1 = c1 < ntok ? __uint_as_float(lds32(L.sx + 4u * (c1 * G + g))) : 0.f;
-            const int q0 = c0 < ntok ? (int)lds32(L.sq + 4u * (c0 * G + g)) : 0;
-            const int q1 = c1 < ntok ? (int)lds32(L.sq + 4u * (c1 * G + g)) : 0;
-            acc[0] = fmaf(dA[j] * s0, (float)(c[0] - 8 * q0), acc[0]);
-            acc[1] = fmaf(dA[j] * s1, (float)(c[1] - 8 * q1), acc[1]);
-            acc[2] = fmaf(dB[j] * s0, (float)(c[2] - 8 * q0), acc[2]);
-            acc[3] = fmaf(dB[j] * s1, (float)(c[3] - 8 * q1), acc[3]);
+            const uint2 p0 = c0 < ntok ? lds64(L.ssq + 8u * (c0 * G + g)) : make_uint2(0u, 0u);
+            const uint2 p1 = c1 < ntok ? lds64(L.ssq + 8u * (c1 * G + g)) : make_uint2(0u, 0u);
+            const float s0 = __uint_as_float(p0.x), s1 = __uint_as_float(p1.x);
+            acc[0] = fmaf(dA[j] * s0, (float)(c[0] - (int)p0.y), acc[0]);
+            acc[1] = fmaf(dA[j] * s1, (float)(c[1] - (int)p1.y), acc[1]);
+            acc[2] = fmaf(dB[j] * s0, (float)(c[2] - (int)p0.y), acc[2]);
+            acc[3] = fmaf(dB[j] * s1, (float)(c[3] - (int)p1.y), acc[3]);
         } else {
             uint4 bx = make_uint4(0, 0, 0, 0);
             if (gid < ntok) bx = lds128(L.act + (uint32_t)gid * L.tsz + 64u * g + 16u * t);
