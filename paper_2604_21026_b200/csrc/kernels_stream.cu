@@ -352,7 +352,8 @@ size_t round_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 //   MCAPQ_STREAM_NOCOMPUTE 1 = consumers only drain the ring (bandwidth probe; outputs garbage)
 //   MCAPQ_STREAM_PDL       1 = API calls also launch with programmatic dependent launch
 struct Tune {
-    int smem_kb = 112, max_stages = 12, nocompute = 0, pdl = 0, trace = 0, step_smem_kb = 220, step = 1;
+    int smem_kb = 112, max_stages = 12, nocompute = 0, pdl = 0, trace = 0, step_smem_kb = 220, step = 1,
+        step_flags = 0;
 };
 const Tune &tune()
 {
@@ -365,6 +366,7 @@ const Tune &tune()
         if (const char *e = getenv("MCAPQ_STREAM_TRACE")) v.trace = atoi(e);
         if (const char *e = getenv("MCAPQ_STEP_SMEM_KB")) v.step_smem_kb = atoi(e);
         if (const char *e = getenv("MCAPQ_STEP_KERNEL")) v.step = atoi(e);
+        if (const char *e = getenv("MCAPQ_STEP_FLAGS")) v.step_flags = atoi(e);
         if (v.step_smem_kb < 60) v.step_smem_kb = 60;
         if (v.step_smem_kb > 226) v.step_smem_kb = 226;
         if (v.smem_kb < 40) v.smem_kb = 40;
@@ -533,6 +535,7 @@ cudaError_t launch_stack_step(const void *ops_dev, int nops, unsigned int *count
     a.ops = reinterpret_cast<const StackOp *>(ops_dev);
     a.nops = nops;
     a.counters = counters_dev;
+    a.flags = tune().step_flags;
     // one CTA per SM: activations for the largest K under either route, the rest is ring
     const size_t act = round_up(act_bytes(HMMA1, max_k, 1) > act_bytes(DP4A, max_k, 1) ? act_bytes(HMMA1, max_k, 1)
                                                                                            : act_bytes(DP4A, max_k, 1),

@@ -37,6 +37,7 @@ struct StackArgs {
     int stages;
     int act_off, red_off;
     unsigned long long *trace;   // debug: [nops][grid][8] or null
+    int flags;                   // debug (MCAPQ_STEP_FLAGS): 1 no compute, 2 no barrier, 4 no staging
 };
 
 __device__ __forceinline__ unsigned int ld_acquire_gpu(const unsigned int *p)
@@ -130,7 +131,7 @@ __global__ void __launch_bounds__(kThreads, 1) stack_step(const __grid_constant_
         if (a.trace) tr0 = globaltimer();
 
         // ---- wait for linear i-1 everywhere (its outputs may be this linear's input)
-        if (i > 0) {
+        if (i > 0 && !(a.flags & 2)) {
             if (threadIdx.x == 0)
                 while (ld_acquire_gpu(a.counters + (i - 1)) < gridDim.x) __nanosleep(32);
             bar_consumers();
@@ -138,10 +139,12 @@ __global__ void __launch_bounds__(kThreads, 1) stack_step(const __grid_constant_
         if (a.trace) tr1 = globaltimer();
         const bool a16 = route == MCAPQ_W4A16;
         const ActSmem L = act_layout(a16, act, k, 1);
-        if (a16)
-            stage_a16<true>(op.x, k, 1, k, L, threadIdx.x, kConsumerWarps * 32);
-        else
-            stage_a8<true>(op.x, k, 1, k, L, threadIdx.x, kConsumerWarps * 32);
+        if (!(a.flags & 4)) {
+            if (a16)
+                stage_a16<true>(op.x, k, 1, k, L, threadIdx.x, kConsumerWarps * 32);
+            else
+                stage_a8<true>(op.x, k, 1, k, L, threadIdx.x, kConsumerWarps * 32);
+        }
         bar_consumers();
         if (a.trace) tr2 = globaltimer();
 
@@ -155,10 +158,13 @@ __global__ void __launch_bounds__(kThreads, 1) stack_step(const __grid_constant_
                 const int blk0 = ch * kChunkBlocks;
                 mbar_wait(full + 8u * s, ph);
                 const uint32_t st = ring + (uint32_t)s * kStageBytes;
-                if (a16)
+                if (a.flags & 1) {
+                    // debug: drain only
+                } else if (a16) {
                     chunk_mma<HMMA1>(st, nblk, blk0, (uint32_t)K2, L, G, 1, warp, lane, kNib2, kMagic, acc);
-                else
+                } else {
                     chunk_dp4a(st, nblk, blk0, (uint32_t)K2, L, warp, lane, acc[0]);
+                }
                 __syncwarp();
                 if (lane == 0) mbar_arrive(empty + 8u * s);
                 if (++s == S) {
