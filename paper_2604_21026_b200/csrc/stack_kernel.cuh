@@ -74,7 +74,20 @@ __global__ void __launch_bounds__(kThreads, 1) stack_step(const __grid_constant_
             const uint64_t pol = evict_first_policy();
             int s = 0;
             uint32_t ph = 0;
+            auto prefetch_maps = [&](int j) {
+                // TMA descriptors of linear j into the TMA unit's cache before first use
+                if (j >= a.nops) return;
+                for (int m = 0; m < a.ops[j].count; ++m) {
+                    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(a.ops[j].maps[m]))
+                                 : "memory");
+                    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(a.ops[j].maps[m] + 1))
+                                 : "memory");
+                }
+            };
+            prefetch_maps(0);
+            prefetch_maps(1);
             for (int i = 0; i < a.nops; ++i) {
+                prefetch_maps(i + 2);
                 const StackOp &op = a.ops[i];
                 const int count = op.count;
                 const int K2 = (int)(op.k / 2);
