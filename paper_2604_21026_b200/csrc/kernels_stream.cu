@@ -543,10 +543,15 @@ cudaError_t launch_stack_step(const void *ops_dev, int nops, unsigned int *count
     const size_t budget = (size_t)tune().step_smem_kb * 1024;
     int S = (int)(((long)budget - 1024 - 128 - (long)act - kRedBytes) / kStageBytes);
     S = S < 2 ? 2 : (S > 16 ? 16 : S);
+    const size_t prog = round_up(sizeof(StackOp) * (size_t)nops, 128);
+    S = (int)((long)S - (long)((prog + kStageBytes - 1) / kStageBytes));   // the program copy shares the budget
+    S = S < 2 ? 2 : S;
     a.stages = S;
-    a.act_off = S * kStageBytes + 128;
+    a.ops_off = S * kStageBytes + 128;
+    a.act_off = (int)(a.ops_off + prog);
     a.red_off = (int)(a.act_off + act);
     const size_t smem = 1024 + (size_t)a.red_off + kRedBytes;
+    if (smem > 227 * 1024) return cudaErrorInvalidValue;
     const int grid = device_sms();
     if (tune().trace) {
         // debug timeline: [op][cta] records at the start of the trace buffer

@@ -29,13 +29,14 @@ struct StackOp {
     int64_t k;
     const uint16_t *x;
 };
+static_assert(sizeof(StackOp) % 16 == 0, "StackOp is copied to shared memory in 16-byte pieces");
 
 struct StackArgs {
     const StackOp *ops;          // device array [nops]
     int nops;
     unsigned int *counters;      // [nops], zero at launch: CTAs done with linear i
     int stages;
-    int act_off, red_off;
+    int ops_off, act_off, red_off;   // shared-memory offsets of the program copy, activations, reduction
     unsigned long long *trace;   // debug: [nops][grid][8] or null
     int flags;                   // debug (MCAPQ_STEP_FLAGS): 1 no compute, 2 no barrier, 4 no staging
 };
@@ -66,6 +67,15 @@ __global__ void __launch_bounds__(kThreads, 1) stack_step(const __grid_constant_
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
+    // the program (a few KB) into shared memory once: op records are read at every
+    // linear boundary by the producer and the consumers, never from global again
+    StackOp *ops = reinterpret_cast<StackOp *>(smem_raw + (sb - smem_addr(smem_raw)) + a.ops_off);
+    {
+        const uint4 *src = reinterpret_cast<const uint4 *>(a.ops);
+        uint4 *dst = reinterpret_cast<uint4 *>(ops);
+        const int n16 = (int)(sizeof(StackOp) * a.nops / 16);
+        for (int i = threadIdx.x; i < n16; i += blockDim.x) dst[i] = src[i];
+    }
     __syncthreads();
 
     if (warp == kConsumerWarps) {
@@ -77,10 +87,10 @@ __global__ void __launch_bounds__(kThreads, 1) stack_step(const __grid_constant_
             auto prefetch_maps = [&](int j) {
                 // TMA descriptors of linear j into the TMA unit's cache before first use
                 if (j >= a.nops) return;
-                for (int m = 0; m < a.ops[j].count; ++m) {
-                    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(a.ops[j].maps[m]))
+                for (int m = 0; m < ops[j].count; ++m) {
+                    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(ops[j].maps[m]))
                                  : "memory");
-                    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(a.ops[j].maps[m] + 1))
+                    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(ops[j].maps[m] + 1))
                                  : "memory");
                 }
             };
@@ -88,7 +98,7 @@ __global__ void __launch_bounds__(kThreads, 1) stack_step(const __grid_constant_
             prefetch_maps(1);
             for (int i = 0; i < a.nops; ++i) {
                 prefetch_maps(i + 2);
-                const StackOp &op = a.ops[i];
+                const StackOp &op = ops[i];
                 const int count = op.count;
                 const int K2 = (int)(op.k / 2);
                 const int nchunks = (K2 + kChunkBytes - 1) / kChunkBytes;
@@ -131,7 +141,7 @@ __global__ void __launch_bounds__(kThreads, 1) stack_step(const __grid_constant_
     int s = 0;
     uint32_t ph = 0;
     for (int i = 0; i < a.nops; ++i) {
-        const StackOp &op = a.ops[i];
+        const StackOp &op = ops[i];
         const int count = op.count, route = op.route;
         const int64_t k = op.k;
         const int G = (int)(k / 32);
