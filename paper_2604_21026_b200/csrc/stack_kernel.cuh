@@ -203,10 +203,8 @@ __global__ void __launch_bounds__(kThreads, 1) stack_step(const __grid_constant_
         }
         // ---- publish: this CTA's rows of every y of linear i are stored
         bar_consumers();
-        if (threadIdx.x == 0) {
-            __threadfence();
-            atomicAdd(a.counters + i, 1u);
-        }
+        if (threadIdx.x == 0)   // release RMW at gpu scope: the CTA's y stores (ordered by bar.sync) first
+            asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(a.counters + i) : "memory");
         if (a.trace && threadIdx.x == 0) {
             unsigned long long *r = a.trace + 8ull * ((unsigned long long)i * gridDim.x + blockIdx.x);
             r[0] = (unsigned long long)i;
