@@ -53,6 +53,8 @@ constexpr int kChunkBlocks = kChunkBytes / 16;     // 64 Q4_0 blocks
 constexpr int kBox = 128 * kTileRows;              // one {128 B x 16 rows} TMA box
 constexpr int kStageBytes = 8 * kBox + kBox;       // 8 nibble boxes + 1 scale box (18 KiB)
 constexpr int kRedBytes = kConsumerWarps * kTileRows * 8 * 4;
+constexpr int kMaxStages = 16;
+constexpr int kBarBytes = 512;                     // mbarriers: full[S] + empty[S] + done + go <= 16*16 + 16
 
 // HMMA1: W4A16 with a single token (only MMA column 0 is computed);  NONE: bandwidth probe
 enum Engine { DP4A = 0, IMMA = 1, HMMA = 2, NONE = 3, HMMA1 = 4 };
@@ -386,12 +388,13 @@ size_t plan_smem(int engine, int64_t k, int ntok, StreamArgs &a)
     const size_t xraw = 0;   // x is read from global directly (no smem staging copy)
     (void)ntok;
     const size_t act = round_up(act_bytes(engine, k, ntok), 128);
-    const size_t fixed = 128 + xraw + act + kRedBytes;
+    const size_t fixed = kBarBytes + xraw + act + kRedBytes;
     const size_t budget = (size_t)tune().smem_kb * 1024;
     int S = (int)(((long)budget - (long)fixed - 1024) / kStageBytes);
     S = S < 2 ? 2 : (S > tune().max_stages ? tune().max_stages : S);
+    S = S > kMaxStages ? kMaxStages : S;
     a.stages = S;
-    a.xraw_off = (int)((size_t)S * kStageBytes + 128);
+    a.xraw_off = (int)((size_t)S * kStageBytes + kBarBytes);
     a.act_off = (int)(a.xraw_off + xraw);
     a.red_off = (int)(a.act_off + act);
     return 1024 + (size_t)a.red_off + kRedBytes;
@@ -541,13 +544,11 @@ cudaError_t launch_stack_step(const void *ops_dev, int nops, unsigned int *count
                                                                                            : act_bytes(DP4A, max_k, 1),
                                 128);
     const size_t budget = (size_t)tune().step_smem_kb * 1024;
-    int S = (int)(((long)budget - 1024 - 128 - (long)act - kRedBytes) / kStageBytes);
-    S = S < 2 ? 2 : (S > 16 ? 16 : S);
     const size_t prog = round_up(sizeof(StackOp) * (size_t)nops, 128);
-    S = (int)((long)S - (long)((prog + kStageBytes - 1) / kStageBytes));   // the program copy shares the budget
-    S = S < 2 ? 2 : S;
+    int S = (int)(((long)budget - 1024 - (long)kBarBytes - (long)prog - (long)act - kRedBytes) / kStageBytes);
+    S = S < 2 ? 2 : (S > kMaxStages ? kMaxStages : S);
     a.stages = S;
-    a.ops_off = S * kStageBytes + 128;
+    a.ops_off = S * kStageBytes + kBarBytes;
     a.act_off = (int)(a.ops_off + prog);
     a.red_off = (int)(a.act_off + act);
     const size_t smem = 1024 + (size_t)a.red_off + kRedBytes;
@@ -564,7 +565,7 @@ cudaError_t launch_stack_step(const void *ops_dev, int nops, unsigned int *count
     }
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid);
-    cfg.blockDim = dim3(kThreads);
+    cfg.blockDim = dim3(kStepThreads);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = s;
     cudaLaunchAttribute attr[1];
@@ -592,7 +593,7 @@ int stream_tokens_per_pass(int route, int64_t k)
     const int engine = route == MCAPQ_W4A16 ? HMMA : IMMA;
     int tp = 8;
     while (tp > 1) {
-        const size_t need = 1024 + 128 +
+        const size_t need = 1024 + kBarBytes +
                             round_up(act_bytes(engine, k, tp), 128) + kRedBytes + 2 * (size_t)kStageBytes;
         if (need <= 112 * 1024) break;
         --tp;

@@ -48,7 +48,9 @@ __device__ __forceinline__ unsigned int ld_acquire_gpu(const unsigned int *p)
     return v;
 }
 
-__global__ void __launch_bounds__(kThreads, 1) stack_step(const __grid_constant__ StackArgs a)
+constexpr int kStepThreads = (kConsumerWarps + 2) * 32;   // consumers + producer warp + sync warp
+
+__global__ void __launch_bounds__(kStepThreads, 1) stack_step(const __grid_constant__ StackArgs a)
 {
     extern __shared__ __align__(16) uint8_t smem_raw[];
     const uint32_t sb = (smem_addr(smem_raw) + 1023u) & ~1023u;
@@ -57,6 +59,8 @@ __global__ void __launch_bounds__(kThreads, 1) stack_step(const __grid_constant_
     const uint32_t ring = sb;
     const uint32_t full = sb + (uint32_t)S * kStageBytes;
     const uint32_t empty = full + 8u * S;
+    const uint32_t done = empty + 8u * S;   // phase i: every consumer warp finished linear i
+    const uint32_t go = done + 8u;          // phase i: linear i finished in every CTA
     const uint32_t act = sb + a.act_off;
     const uint32_t red = sb + a.red_off;
 
@@ -65,6 +69,8 @@ __global__ void __launch_bounds__(kThreads, 1) stack_step(const __grid_constant_
             mbar_init(full + 8u * s, 1);
             mbar_init(empty + 8u * s, kConsumerWarps);
         }
+        mbar_init(done, kConsumerWarps);
+        mbar_init(go, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     // the program (a few KB) into shared memory once: op records are read at every
@@ -77,6 +83,24 @@ __global__ void __launch_bounds__(kThreads, 1) stack_step(const __grid_constant_
         for (int i = threadIdx.x; i < n16; i += blockDim.x) dst[i] = src[i];
     }
     __syncthreads();
+
+    if (warp == kConsumerWarps + 1) {
+        // ================= sync warp: publish and await linears, off the consumers' path =====
+        // done(i) -> release-add counters[i] (the CTA's y_i stores, ordered by the
+        // consumers' mbarrier arrives, become visible at gpu scope first) -> poll until
+        // every CTA published -> go(i) releases the consumers into linear i+1.
+        if (lane == 0) {
+            for (int i = 0; i < a.nops; ++i) {
+                mbar_wait(done, (uint32_t)i & 1u);
+                asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(a.counters + i) : "memory");
+                if (i + 1 == a.nops) break;
+                if (!(a.flags & 2))
+                    while (ld_acquire_gpu(a.counters + i) < gridDim.x) __nanosleep(20);
+                mbar_arrive(go);
+            }
+        }
+        return;
+    }
 
     if (warp == kConsumerWarps) {
         // ================= producer: the whole step's weights, in op order =================
@@ -154,11 +178,7 @@ __global__ void __launch_bounds__(kThreads, 1) stack_step(const __grid_constant_
         if (a.trace) tr0 = globaltimer();
 
         // ---- wait for linear i-1 everywhere (its outputs may be this linear's input)
-        if (i > 0 && !(a.flags & 2)) {
-            if (threadIdx.x == 0)
-                while (ld_acquire_gpu(a.counters + (i - 1)) < gridDim.x) __nanosleep(32);
-            bar_consumers();
-        }
+        if (i > 0) mbar_wait(go, (uint32_t)(i - 1) & 1u);
         if (a.trace) tr1 = globaltimer();
         const bool a16 = route == MCAPQ_W4A16;
         const ActSmem L = act_layout(a16, act, k, 1);
@@ -201,10 +221,9 @@ __global__ void __launch_bounds__(kThreads, 1) stack_step(const __grid_constant_
             else
                 epilogue_dp4a(acc[0], row0, op.n[li], op.y[li], op.ydt, 0, warp, lane);
         }
-        // ---- publish: this CTA's rows of every y of linear i are stored
-        bar_consumers();
-        if (threadIdx.x == 0)   // release RMW at gpu scope: the CTA's y stores (ordered by bar.sync) first
-            asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(a.counters + i) : "memory");
+        // ---- this warp's rows of linear i are stored: tell the sync warp (no CTA-wide wait)
+        __syncwarp();
+        if (lane == 0) mbar_arrive(done);
         if (a.trace && threadIdx.x == 0) {
             unsigned long long *r = a.trace + 8ull * ((unsigned long long)i * gridDim.x + blockIdx.x);
             r[0] = (unsigned long long)i;
