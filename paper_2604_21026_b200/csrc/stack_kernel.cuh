@@ -89,7 +89,7 @@ __global__ void __launch_bounds__(kStepThreads, 1) stack_step(const __grid_const
         // done(i) -> release-add counters[i] (the CTA's y_i stores, ordered by the
         // consumers' mbarrier arrives, become visible at gpu scope first) -> poll until
         // every CTA published -> go(i) releases the consumers into linear i+1.
-        if (lane == 0) {
+        if (lane == 0 && !(a.flags & 8)) {
             for (int i = 0; i < a.nops; ++i) {
                 mbar_wait(done, (uint32_t)i & 1u);
                 asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(a.counters + i) : "memory");
@@ -178,7 +178,7 @@ __global__ void __launch_bounds__(kStepThreads, 1) stack_step(const __grid_const
         if (a.trace) tr0 = globaltimer();
 
         // ---- wait for linear i-1 everywhere (its outputs may be this linear's input)
-        if (i > 0) mbar_wait(go, (uint32_t)(i - 1) & 1u);
+        if (i > 0 && !(a.flags & 8)) mbar_wait(go, (uint32_t)(i - 1) & 1u);
         if (a.trace) tr1 = globaltimer();
         const bool a16 = route == MCAPQ_W4A16;
         const ActSmem L = act_layout(a16, act, k, 1);
