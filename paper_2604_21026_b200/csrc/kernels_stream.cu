@@ -354,7 +354,9 @@ size_t round_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 //   MCAPQ_STREAM_NOCOMPUTE 1 = consumers only drain the ring (bandwidth probe; outputs garbage)
 //   MCAPQ_STREAM_PDL       1 = API calls also launch with programmatic dependent launch
 struct Tune {
-    int smem_kb = 112, max_stages = 12, nocompute = 0, pdl = 0, trace = 0, step_smem_kb = 220, step = 1,
+    // step_smem_kb 120: a ~5-stage ring keeps the HBM pipe busy while bounding the
+    // per-SM queue of in-flight weight data that the chain's L2 accesses wait behind
+    int smem_kb = 112, max_stages = 12, nocompute = 0, pdl = 0, trace = 0, step_smem_kb = 120, step = 1,
         step_flags = 0;
 };
 const Tune &tune()

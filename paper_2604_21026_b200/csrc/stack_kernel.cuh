@@ -38,7 +38,7 @@ struct StackArgs {
     int stages;
     int ops_off, act_off, red_off;   // shared-memory offsets of the program copy, activations, reduction
     unsigned long long *trace;   // debug: [nops][grid][8] or null
-    int flags;                   // debug (MCAPQ_STEP_FLAGS): 1 no compute, 2 no barrier, 4 no staging
+    int flags;                   // debug (MCAPQ_STEP_FLAGS): 1 no compute, 2 no grid barrier, 4 no staging, 8 no chain
 };
 
 __device__ __forceinline__ unsigned int ld_acquire_gpu(const unsigned int *p)

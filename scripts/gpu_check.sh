@@ -1,5 +1,5 @@
 #!/bin/bash
-# One gpurun call: GPU parity tests, smoke, bench, ncu launch list + one full capture.
+# One gpurun call: GPU parity tests, smoke, bench, ncu launch list + full captures.
 # Usage (from the repo root, on the GPU box): bash scripts/gpu_check.sh [tag]
 TAG=${1:-r1}
 OUT=gpurun_out/$TAG
@@ -9,12 +9,19 @@ python __graft_entry__.py > $OUT/build.log 2>&1
 timeout 1200 python -m pytest tests -m gpu -x -q > $OUT/pytest_gpu.log 2>&1; echo "pytest exit $?" >> $OUT/pytest_gpu.log
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $OUT/smoke.log 2>&1; echo "smoke exit $?" >> $OUT/smoke.log
 timeout 900 python bench.py > $OUT/bench.json 2> $OUT/bench.err; echo "bench exit $?" >> $OUT/bench.err
+timeout 300 python scripts/kbench.py --cases o_1b,qkv_1b,gateup_1b,down_1b,gate_8b,down_8b,lmhead_8b > $OUT/kbench.jsonl 2>&1
 if [ "${NCU:-1}" = "1" ]; then
-  timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:'gemv|tc_linear|quant_a8|stream_linear' -c 300 --csv \
-     --log-file $OUT/launches.csv python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-extras > $OUT/ncu_launch.log 2>&1
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:stream_linear -s 42 -c 1 \
-     -o $OUT/prof_w4a8 python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-extras > $OUT/ncu_full.log 2>&1
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:stream_linear -s 62 -c 1 \
-     -o $OUT/prof_w4a16 python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-extras > $OUT/ncu_full16.log 2>&1
+  # every launch of a short bench run with its device time (cold-cache, serialised: compare shares)
+  timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:'stack_step|stream_linear|gemv|tc_linear|quant_a8' \
+     -c 400 --csv --log-file $OUT/launches.csv python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-extras > $OUT/ncu_launch.log 2>&1
+  # the headline step kernel (whole 16-layer step in one launch)
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:stack_step -s 3 -c 1 \
+     -o $OUT/prof_step python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-extras > $OUT/ncu_step.log 2>&1
+  # the dominant per-linear kernel: W4A8 grouped gate+up (bench's roofline kernel)
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:stream_linear -s 8 -c 1 \
+     -o $OUT/prof_w4a8 python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-extras > $OUT/ncu_w4a8.log 2>&1
+  # W4A16 (HMMA1 engine) on the 8B lm_head
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:stream_linear -s 2 -c 1 \
+     -o $OUT/prof_w4a16 python scripts/kbench.py --cases lmhead_8b --routes 1 --reps 2 > $OUT/ncu_w4a16.log 2>&1
 fi
 echo done > $OUT/DONE
