@@ -40,6 +40,22 @@ MODEL = "llama-3.2-1b"
 CONFIG_ID = 2
 
 
+def traffic_from_profiles(kernel_prefix):
+    """DRAM bytes (read + write) per launch of `kernel_prefix` from the newest committed
+    ncu --set full summary (profiles/<round>/summary.json), or None."""
+    pdir = os.path.join(ROOT, "profiles")
+    if not os.path.isdir(pdir):
+        return None, None
+    for sub in sorted(os.listdir(pdir), reverse=True):
+        p = os.path.join(pdir, sub, "summary.json")
+        if not os.path.exists(p):
+            continue
+        for cap, e in json.load(open(p)).get("captures", {}).items():
+            if kernel_prefix in e.get("kernel", "") and e.get("dram_read_bytes") is not None:
+                return int(e["dram_read_bytes"] + (e.get("dram_write_bytes") or 0)), f"profiles/{sub}/{cap}"
+    return None, None
+
+
 def peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
@@ -411,6 +427,7 @@ def main():
     k_ms, k_bytes, k_reps = time_dominant_kernel(mq, weights, xs, stream)
     peak, peak_src = peaks()
     achieved = k_bytes / (k_ms * 1e-3) / 1e9
+    traffic, traffic_src = traffic_from_profiles("stream_linear<0>")
 
     extras = [] if args.no_extras or rank != 0 else time_single_linears(mq, dev, stream)
 
@@ -441,7 +458,8 @@ def main():
                                  "all_w4a16_us_per_layer": round(ms16 * 1000 / L, 3),
                                  "w4a8_over_w4a16": round(ms16 / ms8, 3)},
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-                         "frac": round(achieved / peak, 4), "traffic": None,
+                         "frac": round(achieved / peak, 4), "traffic": traffic,
+                         "traffic_source": traffic_src,
                          "kernel": "stream_linear<DP4A> grouped gate+up (2 x 8192x2048, M=1, fused quantiser)",
                          "alg_bytes_per_launch": k_bytes, "us_per_launch": round(k_ms * 1000, 3),
                          "launches_timed": k_reps, "peak_source": peak_src,
