@@ -235,6 +235,14 @@ void mcapq_profile_free(mcapq_profile *p);
  * (A15).  The library owns a workspace and, after mcapq_stack_capture, a CUDA
  * graph that replays the whole step.
  *
+ * Chaining: a slot's x may be an earlier slot's y (the decode chain, e.g. the
+ * o input = the q output).  Ordering follows the buffers: a slot reads its x
+ * only after every earlier writer of those bytes stored it, and writes its y
+ * only after earlier readers/writers of those bytes are done.  At m = 1 an x
+ * that is exactly an earlier bf16 y is passed by dataflow inside the
+ * persistent step kernel (no grid barrier).  A slot's y must not overlap its
+ * own x.
+ *
  * mcapq_stack_create   : L layers, routes_host[L] (0/1), max_m tokens.
  * mcapq_stack_set      : register slot s of layer l: weight (device), the
  *                        device input x [m][k] bf16 and output y [m][n] (ydt),
@@ -245,14 +253,19 @@ void mcapq_profile_free(mcapq_profile *p);
  * mcapq_stack_weight_bytes : total packed weight bytes (nib + scale).
  * mcapq_stack_launches : kernels one run launches.
  * mcapq_stack_host_bytes : bytes of one step's inputs (which = 0: every distinct
- *                        (layer, input_id) x, in that order, [m][k] bf16 each)
+ *                        (layer, input_id) x that is a step input -- not written
+ *                        by an earlier slot's y -- in that order, [m][k] bf16 each)
  *                        or outputs (which = 1: every slot's y in (layer, slot)
  *                        order, [m][n] of its ydt), packed back to back.
  * mcapq_stack_step_host : one end-to-end step from HOST memory: copy x_host
  *                        (pinned, the packed inputs) into the registered device
  *                        inputs, replay the captured graph (or run, if none was
  *                        captured for m), copy every output into y_host (pinned,
- *                        packed).  Asynchronous on `stream`.
+ *                        packed).  Asynchronous on `stream`.  Copies are merged
+ *                        wherever consecutive slots are contiguous in device
+ *                        memory (inputs placed in one arena in (layer, input_id)
+ *                        order and outputs in (layer, slot) order => one H2D and
+ *                        one D2H per step).
  */
 typedef struct mcapq_stack mcapq_stack;
 mcapq_status mcapq_stack_create(int layers, const uint8_t *routes_host, int64_t max_m, mcapq_stack **out);

@@ -356,8 +356,8 @@ size_t round_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 struct Tune {
     // step_smem_kb 120: a ~5-stage ring keeps the HBM pipe busy while bounding the
     // per-SM queue of in-flight weight data that the chain's L2 accesses wait behind
-    int smem_kb = 112, max_stages = 12, nocompute = 0, pdl = 0, trace = 0, step_smem_kb = 120, step = 1,
-        step_flags = 0;
+    int smem_kb = 112, max_stages = 12, nocompute = 0, pdl = 0, trace = 0, step_smem_kb = 200, step = 1,
+        step_flags = 0, step_spin_ns = 32, step_polls = 3;
 };
 const Tune &tune()
 {
@@ -371,6 +371,8 @@ const Tune &tune()
         if (const char *e = getenv("MCAPQ_STEP_SMEM_KB")) v.step_smem_kb = atoi(e);
         if (const char *e = getenv("MCAPQ_STEP_KERNEL")) v.step = atoi(e);
         if (const char *e = getenv("MCAPQ_STEP_FLAGS")) v.step_flags = atoi(e);
+        if (const char *e = getenv("MCAPQ_STEP_SPIN_NS")) v.step_spin_ns = atoi(e);
+        if (const char *e = getenv("MCAPQ_STEP_POLLS")) v.step_polls = atoi(e);
         if (v.step_smem_kb < 60) v.step_smem_kb = 60;
         if (v.step_smem_kb > 226) v.step_smem_kb = 226;
         if (v.smem_kb < 40) v.smem_kb = 40;
@@ -501,7 +503,8 @@ const CUtensorMap *stream_descriptors(const uint8_t *nib, const uint16_t *scale,
 size_t stack_op_bytes() { return sizeof(StackOp); }
 bool stack_step_enabled() { return tune().step != 0 && encode_fn() != nullptr; }
 
-bool stack_fill_op(void *host_op, int route, const StreamGroup &g, const uint16_t *x, int ydt, cudaStream_t s)
+bool stack_fill_op(void *host_op, int route, const StreamGroup &g, const uint16_t *x, int ydt, const StackDeps &d,
+                   cudaStream_t s)
 {
     StackOp op;
     memset(&op, 0, sizeof(op));
@@ -510,7 +513,7 @@ bool stack_fill_op(void *host_op, int route, const StreamGroup &g, const uint16_
         op.maps[i] = stream_descriptors(g.nib[i], g.scale[i], g.n[i], g.k, s);
         if (!op.maps[i]) return false;
         op.y[i] = g.y[i];
-        op.n[i] = g.n[i];
+        op.n[i] = (int)g.n[i];
         op.tile_start[i] = tiles;
         tiles += (int)((g.n[i] + kTileRows - 1) / kTileRows);
     }
@@ -520,6 +523,11 @@ bool stack_fill_op(void *host_op, int route, const StreamGroup &g, const uint16_
     op.ydt = ydt;
     op.k = g.k;
     op.x = x;
+    op.xt = d.xt;
+    op.xt_op = d.xt_op;
+    for (int i = 0; i < g.count; ++i) op.yt[i] = d.yt[i];
+    op.wait_op = d.wait_op;
+    op.publish = d.publish;
     memcpy(host_op, &op, sizeof(op));
     return true;
 }
@@ -529,18 +537,21 @@ cudaError_t launch_stack_step(const void *ops_dev, int nops, unsigned int *count
 {
     static int attr_done = 0;
     if (!attr_done) {
-        cudaError_t e = cudaFuncSetAttribute(stack_step, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+        cudaError_t e = cudaFuncSetAttribute(stack_step<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             227 * 1024);
+        if (e == cudaSuccess)
+            e = cudaFuncSetAttribute(stack_step<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
         if (e != cudaSuccess) return e;
         attr_done = 1;
     }
-    cudaError_t e = cudaMemsetAsync(counters_dev, 0, sizeof(unsigned int) * (size_t)nops, s);
-    if (e != cudaSuccess) return e;
     StackArgs a;
     memset(&a, 0, sizeof(a));
     a.ops = reinterpret_cast<const StackOp *>(ops_dev);
     a.nops = nops;
     a.counters = counters_dev;
     a.flags = tune().step_flags;
+    a.spin_ns = tune().step_spin_ns;
+    a.polls = tune().step_polls;
     // one CTA per SM: activations for the largest K under either route, the rest is ring
     const size_t act = round_up(act_bytes(HMMA1, max_k, 1) > act_bytes(DP4A, max_k, 1) ? act_bytes(HMMA1, max_k, 1)
                                                                                            : act_bytes(DP4A, max_k, 1),
@@ -575,7 +586,7 @@ cudaError_t launch_stack_step(const void *ops_dev, int nops, unsigned int *count
     attr[0].val.cooperative = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, stack_step, a);
+    return a.trace ? cudaLaunchKernelEx(&cfg, stack_step<true>, a) : cudaLaunchKernelEx(&cfg, stack_step<false>, a);
 }
 
 size_t stream_trace_read(unsigned long long *host_out, size_t max_records)

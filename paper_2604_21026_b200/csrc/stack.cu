@@ -42,7 +42,8 @@ struct mcapq_stack {
     // persistent step program (M = 1): one op per launch group, executed by stack_step
     bool prog_dirty = true, prog_ok = false;
     void *ops_dev = nullptr, *ops_host = nullptr;
-    unsigned int *counters = nullptr;
+    unsigned int *counters = nullptr;   // [nops] + exit count + epoch
+    uint32_t *tags = nullptr;           // tagged copies of outputs consumed inside the step
     int nops = 0;
     int64_t max_k = 0;
 };
@@ -54,8 +55,10 @@ static void free_program(mcapq_stack *st)
     if (st->ops_dev) cudaFree(st->ops_dev);
     if (st->ops_host) cudaFreeHost(st->ops_host);
     if (st->counters) cudaFree(st->counters);
+    if (st->tags) cudaFree(st->tags);
     st->ops_dev = st->ops_host = nullptr;
     st->counters = nullptr;
+    st->tags = nullptr;
     st->nops = 0;
     st->prog_ok = false;
 }
@@ -166,9 +169,22 @@ static StreamGroup group_of(const mcapq_stack *st, int l, int first, int cnt)
     return g;
 }
 
+// Byte range [lo, hi) of a buffer.
+struct Range {
+    uintptr_t lo, hi;
+    bool overlaps(const Range &o) const { return lo < o.hi && o.lo < hi; }
+};
+
 // Build the persistent-step program (one op per launch group, in decode order) in
 // device memory.  Host-synchronous: call outside graph capture.  prog_ok stays
 // false when a group is off the TMA fast path (then the per-linear path runs).
+//
+// Dependencies between ops come from the registered buffers (M = 1):
+//   x_i == y_j (latest writer of any byte of x_i, whole buffer, bf16) -> dataflow:
+//       op j also writes a tagged copy of y_j, op i reads it (no barrier);
+//   any other overlap of x_i with an earlier y, or of y_i with an earlier plain-read
+//       x or an earlier y (WAR / WAW)  -> barrier on the latest such op;
+//   otherwise none: x_i is an input of the step.
 static mcapq_status build_program(mcapq_stack *st)
 {
     free_program(st);
@@ -183,22 +199,102 @@ static mcapq_status build_program(mcapq_stack *st)
             return MCAPQ_OK;
         });
     if (!all_fast || groups.empty()) return MCAPQ_OK;
-    const size_t ob = stack_op_bytes();
-    st->nops = (int)groups.size();
-    MCAPQ_CUDA_TRY(cudaMallocHost(&st->ops_host, ob * st->nops));
-    MCAPQ_CUDA_TRY(cudaMalloc(&st->ops_dev, ob * st->nops));
-    MCAPQ_CUDA_TRY(cudaMalloc(&st->counters, sizeof(unsigned int) * st->nops));
+    const int nops = (int)groups.size();
+    std::vector<StreamGroup> gs(nops);
+    std::vector<const Slot *> heads(nops);
     st->max_k = 0;
-    for (int i = 0; i < st->nops; ++i) {
+    for (int i = 0; i < nops; ++i) {
         const int l = groups[i].first, first = groups[i].second.first, cnt = groups[i].second.second;
-        const StreamGroup g = group_of(st, l, first, cnt);
-        const Slot &a = st->slots[(size_t)l * kMaxSlots + first];
-        MCAPQ_REQUIRE(stack_fill_op(reinterpret_cast<uint8_t *>(st->ops_host) + ob * i, st->routes[l], g, a.x,
-                                    a.ydt, nullptr),
-                      MCAPQ_ECUDA, "stack op %d: TMA descriptor encode failed", i);
-        st->max_k = g.k > st->max_k ? g.k : st->max_k;
+        gs[i] = group_of(st, l, first, cnt);
+        heads[i] = &st->slots[(size_t)l * kMaxSlots + first];
+        st->max_k = gs[i].k > st->max_k ? gs[i].k : st->max_k;
     }
-    MCAPQ_CUDA_TRY(cudaMemcpy(st->ops_dev, st->ops_host, ob * st->nops, cudaMemcpyHostToDevice));
+    if (st->max_k > kStepMaxK) return MCAPQ_OK;
+
+    // ---- dependencies
+    auto xr = [&](int i) {
+        const uintptr_t p = reinterpret_cast<uintptr_t>(heads[i]->x);
+        return Range{p, p + (uintptr_t)(2 * gs[i].k)};
+    };
+    auto yr = [&](int i, int m) {
+        const uintptr_t p = reinterpret_cast<uintptr_t>(gs[i].y[m]);
+        return Range{p, p + (uintptr_t)(gs[i].n[m] * (heads[i]->ydt == MCAPQ_F32 ? 4 : 2))};
+    };
+    std::vector<StackDeps> deps(nops);
+    std::vector<int> src_op(nops, -1), src_m(nops, -1);
+    for (int i = 0; i < nops; ++i) {
+        StackDeps &d = deps[i];
+        d.xt = nullptr;
+        d.xt_op = -1;
+        for (int m = 0; m < kMaxGroup; ++m) d.yt[m] = nullptr;
+        d.wait_op = -1;
+        d.publish = 0;
+        // RAW on x_i: the latest earlier writer of any byte of x_i
+        const Range x = xr(i);
+        for (int j = i - 1; j >= 0 && src_op[i] < 0 && d.wait_op < 0; --j)
+            for (int m = 0; m < gs[j].count; ++m) {
+                const Range y = yr(j, m);
+                if (!y.overlaps(x)) continue;
+                if (y.lo == x.lo && y.hi == x.hi && heads[j]->ydt == MCAPQ_BF16) {
+                    src_op[i] = j;
+                    src_m[i] = m;
+                } else {
+                    d.wait_op = j;
+                }
+                break;
+            }
+        // WAR / WAW on y_i
+        for (int j = i - 1; j > d.wait_op; --j) {
+            bool hit = false;
+            for (int m = 0; m < gs[i].count && !hit; ++m) {
+                const Range y = yr(i, m);
+                // an earlier op reads its x from memory unless it is a dataflow consumer
+                if (src_op[j] < 0 && xr(j).overlaps(y)) hit = true;
+                for (int mm = 0; mm < gs[j].count && !hit; ++mm)
+                    if (yr(j, mm).overlaps(y)) hit = true;
+            }
+            if (hit) {
+                d.wait_op = j;
+                break;
+            }
+        }
+    }
+    // tagged buffers: one per (producer op, member) that feeds a dataflow consumer
+    std::vector<std::vector<size_t>> tag_off(nops, std::vector<size_t>(kMaxGroup, (size_t)-1));
+    size_t tag_words = 0;
+    for (int i = 0; i < nops; ++i)
+        if (src_op[i] >= 0 && tag_off[src_op[i]][src_m[i]] == (size_t)-1) {
+            tag_off[src_op[i]][src_m[i]] = tag_words;
+            tag_words += (size_t)((gs[src_op[i]].n[src_m[i]] + 3) / 4 * 4);
+        }
+    if (tag_words) {
+        MCAPQ_CUDA_TRY(cudaMalloc(&st->tags, tag_words * 4));
+        MCAPQ_CUDA_TRY(cudaMemset(st->tags, 0, tag_words * 4));
+    }
+    for (int i = 0; i < nops; ++i) {
+        for (int m = 0; m < gs[i].count; ++m)
+            if (tag_off[i][m] != (size_t)-1) deps[i].yt[m] = st->tags + tag_off[i][m];
+        if (src_op[i] >= 0) {
+            deps[i].xt = st->tags + tag_off[src_op[i]][src_m[i]];
+            deps[i].xt_op = src_op[i];
+            deps[src_op[i]].publish = 1;   // the consumer's slow path waits on its counter
+        }
+        if (deps[i].wait_op >= 0) deps[deps[i].wait_op].publish = 1;
+    }
+
+    const size_t ob = stack_op_bytes();
+    st->nops = nops;
+    MCAPQ_CUDA_TRY(cudaMallocHost(&st->ops_host, ob * nops));
+    MCAPQ_CUDA_TRY(cudaMalloc(&st->ops_dev, ob * nops));
+    MCAPQ_CUDA_TRY(cudaMalloc(&st->counters, sizeof(unsigned int) * (nops + 2)));
+    MCAPQ_CUDA_TRY(cudaMemset(st->counters, 0, sizeof(unsigned int) * (nops + 2)));
+    for (int i = 0; i < nops; ++i) {
+        const int l = groups[i].first;
+        MCAPQ_REQUIRE(stack_fill_op(reinterpret_cast<uint8_t *>(st->ops_host) + ob * i, st->routes[l], gs[i],
+                                    heads[i]->x, heads[i]->ydt, deps[i], nullptr),
+                      MCAPQ_ECUDA, "stack op %d: TMA descriptor encode failed", i);
+    }
+    MCAPQ_CUDA_TRY(cudaMemcpy(st->ops_dev, st->ops_host, ob * nops, cudaMemcpyHostToDevice));
     st->prog_ok = true;
     return MCAPQ_OK;
 }
@@ -339,6 +435,28 @@ int mcapq_stack_launches(const mcapq_stack *st, int64_t m)
     return c;
 }
 
+}  // extern "C"
+
+// Is the input of slot (l, sl) a step input, i.e. not written by an earlier slot's
+// output (decode order)?  Only step inputs travel from the host in step_host.
+static bool step_input(const mcapq_stack *st, int l, int sl, int64_t m)
+{
+    const Slot &a = st->slots[(size_t)l * kMaxSlots + sl];
+    const uintptr_t x0 = reinterpret_cast<uintptr_t>(a.x), x1 = x0 + (uintptr_t)(m * a.k * 2);
+    for (int l2 = 0; l2 <= l; ++l2)
+        for (int s2 = 0; s2 < kMaxSlots; ++s2) {
+            if (l2 == l && s2 >= sl) break;
+            const Slot &b = st->slots[(size_t)l2 * kMaxSlots + s2];
+            if (!b.set || (l2 == l && b.input_id == a.input_id)) continue;
+            const uintptr_t y0 = reinterpret_cast<uintptr_t>(b.y);
+            const uintptr_t y1 = y0 + (uintptr_t)(m * b.n * (b.ydt == MCAPQ_F32 ? 4 : 2));
+            if (y0 < x1 && x0 < y1) return false;
+        }
+    return true;
+}
+
+extern "C" {
+
 size_t mcapq_stack_host_bytes(const mcapq_stack *st, int64_t m, int which)
 {
     if (!st || m < 1) return 0;
@@ -349,7 +467,7 @@ size_t mcapq_stack_host_bytes(const mcapq_stack *st, int64_t m, int which)
             const Slot &s = st->slots[(size_t)l * kMaxSlots + sl];
             if (!s.set) continue;
             if (which == 0) {
-                if (s.input_id != last) b += (size_t)(m * s.k) * 2;
+                if (s.input_id != last && step_input(st, l, sl, m)) b += (size_t)(m * s.k) * 2;
                 last = s.input_id;
             } else {
                 b += (size_t)(m * s.n) * (s.ydt == MCAPQ_F32 ? 4 : 2);
@@ -364,32 +482,50 @@ mcapq_status mcapq_stack_step_host(mcapq_stack *st, int64_t m, const void *x_hos
     clear_error();
     MCAPQ_REQUIRE(st && x_host && y_host && m >= 1 && m <= st->max_m, MCAPQ_EINVAL, "bad stack_step_host arguments");
     cudaStream_t s = as_stream(stream);
-    const uint8_t *xp = reinterpret_cast<const uint8_t *>(x_host);
+    // One copy per maximal run that is contiguous on both sides: callers that place
+    // the step's inputs (and outputs) in one device arena in slot order get a single
+    // H2D and a single D2H per step instead of one per slot.
+    struct Run {
+        char *dev;
+        char *host;
+        size_t bytes;
+    };
+    auto push = [](std::vector<Run> &runs, char *dev, char *host, size_t b) {
+        if (!runs.empty() && runs.back().dev + runs.back().bytes == dev && runs.back().host + runs.back().bytes == host)
+            runs.back().bytes += b;
+        else
+            runs.push_back({dev, host, b});
+    };
+    std::vector<Run> xin, yout;
+    char *xp = reinterpret_cast<char *>(const_cast<void *>(x_host));
     for (int l = 0; l < st->layers; ++l) {
         int last = -1 << 30;
         for (int sl = 0; sl < kMaxSlots; ++sl) {
             const Slot &s_ = st->slots[(size_t)l * kMaxSlots + sl];
             if (!s_.set || s_.input_id == last) continue;
             last = s_.input_id;
+            if (!step_input(st, l, sl, m)) continue;   // produced inside the step
             const size_t b = (size_t)(m * s_.k) * 2;
-            MCAPQ_CUDA_TRY(cudaMemcpyAsync(const_cast<uint16_t *>(s_.x), xp, b, cudaMemcpyHostToDevice, s));
+            push(xin, reinterpret_cast<char *>(const_cast<uint16_t *>(s_.x)), xp, b);
             xp += b;
         }
     }
+    char *yp = reinterpret_cast<char *>(y_host);
+    for (size_t i = 0; i < st->slots.size(); ++i) {
+        const Slot &s_ = st->slots[i];
+        if (!s_.set) continue;
+        const size_t b = (size_t)(m * s_.n) * (s_.ydt == MCAPQ_F32 ? 4 : 2);
+        push(yout, reinterpret_cast<char *>(s_.y), yp, b);
+        yp += b;
+    }
+    for (const Run &r : xin) MCAPQ_CUDA_TRY(cudaMemcpyAsync(r.dev, r.host, r.bytes, cudaMemcpyHostToDevice, s));
     if (st->exec && st->graph_m == m) {
         MCAPQ_CUDA_TRY(cudaGraphLaunch(st->exec, s));
     } else {
         mcapq_status r = mcapq_stack_run(st, m, stream);
         if (r != MCAPQ_OK) return r;
     }
-    uint8_t *yp = reinterpret_cast<uint8_t *>(y_host);
-    for (size_t i = 0; i < st->slots.size(); ++i) {
-        const Slot &s_ = st->slots[i];
-        if (!s_.set) continue;
-        const size_t b = (size_t)(m * s_.n) * (s_.ydt == MCAPQ_F32 ? 4 : 2);
-        MCAPQ_CUDA_TRY(cudaMemcpyAsync(yp, s_.y, b, cudaMemcpyDeviceToHost, s));
-        yp += b;
-    }
+    for (const Run &r : yout) MCAPQ_CUDA_TRY(cudaMemcpyAsync(r.host, r.dev, r.bytes, cudaMemcpyDeviceToHost, s));
     return MCAPQ_OK;
 }
 

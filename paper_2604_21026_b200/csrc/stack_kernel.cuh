@@ -7,38 +7,57 @@
 //                   Weights never depend on activations, so the weight stream
 //                   never stops at a linear boundary: the HBM pipe stays full
 //                   while consumers wait for the previous linear's outputs.
-//   consumers     : per linear i: grid barrier on linear i-1 (a global counter
-//                   reaching gridDim: every CTA has stored its rows of y_{i-1}),
-//                   stage x_i (W4A8: fused per-token quantiser; W4A16: fragment
-//                   order), consume linear i's stages (DP4A / HMMA1 engines, the
-//                   same code as stream_linear), store y_i, arrive on counter i.
-// The dependency order is the decode chain: linear i reads its input only after
-// linear i-1 completed everywhere (the whole decode step
-// replayed as one graph; here as one kernel).  route(layer) from the MCAP
+//   consumers     : per linear i: stage x_i (W4A8: fused per-token quantiser;
+//                   W4A16: fragment order), consume linear i's stages (DP4A / HMMA1
+//                   engines, the same code as stream_linear), store y_i.
+//   sync warp     : publishes linears other linears wait on (global counters) and
+//                   releases consumers into a linear whose wait is a barrier.
+//
+// Dependencies are the data's own (the program builder, stack.cu, derives them
+// from the registered buffers):
+//   * dataflow (x_i is exactly y_j of an earlier linear j, bf16): linear j also
+//     stores y_j as tagged words {bf16 | tag << 16} (tag = this launch's epoch);
+//     linear i reads those words and re-reads any whose tag is stale.  The load IS
+//     the wait: one L2 round trip instead of publish + poll + load.
+//   * barrier (any other overlap: partial aliasing, WAR, WAW): linear i waits
+//     until every CTA published linear j (counter j == gridDim).
+//   * none (x_i is a step input): linear i starts as soon as its CTA gets there.
+// The dependency order is the decode chain (the whole decode
+// step replayed as one graph; here as one kernel).  route(layer) from the MCAP
 // dispatch table selects the engine per linear.
 #pragma once
 
 struct StackOp {
     const CUtensorMap *maps[kMaxGroup];
     void *y[kMaxGroup];
-    int64_t n[kMaxGroup];
+    uint32_t *yt[kMaxGroup];   // tagged copy of y[m] read by a later linear of the step, or null
+    int n[kMaxGroup];
     int tile_start[kMaxGroup + 1];
     int count;
     int route;        // MCAPQ_W4A8 (DP4A engine) or MCAPQ_W4A16 (HMMA1 engine)
     int ydt;
     int64_t k;
     const uint16_t *x;
+    const uint32_t *xt;   // dataflow source: tagged y of the producing linear (then x is not read)
+    int xt_op;            // the producing linear (its counter is the slow-path wait), or -1
+    int wait_op;          // barrier dependency: linear index, or -1
+    int publish;          // a later linear waits on this one's counter
+    int pad_[3];
 };
 static_assert(sizeof(StackOp) % 16 == 0, "StackOp is copied to shared memory in 16-byte pieces");
 
 struct StackArgs {
     const StackOp *ops;          // device array [nops]
     int nops;
-    unsigned int *counters;      // [nops], zero at launch: CTAs done with linear i
+    unsigned int *counters;      // [nops] CTAs done with linear i, [nops] exit count, [nops + 1] epoch;
+                                 // zero-initialised once, reset by the last CTA to leave
     int stages;
-    int ops_off, act_off, red_off;   // shared-memory offsets of the program copy, activations, reduction
+    int ops_off, act_off, red_off;   // shared-memory offsets (program copy, activations, tile slots)
     unsigned long long *trace;   // debug: [nops][grid][8] or null
-    int flags;                   // debug (MCAPQ_STEP_FLAGS): 1 no compute, 2 no grid barrier, 4 no staging, 8 no chain
+    int flags;                   // debug (MCAPQ_STEP_FLAGS): 1 no compute, 2 no barrier polls, 4 no staging,
+                                 // 8 no waits at all (barriers skipped, tags not checked),
+    int spin_ns;                 // first back-off between re-reads of stale tagged words (doubles, <= 1 us)
+    int polls;                   // CTA-wide re-read rounds before waiting on the producer's counter
 };
 
 __device__ __forceinline__ unsigned int ld_acquire_gpu(const unsigned int *p)
@@ -47,9 +66,172 @@ __device__ __forceinline__ unsigned int ld_acquire_gpu(const unsigned int *p)
     asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
     return v;
 }
+__device__ __forceinline__ uint4 ld_relaxed_128(const void *p)
+{
+    uint4 v;
+    asm volatile("ld.relaxed.gpu.global.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                 : "l"(p)
+                 : "memory");
+    return v;
+}
+__device__ __forceinline__ bool tags_ok(uint4 a, uint32_t t16)
+{
+    return (((a.x ^ t16) | (a.y ^ t16) | (a.z ^ t16) | (a.w ^ t16)) >> 16) == 0u;
+}
+// tagged words -> packed bf16 pairs
+__device__ __forceinline__ uint2 untag(uint4 a)
+{
+    return make_uint2(__byte_perm(a.x, a.y, 0x5410), __byte_perm(a.z, a.w, 0x5410));
+}
 
 constexpr int kStepThreads = (kConsumerWarps + 2) * 32;   // consumers + producer warp + sync warp
+constexpr int kStepMaxRounds = 4;                         // K <= 16384: G*4 quads over 512 consumer threads
 
+__device__ __forceinline__ bool mbar_test(uint32_t bar, uint32_t parity)
+{
+    uint32_t r;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tmbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(r)
+        : "r"(bar), "r"(parity)
+        : "memory");
+    return r != 0;
+}
+
+// AND of a predicate over the consumer threads (also a consumer barrier).
+__device__ __forceinline__ bool bar_consumers_and(bool v)
+{
+    uint32_t r;
+    asm volatile(
+        "{\n\t.reg .pred p, q;\n\tsetp.ne.u32 q, %1, 0;\n\tbar.red.and.pred p, 1, %2, q;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(r)
+        : "r"((uint32_t)v), "n"(kConsumerWarps * 32)
+        : "memory");
+    return r != 0;
+}
+
+// Stage one linear's input (M = 1) into shared memory: all loads of this thread are
+// issued first (up to kStepMaxRounds x 32 B).  A dataflow input is then checked:
+// if every tagged word is current (the producing linear finished everywhere before
+// this CTA got here: the load was the only round trip) staging goes on; otherwise
+// one thread waits for the producer's counter (low-traffic polling, no storm of
+// data re-reads) and the stale words are re-read once.
+__device__ __forceinline__ void stage_step(const StackOp &op, bool a16, const ActSmem &L, int tid, uint32_t t16,
+                                           bool check, int spin_ns, int polls, const unsigned int *counters)
+{
+    const int G = (int)(op.k / 32);
+    const uint32_t K2 = (uint32_t)(op.k / 2);
+    const int nq = G * 4;
+    const bool tagged = op.xt != nullptr;
+    constexpr int NT = kConsumerWarps * 32;
+    if (a16)
+        for (int idx = tid; idx < G * 8; idx += NT)     // tokens 1..7 of corr: zero
+            if ((idx & 7) != 0) sts32(L.corr + 4u * (uint32_t)idx, 0u);
+    uint4 ra[kStepMaxRounds], rb[kStepMaxRounds];
+#pragma unroll
+    for (int r = 0; r < kStepMaxRounds; ++r) {
+        const int idx = r * NT + tid;
+        if (r * NT < nq && idx < nq) {
+            const int g = idx >> 2, sub = idx & 3;
+            // element offsets: W4A8 quad member sub holds 8 sub .. 8 sub + 7; W4A16 4t..4t+3, 4t+16..4t+19
+            const int e0 = 32 * g + (a16 ? 4 * sub : 8 * sub);
+            const int e1 = a16 ? e0 + 16 : e0 + 4;
+            if (tagged) {
+                ra[r] = ld_relaxed_128(op.xt + e0);
+                rb[r] = ld_relaxed_128(op.xt + e1);
+            } else if (a16) {
+                const uint2 lo = ldg_x64<true>(op.x + e0), hi = ldg_x64<true>(op.x + e1);
+                ra[r] = make_uint4(lo.x, lo.y, hi.x, hi.y);
+            } else {
+                ra[r] = ldg_x128<true>(op.x + e0);
+            }
+        }
+    }
+    if (tagged && check) {
+        // re-read only this thread's stale words, with exponential back-off; after
+        // `polls` CTA-wide rounds fall back to the producer's counter
+        auto reload_stale = [&]() {
+#pragma unroll
+            for (int r = 0; r < kStepMaxRounds; ++r) {
+                const int idx = r * NT + tid;
+                if (r * NT < nq && idx < nq && !(tags_ok(ra[r], t16) && tags_ok(rb[r], t16))) {
+                    const int g = idx >> 2, sub = idx & 3;
+                    const int e0 = 32 * g + (a16 ? 4 * sub : 8 * sub);
+                    const int e1 = a16 ? e0 + 16 : e0 + 4;
+                    ra[r] = ld_relaxed_128(op.xt + e0);
+                    rb[r] = ld_relaxed_128(op.xt + e1);
+                }
+            }
+        };
+        int backoff = spin_ns;
+        for (int p = 0;; ++p) {
+            bool ok = true;
+#pragma unroll
+            for (int r = 0; r < kStepMaxRounds; ++r)
+                if (r * NT + tid < nq) ok = ok && tags_ok(ra[r], t16) && tags_ok(rb[r], t16);
+            if (bar_consumers_and(ok)) break;
+            if (p >= polls) {
+                if (tid == 0)
+                    while (ld_acquire_gpu(counters + op.xt_op) < gridDim.x) __nanosleep(spin_ns);
+                bar_consumers();
+                if (!ok) reload_stale();
+                break;
+            }
+            if (!ok) {
+                __nanosleep(backoff);
+                reload_stale();
+            }
+            backoff = backoff < 1024 ? 2 * backoff : 1024;
+        }
+    }
+#pragma unroll
+    for (int r = 0; r < kStepMaxRounds; ++r) {
+        if (r * NT >= nq) break;   // CTA-uniform
+        const int idx = r * NT + tid;
+        const bool on = idx < nq;
+        const int q = on ? idx : 0;
+        const int g = q >> 2, sub = q & 3;
+        uint32_t w4[4];
+        if (tagged) {
+            if (on && check) {
+                // the producer published: current now (guards the relaxed re-read)
+                const int e0 = 32 * g + (a16 ? 4 * sub : 8 * sub);
+                const int e1 = a16 ? e0 + 16 : e0 + 4;
+                while (!(tags_ok(ra[r], t16) && tags_ok(rb[r], t16))) {
+                    __nanosleep(spin_ns);
+                    ra[r] = ld_relaxed_128(op.xt + e0);
+                    rb[r] = ld_relaxed_128(op.xt + e1);
+                }
+            }
+            const uint2 lo = untag(ra[r]), hi = untag(rb[r]);
+            w4[0] = lo.x; w4[1] = lo.y; w4[2] = hi.x; w4[3] = hi.y;
+        } else {
+            w4[0] = ra[r].x; w4[1] = ra[r].y; w4[2] = ra[r].z; w4[3] = ra[r].w;
+        }
+        if (a16) {
+            a16_quad_store(make_uint2(w4[0], w4[1]), make_uint2(w4[2], w4[3]), on, 0, g, sub, L);
+        } else {
+            float v[8];
+            bf16x8_to_f32(w4, v);
+            a8_quad_store(v, on, 0, g, sub, G, K2, L);
+        }
+    }
+}
+
+// Store one output element: the caller's y and, when a later linear reads it in
+// this step, its tagged copy.
+__device__ __forceinline__ void store_step(const StackOp &op, int m, int64_t row, float v, uint32_t t16)
+{
+    dev::store_out(op.y[m], op.ydt, row, v);
+    if (op.yt[m]) {
+        const uint32_t w = (uint32_t)dev::float_to_bf16_bits(v) | t16;
+        asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(op.yt[m] + row), "r"(w) : "memory");
+    }
+}
+
+template <bool kTrace>
 __global__ void __launch_bounds__(kStepThreads, 1) stack_step(const __grid_constant__ StackArgs a)
 {
     extern __shared__ __align__(16) uint8_t smem_raw[];
@@ -59,18 +241,25 @@ __global__ void __launch_bounds__(kStepThreads, 1) stack_step(const __grid_const
     const uint32_t ring = sb;
     const uint32_t full = sb + (uint32_t)S * kStageBytes;
     const uint32_t empty = full + 8u * S;
-    const uint32_t done = empty + 8u * S;   // phase i: every consumer warp finished linear i
-    const uint32_t go = done + 8u;          // phase i: linear i finished in every CTA
+    const uint32_t go = empty + 8u * S;   // phase j: the j-th barrier-waiting linear may start
+    const uint32_t epf = go + 8u;         // [2] tile slot written by every consumer warp
+    const uint32_t epe = go + 24u;        // [2] tile slot stored out by the epilogue warp
     const uint32_t act = sb + a.act_off;
-    const uint32_t red = sb + a.red_off;
+    const uint32_t red = sb + a.red_off;  // [2] tile slots: [16 warps][16 rows] fp32
+    // this launch's tag (epoch + 1, never 0): the epoch only changes after every CTA left
+    const uint32_t epoch = *reinterpret_cast<volatile unsigned int *>(a.counters + a.nops + 1);
+    const uint32_t t16 = ((epoch % 65535u) + 1u) << 16;
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < S; ++s) {
             mbar_init(full + 8u * s, 1);
             mbar_init(empty + 8u * s, kConsumerWarps);
         }
-        mbar_init(done, kConsumerWarps);
         mbar_init(go, 1);
+        for (int j = 0; j < 2; ++j) {
+            mbar_init(epf + 8u * j, kConsumerWarps);
+            mbar_init(epe + 8u * j, 1);
+        }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     // the program (a few KB) into shared memory once: op records are read at every
@@ -84,19 +273,73 @@ __global__ void __launch_bounds__(kStepThreads, 1) stack_step(const __grid_const
     }
     __syncthreads();
 
+    auto cta_tiles = [&](const StackOp &op, int &t0, int &t1) {
+        const int T = op.tile_start[op.count];
+        t0 = (int)(((int64_t)T * blockIdx.x) / gridDim.x);
+        t1 = (int)(((int64_t)T * (blockIdx.x + 1)) / gridDim.x);
+    };
+
     if (warp == kConsumerWarps + 1) {
-        // ================= sync warp: publish and await linears, off the consumers' path =====
-        // done(i) -> release-add counters[i] (the CTA's y_i stores, ordered by the
-        // consumers' mbarrier arrives, become visible at gpu scope first) -> poll until
-        // every CTA published -> go(i) releases the consumers into linear i+1.
-        if (lane == 0 && !(a.flags & 8)) {
-            for (int i = 0; i < a.nops; ++i) {
-                mbar_wait(done, (uint32_t)i & 1u);
+        // ================= epilogue / sync warp =================
+        // Per tile (in the consumers' order): wait until the 16 consumer warps left
+        // their partial row sums in the tile slot, reduce them in a fixed order
+        // (W4A16: 16 warp partials per row; W4A8: one value per row), store the 16 rows
+        // (caller's y + tagged copy) in one instruction, release the slot.  Per linear:
+        // barrier waits (poll counter[wait_op], then `go`) and publishing (its own
+        // stores, then release-add counter[i]).  Last: the exit count; the last CTA out
+        // resets the counters and advances the epoch for the next launch.
+        const bool nowait = (a.flags & 10) != 0;
+        uint32_t ts = 0;   // tile sequence number of this CTA
+        for (int i = 0; i < a.nops; ++i) {
+            const StackOp &op = ops[i];
+            int t0, t1;
+            cta_tiles(op, t0, t1);
+            if (op.wait_op >= 0 && t1 > t0) {
+                if (lane == 0) {
+                    if (!nowait)
+                        while (ld_acquire_gpu(a.counters + op.wait_op) < gridDim.x) __nanosleep(20);
+                    // one go phase in flight at a time: the consumers passed every earlier
+                    // one (this warp already stored every earlier tile they computed)
+                    mbar_arrive(go);
+                }
+                __syncwarp();
+            }
+            const bool a16 = op.route == MCAPQ_W4A16;
+            int li = 0;
+            for (int tile = t0; tile < t1; ++tile, ++ts) {
+                while (li + 1 < op.count && tile >= op.tile_start[li + 1]) ++li;
+                const uint32_t slot = ts & 1u;
+                mbar_wait(epf + 8u * slot, (ts >> 1) & 1u);
+                const uint32_t sl = red + 1024u * slot;
+                if (lane < kTileRows) {
+                    float v;
+                    if (a16) {
+                        v = __uint_as_float(lds32(sl + 4u * lane));
+#pragma unroll
+                        for (int w = 1; w < kConsumerWarps; ++w) v += __uint_as_float(lds32(sl + 64u * w + 4u * lane));
+                    } else {
+                        v = __uint_as_float(lds32(sl + 4u * lane));
+                    }
+                    const int64_t row = (int64_t)(tile - op.tile_start[li]) * kTileRows + lane;
+                    if (row < op.n[li]) store_step(op, li, row, v, t16);
+                }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(epe + 8u * slot);
+            }
+            if (op.publish && lane == 0)
                 asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(a.counters + i) : "memory");
-                if (i + 1 == a.nops) break;
-                if (!(a.flags & 2))
-                    while (ld_acquire_gpu(a.counters + i) < gridDim.x) __nanosleep(20);
-                mbar_arrive(go);
+        }
+        if (lane == 0) {
+            unsigned int prev;
+            asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;"
+                         : "=r"(prev)
+                         : "l"(a.counters + a.nops)
+                         : "memory");
+            if (prev == gridDim.x - 1) {
+                for (int i = 0; i < a.nops; ++i) a.counters[i] = 0u;
+                a.counters[a.nops] = 0u;
+                a.counters[a.nops + 1] = epoch + 1u;
+                __threadfence();
             }
         }
         return;
@@ -126,16 +369,14 @@ __global__ void __launch_bounds__(kStepThreads, 1) stack_step(const __grid_const
                 const int count = op.count;
                 const int K2 = (int)(op.k / 2);
                 const int nchunks = (K2 + kChunkBytes - 1) / kChunkBytes;
-                const int T = op.tile_start[count];
-                const int t0 = (int)(((int64_t)T * blockIdx.x) / gridDim.x);
-                const int t1 = (int)(((int64_t)T * (blockIdx.x + 1)) / gridDim.x);
-                // warm this linear's input in L2 (evict_last) while its weights stream: the
-                // consumers read x on the dependent chain, an L2 hit instead of a DRAM trip
-                // queued behind the weight stream.  A prefetch only fills L2, so it is safe
-                // even when x is written by the previous linear later (L2 is coherent).
-                const int xlines = (int)((op.k * 2 + 127) / 128);
-                for (int ln = blockIdx.x; ln < xlines; ln += gridDim.x)
-                    asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(op.x + 64 * ln) : "memory");
+                int t0, t1;
+                cta_tiles(op, t0, t1);
+                if (!op.xt) {
+                    // a step input: warm it in L2 (evict_last) while the weights stream
+                    const int xlines = (int)((op.k * 2 + 127) / 128);
+                    for (int ln = blockIdx.x; ln < xlines; ln += gridDim.x)
+                        asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(op.x + 64 * ln) : "memory");
+                }
                 int li = 0;
                 for (int tile = t0; tile < t1; ++tile) {
                     while (li + 1 < count && tile >= op.tile_start[li + 1]) ++li;
@@ -163,7 +404,7 @@ __global__ void __launch_bounds__(kStepThreads, 1) stack_step(const __grid_const
     uint32_t kNib2 = 0x000F000Fu, kMagic = 0x43004300u;
     asm volatile("" : "+r"(kNib2), "+r"(kMagic));
     int s = 0;
-    uint32_t ph = 0;
+    uint32_t ph = 0, goph = 0, ts = 0;
     for (int i = 0; i < a.nops; ++i) {
         const StackOp &op = ops[i];
         const int count = op.count, route = op.route;
@@ -171,69 +412,83 @@ __global__ void __launch_bounds__(kStepThreads, 1) stack_step(const __grid_const
         const int G = (int)(k / 32);
         const int K2 = (int)(k / 2);
         const int nchunks = (K2 + kChunkBytes - 1) / kChunkBytes;
-        const int T = op.tile_start[count];
-        const int t0 = (int)(((int64_t)T * blockIdx.x) / gridDim.x);
-        const int t1 = (int)(((int64_t)T * (blockIdx.x + 1)) / gridDim.x);
-        unsigned long long tr0 = 0, tr1 = 0, tr2 = 0;
-        if (a.trace) tr0 = globaltimer();
+        int t0, t1;
+        cta_tiles(op, t0, t1);
+        unsigned long long tr0 = 0, tr1 = 0, tr2 = 0, tr3 = 0, tr4 = 0;
+        unsigned int stalls = 0, nstages = 0;
+        if (kTrace) tr0 = globaltimer();
+        if (t1 > t0) {
+            // ---- barrier dependency: wait for the sync warp's release
+            if (op.wait_op >= 0) {
+                mbar_wait(go, goph);
+                goph ^= 1u;
+            }
+            if (kTrace) tr1 = globaltimer();
+            const bool a16 = route == MCAPQ_W4A16;
+            const ActSmem L = act_layout(a16, act, k, 1);
+            bar_consumers();   // every warp is done reading the previous linear's activations
+            if (!(a.flags & 4)) stage_step(op, a16, L, threadIdx.x, t16, !(a.flags & 8), a.spin_ns, a.polls, a.counters);
+            bar_consumers();
+            if (kTrace) tr2 = globaltimer();
 
-        // ---- wait for linear i-1 everywhere (its outputs may be this linear's input)
-        if (i > 0 && !(a.flags & 8)) mbar_wait(go, (uint32_t)(i - 1) & 1u);
-        if (a.trace) tr1 = globaltimer();
-        const bool a16 = route == MCAPQ_W4A16;
-        const ActSmem L = act_layout(a16, act, k, 1);
-        if (!(a.flags & 4)) {
-            if (a16)
-                stage_a16<true>(op.x, k, 1, k, L, threadIdx.x, kConsumerWarps * 32);
-            else
-                stage_a8<true>(op.x, k, 1, k, L, threadIdx.x, kConsumerWarps * 32);
-        }
-        bar_consumers();
-        if (a.trace) tr2 = globaltimer();
-
-        int li = 0;
-        for (int tile = t0; tile < t1; ++tile) {
-            while (li + 1 < count && tile >= op.tile_start[li + 1]) ++li;
-            float acc[4] = {0.f, 0.f, 0.f, 0.f};
-            for (int ch = 0; ch < nchunks; ++ch) {
-                const int rem = K2 - ch * kChunkBytes;
-                const int nblk = (rem < kChunkBytes ? rem : kChunkBytes) / 16;
-                const int blk0 = ch * kChunkBlocks;
-                mbar_wait(full + 8u * s, ph);
-                const uint32_t st = ring + (uint32_t)s * kStageBytes;
-                if (a.flags & 1) {
-                    // debug: drain only
-                } else if (a16) {
-                    chunk_mma<HMMA1>(st, nblk, blk0, (uint32_t)K2, L, G, 1, warp, lane, kNib2, kMagic, acc);
+            for (int tile = t0; tile < t1; ++tile, ++ts) {
+                float acc[4] = {0.f, 0.f, 0.f, 0.f};
+                for (int ch = 0; ch < nchunks; ++ch) {
+                    const int rem = K2 - ch * kChunkBytes;
+                    const int nblk = (rem < kChunkBytes ? rem : kChunkBytes) / 16;
+                    const int blk0 = ch * kChunkBlocks;
+                    if (kTrace) {
+                        ++nstages;
+                        if (!mbar_test(full + 8u * s, ph)) ++stalls;   // stage not resident yet
+                    }
+                    mbar_wait(full + 8u * s, ph);
+                    if (kTrace && tile == t0 && ch == 0) tr3 = globaltimer();
+                    const uint32_t st = ring + (uint32_t)s * kStageBytes;
+                    if (a.flags & 1) {
+                        // debug: drain only
+                    } else if (a16) {
+                        chunk_mma<HMMA1>(st, nblk, blk0, (uint32_t)K2, L, G, 1, warp, lane, kNib2, kMagic, acc);
+                    } else {
+                        chunk_dp4a(st, nblk, blk0, (uint32_t)K2, L, warp, lane, acc[0]);
+                    }
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(empty + 8u * s);
+                    if (++s == S) {
+                        s = 0;
+                        ph ^= 1u;
+                    }
+                }
+                if (kTrace) tr4 = globaltimer();
+                // ---- hand the tile's partials to the epilogue warp (slot by tile parity)
+                const uint32_t slot = ts & 1u;
+                if (ts >= 2) mbar_wait(epe + 8u * slot, ((ts >> 1) - 1u) & 1u);
+                const uint32_t sl = red + 1024u * slot;
+                if (a16) {
+                    // HMMA1: lanes t == 0 hold rows gid (acc[0]) and gid + 8 (acc[2]) of token 0
+                    if ((lane & 3) == 0) {
+                        sts32(sl + 64u * warp + 4u * (lane >> 2), __float_as_uint(acc[0]));
+                        sts32(sl + 64u * warp + 4u * ((lane >> 2) + 8), __float_as_uint(acc[2]));
+                    }
                 } else {
-                    chunk_dp4a(st, nblk, blk0, (uint32_t)K2, L, warp, lane, acc[0]);
+                    float v = acc[0];
+#pragma unroll
+                    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+                    if (lane == 0) sts32(sl + 4u * warp, __float_as_uint(v));
                 }
                 __syncwarp();
-                if (lane == 0) mbar_arrive(empty + 8u * s);
-                if (++s == S) {
-                    s = 0;
-                    ph ^= 1u;
-                }
+                if (lane == 0) mbar_arrive(epf + 8u * slot);
             }
-            const int64_t row0 = (int64_t)(tile - op.tile_start[li]) * kTileRows;
-            if (a16)
-                epilogue_mma(acc, red, row0, op.n[li], op.y[li], op.ydt, op.n[li], 0, 1, warp, lane);
-            else
-                epilogue_dp4a(acc[0], row0, op.n[li], op.y[li], op.ydt, 0, warp, lane);
         }
-        // ---- this warp's rows of linear i are stored: tell the sync warp (no CTA-wide wait)
-        __syncwarp();
-        if (lane == 0) mbar_arrive(done);
-        if (a.trace && threadIdx.x == 0) {
+        if (kTrace && threadIdx.x == 0) {
             unsigned long long *r = a.trace + 8ull * ((unsigned long long)i * gridDim.x + blockIdx.x);
             r[0] = (unsigned long long)i;
-            r[1] = blockIdx.x;
+            r[1] = ((unsigned long long)blockIdx.x << 32) | ((unsigned long long)stalls << 16) | nstages;
             r[2] = tr0;
             r[3] = tr1;
             r[4] = tr2;
             r[5] = globaltimer();
-            r[6] = 0;
-            r[7] = 0;
+            r[6] = tr3;
+            r[7] = tr4;
         }
     }
 }

@@ -56,11 +56,23 @@ bool stream_supported(int64_t k);
 // grouped linear, executed in order in ONE cooperative launch (M = 1 tokens).
 size_t stack_op_bytes();
 bool stack_step_enabled();   // MCAPQ_STEP_KERNEL (default 1)
+// Dependencies of one op inside the step (stack.cu derives them from the buffers).
+struct StackDeps {
+    const uint32_t *xt;           // x is the tagged output of an earlier op (dataflow), or null
+    int xt_op;                    // that op
+    uint32_t *yt[kMaxGroup];      // tagged copies of this op's outputs read later, or null
+    int wait_op;                  // barrier: wait until every CTA finished op wait_op, or -1
+    int publish;                  // some later op waits on this one
+};
+// Largest K the step kernel stages (4 rounds of 512 quad threads).
+constexpr int64_t kStepMaxK = 16384;
 // Fill one op (host memory, stack_op_bytes() bytes) for `route` over group g with
 // input x [k] bf16 and outputs g.y (ydt); encodes/uploads descriptors on `s`.
-bool stack_fill_op(void *host_op, int route, const StreamGroup &g, const uint16_t *x, int ydt, cudaStream_t s);
-// Launch the step: ops_dev = nops filled ops in device memory; counters_dev = nops
-// uint32 (zeroed here, stream-ordered); max_k = the largest K of the program.
+bool stack_fill_op(void *host_op, int route, const StreamGroup &g, const uint16_t *x, int ydt, const StackDeps &d,
+                   cudaStream_t s);
+// Launch the step: ops_dev = nops filled ops in device memory; counters_dev = nops + 2
+// uint32 (zeroed once at allocation; the kernel's last CTA resets them and advances
+// the epoch at [nops + 1]); max_k = the largest K of the program.
 cudaError_t launch_stack_step(const void *ops_dev, int nops, unsigned int *counters_dev, int64_t max_k,
                               cudaStream_t s);
 

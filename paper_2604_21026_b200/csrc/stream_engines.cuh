@@ -82,6 +82,60 @@ __device__ __forceinline__ uint2 ldg_x64(const void *p)
     }
 }
 
+// The 8 bf16 values (4 packed words) one quad member holds, as fp32 (exact).
+__device__ __forceinline__ void bf16x8_to_f32(const uint32_t w4[4], float v[8])
+{
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+        v[2 * e] = __uint_as_float(w4[e] << 16);
+        v[2 * e + 1] = __uint_as_float(w4[e] & 0xffff0000u);
+    }
+}
+
+// Quantise group (i, g): quad member `sub` holds elements 8 sub .. 8 sub + 7 in v.
+// Stores its 8 codes and (sub 0) the group's {s, 8 sum q}.  All 32 lanes call it
+// (quad shuffles); `on` masks the stores of lanes past the end.
+__device__ __forceinline__ void a8_quad_store(const float v[8], bool on, int i, int g, int sub, int G, uint32_t K2,
+                                              const ActSmem &L)
+{
+    float amax = 0.0f;
+    int fin = 1;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+        fin &= isfinite(v[j]) ? 1 : 0;
+        amax = fmaxf(amax, fabsf(v[j]));
+    }
+    amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, 1));
+    amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, 2));
+    fin &= __shfl_xor_sync(0xffffffffu, fin, 1);
+    fin &= __shfl_xor_sync(0xffffffffu, fin, 2);
+    const float s = __fdiv_rn(amax, 127.0f);
+    const bool live = fin && s != 0.0f;
+    const float inv = __frcp_rn(s);
+    uint32_t lo = 0, hi = 0;
+    int sum = 0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+        const int code = live ? quant_code(v[j], s, inv) : 0;
+        sum += code;
+        if (j < 4)
+            lo |= ((uint32_t)code & 0xffu) << (8 * j);
+        else
+            hi |= ((uint32_t)code & 0xffu) << (8 * (j - 4));
+    }
+    sum += __shfl_xor_sync(0xffffffffu, sum, 1);
+    sum += __shfl_xor_sync(0xffffffffu, sum, 2);
+    if (on) {
+        // elements 8sub..8sub+7: sub 0/1 -> q_lo, sub 2/3 -> q_hi
+        const uint32_t qt = L.act + (uint32_t)i * L.tsz + (sub < 2 ? 0u : K2) + 16u * g + 8u * (sub & 1);
+        asm volatile("st.shared.v2.u32 [%0], {%1,%2};" ::"r"(qt), "r"(lo), "r"(hi) : "memory");
+        if (sub == 0)
+            asm volatile("st.shared.v2.u32 [%0], {%1,%2};" ::"r"(L.ssq + 8u * (uint32_t)(i * G + g)),
+                         "r"(__float_as_uint(live ? s : 0.0f)), "r"((uint32_t)(8 * sum))
+                         : "memory");
+    }
+}
+
 template <bool kCoherent>
 __device__ __forceinline__ void stage_a8(const uint16_t *xg, int64_t ldx, int ntok, int64_t k, const ActSmem &L,
                                          int tid, int nthreads)
@@ -97,47 +151,32 @@ __device__ __forceinline__ void stage_a8(const uint16_t *xg, int64_t ldx, int nt
         const uint4 u = ldg_x128<kCoherent>(xg + i * ldx + 32 * g + 8 * sub);
         const uint32_t w4[4] = {u.x, u.y, u.z, u.w};
         float v[8];
+        bf16x8_to_f32(w4, v);
+        a8_quad_store(v, on, i, g, sub, G, K2, L);
+    }
+}
+
+// W4A16 fragment-order store of x[4t..4t+3] (lo) and x[4t+16..4t+19] (hi) of group
+// (tk, g) + corr[g][tk] = -136 * sum of the group (quad butterfly; all lanes call).
+__device__ __forceinline__ void a16_quad_store(uint2 lo, uint2 hi, bool on, int tk, int g, int tt, const ActSmem &L)
+{
+    float part = 0.0f;
+    const uint32_t e8[4] = {lo.x, lo.y, hi.x, hi.y};
 #pragma unroll
-        for (int e = 0; e < 4; ++e) {
-            v[2 * e] = __uint_as_float(w4[e] << 16);
-            v[2 * e + 1] = __uint_as_float(w4[e] & 0xffff0000u);
-        }
-        float amax = 0.0f;
-        int fin = 1;
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-            fin &= isfinite(v[j]) ? 1 : 0;
-            amax = fmaxf(amax, fabsf(v[j]));
-        }
-        amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, 1));
-        amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, 2));
-        fin &= __shfl_xor_sync(0xffffffffu, fin, 1);
-        fin &= __shfl_xor_sync(0xffffffffu, fin, 2);
-        const float s = __fdiv_rn(amax, 127.0f);
-        const bool live = fin && s != 0.0f;
-        const float inv = __frcp_rn(s);
-        uint32_t lo = 0, hi = 0;
-        int sum = 0;
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-            const int code = live ? quant_code(v[j], s, inv) : 0;
-            sum += code;
-            if (j < 4)
-                lo |= ((uint32_t)code & 0xffu) << (8 * j);
-            else
-                hi |= ((uint32_t)code & 0xffu) << (8 * (j - 4));
-        }
-        sum += __shfl_xor_sync(0xffffffffu, sum, 1);
-        sum += __shfl_xor_sync(0xffffffffu, sum, 2);
-        if (on) {
-            // elements 8sub..8sub+7: sub 0/1 -> q_lo, sub 2/3 -> q_hi
-            const uint32_t qt = L.act + (uint32_t)i * L.tsz + (sub < 2 ? 0u : K2) + 16u * g + 8u * (sub & 1);
-            asm volatile("st.shared.v2.u32 [%0], {%1,%2};" ::"r"(qt), "r"(lo), "r"(hi) : "memory");
-            if (sub == 0)
-                asm volatile("st.shared.v2.u32 [%0], {%1,%2};" ::"r"(L.ssq + 8u * (uint32_t)(i * G + g)),
-                             "r"(__float_as_uint(live ? s : 0.0f)), "r"((uint32_t)(8 * sum))
-                             : "memory");
-        }
+    for (int e = 0; e < 4; ++e) {
+        part += __uint_as_float(e8[e] << 16);
+        part += __uint_as_float(e8[e] & 0xffff0000u);
+    }
+    part += __shfl_xor_sync(0xffffffffu, part, 1);
+    part += __shfl_xor_sync(0xffffffffu, part, 2);
+    if (on) {
+        uint4 o;
+        o.x = __byte_perm(lo.x, lo.y, 0x5410);
+        o.y = __byte_perm(lo.x, lo.y, 0x7632);
+        o.z = __byte_perm(hi.x, hi.y, 0x5410);
+        o.w = __byte_perm(hi.x, hi.y, 0x7632);
+        sts128(L.act + (uint32_t)tk * L.tsz + 64u * g + 16u * tt, o);
+        if (tt == 0) sts32(L.corr + 4u * (uint32_t)(g * 8 + tk), __float_as_uint(-136.0f * part));
     }
 }
 
@@ -159,24 +198,7 @@ __device__ __forceinline__ void stage_a16(const uint16_t *xg, int64_t ldx, int n
         const uint16_t *src = xg + tk * ldx + 32 * g + 4 * tt;
         const uint2 lo = ldg_x64<kCoherent>(src);        // x[4t..4t+3]
         const uint2 hi = ldg_x64<kCoherent>(src + 16);   // x[4t+16..4t+19]
-        float part = 0.0f;
-        const uint32_t e8[4] = {lo.x, lo.y, hi.x, hi.y};
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-            part += __uint_as_float(e8[e] << 16);
-            part += __uint_as_float(e8[e] & 0xffff0000u);
-        }
-        part += __shfl_xor_sync(0xffffffffu, part, 1);
-        part += __shfl_xor_sync(0xffffffffu, part, 2);
-        if (on) {
-            uint4 o;
-            o.x = __byte_perm(lo.x, lo.y, 0x5410);
-            o.y = __byte_perm(lo.x, lo.y, 0x7632);
-            o.z = __byte_perm(hi.x, hi.y, 0x5410);
-            o.w = __byte_perm(hi.x, hi.y, 0x7632);
-            sts128(L.act + (uint32_t)tk * L.tsz + 64u * g + 16u * tt, o);
-            if (tt == 0) sts32(L.corr + 4u * (uint32_t)(g * 8 + tk), __float_as_uint(-136.0f * part));
-        }
+        a16_quad_store(lo, hi, on, tk, g, tt, L);
     }
 }
 

@@ -321,3 +321,88 @@ def test_stack_matches_oracle_and_graph_replay(mq, orc, kind):
     for a, (_, y, _, _) in zip(first, ref):
         assert torch.equal(a, y)
     assert st.weight_bytes == sum(pw_n * k // 2 + pw_n * k // 32 * 2 for pw_n, k in dims.values()) * L
+
+
+# ---------------------------------------------------------------- a9: the persistent step kernel (M = 1)
+# Llama-3.2-1B widths at 4 layers (K up to 8192: multi-round staging), routes [0, 1, 0, 1].
+STEP_DIMS = {"q": (2048, 2048), "k": (512, 2048), "v": (512, 2048), "o": (2048, 2048), "gate": (8192, 2048),
+             "up": (8192, 2048), "down": (2048, 8192)}
+STEP_INPUT = {"q": 0, "k": 0, "v": 0, "o": 1, "gate": 2, "up": 2, "down": 3}
+
+
+def _step_stack(mq, mode, L=4, routes=(0, 1, 0, 1)):
+    """mode: 'independent' (every input a step input), 'dataflow' (the decode chain:
+    x_o = y_q, x_gate/up = y_o, x_down = y_up, x_q(l+1) = y_down(l) -- exact aliases,
+    passed by tagged dataflow), 'barrier' (x_q(l+1) is a view half-overlapping
+    y_down(l): a partial alias -> grid-barrier dependency)."""
+    st = mq.Stack(list(routes), max_m=1)
+    ops, ys, xs = [], {}, {}
+    for l in range(L):
+        for slot_id, (slot, (n, k)) in enumerate(STEP_DIMS.items()):
+            key = (l, STEP_INPUT[slot])
+            if key not in xs:
+                if mode == "dataflow" and not (l == 0 and slot == "q"):
+                    src = {"q": (l - 1, "down"), "o": (l, "q"), "gate": (l, "o"), "down": (l, "up")}[slot]
+                    xs[key] = ys[src]
+                elif mode == "barrier" and l > 0 and slot == "q":
+                    xs[key] = ys[("buf", l - 1)][1024:1024 + k].view(1, k)
+                else:
+                    xs[key] = si.activation(1, k, si.seed_for(2, l, slot, True), si.activation_kind(slot)).to(DEV)
+            w = si.weight(n, k, si.seed_for(2, l, slot))
+            pw = mq.pack_w4(w.to(DEV))
+            if mode == "barrier" and slot == "down":
+                buf = si.activation(1, 2 * n, si.seed_for(3, l, slot, True)).to(DEV).view(-1)
+                ys[("buf", l)] = buf
+                y = buf[:n].view(1, n)
+            else:
+                y = torch.empty(1, n, dtype=torch.bfloat16, device=DEV)
+            ys[(l, slot)] = y
+            st.set(l, slot_id, STEP_INPUT[slot], pw, xs[key], y)
+            ops.append((l, slot, w, xs[key], y))
+    return st, ops
+
+
+@pytest.mark.parametrize("mode", ["independent", "dataflow", "barrier"])
+def test_step_kernel_m1_vs_oracle(mq, orc, mode):
+    routes = (0, 1, 0, 1)
+    st, ops = _step_stack(mq, mode, routes=routes)
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        st.run(1, stream=s)
+    s.synchronize()
+    assert st.launches(1) == 1        # one persistent kernel per step
+    # every linear against the oracle on the input it actually read (for chained
+    # linears: the GPU's own output of the producing linear, final after the step)
+    first = []
+    for (l, slot, w, x, y) in ops:
+        nib, sc = orc.pack_w4(_f32(w))
+        xin = _f32(x)
+        if routes[l] == 0:
+            _, y64 = orc.w4a8_from_x(nib, sc, xin)
+        else:
+            _, y64 = orc.w4a16(nib, sc, xin)
+        _assert_close(y, y64, 2e-3)
+        first.append(y.clone())
+    # replays (the epoch advances every launch; counters reset by the kernel) are bit-identical
+    with torch.cuda.stream(s):
+        st.capture(1, stream=s)
+        for _ in range(3):
+            for (_, _, _, _, y) in ops:    # every output is recomputed (chained inputs included)
+                y.zero_()
+            st.replay(stream=s)
+            s.synchronize()
+            for a, (_, _, _, _, y) in zip(first, ops):
+                assert torch.equal(a, y)
+
+
+def test_step_kernel_equals_per_linear_path(mq):
+    """The persistent step kernel (M = 1, chained) and single mcapq_linear calls on
+    the same inputs give bit-identical outputs (same engines, same K-only order)."""
+    routes = (0, 1, 0, 1)
+    st, ops = _step_stack(mq, "dataflow", routes=routes)
+    st.run(1)
+    torch.cuda.synchronize()
+    for (l, slot, w, x, y) in ops:
+        pw = mq.pack_w4(w.to(DEV))
+        ref = mq.linear(routes[l], pw, x.clone(), out_dtype=torch.bfloat16)
+        assert torch.equal(ref, y), (l, slot)
