@@ -166,7 +166,22 @@ __device__ __forceinline__ void stage_step(const StackOp &op, bool a16, const Ac
             }
         };
         int backoff = spin_ns;
-        for (int p = 0;; ++p) {
+        if (polls < 0) {
+            // independent per-thread spin on this thread's stale words (back-off capped at
+            // -polls ns), no CTA-wide rounds
+            const int cap = -polls;
+            for (;;) {
+                bool ok = true;
+#pragma unroll
+                for (int r = 0; r < kStepMaxRounds; ++r)
+                    if (r * NT + tid < nq) ok = ok && tags_ok(ra[r], t16) && tags_ok(rb[r], t16);
+                if (ok) break;
+                __nanosleep(backoff);
+                reload_stale();
+                backoff = backoff < cap ? 2 * backoff : cap;
+            }
+        }
+        for (int p = 0; polls >= 0; ++p) {
             bool ok = true;
 #pragma unroll
             for (int r = 0; r < kStepMaxRounds; ++r)
