@@ -124,7 +124,9 @@ mcapq_status mcapq_quant_a8(const uint16_t *x, int64_t m, int64_t k, int64_t ldx
  *   y[i][n]    = sum_g (f32(d_{n,g}) * sx[i][g]) * f32(D)      (fp32 accumulate)
  * nib/scale: packed weight [n, k].  q/sx/sq: as written by mcapq_quant_a8 for m
  * tokens (row strides k, k/32, k/32).  y: out [m][ldy] of dtype ydt.
- * m == 1 runs the batch-1 GEMV (dp4a), m > 1 the int8 tensor-core kernel.
+ * m == 1 runs the batch-1 GEMV (dp4a), m > 1 the int8 tensor-core kernel; for
+ * m >= 9 with K % 256 == 0 (and sx, sq 16-byte aligned) the batched kernel
+ * streams each weight once per 64 tokens (rows a5, IMMA m16n8k32 per block).
  * The fp32 summation order depends on K only (never on N, M or the grid), so a
  * column shard of the weight gives bit-identical rows (A22).
  */
@@ -153,7 +155,8 @@ mcapq_status mcapq_w4a8_x(const uint8_t *nib, const uint16_t *scale, int64_t n, 
  *   y[i][n] = sum_k (f32(d_{n,k/32}) (c_{n,k} - 8)) x_{i,k}, fp32 accumulation.
  * Each term is exact in fp32; the inner per-group sums run on bf16 tensor cores
  * (c - 8 is exact in bf16) with fp32 accumulation, the scale d is applied per
- * group in fp32.  x: [m][ldx] bf16.  y: out [m][ldy].
+ * group in fp32.  x: [m][ldx] bf16.  y: out [m][ldy].  m >= 9 with K % 256 == 0
+ * runs the batched kernel (row a6: one weight pass per 64 tokens, HMMA on c - 8).
  */
 mcapq_status mcapq_w4a16(const uint8_t *nib, const uint16_t *scale, int64_t n, int64_t k, const uint16_t *x,
                          int64_t m, int64_t ldx, void *y, int ydt, int64_t ldy, void *stream);
@@ -169,7 +172,9 @@ mcapq_status mcapq_linear(int route, const uint8_t *nib, const uint16_t *scale, 
  * arrays nibs/scales/ns/ys/ldys give each linear's packed weight, N, output and
  * its leading dimension; k, x, m, ldx, ydt are shared.  Results are identical
  * to `count` separate mcapq_linear calls (bit-for-bit).  ws: as mcapq_linear
- * (used only when a linear falls off the K % 256 == 0 fast path).
+ * (route W4A8 needs it when a linear falls off the K % 256 == 0 fast path, and
+ * for m >= 9, where x is quantised once into ws for the batched kernel; else
+ * MCAPQ_ENOSPACE / MCAPQ_EINVAL).
  */
 mcapq_status mcapq_linear_group(int route, int count, const uint8_t *const *nibs, const uint16_t *const *scales,
                                 const int64_t *ns, int64_t k, const uint16_t *x, int64_t m, int64_t ldx,

@@ -161,6 +161,11 @@ mcapq_status mcapq_w4a8(const uint8_t *nib, const uint16_t *scale, int64_t n, in
     CHECK_AL16(y, "y");
     CHECK_YDT(ydt);
     CHECK_LD(ldy, n, "ldy");
+    if (m >= kGemmMinTokens && gemm_supported(k) && aligned16(scale) && aligned16(sx) && aligned16(sq)) {
+        LAUNCH_TRY(launch_gemm(MCAPQ_W4A8, nib, scale, n, k, nullptr, 0, q, sx, sq, m, y, ydt, ldy, as_stream(stream),
+                               false));
+        return MCAPQ_OK;
+    }
     LAUNCH_TRY(launch_w4a8(nib, scale, n, k, q, sx, sq, m, y, ydt, ldy, as_stream(stream), false));
     return MCAPQ_OK;
 }
@@ -202,7 +207,7 @@ mcapq_status mcapq_w4a8_x(const uint8_t *nib, const uint16_t *scale, int64_t n, 
         g.n[0] = n;
         g.y[0] = y;
         g.ldy[0] = ldy;
-        LAUNCH_TRY(launch_stream_group(MCAPQ_W4A8, g, x, m, ldx, ydt, s, false));
+        LAUNCH_TRY(launch_linear_group(MCAPQ_W4A8, g, x, m, ldx, ydt, ws, s, false));
         return MCAPQ_OK;
     }
     const A8Workspace w = a8_workspace(ws, m, k);
@@ -234,7 +239,7 @@ mcapq_status mcapq_w4a16(const uint8_t *nib, const uint16_t *scale, int64_t n, i
         g.n[0] = n;
         g.y[0] = y;
         g.ldy[0] = ldy;
-        LAUNCH_TRY(launch_stream_group(MCAPQ_W4A16, g, x, m, ldx, ydt, as_stream(stream), false));
+        LAUNCH_TRY(launch_linear_group(MCAPQ_W4A16, g, x, m, ldx, ydt, nullptr, as_stream(stream), false));
         return MCAPQ_OK;
     }
     LAUNCH_TRY(launch_w4a16(nib, scale, n, k, x, m, ldx, y, ydt, ldy, as_stream(stream), false));
@@ -286,7 +291,13 @@ mcapq_status mcapq_linear_group(int route, int count, const uint8_t *const *nibs
             g.y[i] = ys[i];
             g.ldy[i] = ldys[i];
         }
-        LAUNCH_TRY(launch_stream_group(route, g, x, m, ldx, ydt, as_stream(stream), false));
+        if (route == MCAPQ_W4A8 && m >= kGemmMinTokens && gemm_supported(k)) {
+            CHECK_PTR(ws, "ws");
+            CHECK_AL16(ws, "ws");
+            MCAPQ_REQUIRE(ws_bytes >= a8_workspace_bytes(m, k), MCAPQ_ENOSPACE, "workspace %zu < %zu", ws_bytes,
+                          a8_workspace_bytes(m, k));
+        }
+        LAUNCH_TRY(launch_linear_group(route, g, x, m, ldx, ydt, ws, as_stream(stream), false));
         return MCAPQ_OK;
     }
     for (int i = 0; i < count; ++i) {

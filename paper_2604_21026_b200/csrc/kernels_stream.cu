@@ -294,6 +294,7 @@ __device__ __forceinline__ void hmma(uint32_t a0, uint32_t a1, uint32_t a2, uint
 #include "stream_engines.cuh"
 #include "stream_kernel.cuh"
 #include "stack_kernel.cuh"
+#include "gemm_kernel.cuh"
 
 // ------------------------------------------------------------------ host side
 typedef CUresult (*EncodeTiledFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
@@ -449,12 +450,17 @@ namespace {
 struct DescKey {
     const void *nib, *scale;
     int64_t n, k;
-    bool operator==(const DescKey &o) const { return nib == o.nib && scale == o.scale && n == o.n && k == o.k; }
+    int kind;   // 0: stream maps (16-row x 2048-K stages); BN > 0: gemm maps (BN rows x 256 K)
+    bool operator==(const DescKey &o) const
+    {
+        return nib == o.nib && scale == o.scale && n == o.n && k == o.k && kind == o.kind;
+    }
 };
 struct DescKeyHash {
     size_t operator()(const DescKey &d) const
     {
-        return std::hash<const void *>()(d.nib) ^ (std::hash<const void *>()(d.scale) << 1) ^ (size_t)(d.n * 31 + d.k);
+        return std::hash<const void *>()(d.nib) ^ (std::hash<const void *>()(d.scale) << 1) ^
+               (size_t)(d.n * 31 + d.k * 7 + d.kind);
     }
 };
 struct DescTable {
@@ -471,12 +477,35 @@ DescTable &desc_table()
 }
 }  // namespace
 
-const CUtensorMap *stream_descriptors(const uint8_t *nib, const uint16_t *scale, int64_t n, int64_t k,
-                                      cudaStream_t s)
+// gemm maps: nibbles 2-D {K/2, N}, box {128 B, bn rows}, 128B swizzle (row r's 16-B
+// chunk c at c ^ (r & 7)); scales 2-D {K/32, N}, box {8, bn rows}, no swizzle (16 B/row).
+bool encode_gemm_maps(CUtensorMap *tn, CUtensorMap *ts, const uint8_t *nib, const uint16_t *scale, int64_t n,
+                      int64_t k, int bn)
+{
+    EncodeTiledFn fn = encode_fn();
+    if (!fn) return false;
+    const cuuint64_t nd[2] = {(cuuint64_t)(k / 2), (cuuint64_t)n};
+    const cuuint64_t ns[1] = {(cuuint64_t)(k / 2)};
+    const cuuint32_t nbox[2] = {128, (cuuint32_t)bn};
+    const cuuint32_t es[2] = {1, 1};
+    if (fn(tn, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<uint8_t *>(nib), nd, ns, nbox, es,
+           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+        return false;
+    const cuuint64_t sd[2] = {(cuuint64_t)(k / 32), (cuuint64_t)n};
+    const cuuint64_t ss[1] = {(cuuint64_t)(k / 16)};
+    const cuuint32_t sbox[2] = {8, (cuuint32_t)bn};
+    return fn(ts, CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, const_cast<uint16_t *>(scale), sd, ss, sbox, es,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+const CUtensorMap *descriptors_of_kind(const uint8_t *nib, const uint16_t *scale, int64_t n, int64_t k, int kind,
+                                       cudaStream_t s)
 {
     DescTable &t = desc_table();
     std::lock_guard<std::mutex> lock(t.mu);
-    const DescKey key{nib, scale, n, k};
+    const DescKey key{nib, scale, n, k, kind};
     auto it = t.map.find(key);
     if (it != t.map.end()) return it->second;
     if (t.blocks.empty() || t.used == DescTable::kPairs) {
@@ -491,12 +520,148 @@ const CUtensorMap *stream_descriptors(const uint8_t *nib, const uint16_t *scale,
     }
     CUtensorMap *dpair = t.blocks.back().first + 2 * t.used;
     CUtensorMap *hpair = t.blocks.back().second + 2 * t.used;
-    if (!encode_maps(&hpair[0], &hpair[1], nib, scale, n, k)) return nullptr;
+    if (!(kind == 0 ? encode_maps(&hpair[0], &hpair[1], nib, scale, n, k)
+                    : encode_gemm_maps(&hpair[0], &hpair[1], nib, scale, n, k, kind)))
+        return nullptr;
     if (cudaMemcpyAsync(dpair, hpair, 2 * sizeof(CUtensorMap), cudaMemcpyHostToDevice, s) != cudaSuccess)
         return nullptr;
     ++t.used;
     t.map.emplace(key, dpair);
     return dpair;
+}
+
+const CUtensorMap *stream_descriptors(const uint8_t *nib, const uint16_t *scale, int64_t n, int64_t k,
+                                      cudaStream_t s)
+{
+    return descriptors_of_kind(nib, scale, n, k, 0, s);
+}
+
+// ------------------------------------------------------------------ batched decode (gemm_w4)
+bool gemm_supported(int64_t k) { return k >= 256 && k % 256 == 0 && encode_fn() != nullptr; }
+
+namespace {
+// Tile configurations per padded pass width Mp: (MT, NT, WT) -> BN = 16 MT (8 / WT), Mp = 8 NT WT.
+struct GemmCfg {
+    int mt, nt, wt;
+    int bn() const { return 16 * mt * (kGemmWarps / wt); }
+    int mp() const { return 8 * nt * wt; }
+};
+constexpr GemmCfg kCfg16[] = {{2, 1, 2}, {1, 1, 2}};
+constexpr GemmCfg kCfg32[] = {{2, 2, 2}, {1, 2, 2}, {1, 1, 4}};
+constexpr GemmCfg kCfg64[] = {{4, 2, 4}, {2, 2, 4}, {1, 2, 4}};
+// W4A16 at Mp = 64: fewer token-warps (each weight dequantised by WT warps of the CTA)
+constexpr GemmCfg kCfg64h[] = {{2, 4, 2}, {1, 4, 2}, {1, 2, 4}};
+
+template <bool A8, int MT, int NT>
+cudaError_t launch_gemm_cfg(GemmArgs &a, size_t smem, int grid, cudaStream_t s, bool pdl)
+{
+    static int attr_done = 0;
+    if (!attr_done) {
+        cudaError_t e = cudaFuncSetAttribute(gemm_w4<A8, MT, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+        if (e != cudaSuccess) return e;
+        attr_done = 1;
+    }
+    return launch_pdl(gemm_w4<A8, MT, NT>, dim3(grid), dim3(kGemmThreads), smem, s, pdl, a);
+}
+
+template <bool A8>
+cudaError_t dispatch_gemm(const GemmCfg &c, GemmArgs &a, size_t smem, int grid, cudaStream_t s, bool pdl)
+{
+    if (c.mt == 4 && c.nt == 2) return launch_gemm_cfg<A8, 4, 2>(a, smem, grid, s, pdl);
+    if (c.mt == 2 && c.nt == 4) return launch_gemm_cfg<A8, 2, 4>(a, smem, grid, s, pdl);
+    if (c.mt == 1 && c.nt == 4) return launch_gemm_cfg<A8, 1, 4>(a, smem, grid, s, pdl);
+    if (c.mt == 2 && c.nt == 2) return launch_gemm_cfg<A8, 2, 2>(a, smem, grid, s, pdl);
+    if (c.mt == 1 && c.nt == 2) return launch_gemm_cfg<A8, 1, 2>(a, smem, grid, s, pdl);
+    if (c.mt == 2 && c.nt == 1) return launch_gemm_cfg<A8, 2, 1>(a, smem, grid, s, pdl);
+    if (c.mt == 1 && c.nt == 1) return launch_gemm_cfg<A8, 1, 1>(a, smem, grid, s, pdl);
+    return cudaErrorInvalidValue;
+}
+}  // namespace
+
+cudaError_t launch_gemm(int route, const uint8_t *nib, const uint16_t *scale, int64_t n, int64_t k, const uint16_t *x,
+                        int64_t ldx, const int8_t *q, const float *sx, const int32_t *sq, int64_t m, void *y, int ydt,
+                        int64_t ldy, cudaStream_t s, bool pdl)
+{
+    const bool a8 = route == MCAPQ_W4A8;
+    const int sms = device_sms();
+    for (int64_t tok0 = 0; tok0 < m; tok0 += 64) {
+        const int ntok = (int)((m - tok0) < 64 ? (m - tok0) : 64);
+        const GemmCfg *cfgs = ntok <= 16 ? kCfg16 : (ntok <= 32 ? kCfg32 : (a8 ? kCfg64 : kCfg64h));
+        const int ncfg = ntok <= 16 ? 2 : 3;
+        // the largest tile that still fills ~the machine, else the smallest
+        GemmCfg c = cfgs[ncfg - 1];
+        for (int i = 0; i < ncfg; ++i)
+            if ((n + cfgs[i].bn() - 1) / cfgs[i].bn() >= (sms * 4) / 5) {
+                c = cfgs[i];
+                break;
+            }
+        const int bn = c.bn(), mp = c.mp();
+        GemmArgs a;
+        memset(&a, 0, sizeof(a));
+        a.maps = descriptors_of_kind(nib, scale, n, k, bn, s);
+        if (!a.maps) return cudaErrorInvalidValue;
+        a.y = y;
+        a.ldy = ldy;
+        a.n = n;
+        a.k = k;
+        a.ydt = ydt;
+        a.x = x;
+        a.ldx = ldx;
+        a.q = q;
+        a.sx = sx;
+        a.sq = sq;
+        a.tok0 = tok0;
+        a.ntok = ntok;
+        a.bn = bn;
+        a.wt = c.wt;
+        a.row_tiles = (int)((n + bn - 1) / bn);
+        // stage: nibbles | scales | activations (| W4A8 s, sq), 1 KiB aligned pieces
+        a.nib_bytes = (uint32_t)bn * 128u;
+        a.sc_off = (uint32_t)round_up(a.nib_bytes, 1024);
+        a.act_off = (uint32_t)round_up(a.sc_off + (size_t)bn * 16, 1024);
+        const size_t act = a8 ? (size_t)mp * kGemmQStride : (size_t)mp * kGemmXStride;
+        a.ss_off = (uint32_t)round_up(a.act_off + act, 128);
+        a.stage_bytes = (uint32_t)round_up(a.ss_off + (a8 ? (size_t)mp * kGemmSSStride : 0), 1024);
+        int S = (int)((227 * 1024 - 1024 - 256) / a.stage_bytes);
+        S = S > kGemmMaxStages ? kGemmMaxStages : S;
+        if (S < 2) return cudaErrorInvalidValue;
+        a.stages = S;
+        const size_t smem = 1024 + (size_t)S * a.stage_bytes + 16 * (size_t)S;
+        const int grid = a.row_tiles < sms ? a.row_tiles : sms;
+        cudaError_t e = a8 ? dispatch_gemm<true>(c, a, smem, grid, s, pdl) : dispatch_gemm<false>(c, a, smem, grid, s, pdl);
+        if (e != cudaSuccess) return e;
+        pdl = true;
+    }
+    return cudaSuccess;
+}
+
+cudaError_t launch_linear_group(int route, const StreamGroup &g, const uint16_t *x, int64_t m, int64_t ldx, int ydt,
+                                void *ws, cudaStream_t s, bool pdl)
+{
+    if (m >= kGemmMinTokens && gemm_supported(g.k)) {
+        const int8_t *q = nullptr;
+        const float *sx = nullptr;
+        const int32_t *sq = nullptr;
+        if (route == MCAPQ_W4A8) {
+            // quantise once into the workspace, shared by every member of the group (A15)
+            if (!ws) return cudaErrorInvalidValue;
+            const A8Workspace w = a8_workspace(ws, m, g.k);
+            cudaError_t e = launch_quant_a8(x, m, g.k, ldx, w.q, w.sx, w.sq, s, pdl);
+            if (e != cudaSuccess) return e;
+            q = w.q;
+            sx = w.sx;
+            sq = w.sq;
+            pdl = true;
+        }
+        for (int i = 0; i < g.count; ++i) {
+            cudaError_t e =
+                launch_gemm(route, g.nib[i], g.scale[i], g.n[i], g.k, x, ldx, q, sx, sq, m, g.y[i], ydt, g.ldy[i], s, pdl);
+            if (e != cudaSuccess) return e;
+            pdl = true;
+        }
+        return cudaSuccess;
+    }
+    return launch_stream_group(route, g, x, m, ldx, ydt, s, pdl);
 }
 
 // ------------------------------------------------------------------ persistent step

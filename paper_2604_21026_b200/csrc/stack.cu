@@ -338,7 +338,8 @@ mcapq_status mcapq_stack_run(mcapq_stack *st, int64_t m, void *stream)
                     g.y[i] = b.y;
                     g.ldy[i] = b.n;
                 }
-                cudaError_t e = launch_stream_group(route, g, a.x, m, a.k, a.ydt, s, true);
+                cudaError_t e = launch_linear_group(route, g, a.x, m, a.k, a.ydt, route == MCAPQ_W4A8 ? st->ws : nullptr,
+                                                    s, true);
                 MCAPQ_REQUIRE(e == cudaSuccess, MCAPQ_ECUDA, "stream launch: %s", cudaGetErrorString(e));
                 return MCAPQ_OK;
             }

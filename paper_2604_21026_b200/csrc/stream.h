@@ -82,6 +82,19 @@ cudaError_t launch_stack_step(const void *ops_dev, int nops, unsigned int *count
 const CUtensorMap *stream_descriptors(const uint8_t *nib, const uint16_t *scale, int64_t n, int64_t k,
                                       cudaStream_t s);
 int stream_tokens_per_pass(int route, int64_t k);
+
+// Batched decode (rows a5/a6): one weight pass per 64 tokens (gemm_kernel.cuh).
+// Used for m >= kGemmMinTokens when K % 256 == 0.  W4A8 reads the quant_a8
+// workspace (q [m][k], sx/sq [m][k/32]); W4A16 reads x [m][ldx] directly.
+constexpr int64_t kGemmMinTokens = 9;
+bool gemm_supported(int64_t k);
+cudaError_t launch_gemm(int route, const uint8_t *nib, const uint16_t *scale, int64_t n, int64_t k, const uint16_t *x,
+                        int64_t ldx, const int8_t *q, const float *sx, const int32_t *sq, int64_t m, void *y, int ydt,
+                        int64_t ldy, cudaStream_t s, bool pdl);
+// A group of linears sharing x: the gemm path for m >= kGemmMinTokens (W4A8 quantises
+// into ws first: a8_workspace_bytes(m, k) bytes), else the stream kernels.
+cudaError_t launch_linear_group(int route, const StreamGroup &g, const uint16_t *x, int64_t m, int64_t ldx, int ydt,
+                                void *ws, cudaStream_t s, bool pdl);
 cudaError_t launch_stream_group(int route, const StreamGroup &g, const uint16_t *x, int64_t m, int64_t ldx,
                                 int ydt, cudaStream_t s, bool pdl);
 

@@ -175,12 +175,53 @@ def test_w4a8_prequantised_matches_fused(mq, orc, m):
     y1 = mq.w4a8(pw, q, s, sq)          # separate quantiser + generic kernel
     y2 = mq.w4a8_x(pw, xd)              # TMA stream kernel, quantiser fused
     torch.cuda.synchronize()
-    if m == 1:
-        # both dp4a paths sum a lane's blocks l, l+32, ... in the same order: same bits
+    if m == 1 or m >= 9:
+        # m = 1: both dp4a paths sum a lane's blocks l, l+32, ... in the same order;
+        # m >= 9: both run the batched kernel on the same quantised activations
         assert torch.equal(y1, y2)
     _, y64 = orc.w4a8(nib, sc, *orc.quant_a8(_f32(xd.cpu())))
     _assert_close(y1, y64, 1e-3)
     _assert_close(y2, y64, 1e-3)
+
+
+# ---------------------------------------------------------------- a5/a6 batched kernel (m >= 9)
+GEMM_SHAPES = [(200, 256), (1000, 2048), (4000, 512), (96, 4096)]
+
+
+@pytest.mark.parametrize("n,k", GEMM_SHAPES)
+@pytest.mark.parametrize("m", [9, 16, 17, 33, 64, 100])
+@pytest.mark.parametrize("route", [0, 1])
+def test_batched_vs_oracle(mq, orc, route, m, n, k):
+    """One weight pass per 64 tokens; ragged token passes (9, 17, 33, 100 = 64 + 36), ragged
+    row tiles (200, 1000, 4000 rows over 32/64/128-row tiles), K from one 256-slice up."""
+    w = si.weight(n, k, 1401 + n + k)
+    x = si.activation(m, k, 1402 + m + k)
+    pw, nib, sc = _pack_both(mq, orc, w)
+    y = mq.linear(route, pw, x.to(DEV), out_dtype=torch.float32)
+    if route == 0:
+        _, y64 = orc.w4a8_from_x(nib, sc, _f32(x))
+    else:
+        _, y64 = orc.w4a16(nib, sc, _f32(x))
+    _assert_close(y, y64, 1e-3)
+
+
+@pytest.mark.parametrize("route", [0, 1])
+def test_batched_ldx_ldy_and_rows_beyond_n(mq, orc, route):
+    """Strided activations/outputs; the last row tile is mostly out of bounds (TMA zero
+    fill must never leak into stored rows)."""
+    n, k, m = 40, 1024, 20
+    w = si.weight(n, k, 1501)
+    xs = si.activation(m, k + 64, 1502)
+    pw, nib, sc = _pack_both(mq, orc, w)
+    xd = xs.to(DEV)[:, :k]
+    yd = torch.full((m, n + 24), 7.0, dtype=torch.float32, device=DEV)
+    mq.linear(route, pw, xd, out=yd[:, :n])
+    if route == 0:
+        _, y64 = orc.w4a8_from_x(nib, sc, _f32(xs[:, :k].contiguous()))
+    else:
+        _, y64 = orc.w4a16(nib, sc, _f32(xs[:, :k].contiguous()))
+    _assert_close(yd[:, :n], y64, 1e-3)
+    assert torch.all(yd[:, n:] == 7.0)
 
 
 def test_zero_activation_and_impulse_rows(mq, orc):
