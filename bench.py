@@ -17,6 +17,7 @@ NCCL all-gather is measured by `--workload lmhead`.  One JSON line on rank 0.
 from __future__ import annotations
 
 import argparse
+import itertools
 import json
 import math
 import os
@@ -246,7 +247,12 @@ def time_single_linears(mq, dev, stream):
         row = {"config": cfg, "model": model, "slot": slot, "N": n, "K": k, "M": m, "weight_bytes": wbytes}
         with torch.cuda.stream(stream):
             wsp = torch.empty(mq.workspace_bytes(0, m, n, k), dtype=torch.uint8, device=dev)
-            for route, name in ((0, "w4a8"), (1, "w4a16")):
+            for (route, name), pdl in itertools.product(((0, "w4a8"), (1, "w4a16")), (True, False)):
+                # pdl: back-to-back linears as a decode engine launches them (mcapq_set_pdl: the
+                # next weight stream starts under the previous kernel's tail); also without
+                prev = mq.set_pdl(pdl)
+                name_ = name if pdl else name + "_nopdl"
+
                 def call(pw):
                     if route == 0:
                         mq.linear(0, pw, x, out=y, ws=wsp, stream=stream)
@@ -269,10 +275,13 @@ def time_single_linears(mq, dev, stream):
                 e1.record(stream)
                 e1.synchronize()
                 us = e0.elapsed_time(e1) * 1000 / (3 * reps)
-                row[f"{name}_us"] = round(us, 3)
-                row[f"{name}_gbs"] = round(wbytes / us / 1e3, 1)
-                if m > 1:   # batched rows are judged on the tensor pipe too: int8 / bf16 MMA ops per second
-                    row[f"{name}_tops"] = round(2 * m * n * k / (us * 1e-6) / 1e12, 1)
+                mq.set_pdl(prev)
+                row[f"{name_}_us"] = round(us, 3)
+                row[f"{name_}_gbs"] = round(wbytes / us / 1e3, 1)
+                if pdl:
+                    row[f"{name_}_frac"] = round(wbytes / us / 1e3 / peaks()[0], 4)
+                if m > 1 and pdl:   # batched rows are judged on the tensor pipe too: int8 / bf16 MMA ops per second
+                    row[f"{name_}_tops"] = round(2 * m * n * k / (us * 1e-6) / 1e12, 1)
         row["w4a8_over_w4a16"] = round(row["w4a16_us"] / row["w4a8_us"], 3)
         out.append(row)
         del ws, pw0

@@ -83,6 +83,17 @@ const char *mcapq_last_error(void);
 const char *mcapq_status_string(int status);
 /* Number of streaming multiprocessors of the current device (0 on error). */
 int mcapq_device_sms(void);
+/*
+ * Launch the linears this host thread issues from now on with programmatic
+ * dependent launch (enable = 1) or plainly (0, the default).  Under PDL a
+ * linear's weight stream starts while the previous kernel on the stream is
+ * still running (activations and outputs still wait for it), which hides the
+ * launch and pipeline ramp of back-to-back decode linears.  The caller
+ * guarantees that no kernel still in flight on the stream writes the packed
+ * weights (true for weights packed and synchronised at load time).
+ * Thread-local; returns the previous setting.
+ */
+int mcapq_set_pdl(int enable);
 
 /* --------------------------------------------------------- packed weights */
 /* Bytes of the nibble plane (N*K/2) and of the scale plane (N*(K/32)*2). */

@@ -26,7 +26,7 @@ BF16, F32 = 0, 1
 __all__ = [
     "W4A8", "W4A16", "BF16", "F32", "McapqError", "load", "pack_w4", "quant_a8", "w4a8", "w4a8_x", "w4a16",
     "linear", "linear_group", "linear_host", "w4a8_group_dots", "workspace_bytes", "host_workspace_bytes", "Profile",
-    "profile_parse", "Stack", "Comm", "linear_colshard", "PackedW4", "device_sms",
+    "profile_parse", "Stack", "Comm", "linear_colshard", "PackedW4", "device_sms", "set_pdl",
 ]
 
 
@@ -152,6 +152,12 @@ def w4a16(w: PackedW4, x: torch.Tensor, out_dtype=torch.float32, out=None, strea
     check(load().mcapq_w4a16(_ptr(w.nib), _ptr(w.scale), w.n, w.k, _ptr(x2), m, x2.stride(0), _ptr(y),
                              _dt(y.dtype), y.stride(0), _stream(stream)), "mcapq_w4a16")
     return y
+
+
+def set_pdl(enable: bool) -> bool:
+    """Launch this thread's subsequent linears with programmatic dependent launch
+    (mcapq_set_pdl); returns the previous setting."""
+    return bool(load().mcapq_set_pdl(1 if enable else 0))
 
 
 def linear(route: int, w: PackedW4, x: torch.Tensor, out_dtype=torch.float32, out=None, ws=None, stream=None):

@@ -24,6 +24,7 @@ SIGNATURES = {
     "mcapq_last_error": (ctypes.c_char_p, []),
     "mcapq_status_string": (ctypes.c_char_p, [I32]),
     "mcapq_device_sms": (I32, []),
+    "mcapq_set_pdl": (I32, [I32]),
     "mcapq_debug_stream_trace": (SZ, [P, SZ]),
     "mcapq_w4_nib_bytes": (SZ, [I64, I64]),
     "mcapq_w4_scale_bytes": (SZ, [I64, I64]),

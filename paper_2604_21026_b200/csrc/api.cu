@@ -106,6 +106,13 @@ const char *mcapq_status_string(int s)
 
 int mcapq_device_sms(void) { return device_sms(); }
 
+int mcapq_set_pdl(int enable)
+{
+    const int prev = api_pdl() ? 1 : 0;
+    set_api_pdl(enable != 0);
+    return prev;
+}
+
 size_t mcapq_debug_stream_trace(uint64_t *host_out, size_t max_records)
 {
     if (!host_out) return 0;

@@ -123,7 +123,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_w4(const __grid_constant
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
-    dev::griddep_wait();   // activations (and outputs) are ordered after the predecessor
+    dev::griddep_launch();   // the next kernel may launch: it only touches weights until its own wait
 
     if (warp == kGemmWarps) {
         // ================= producer =================
@@ -135,6 +135,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_w4(const __grid_constant
         const uint32_t tx = a.nib_bytes + (uint32_t)a.bn * 16u;
         int s = 0;
         uint32_t ph = 0;
+        bool waited = false;
         for (int tile = blockIdx.x; tile < a.row_tiles; tile += gridDim.x) {
             const int row0 = tile * a.bn;
             for (int sl = 0; sl < nslices; ++sl) {
@@ -146,8 +147,13 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_w4(const __grid_constant
                     tma_2d(st, a.maps, sl * 128, row0, fb, pol);
                     tma_2d(st + a.sc_off, a.maps + 1, sl * 8, row0, fb, pol);
                 }
-                // activations: 16-B cp.async by the 32 lanes (a warp moves whole token rows,
-                // coalesced), completion tracked by the same mbarrier (one arrive per lane)
+                // activations (after the predecessor, under PDL; weights above never wait):
+                // 16-B cp.async by the 32 lanes (a warp moves whole token rows, coalesced),
+                // completion tracked by the same mbarrier (one arrive per lane)
+                if (!waited) {
+                    dev::griddep_wait();
+                    waited = true;
+                }
                 if (A8) {
                     for (int idx = lane; idx < a.ntok * 16; idx += 32) {   // q: 16 chunks per token
                         const int i = idx >> 4, c = idx & 15;
@@ -293,6 +299,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_w4(const __grid_constant
             }
         }
         // ---- store: thread holds rows (gid, gid + 8) x tokens (2t, 2t + 1) of each tile pair
+        dev::griddep_wait();   // outputs are ordered after the predecessor (no-op once satisfied)
         const int64_t row0 = (int64_t)tile * a.bn + rbase;
 #pragma unroll
         for (int mt = 0; mt < MT; ++mt)

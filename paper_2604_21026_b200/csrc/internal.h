@@ -37,6 +37,9 @@ void clear_error();
     } while (0)
 
 inline bool aligned16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+// thread-local: API linears launch with programmatic dependent launch (mcapq_set_pdl)
+bool api_pdl();
+void set_api_pdl(bool on);
 inline cudaStream_t as_stream(void *s) { return reinterpret_cast<cudaStream_t>(s); }
 
 // Launch a kernel with the programmatic-stream-serialization attribute (PDL):

@@ -635,9 +635,16 @@ cudaError_t launch_gemm(int route, const uint8_t *nib, const uint16_t *scale, in
     return cudaSuccess;
 }
 
+namespace {
+thread_local bool t_api_pdl = false;
+}
+bool api_pdl() { return t_api_pdl; }
+void set_api_pdl(bool on) { t_api_pdl = on; }
+
 cudaError_t launch_linear_group(int route, const StreamGroup &g, const uint16_t *x, int64_t m, int64_t ldx, int ydt,
                                 void *ws, cudaStream_t s, bool pdl)
 {
+    pdl = pdl || api_pdl();
     if (m >= kGemmMinTokens && gemm_supported(g.k)) {
         const int8_t *q = nullptr;
         const float *sx = nullptr;
@@ -802,7 +809,7 @@ cudaError_t launch_stream_group(int route, const StreamGroup &g, const uint16_t 
     a.ydt = ydt;
     const int sms = device_sms();
     const int tp = stream_tokens_per_pass(route, g.k);
-    pdl = pdl || tune().pdl;
+    pdl = pdl || tune().pdl || api_pdl();
     for (int64_t tok0 = 0; tok0 < m; tok0 += tp) {
         a.tok0 = tok0;
         a.ntok = (int)((m - tok0) < tp ? (m - tok0) : tp);

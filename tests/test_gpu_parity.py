@@ -447,3 +447,32 @@ def test_step_kernel_equals_per_linear_path(mq):
         pw = mq.pack_w4(w.to(DEV))
         ref = mq.linear(routes[l], pw, x.clone(), out_dtype=torch.bfloat16)
         assert torch.equal(ref, y), (l, slot)
+
+
+@pytest.mark.parametrize("m", [1, 4, 16, 64])
+def test_pdl_chain_matches_plain(mq, m):
+    """mcapq_set_pdl(1): a chain of dependent linears (each input the previous output)
+    launched with programmatic dependent launch gives the same bits as plain launches
+    (activations/outputs wait for the predecessor; only weights stream early)."""
+    k = 2048
+    ws = [mq.pack_w4(si.weight(k, k, 1600 + i).to(DEV)) for i in range(4)]
+    x0 = si.activation(m, k, 1610 + m).to(DEV)
+    torch.cuda.synchronize()
+
+    def chain():
+        y = x0
+        outs = []
+        for i, w in enumerate(ws):
+            y = mq.linear(i % 2, w, y, out_dtype=torch.bfloat16)
+            outs.append(y)
+        return outs
+
+    ref = chain()
+    prev = mq.set_pdl(True)
+    try:
+        got = chain()
+    finally:
+        mq.set_pdl(prev)
+    torch.cuda.synchronize()
+    for a, b in zip(ref, got):
+        assert torch.equal(a, b)
