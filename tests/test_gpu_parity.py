@@ -476,3 +476,29 @@ def test_pdl_chain_matches_plain(mq, m):
     torch.cuda.synchronize()
     for a, b in zip(ref, got):
         assert torch.equal(a, b)
+
+
+def test_colshard_nccl_world1(mq):
+    """a8 through NCCL on this box's one GPU: mcapq_comm_init + mcapq_linear_colshard
+    (local rows, ncclAllGather, the rank-major permute for M > 1) equals mcapq_linear."""
+    import socket
+    import torch.distributed as dist
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", world_size=1, rank=0,
+                            device_id=torch.device(DEV))
+    try:
+        comm = mq.Comm()
+        n, k = 4096, 2048
+        pw = mq.pack_w4(si.weight(n, k, 1701).to(DEV))
+        for m in (1, 16):
+            x = si.activation(m, k, 1702 + m).to(DEV)
+            for route in (0, 1):
+                y = mq.linear_colshard(comm, route, pw.shard(1, 0), n, x)
+                torch.cuda.synchronize()
+                assert torch.equal(y, mq.linear(route, pw, x, out_dtype=torch.bfloat16))
+        del comm
+    finally:
+        dist.destroy_process_group()
