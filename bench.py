@@ -224,6 +224,46 @@ def time_dominant_kernel(mq, weights, xs, stream, reps_per_layer=4):
     return per_launch_ms, alg_bytes, len(seq)
 
 
+def time_colshard_lm_head(mq, dev, stream, dist, world, rank, m=1, reps=20):
+    """cfg5 a8: the 8B lm_head (128256 x 4096) column-sharded over the job's ranks, each
+    rank computing its N/P rows and all-gathering y over NCCL (mcapq_linear_colshard),
+    captured in a CUDA graph.  Per-call time = max over ranks (CUDA events)."""
+    n, k = si.linear_shape("llama-3.1-8b", "lm_head")
+    per = n // world
+    w = si.weight(n, k, si.seed_for(5, 0, "lm_head"))[rank * per:(rank + 1) * per].contiguous().to(dev)
+    pw = mq.pack_w4(w)
+    del w
+    x = si.activation(m, k, si.seed_for(5, 0, "lm_head", True)).to(dev)
+    comm = mq.Comm()
+    out = {}
+    for route, name in ((0, "w4a8"), (1, "w4a16")):
+        y = torch.empty(m, n, dtype=torch.bfloat16, device=dev)
+        ws = torch.empty(max(256, comm.workspace_bytes(route, m, n, k)), dtype=torch.uint8, device=dev)
+        with torch.cuda.stream(stream):
+            mq.linear_colshard(comm, route, pw, n, x, out=y, ws=ws, stream=stream)
+            stream.synchronize()
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=stream):
+                for _ in range(reps):
+                    mq.linear_colshard(comm, route, pw, n, x, out=y, ws=ws, stream=stream)
+            g.replay()
+            stream.synchronize()
+            dist.barrier()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            g.replay()
+            e1.record(stream)
+            e1.synchronize()
+        t = torch.tensor([e0.elapsed_time(e1) * 1000 / reps], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        us = float(t.item())
+        out[f"{name}_us"] = round(us, 3)
+        out[f"{name}_gbs_total"] = round((n * k // 2 + n * (k // 32) * 2) / us / 1e3, 1)
+    del comm
+    return {"N": n, "K": k, "M": m, "P": world, "rows_per_rank": per, **out,
+            "timing": "graph of 20 calls, CUDA events, max over ranks; includes the NCCL all-gather"}
+
+
 def time_single_linears(mq, dev, stream):
     """Single-linear rows of the metric at the other configs (cfg1 q_proj, cfg4 8B MLP,
     cfg5 lm_head), both routes, M = 1, rotating weight copies so each launch reads HBM."""
@@ -471,6 +511,12 @@ def main():
     k_traffic, k_traffic_src = traffic_from_profiles("stream_linear<0>")
 
     extras = [] if args.no_extras or rank != 0 else time_single_linears(mq, dev, stream)
+    colshard = None
+    if world > 1 and not args.no_extras:
+        try:
+            colshard = time_colshard_lm_head(mq, dev, stream, dist, world, rank)
+        except Exception as e:   # the headline line must still print
+            colshard = {"error": f"{type(e).__name__}: {e}"[:200]}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -517,6 +563,7 @@ def main():
             "kernels_per_step": kernels_per_step,
             "clocks": clk.report(),
             "single_linears": extras,
+            "lm_head_colshard": colshard,
         }
         if cpu is not None:
             line["cpu_baseline"] = cpu
