@@ -118,9 +118,69 @@ __device__ __forceinline__ bool bar_consumers_and(bool v)
 // this CTA got here: the load was the only round trip) staging goes on; otherwise
 // one thread waits for the producer's counter (low-traffic polling, no storm of
 // data re-reads) and the stale words are re-read once.
+// W4A8 with K <= 2048: one group per 8 threads (all 512 consumer threads busy at
+// K = 2048, half the per-thread quantiser work of the quad layout).
+__device__ __forceinline__ void stage_step_a8_oct(const StackOp &op, const ActSmem &L, int tid, uint32_t t16,
+                                                  bool check, int spin_ns, int polls, const unsigned int *counters)
+{
+    const int G = (int)(op.k / 32);
+    const uint32_t K2 = (uint32_t)(op.k / 2);
+    const bool tagged = op.xt != nullptr;
+    const bool on = tid < G * 8;
+    const int g = on ? tid >> 3 : 0, sub8 = tid & 7;
+    const int e0 = 32 * g + 4 * sub8;
+    uint4 ra = make_uint4(0, 0, 0, 0);
+    if (on) {
+        if (tagged) {
+            ra = ld_relaxed_128(op.xt + e0);
+        } else {
+            const uint2 p = ldg_x64<true>(op.x + e0);
+            ra = make_uint4(p.x, p.y, 0, 0);
+        }
+    }
+    if (tagged && check) {
+        int backoff = spin_ns;
+        for (int p = 0;; ++p) {
+            const bool ok = !on || tags_ok(ra, t16);
+            if (bar_consumers_and(ok)) break;
+            if (p >= polls) {
+                if (tid == 0)
+                    while (ld_acquire_gpu(counters + op.xt_op) < gridDim.x) __nanosleep(spin_ns);
+                bar_consumers();
+                if (!ok) {
+                    ra = ld_relaxed_128(op.xt + e0);
+                    while (!tags_ok(ra, t16)) {   // the producer published: current now
+                        __nanosleep(spin_ns);
+                        ra = ld_relaxed_128(op.xt + e0);
+                    }
+                }
+                break;
+            }
+            if (!ok) {
+                __nanosleep(backoff);
+                ra = ld_relaxed_128(op.xt + e0);
+            }
+            backoff = backoff < 1024 ? 2 * backoff : 1024;
+        }
+    }
+    uint2 w2;
+    if (tagged) w2 = untag(ra);
+    else w2 = make_uint2(ra.x, ra.y);
+    float v[4];
+    v[0] = __uint_as_float(w2.x << 16);
+    v[1] = __uint_as_float(w2.x & 0xffff0000u);
+    v[2] = __uint_as_float(w2.y << 16);
+    v[3] = __uint_as_float(w2.y & 0xffff0000u);
+    a8_oct_store(v, on, g, sub8, K2, L);
+}
+
 __device__ __forceinline__ void stage_step(const StackOp &op, bool a16, const ActSmem &L, int tid, uint32_t t16,
                                            bool check, int spin_ns, int polls, const unsigned int *counters)
 {
+    if (!a16 && op.k <= 2048) {
+        stage_step_a8_oct(op, L, tid, t16, check, spin_ns, polls, counters);
+        return;
+    }
     const int G = (int)(op.k / 32);
     const uint32_t K2 = (uint32_t)(op.k / 2);
     const int nq = G * 4;

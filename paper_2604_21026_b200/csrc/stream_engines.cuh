@@ -136,6 +136,45 @@ __device__ __forceinline__ void a8_quad_store(const float v[8], bool on, int i, 
     }
 }
 
+// Octet variant (one token): 8 threads per group, 4 elements each (elements 4 sub8 ..
+// 4 sub8 + 3); the same per-element arithmetic as a8_quad_store, so the codes, s and
+// sum q are bit-identical -- only the reduction tree spans 8 lanes instead of 4.
+__device__ __forceinline__ void a8_oct_store(const float v[4], bool on, int g, int sub8, uint32_t K2, const ActSmem &L)
+{
+    float amax = 0.0f;
+    int fin = 1;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        fin &= isfinite(v[j]) ? 1 : 0;
+        amax = fmaxf(amax, fabsf(v[j]));
+    }
+#pragma unroll
+    for (int o = 1; o < 8; o <<= 1) {
+        amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+        fin &= __shfl_xor_sync(0xffffffffu, fin, o);
+    }
+    const float s = __fdiv_rn(amax, 127.0f);
+    const bool live = fin && s != 0.0f;
+    const float inv = __frcp_rn(s);
+    uint32_t w = 0;
+    int sum = 0;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        const int code = live ? quant_code(v[j], s, inv) : 0;
+        sum += code;
+        w |= ((uint32_t)code & 0xffu) << (8 * j);
+    }
+#pragma unroll
+    for (int o = 1; o < 8; o <<= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+    if (on) {
+        sts32(L.act + (sub8 < 4 ? 0u : K2) + 16u * g + 4u * (sub8 & 3), w);
+        if (sub8 == 0)
+            asm volatile("st.shared.v2.u32 [%0], {%1,%2};" ::"r"(L.ssq + 8u * (uint32_t)g),
+                         "r"(__float_as_uint(live ? s : 0.0f)), "r"((uint32_t)(8 * sum))
+                         : "memory");
+    }
+}
+
 template <bool kCoherent>
 __device__ __forceinline__ void stage_a8(const uint16_t *xg, int64_t ldx, int ntok, int64_t k, const ActSmem &L,
                                          int tid, int nthreads)
