@@ -264,6 +264,40 @@ def time_colshard_lm_head(mq, dev, stream, dist, world, rank, m=1, reps=20):
             "timing": "graph of 20 calls, CUDA events, max over ranks; includes the NCCL all-gather"}
 
 
+def time_mlp8b_stack(mq, dev, stream, layers=8, steps=20):
+    """cfg4 shapes in the decode setting: an 8-layer Llama-3.1-8B MLP stack (gate/up
+    14336x4096, down 4096x14336) chained like decode (x_gate/up(l) = y_down(l-1),
+    x_down(l) = y_up(l)), one persistent stack_step launch per step, all W4A8 and all
+    W4A16.  One packed layer cloned per layer (distinct HBM copies: 793 MB per step > L2)."""
+    shapes = {s_: si.linear_shape("llama-3.1-8b", s_) for s_ in ("gate", "up", "down")}
+    base = {s_: mq.pack_w4(si.weight(n, k, si.seed_for(4, 0, s_)).to(dev)) for s_, (n, k) in shapes.items()}
+    weights = {(l, s_): mq.PackedW4(base[s_].nib.clone(), base[s_].scale.clone())
+               for l in range(layers) for s_ in shapes}
+    ys = {(l, s_): torch.empty(1, shapes[s_][0], dtype=torch.bfloat16, device=dev) for l in range(layers)
+          for s_ in shapes}
+    x0 = si.activation(1, shapes["gate"][1], si.seed_for(4, 0, "gate", True)).to(dev)
+    wbytes = sum(w.nbytes for w in weights.values())
+    out = {"layers": layers, "weight_bytes_per_step": wbytes, "shapes": "gate/up 14336x4096, down 4096x14336"}
+    for route, name in ((0, "w4a8"), (1, "w4a16")):
+        st = mq.Stack([route] * layers, max_m=1)
+        for l in range(layers):
+            xg = x0 if l == 0 else ys[(l - 1, "down")]
+            st.set(l, 0, 0, weights[(l, "gate")], xg, ys[(l, "gate")])
+            st.set(l, 1, 0, weights[(l, "up")], xg, ys[(l, "up")])
+            st.set(l, 2, 1, weights[(l, "down")], ys[(l, "up")], ys[(l, "down")])
+        with torch.cuda.stream(stream):
+            st.capture(1, stream=stream)
+        ms = time_graph(st, stream, steps, 3)
+        out[f"{name}_us_per_layer"] = round(ms * 1000 / layers, 3)
+        out[f"{name}_gbs"] = round(wbytes / (ms * 1e-3) / 1e9, 1)
+        out[f"{name}_frac"] = round(wbytes / (ms * 1e-3) / 1e9 / peaks()[0], 4)
+        out[f"{name}_kernels_per_step"] = st.launches(1)
+        del st
+    del weights, base
+    torch.cuda.empty_cache()
+    return out
+
+
 def time_single_linears(mq, dev, stream):
     """Single-linear rows of the metric at the other configs (cfg1 q_proj, cfg4 8B MLP,
     cfg5 lm_head), both routes, M = 1, rotating weight copies so each launch reads HBM."""
@@ -511,6 +545,7 @@ def main():
     k_traffic, k_traffic_src = traffic_from_profiles("stream_linear<0>")
 
     extras = [] if args.no_extras or rank != 0 else time_single_linears(mq, dev, stream)
+    mlp8b = None if args.no_extras or rank != 0 else time_mlp8b_stack(mq, dev, stream)
     colshard = None
     if world > 1 and not args.no_extras:
         try:
@@ -563,6 +598,7 @@ def main():
             "kernels_per_step": kernels_per_step,
             "clocks": clk.report(),
             "single_linears": extras,
+            "mlp_8b_stack": mlp8b,
             "lm_head_colshard": colshard,
         }
         if cpu is not None:

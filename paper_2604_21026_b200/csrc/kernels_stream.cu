@@ -358,7 +358,7 @@ struct Tune {
     // step_smem_kb 120: a ~5-stage ring keeps the HBM pipe busy while bounding the
     // per-SM queue of in-flight weight data that the chain's L2 accesses wait behind
     int smem_kb = 112, max_stages = 12, nocompute = 0, pdl = 0, trace = 0, step_smem_kb = 200, step = 1,
-        step_flags = 0, step_spin_ns = 32, step_polls = 3;
+        step_flags = 0, step_spin_ns = 32, step_polls = 3, ctas_per_sm = 0;
 };
 const Tune &tune()
 {
@@ -374,6 +374,8 @@ const Tune &tune()
         if (const char *e = getenv("MCAPQ_STEP_FLAGS")) v.step_flags = atoi(e);
         if (const char *e = getenv("MCAPQ_STEP_SPIN_NS")) v.step_spin_ns = atoi(e);
         if (const char *e = getenv("MCAPQ_STEP_POLLS")) v.step_polls = atoi(e);
+        if (const char *e = getenv("MCAPQ_STREAM_CTAS_PER_SM")) v.ctas_per_sm = atoi(e);
+        if (v.ctas_per_sm < 0 || v.ctas_per_sm > 2) v.ctas_per_sm = 0;
         if (v.step_smem_kb < 60) v.step_smem_kb = 60;
         if (v.step_smem_kb > 226) v.step_smem_kb = 226;
         if (v.smem_kb < 40) v.smem_kb = 40;
@@ -807,7 +809,12 @@ cudaError_t launch_stream_group(int route, const StreamGroup &g, const uint16_t 
     a.x = x;
     a.ldx = ldx;
     a.ydt = ydt;
-    const int sms = device_sms();
+    // grid: one CTA per SM leaves room for the next linear's CTA under PDL (hides the
+    // ramp of back-to-back linears); a long linear (>= 16 tiles per SM) instead runs two
+    // CTAs per SM -- twice the consumer warps per SM, and its ramp is amortised anyway
+    // (8B lm_head: 6.08 -> 6.47 TB/s).  MCAPQ_STREAM_CTAS_PER_SM forces 1 or 2.
+    const int per_sm = tune().ctas_per_sm ? tune().ctas_per_sm : (tiles >= 16 * device_sms() ? 2 : 1);
+    const int sms = device_sms() * per_sm;
     const int tp = stream_tokens_per_pass(route, g.k);
     pdl = pdl || tune().pdl || api_pdl();
     for (int64_t tok0 = 0; tok0 < m; tok0 += tp) {

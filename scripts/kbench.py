@@ -41,9 +41,11 @@ def main():
     ap.add_argument("--routes", default="0,1")
     ap.add_argument("--reps", type=int, default=0)
     ap.add_argument("--tag", default="")
+    ap.add_argument("--pdl", type=int, default=1, help="launch with programmatic dependent launch (mcapq_set_pdl)")
     args = ap.parse_args()
     dev = torch.device("cuda:0")
     mq.load()
+    mq.set_pdl(bool(args.pdl))
     l2 = torch.cuda.get_device_properties(dev).L2_cache_size
     stream = torch.cuda.Stream()
     env = {k: v for k, v in os.environ.items() if k.startswith("MCAPQ_")}

@@ -26,13 +26,32 @@ def main():
     ap.add_argument("--routes", default="golden")
     ap.add_argument("--independent", action="store_true")
     ap.add_argument("--ops", type=int, default=64)
+    ap.add_argument("--mlp8b", action="store_true", help="the 8-layer Llama-3.1-8B MLP stack instead")
     args = ap.parse_args()
     assert os.environ.get("MCAPQ_STREAM_TRACE") == "1"
     dev = torch.device("cuda:0")
     mq.load()
     routes = (mq.profile_parse(open(bench.GOLDEN_PROFILE).read()).routes() if args.routes == "golden"
               else [int(args.routes)] * 16)
-    st, _, _, _ = bench.build_stack(mq, dev, routes, chain=not args.independent)
+    if args.mlp8b:
+        import synth_inputs as si
+        L = 8
+        route = 0 if args.routes in ("golden", "0") else 1
+        shapes = {s_: si.linear_shape("llama-3.1-8b", s_) for s_ in ("gate", "up", "down")}
+        base = {s_: mq.pack_w4(si.weight(n, k, 7 + i).to(dev)) for i, (s_, (n, k)) in enumerate(shapes.items())}
+        keep = []
+        st = mq.Stack([route] * L, max_m=1)
+        prev = si.activation(1, 4096, 9).to(dev)
+        for l in range(L):
+            w = {s_: mq.PackedW4(base[s_].nib.clone(), base[s_].scale.clone()) for s_ in shapes}
+            y = {s_: torch.empty(1, shapes[s_][0], dtype=torch.bfloat16, device=dev) for s_ in shapes}
+            st.set(l, 0, 0, w["gate"], prev, y["gate"])
+            st.set(l, 1, 0, w["up"], prev, y["up"])
+            st.set(l, 2, 1, w["down"], y["up"], y["down"])
+            keep.append((w, y, prev))
+            prev = y["down"]
+    else:
+        st, _, _, _ = bench.build_stack(mq, dev, routes, chain=not args.independent)
     stream = torch.cuda.Stream()
     with torch.cuda.stream(stream):
         st.run(1, stream=stream)

@@ -502,3 +502,33 @@ def test_colshard_nccl_world1(mq):
         del comm
     finally:
         dist.destroy_process_group()
+
+
+def test_step_kernel_k14336_chain(mq, orc):
+    """The 8B MLP chain through the persistent step (K = 14336 input: 4 staging rounds per
+    thread; both routes), each linear against the oracle on the input it actually read."""
+    L, routes = 2, (0, 1)
+    gate_n, hid = 14336, 2048
+    st = mq.Stack(list(routes), max_m=1)
+    ops = []
+    prev = si.activation(1, hid, 1801).to(DEV)
+    for l in range(L):
+        ws = {s_: si.weight(n, k, 1810 + 3 * l + i) for i, (s_, (n, k)) in
+              enumerate((("gate", (gate_n, hid)), ("up", (gate_n, hid)), ("down", (hid, gate_n)))))}
+        y = {s_: torch.empty(1, w.shape[0], dtype=torch.bfloat16, device=DEV) for s_, w in ws.items()}
+        pw = {s_: mq.pack_w4(w.to(DEV)) for s_, w in ws.items()}
+        st.set(l, 0, 0, pw["gate"], prev, y["gate"])
+        st.set(l, 1, 0, pw["up"], prev, y["up"])
+        st.set(l, 2, 1, pw["down"], y["up"], y["down"])
+        ops += [(l, ws["gate"], prev, y["gate"]), (l, ws["up"], prev, y["up"]), (l, ws["down"], y["up"], y["down"])]
+        prev = y["down"]
+    st.run(1)
+    torch.cuda.synchronize()
+    assert st.launches(1) == 1
+    for (l, w, x, y) in ops:
+        nib, sc = orc.pack_w4(_f32(w))
+        if routes[l] == 0:
+            _, y64 = orc.w4a8_from_x(nib, sc, _f32(x))
+        else:
+            _, y64 = orc.w4a16(nib, sc, _f32(x))
+        _assert_close(y, y64, 2e-3)
