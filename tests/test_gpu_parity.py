@@ -513,8 +513,8 @@ def test_step_kernel_k14336_chain(mq, orc):
     ops = []
     prev = si.activation(1, hid, 1801).to(DEV)
     for l in range(L):
-        ws = {s_: si.weight(n, k, 1810 + 3 * l + i) for i, (s_, (n, k)) in
-              enumerate((("gate", (gate_n, hid)), ("up", (gate_n, hid)), ("down", (hid, gate_n)))))}
+        shapes = (("gate", (gate_n, hid)), ("up", (gate_n, hid)), ("down", (hid, gate_n)))
+        ws = {s_: si.weight(n, k, 1810 + 3 * l + i) for i, (s_, (n, k)) in enumerate(shapes)}
         y = {s_: torch.empty(1, w.shape[0], dtype=torch.bfloat16, device=DEV) for s_, w in ws.items()}
         pw = {s_: mq.pack_w4(w.to(DEV)) for s_, w in ws.items()}
         st.set(l, 0, 0, pw["gate"], prev, y["gate"])
