@@ -257,19 +257,18 @@ __device__ __forceinline__ void magic_bf16(uint32_t w, uint32_t mask, uint32_t m
 // Exact per-token activation code q = clamp(round_half_away(fl(v / s)), -127, 127)
 // from a per-group reciprocal: v * fl(1/s) is within 2.3e-5 of fl(v/s) for
 // |v/s| <= 127.01, so both round to the same integer unless v * inv lies within
-// 1e-4 of a half-integer; those rare cases take the IEEE division.  The fast path
-// rounds with the 1.5 * 2^23 magic (round-to-nearest-even == half-away off the
-// half-integers) and reads the integer out of the float's bits: no F2I, no FRND.
-// Bit-identical to roundf(__fdiv_rn(v, s)) clamped (test_gpu_parity: quantiser
-// bit-exact vs oracle; fused == separate).
+// 1e-4 of a half-integer; those rare cases take the IEEE division.  Bit-identical to
+// roundf(__fdiv_rn(v, s)) clamped (test_gpu_parity: quantiser bit-exact vs oracle).
 __device__ __forceinline__ int quant_code(float v, float s, float inv)
 {
     const float qa = v * inv;
-    const float t = qa + 12582912.0f;      // 1.5 * 2^23: t's low mantissa bits = rne(qa)
-    const float d = fabsf(qa - (t - 12582912.0f));   // distance to the nearest integer (exact)
-    int code = __float_as_int(t) - 0x4B400000;
-    if (d >= 0.5f - 1e-4f || !(fabsf(qa) <= 128.0f)) code = (int)roundf(__fdiv_rn(v, s));
-    return code < -127 ? -127 : (code > 127 ? 127 : code);
+    const float aq = fabsf(qa);
+    const float fr = aq - truncf(aq);
+    float r = roundf(qa);
+    // near a half-integer, or inv not finite (s subnormal): the IEEE division decides
+    if (fabsf(fr - 0.5f) <= 1e-4f || !(aq <= 128.0f)) r = roundf(__fdiv_rn(v, s));
+    r = fminf(fmaxf(r, -127.0f), 127.0f);
+    return (int)r;
 }
 
 // D = A.B + C with an explicit accumulator init (C may repeat registers).
