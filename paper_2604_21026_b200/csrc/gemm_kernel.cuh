@@ -21,39 +21,23 @@
 constexpr int kGemmWarps = 8;
 constexpr int kGemmThreads = (kGemmWarps + 1) * 32;
 constexpr int kGemmKS = 256;                 // K per slice (stage)
-constexpr int kGemmQStride = 272;            // W4A8 q row in smem: 256 B + 16 (conflict-free B loads)
-constexpr int kGemmXStride = 544;            // W4A16 x row in smem: 512 B + 32
-constexpr int kGemmSSStride = 80;            // W4A8 {s[8], sq[8]} per token: 64 B + 16 (conflict-free pairs)
 constexpr int kGemmMaxStages = 8;
 
 struct GemmArgs {
-    const CUtensorMap *maps;   // {nib box {128 B, bn}, scale box {8, bn}}
+    const CUtensorMap *maps;    // {nib box {128 B, bn}, scale box {8, bn}}
+    const CUtensorMap *amaps;   // activations: W4A8 {q, sx, sq}, W4A16 {x} (gemm_act_descriptors)
     void *y;
     int64_t ldy;
     int64_t n, k;
     int ydt;
-    const uint16_t *x;         // W4A16: [m][ldx] bf16
-    int64_t ldx;
-    const int8_t *q;           // W4A8: quant_a8 workspace (q [m][k], sx [m][k/32], sq [m][k/32])
-    const float *sx;
-    const int32_t *sq;
     int64_t tok0;              // first token of this pass
     int ntok;                  // tokens in this pass (<= 64)
+    int mp;                    // padded tokens of the pass (activation box rows)
     int bn, wt;                // CTA rows; token-warps (row-warps = 8 / wt)
     int row_tiles;
     int stages;
-    uint32_t nib_bytes, sc_off, act_off, ss_off, stage_bytes;   // per-stage layout
+    uint32_t nib_bytes, sc_off, act_off, ss_off, sq_off, stage_bytes;   // per-stage layout
 };
-
-__device__ __forceinline__ void cp_async16(uint32_t dst, const void *src)
-{
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
-}
-// arrive on `bar` once this thread's outstanding cp.async copies have landed
-__device__ __forceinline__ void cp_async_arrive(uint32_t bar)
-{
-    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(bar) : "memory");
-}
 
 // fp32 pairs in one 64-bit register (FFMA2 / FADD2 / FMUL2: two independent IEEE ops)
 typedef unsigned long long f2_t;
@@ -117,7 +101,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_w4(const __grid_constant
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < S; ++s) {
-            mbar_init(full + 8u * s, 1 + 32);   // the TMA expect_tx arrive + one cp.async arrive per producer lane
+            mbar_init(full + 8u * s, 1);
             mbar_init(empty + 8u * s, kGemmWarps);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -126,57 +110,44 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_w4(const __grid_constant
     dev::griddep_launch();   // the next kernel may launch: it only touches weights until its own wait
 
     if (warp == kGemmWarps) {
-        // ================= producer =================
+        // ================= producer: one thread, TMA only =================
         if (lane == 0) {
-            asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(a.maps)) : "memory");
-            asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(a.maps + 1)) : "memory");
-        }
-        const uint64_t pol = evict_first_policy();
-        const uint32_t tx = a.nib_bytes + (uint32_t)a.bn * 16u;
-        int s = 0;
-        uint32_t ph = 0;
-        bool waited = false;
-        for (int tile = blockIdx.x; tile < a.row_tiles; tile += gridDim.x) {
-            const int row0 = tile * a.bn;
-            for (int sl = 0; sl < nslices; ++sl) {
-                mbar_wait(empty + 8u * s, ph ^ 1u);
-                const uint32_t st = sb + (uint32_t)s * a.stage_bytes;
-                const uint32_t fb = full + 8u * s;
-                if (lane == 0) {
+            for (int j = 0; j < 2; ++j) {
+                asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(a.maps + j)) : "memory");
+                asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(a.amaps + j)) : "memory");
+            }
+            const uint64_t pol = evict_first_policy();
+            const uint32_t act_tx = A8 ? (uint32_t)a.mp * (256u + 64u) : (uint32_t)a.mp * 512u;
+            const uint32_t tx = a.nib_bytes + (uint32_t)a.bn * 16u + act_tx;
+            const int y0 = (int)a.tok0;
+            int s = 0;
+            uint32_t ph = 0;
+            bool waited = false;
+            for (int tile = blockIdx.x; tile < a.row_tiles; tile += gridDim.x) {
+                const int row0 = tile * a.bn;
+                for (int sl = 0; sl < nslices; ++sl) {
+                    mbar_wait(empty + 8u * s, ph ^ 1u);
+                    const uint32_t st = sb + (uint32_t)s * a.stage_bytes;
+                    const uint32_t fb = full + 8u * s;
                     mbar_expect_tx(fb, tx);
                     tma_2d(st, a.maps, sl * 128, row0, fb, pol);
                     tma_2d(st + a.sc_off, a.maps + 1, sl * 8, row0, fb, pol);
-                }
-                // activations (after the predecessor, under PDL; weights above never wait):
-                // 16-B cp.async by the 32 lanes (a warp moves whole token rows, coalesced),
-                // completion tracked by the same mbarrier (one arrive per lane)
-                if (!waited) {
-                    dev::griddep_wait();
-                    waited = true;
-                }
-                if (A8) {
-                    for (int idx = lane; idx < a.ntok * 16; idx += 32) {   // q: 16 chunks per token
-                        const int i = idx >> 4, c = idx & 15;
-                        cp_async16(st + a.act_off + (uint32_t)i * kGemmQStride + 16u * c,
-                                   a.q + (a.tok0 + i) * a.k + (int64_t)sl * kGemmKS + 16 * c);
+                    // activations only after the predecessor (PDL); weights above never wait
+                    if (!waited) {
+                        dev::griddep_wait();
+                        waited = true;
                     }
-                    for (int idx = lane; idx < a.ntok * 4; idx += 32) {    // s (2 chunks), sq (2 chunks)
-                        const int i = idx >> 2, c = idx & 3;
-                        const int64_t off = (a.tok0 + i) * G + sl * 8 + 4 * (c & 1);
-                        const void *src = (c < 2) ? (const void *)(a.sx + off) : (const void *)(a.sq + off);
-                        cp_async16(st + a.ss_off + (uint32_t)i * kGemmSSStride + 16u * c, src);
+                    if (A8) {
+                        tma_3d(st + a.act_off, a.amaps, 0, y0, sl * 2, fb, 0);
+                        tma_2d(st + a.ss_off, a.amaps + 1, sl * 8, y0, fb, 0);
+                        tma_2d(st + a.sq_off, a.amaps + 2, sl * 8, y0, fb, 0);
+                    } else {
+                        tma_3d(st + a.act_off, a.amaps, 0, y0, sl * 4, fb, 0);
                     }
-                } else {
-                    for (int idx = lane; idx < a.ntok * 32; idx += 32) {   // x: 32 chunks per token row
-                        const int i = idx >> 5, c = idx & 31;
-                        cp_async16(st + a.act_off + (uint32_t)i * kGemmXStride + 16u * c,
-                                   a.x + (a.tok0 + i) * a.ldx + (int64_t)sl * kGemmKS + 8 * c);
+                    if (++s == S) {
+                        s = 0;
+                        ph ^= 1u;
                     }
-                }
-                cp_async_arrive(fb);
-                if (++s == S) {
-                    s = 0;
-                    ph ^= 1u;
                 }
             }
         }
@@ -237,16 +208,21 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_w4(const __grid_constant
 #pragma unroll
                         for (int nt = 0; nt < NT; ++nt) {
                             const int tk = tbase + nt * 8;
-                            const uint32_t qrow = act + (uint32_t)(tk + gid) * kGemmQStride + 32u * g + 4u * t;
-                            const uint32_t b0 = lds32(qrow), b1 = lds32(qrow + 16u);
-                            const uint32_t ss0 = a.ss_off + st + (uint32_t)(tk + 2 * t) * kGemmSSStride + 4u * g;
-                            const uint32_t ss1 = ss0 + kGemmSSStride;
-                            const f2_t s2 = f2_pack_bits(lds32(ss0), lds32(ss1));   // (s of token 2t, 2t+1)
+                            // q of token tk + gid, bytes 32g + 4t (low half) and + 16 (high half):
+                            // smem [2][mp][128 B], 16-B unit u of row r at u ^ (r & 7)
+                            const uint32_t tok = (uint32_t)(tk + gid);
+                            const uint32_t qrow = act + (uint32_t)(g >> 2) * (uint32_t)a.mp * 128u + tok * 128u + 4u * t;
+                            const uint32_t u0 = 2u * (uint32_t)(g & 3);
+                            const uint32_t b0 = lds32(qrow + ((u0 ^ (tok & 7u)) << 4));
+                            const uint32_t b1 = lds32(qrow + (((u0 + 1u) ^ (tok & 7u)) << 4));
+                            const uint32_t ss0 = st + a.ss_off + (uint32_t)(tk + 2 * t) * 32u + 4u * g;
+                            const uint32_t sq0 = st + a.sq_off + (uint32_t)(tk + 2 * t) * 32u + 4u * g;
+                            const f2_t s2 = f2_pack_bits(lds32(ss0), lds32(ss0 + 32u));   // (s of token 2t, 2t+1)
                             // accumulator init 1.5 * 2^23 - 8 sq: the int32 result is the bit
                             // pattern of the float 1.5 * 2^23 + D (|D| < 2^17), so one FADD2
                             // recovers D exactly (no I2F, no separate - 8 sq)
-                            const int m0 = 0x4B400000 - 8 * (int)lds32(ss0 + 32u);
-                            const int m1 = 0x4B400000 - 8 * (int)lds32(ss1 + 32u);
+                            const int m0 = 0x4B400000 - 8 * (int)lds32(sq0);
+                            const int m1 = 0x4B400000 - 8 * (int)lds32(sq0 + 32u);
 #pragma unroll
                             for (int mt = 0; mt < MT; ++mt) {
                                 int c[4];
@@ -265,8 +241,14 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_w4(const __grid_constant
 #pragma unroll
                         for (int nt = 0; nt < NT; ++nt) {
                             const int tk = tbase + nt * 8;
-                            const uint32_t xrow = act + (uint32_t)(tk + gid) * kGemmXStride + 64u * g + 8u * t;
-                            const uint2 lo = lds64(xrow), hi = lds64(xrow + 32u);
+                            // x of token tk + gid, elements 32g + 4t.. (8 B) and + 16: smem
+                            // [4][mp][128 B], 16-B unit u of row r at u ^ (r & 7)
+                            const uint32_t tok = (uint32_t)(tk + gid);
+                            const uint32_t xrow = act + (uint32_t)(g >> 1) * (uint32_t)a.mp * 128u + tok * 128u +
+                                                  8u * (uint32_t)(t & 1);
+                            const uint32_t u0 = 4u * (uint32_t)(g & 1) + (uint32_t)(t >> 1);
+                            const uint2 lo = lds64(xrow + ((u0 ^ (tok & 7u)) << 4));
+                            const uint2 hi = lds64(xrow + (((u0 + 2u) ^ (tok & 7u)) << 4));
                             bx[nt][0] = __byte_perm(lo.x, lo.y, 0x5410);
                             bx[nt][1] = __byte_perm(lo.x, lo.y, 0x7632);
                             bx[nt][2] = __byte_perm(hi.x, hi.y, 0x5410);

@@ -445,37 +445,71 @@ cudaError_t launch_one(StreamArgs &a, cudaStream_t s, bool pdl, int sms)
 }  // namespace
 
 // ------------------------------------------------------------------ descriptor table
-// Device-resident {nib, scale} tensor-map pairs, keyed by (nib, scale, n, k).
-// Entries are written once (pinned staging -> cudaMemcpyAsync, capturable) and
-// never reused, so a kernel in flight or a captured graph always sees its own.
+// Device-resident groups of tensor maps (4 slots each), keyed by what they describe.
+// Entries are written once (pinned staging -> cudaMemcpyAsync, capturable) and never
+// reused, so a kernel in flight or a captured graph always sees its own.
+//   kind 0        : stream maps {nib, scale} of a packed weight (16-row x 2048-K stages)
+//   kind BN > 0   : gemm maps {nib, scale} (BN rows x 256 K)
+//   kind -1 - mp  : gemm W4A8 activation maps {q, sx, sq} of the quant_a8 workspace, mp-row boxes
+//   kind -100 - mp: gemm W4A16 activation map {x}, mp-row boxes
 namespace {
 struct DescKey {
-    const void *nib, *scale;
-    int64_t n, k;
-    int kind;   // 0: stream maps (16-row x 2048-K stages); BN > 0: gemm maps (BN rows x 256 K)
+    const void *p0, *p1;
+    int64_t n, k, ld;
+    int kind;
     bool operator==(const DescKey &o) const
     {
-        return nib == o.nib && scale == o.scale && n == o.n && k == o.k && kind == o.kind;
+        return p0 == o.p0 && p1 == o.p1 && n == o.n && k == o.k && ld == o.ld && kind == o.kind;
     }
 };
 struct DescKeyHash {
     size_t operator()(const DescKey &d) const
     {
-        return std::hash<const void *>()(d.nib) ^ (std::hash<const void *>()(d.scale) << 1) ^
-               (size_t)(d.n * 31 + d.k * 7 + d.kind);
+        return std::hash<const void *>()(d.p0) ^ (std::hash<const void *>()(d.p1) << 1) ^
+               (size_t)(d.n * 31 + d.k * 7 + d.ld * 13 + d.kind);
     }
 };
+constexpr int kDescSlots = 4;
 struct DescTable {
     std::mutex mu;
     std::unordered_map<DescKey, const CUtensorMap *, DescKeyHash> map;
     std::vector<std::pair<CUtensorMap *, CUtensorMap *>> blocks;   // (device, pinned host)
-    int used = 0;                                                   // pairs used in the last block
-    static constexpr int kPairs = 4096;
+    int used = 0;                                                   // groups used in the last block
+    static constexpr int kGroups = 2048;
 };
 DescTable &desc_table()
 {
     static DescTable t;
     return t;
+}
+
+// Look the group up, or encode it (enc fills up to kDescSlots host maps) and upload it.
+template <typename Enc>
+const CUtensorMap *desc_group(const DescKey &key, Enc enc, cudaStream_t s)
+{
+    DescTable &t = desc_table();
+    std::lock_guard<std::mutex> lock(t.mu);
+    auto it = t.map.find(key);
+    if (it != t.map.end()) return it->second;
+    if (t.blocks.empty() || t.used == DescTable::kGroups) {
+        CUtensorMap *d = nullptr, *h = nullptr;
+        if (cudaMalloc(&d, sizeof(CUtensorMap) * kDescSlots * DescTable::kGroups) != cudaSuccess) return nullptr;
+        if (cudaMallocHost(&h, sizeof(CUtensorMap) * kDescSlots * DescTable::kGroups) != cudaSuccess) {
+            cudaFree(d);
+            return nullptr;
+        }
+        t.blocks.emplace_back(d, h);
+        t.used = 0;
+    }
+    CUtensorMap *dg = t.blocks.back().first + kDescSlots * t.used;
+    CUtensorMap *hg = t.blocks.back().second + kDescSlots * t.used;
+    memset(hg, 0, sizeof(CUtensorMap) * kDescSlots);
+    if (!enc(hg)) return nullptr;
+    if (cudaMemcpyAsync(dg, hg, kDescSlots * sizeof(CUtensorMap), cudaMemcpyHostToDevice, s) != cudaSuccess)
+        return nullptr;
+    ++t.used;
+    t.map.emplace(key, dg);
+    return dg;
 }
 }  // namespace
 
@@ -505,31 +539,60 @@ bool encode_gemm_maps(CUtensorMap *tn, CUtensorMap *ts, const uint8_t *nib, cons
 const CUtensorMap *descriptors_of_kind(const uint8_t *nib, const uint16_t *scale, int64_t n, int64_t k, int kind,
                                        cudaStream_t s)
 {
-    DescTable &t = desc_table();
-    std::lock_guard<std::mutex> lock(t.mu);
-    const DescKey key{nib, scale, n, k, kind};
-    auto it = t.map.find(key);
-    if (it != t.map.end()) return it->second;
-    if (t.blocks.empty() || t.used == DescTable::kPairs) {
-        CUtensorMap *d = nullptr, *h = nullptr;
-        if (cudaMalloc(&d, sizeof(CUtensorMap) * 2 * DescTable::kPairs) != cudaSuccess) return nullptr;
-        if (cudaMallocHost(&h, sizeof(CUtensorMap) * 2 * DescTable::kPairs) != cudaSuccess) {
-            cudaFree(d);
-            return nullptr;
-        }
-        t.blocks.emplace_back(d, h);
-        t.used = 0;
-    }
-    CUtensorMap *dpair = t.blocks.back().first + 2 * t.used;
-    CUtensorMap *hpair = t.blocks.back().second + 2 * t.used;
-    if (!(kind == 0 ? encode_maps(&hpair[0], &hpair[1], nib, scale, n, k)
-                    : encode_gemm_maps(&hpair[0], &hpair[1], nib, scale, n, k, kind)))
-        return nullptr;
-    if (cudaMemcpyAsync(dpair, hpair, 2 * sizeof(CUtensorMap), cudaMemcpyHostToDevice, s) != cudaSuccess)
-        return nullptr;
-    ++t.used;
-    t.map.emplace(key, dpair);
-    return dpair;
+    const DescKey key{nib, scale, n, k, 0, kind};
+    return desc_group(
+        key,
+        [&](CUtensorMap *h) {
+            return kind == 0 ? encode_maps(&h[0], &h[1], nib, scale, n, k)
+                             : encode_gemm_maps(&h[0], &h[1], nib, scale, n, k, kind);
+        },
+        s);
+}
+
+// gemm activation maps, boxes of mp token rows (rows past m read as zeros):
+//   W4A8  q  [m][k] int8 as 3-D {128 B, m, k/128}, box {128, mp, 2} (= one 256-K slice),
+//         128B swizzle -> smem [2][mp][128 B];  sx / sq [m][k/32] 2-D, box {8, mp} -> [mp][8]
+//   W4A16 x  [m][ldx] bf16 as 3-D {64, m, k/64}, box {64, mp, 4}, 128B swizzle -> [4][mp][128 B]
+const CUtensorMap *gemm_act_descriptors(bool a8, const void *x_or_q, const float *sx, const int32_t *sq, int64_t m,
+                                        int64_t k, int64_t ldx, int mp, cudaStream_t s)
+{
+    const DescKey key{x_or_q, a8 ? (const void *)sx : nullptr, m, k, a8 ? (int64_t)(uintptr_t)sq : ldx,
+                      a8 ? -1 - mp : -100 - mp};
+    return desc_group(
+        key,
+        [&](CUtensorMap *h) {
+            EncodeTiledFn fn = encode_fn();
+            if (!fn) return false;
+            if (a8) {
+                const cuuint64_t qd[3] = {128, (cuuint64_t)m, (cuuint64_t)(k / 128)};
+                const cuuint64_t qs[2] = {(cuuint64_t)k, 128};
+                const cuuint32_t qb[3] = {128, (cuuint32_t)mp, 2};
+                const cuuint32_t e3[3] = {1, 1, 1};
+                if (fn(&h[0], CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<void *>(x_or_q), qd, qs, qb, e3,
+                       CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+                    return false;
+                const cuuint64_t sd[2] = {(cuuint64_t)(k / 32), (cuuint64_t)m};
+                const cuuint64_t ss[1] = {(cuuint64_t)(k / 32) * 4};
+                const cuuint32_t sb[2] = {8, (cuuint32_t)mp};
+                const cuuint32_t e2[2] = {1, 1};
+                if (fn(&h[1], CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float *>(sx), sd, ss, sb, e2,
+                       CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+                    return false;
+                return fn(&h[2], CU_TENSOR_MAP_DATA_TYPE_INT32, 2, const_cast<int32_t *>(sq), sd, ss, sb, e2,
+                          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                          CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+            }
+            const cuuint64_t xd[3] = {64, (cuuint64_t)m, (cuuint64_t)(k / 64)};
+            const cuuint64_t xs[2] = {(cuuint64_t)ldx * 2, 128};
+            const cuuint32_t xb[3] = {64, (cuuint32_t)mp, 4};
+            const cuuint32_t e3[3] = {1, 1, 1};
+            return fn(&h[0], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void *>(x_or_q), xd, xs, xb, e3,
+                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+        },
+        s);
 }
 
 const CUtensorMap *stream_descriptors(const uint8_t *nib, const uint16_t *scale, int64_t n, int64_t k,
@@ -601,29 +664,27 @@ cudaError_t launch_gemm(int route, const uint8_t *nib, const uint16_t *scale, in
         GemmArgs a;
         memset(&a, 0, sizeof(a));
         a.maps = descriptors_of_kind(nib, scale, n, k, bn, s);
-        if (!a.maps) return cudaErrorInvalidValue;
+        a.amaps = gemm_act_descriptors(a8, a8 ? (const void *)q : (const void *)x, sx, sq, m, k, ldx, mp, s);
+        if (!a.maps || !a.amaps) return cudaErrorInvalidValue;
         a.y = y;
         a.ldy = ldy;
         a.n = n;
         a.k = k;
         a.ydt = ydt;
-        a.x = x;
-        a.ldx = ldx;
-        a.q = q;
-        a.sx = sx;
-        a.sq = sq;
         a.tok0 = tok0;
         a.ntok = ntok;
+        a.mp = mp;
         a.bn = bn;
         a.wt = c.wt;
         a.row_tiles = (int)((n + bn - 1) / bn);
-        // stage: nibbles | scales | activations (| W4A8 s, sq), 1 KiB aligned pieces
+        // stage: nibbles | scales | activations (| W4A8 s, sq), swizzled boxes 1 KiB aligned
         a.nib_bytes = (uint32_t)bn * 128u;
         a.sc_off = (uint32_t)round_up(a.nib_bytes, 1024);
         a.act_off = (uint32_t)round_up(a.sc_off + (size_t)bn * 16, 1024);
-        const size_t act = a8 ? (size_t)mp * kGemmQStride : (size_t)mp * kGemmXStride;
+        const size_t act = a8 ? (size_t)mp * 256 : (size_t)mp * 512;
         a.ss_off = (uint32_t)round_up(a.act_off + act, 128);
-        a.stage_bytes = (uint32_t)round_up(a.ss_off + (a8 ? (size_t)mp * kGemmSSStride : 0), 1024);
+        a.sq_off = a.ss_off + (uint32_t)mp * 32u;
+        a.stage_bytes = (uint32_t)round_up(a.ss_off + (a8 ? (size_t)mp * 64 : 0), 1024);
         int S = (int)((227 * 1024 - 1024 - 256) / a.stage_bytes);
         S = S > kGemmMaxStages ? kGemmMaxStages : S;
         if (S < 2) return cudaErrorInvalidValue;
