@@ -36,6 +36,9 @@ import synth_inputs as si  # noqa: E402
 METRIC = json.load(open(os.path.join(ROOT, "BASELINE.json")))["metric"]
 GOLDEN_PROFILE = os.path.join(ROOT, "tests", "golden", "llama32_1b_profile.json")
 SLOTS = ["q", "k", "v", "o", "gate", "up", "down"]
+WORKLOAD = ("llama-3.2-1b 16-layer decode linear stack (q,k,v,o,gate,up,down), MCAP mask from tab:per_layer_scores "
+            "(L15 W4A16, 15 layers W4A8), batch 1, chained (x_o=y_q, x_gate/up=y_o, x_down=y_up, "
+            "x_qkv(l+1)=y_down(l)), one CUDA graph")
 INPUT_ID = {"q": 0, "k": 0, "v": 0, "o": 1, "gate": 2, "up": 2, "down": 3}
 MODEL = "llama-3.2-1b"
 CONFIG_ID = 2
@@ -439,7 +442,7 @@ def run_reference(args):
         "impl": "reference", "metric": METRIC, "value": round(v, 4), "unit": "GB/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "s8xu4->s32,f32 (W4A8) | f32 (W4A16)", "data": "synthetic",
-        "config": {"workload": "llama-3.2-1b 16-layer decode linear stack, MCAP mask (L15 W4A16), batch 1"},
+        "config": {"workload": WORKLOAD, "m": 1, "layers": 16, "routes": "".join(str(r) for r in routes)},
         "cpu_baseline": {"value": round(v, 4), "unit": "GB/s", "cores": cores, "kind": "oracle",
                          "sample": "per step: layer 0 (W4A8) and layer 15 (W4A16) of the stack run in full by the "
                                    f"C oracle, extrapolated to the 15+1 mask; {secs:.1f} s of CPU work in total"},
@@ -566,9 +569,7 @@ def main():
             "warmup": args.warmup, "ms_per_step": round(ms_max, 5), "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "s8xu4->s32,f32 (W4A8) | bf16->f32 (W4A16)",
             "data": "synthetic (seeded bf16 weights/activations, random init)",
-            "config": {"workload": "llama-3.2-1b 16-layer decode linear stack (q,k,v,o,gate,up,down), MCAP mask "
-                                   "from tab:per_layer_scores (L15 W4A16, 15 layers W4A8), batch 1, chained "
-                                   "(x_o=y_q, x_gate/up=y_o, x_down=y_up, x_qkv(l+1)=y_down(l)), one CUDA graph",
+            "config": {"workload": WORKLOAD,
                        "m": 1, "layers": L, "routes": "".join(str(r) for r in routes),
                        "weight_bytes_per_step": wbytes, "activation_bytes_per_step": act_bytes,
                        "l2_policy": f"no flush: {wbytes / 1e6:.0f} MB of weights per step > {l2 / 1e6:.0f} MB L2",
