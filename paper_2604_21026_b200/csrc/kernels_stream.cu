@@ -772,10 +772,14 @@ cudaError_t launch_stack_step(const void *ops_dev, int nops, unsigned int *count
 {
     static int attr_done = 0;
     if (!attr_done) {
-        cudaError_t e = cudaFuncSetAttribute(stack_step<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaError_t e = cudaFuncSetAttribute(stack_step<false, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              227 * 1024);
         if (e == cudaSuccess)
-            e = cudaFuncSetAttribute(stack_step<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+            e = cudaFuncSetAttribute(stack_step<true, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+        if (e == cudaSuccess)
+            e = cudaFuncSetAttribute(stack_step<false, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+        if (e == cudaSuccess)
+            e = cudaFuncSetAttribute(stack_step<true, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
         if (e != cudaSuccess) return e;
         attr_done = 1;
     }
@@ -821,7 +825,9 @@ cudaError_t launch_stack_step(const void *ops_dev, int nops, unsigned int *count
     attr[0].val.cooperative = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    return a.trace ? cudaLaunchKernelEx(&cfg, stack_step<true>, a) : cudaLaunchKernelEx(&cfg, stack_step<false>, a);
+    if (max_k <= 8192)
+        return a.trace ? cudaLaunchKernelEx(&cfg, stack_step<true, 2>, a) : cudaLaunchKernelEx(&cfg, stack_step<false, 2>, a);
+    return a.trace ? cudaLaunchKernelEx(&cfg, stack_step<true, 4>, a) : cudaLaunchKernelEx(&cfg, stack_step<false, 4>, a);
 }
 
 size_t stream_trace_read(unsigned long long *host_out, size_t max_records)

@@ -174,6 +174,7 @@ __device__ __forceinline__ void stage_step_a8_oct(const StackOp &op, const ActSm
     a8_oct_store(v, on, g, sub8, K2, L);
 }
 
+template <int kRounds>
 __device__ __forceinline__ void stage_step(const StackOp &op, bool a16, const ActSmem &L, int tid, uint32_t t16,
                                            bool check, int spin_ns, int polls, const unsigned int *counters)
 {
@@ -189,9 +190,9 @@ __device__ __forceinline__ void stage_step(const StackOp &op, bool a16, const Ac
     if (a16)
         for (int idx = tid; idx < G * 8; idx += NT)     // tokens 1..7 of corr: zero
             if ((idx & 7) != 0) sts32(L.corr + 4u * (uint32_t)idx, 0u);
-    uint4 ra[kStepMaxRounds], rb[kStepMaxRounds];
+    uint4 ra[kRounds], rb[kRounds];
 #pragma unroll
-    for (int r = 0; r < kStepMaxRounds; ++r) {
+    for (int r = 0; r < kRounds; ++r) {
         const int idx = r * NT + tid;
         if (r * NT < nq && idx < nq) {
             const int g = idx >> 2, sub = idx & 3;
@@ -214,7 +215,7 @@ __device__ __forceinline__ void stage_step(const StackOp &op, bool a16, const Ac
         // `polls` CTA-wide rounds fall back to the producer's counter
         auto reload_stale = [&]() {
 #pragma unroll
-            for (int r = 0; r < kStepMaxRounds; ++r) {
+            for (int r = 0; r < kRounds; ++r) {
                 const int idx = r * NT + tid;
                 if (r * NT < nq && idx < nq && !(tags_ok(ra[r], t16) && tags_ok(rb[r], t16))) {
                     const int g = idx >> 2, sub = idx & 3;
@@ -233,7 +234,7 @@ __device__ __forceinline__ void stage_step(const StackOp &op, bool a16, const Ac
             for (;;) {
                 bool ok = true;
 #pragma unroll
-                for (int r = 0; r < kStepMaxRounds; ++r)
+                for (int r = 0; r < kRounds; ++r)
                     if (r * NT + tid < nq) ok = ok && tags_ok(ra[r], t16) && tags_ok(rb[r], t16);
                 if (ok) break;
                 __nanosleep(backoff);
@@ -244,7 +245,7 @@ __device__ __forceinline__ void stage_step(const StackOp &op, bool a16, const Ac
         for (int p = 0; polls >= 0; ++p) {
             bool ok = true;
 #pragma unroll
-            for (int r = 0; r < kStepMaxRounds; ++r)
+            for (int r = 0; r < kRounds; ++r)
                 if (r * NT + tid < nq) ok = ok && tags_ok(ra[r], t16) && tags_ok(rb[r], t16);
             if (bar_consumers_and(ok)) break;
             if (p >= polls) {
@@ -262,7 +263,7 @@ __device__ __forceinline__ void stage_step(const StackOp &op, bool a16, const Ac
         }
     }
 #pragma unroll
-    for (int r = 0; r < kStepMaxRounds; ++r) {
+    for (int r = 0; r < kRounds; ++r) {
         if (r * NT >= nq) break;   // CTA-uniform
         const int idx = r * NT + tid;
         const bool on = idx < nq;
@@ -306,7 +307,9 @@ __device__ __forceinline__ void store_step(const StackOp &op, int m, int64_t row
     }
 }
 
-template <bool kTrace>
+// kRounds: staging rounds of 512 quads (2: K <= 8192, 4: K <= 16384) -- fewer rounds,
+// fewer live registers under the 96-register cap of 18 warps per SM
+template <bool kTrace, int kRounds>
 __global__ void __launch_bounds__(kStepThreads, 1) stack_step(const __grid_constant__ StackArgs a)
 {
     extern __shared__ __align__(16) uint8_t smem_raw[];
@@ -502,7 +505,7 @@ __global__ void __launch_bounds__(kStepThreads, 1) stack_step(const __grid_const
             const bool a16 = route == MCAPQ_W4A16;
             const ActSmem L = act_layout(a16, act, k, 1);
             bar_consumers();   // every warp is done reading the previous linear's activations
-            if (!(a.flags & 4)) stage_step(op, a16, L, threadIdx.x, t16, !(a.flags & 8), a.spin_ns, a.polls, a.counters);
+            if (!(a.flags & 4)) stage_step<kRounds>(op, a16, L, threadIdx.x, t16, !(a.flags & 8), a.spin_ns, a.polls, a.counters);
             bar_consumers();
             if (kTrace) tr2 = globaltimer();
 
