@@ -215,9 +215,13 @@ mcapq_status mcapq_w4a8_group_dots(const uint8_t *nib, int64_t n, int64_t k, con
 /*
  * DEBUG: per-CTA timeline of the stream kernels, recorded only when the
  * environment has MCAPQ_STREAM_TRACE=1 at library load.  Copies up to
- * max_records records of 8 uint64 {launch id, block, t_start, t_after_wait,
- * t_activations_ready, t_end, 0, 0} (%globaltimer ns) into host memory;
- * synchronises the device.  Returns the number of records.
+ * max_records records of 8 uint64 into host memory (%globaltimer ns) and
+ * synchronises the device; returns the number of records.
+ *   per-linear kernels: {launch id, block, t_start, t_after_wait,
+ *                        t_activations_ready, t_end, 0, t_first_stage}
+ *   persistent step   : one record per (linear, CTA): {linear, block << 32 |
+ *                        stalled stages << 16 | stages, t_start, t_after_go,
+ *                        t_staged, t_end, t_first_stage, t_last_compute}
  */
 size_t mcapq_debug_stream_trace(uint64_t *host_out, size_t max_records);
 
