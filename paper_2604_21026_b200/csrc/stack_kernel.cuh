@@ -509,6 +509,10 @@ __global__ void __launch_bounds__(kStepThreads, 1) stack_step(const __grid_const
             bar_consumers();
             if (kTrace) tr2 = globaltimer();
 
+            // K = 2048 W4A8 linears: the lane's activation blocks are the same in every tile
+            const bool reg_act = !a16 && K2 == kChunkBytes;
+            Dp4aAct A;
+            if (reg_act) A = dp4a_act_load((uint32_t)K2, L, lane);
             for (int tile = t0; tile < t1; ++tile, ++ts) {
                 float acc[4] = {0.f, 0.f, 0.f, 0.f};
                 for (int ch = 0; ch < nchunks; ++ch) {
@@ -526,6 +530,8 @@ __global__ void __launch_bounds__(kStepThreads, 1) stack_step(const __grid_const
                         // debug: drain only
                     } else if (a16) {
                         chunk_mma<HMMA1>(st, nblk, blk0, (uint32_t)K2, L, G, 1, warp, lane, kNib2, kMagic, acc);
+                    } else if (reg_act) {
+                        chunk_dp4a_reg(st, A, warp, lane, acc[0]);
                     } else {
                         chunk_dp4a(st, nblk, blk0, (uint32_t)K2, L, warp, lane, acc[0]);
                     }
