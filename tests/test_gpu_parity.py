@@ -532,3 +532,28 @@ def test_step_kernel_k14336_chain(mq, orc):
         else:
             _, y64 = orc.w4a16(nib, sc, _f32(x))
         _assert_close(y, y64, 2e-3)
+
+
+def test_stack_step_host_chained(mq):
+    """mcapq_stack_step_host on a chained stack: only the step input crosses H2D (one copy),
+    every output comes back (one copy when the outputs share an arena), and the host copy of
+    the outputs equals the device outputs of a plain run."""
+    routes = (0, 1, 0, 1)
+    st, ops = _step_stack(mq, "dataflow", routes=routes)
+    bi, bo = st.host_bytes(1)
+    k0 = STEP_DIMS["q"][1]
+    assert bi == 2 * k0                          # layer 0's q/k/v input only
+    assert bo == 2 * sum(n for n, _ in STEP_DIMS.values()) * len(routes)
+    x0 = ops[0][3]
+    xh = x0.cpu().view(torch.uint8).flatten().clone().pin_memory()
+    yh = torch.empty(bo, dtype=torch.uint8).pin_memory()
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        st.capture(1, stream=s)
+        st.step_host(xh, yh, 1, stream=s)
+    s.synchronize()
+    off = 0
+    for (_, _, _, _, y) in ops:
+        nb = y.numel() * 2
+        assert torch.equal(yh[off:off + nb].view(torch.bfloat16).view(y.shape), y.cpu())
+        off += nb
