@@ -24,8 +24,10 @@ constexpr int kGemmKS = 256;                 // K per slice (stage)
 constexpr int kGemmMaxStages = 8;
 
 struct GemmArgs {
-    const CUtensorMap *maps;    // {nib box {128 B, bn}, scale box {8, bn}}
-    const CUtensorMap *amaps;   // activations: W4A8 {q, sx, sq}, W4A16 {x} (gemm_act_descriptors)
+    // activation maps as kernel parameters (encoded per launch; nothing cached per buffer):
+    // W4A8 {q, sx, sq}, W4A16 {x} (encode_gemm_act_maps)
+    alignas(64) CUtensorMap amaps[3];
+    const CUtensorMap *maps;    // weights {nib box {128 B, bn}, scale box {8, bn}} (device table)
     void *y;
     int64_t ldy;
     int64_t n, k;

@@ -450,8 +450,7 @@ cudaError_t launch_one(StreamArgs &a, cudaStream_t s, bool pdl, int sms)
 // reused, so a kernel in flight or a captured graph always sees its own.
 //   kind 0        : stream maps {nib, scale} of a packed weight (16-row x 2048-K stages)
 //   kind BN > 0   : gemm maps {nib, scale} (BN rows x 256 K)
-//   kind -1 - mp  : gemm W4A8 activation maps {q, sx, sq} of the quant_a8 workspace, mp-row boxes
-//   kind -100 - mp: gemm W4A16 activation map {x}, mp-row boxes
+// (activation maps are not cached: they travel as kernel parameters, see GemmArgs)
 namespace {
 struct DescKey {
     const void *p0, *p1;
@@ -553,46 +552,39 @@ const CUtensorMap *descriptors_of_kind(const uint8_t *nib, const uint16_t *scale
 //   W4A8  q  [m][k] int8 as 3-D {128 B, m, k/128}, box {128, mp, 2} (= one 256-K slice),
 //         128B swizzle -> smem [2][mp][128 B];  sx / sq [m][k/32] 2-D, box {8, mp} -> [mp][8]
 //   W4A16 x  [m][ldx] bf16 as 3-D {64, m, k/64}, box {64, mp, 4}, 128B swizzle -> [4][mp][128 B]
-const CUtensorMap *gemm_act_descriptors(bool a8, const void *x_or_q, const float *sx, const int32_t *sq, int64_t m,
-                                        int64_t k, int64_t ldx, int mp, cudaStream_t s)
+bool encode_gemm_act_maps(CUtensorMap *h, bool a8, const void *x_or_q, const float *sx, const int32_t *sq, int64_t m,
+                          int64_t k, int64_t ldx, int mp)
 {
-    const DescKey key{x_or_q, a8 ? (const void *)sx : nullptr, m, k, a8 ? (int64_t)(uintptr_t)sq : ldx,
-                      a8 ? -1 - mp : -100 - mp};
-    return desc_group(
-        key,
-        [&](CUtensorMap *h) {
-            EncodeTiledFn fn = encode_fn();
-            if (!fn) return false;
-            if (a8) {
-                const cuuint64_t qd[3] = {128, (cuuint64_t)m, (cuuint64_t)(k / 128)};
-                const cuuint64_t qs[2] = {(cuuint64_t)k, 128};
-                const cuuint32_t qb[3] = {128, (cuuint32_t)mp, 2};
-                const cuuint32_t e3[3] = {1, 1, 1};
-                if (fn(&h[0], CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<void *>(x_or_q), qd, qs, qb, e3,
-                       CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
-                    return false;
-                const cuuint64_t sd[2] = {(cuuint64_t)(k / 32), (cuuint64_t)m};
-                const cuuint64_t ss[1] = {(cuuint64_t)(k / 32) * 4};
-                const cuuint32_t sb[2] = {8, (cuuint32_t)mp};
-                const cuuint32_t e2[2] = {1, 1};
-                if (fn(&h[1], CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float *>(sx), sd, ss, sb, e2,
-                       CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
-                    return false;
-                return fn(&h[2], CU_TENSOR_MAP_DATA_TYPE_INT32, 2, const_cast<int32_t *>(sq), sd, ss, sb, e2,
-                          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                          CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
-            }
-            const cuuint64_t xd[3] = {64, (cuuint64_t)m, (cuuint64_t)(k / 64)};
-            const cuuint64_t xs[2] = {(cuuint64_t)ldx * 2, 128};
-            const cuuint32_t xb[3] = {64, (cuuint32_t)mp, 4};
-            const cuuint32_t e3[3] = {1, 1, 1};
-            return fn(&h[0], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void *>(x_or_q), xd, xs, xb, e3,
-                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
-        },
-        s);
+    EncodeTiledFn fn = encode_fn();
+    if (!fn) return false;
+    if (a8) {
+        const cuuint64_t qd[3] = {128, (cuuint64_t)m, (cuuint64_t)(k / 128)};
+        const cuuint64_t qs[2] = {(cuuint64_t)k, 128};
+        const cuuint32_t qb[3] = {128, (cuuint32_t)mp, 2};
+        const cuuint32_t e3[3] = {1, 1, 1};
+        if (fn(&h[0], CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<void *>(x_or_q), qd, qs, qb, e3,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+            return false;
+        const cuuint64_t sd[2] = {(cuuint64_t)(k / 32), (cuuint64_t)m};
+        const cuuint64_t ss[1] = {(cuuint64_t)(k / 32) * 4};
+        const cuuint32_t sb[2] = {8, (cuuint32_t)mp};
+        const cuuint32_t e2[2] = {1, 1};
+        if (fn(&h[1], CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float *>(sx), sd, ss, sb, e2,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+            return false;
+        return fn(&h[2], CU_TENSOR_MAP_DATA_TYPE_INT32, 2, const_cast<int32_t *>(sq), sd, ss, sb, e2,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+    }
+    const cuuint64_t xd[3] = {64, (cuuint64_t)m, (cuuint64_t)(k / 64)};
+    const cuuint64_t xs[2] = {(cuuint64_t)ldx * 2, 128};
+    const cuuint32_t xb[3] = {64, (cuuint32_t)mp, 4};
+    const cuuint32_t e3[3] = {1, 1, 1};
+    return fn(&h[0], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void *>(x_or_q), xd, xs, xb, e3,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 const CUtensorMap *stream_descriptors(const uint8_t *nib, const uint16_t *scale, int64_t n, int64_t k,
@@ -664,8 +656,8 @@ cudaError_t launch_gemm(int route, const uint8_t *nib, const uint16_t *scale, in
         GemmArgs a;
         memset(&a, 0, sizeof(a));
         a.maps = descriptors_of_kind(nib, scale, n, k, bn, s);
-        a.amaps = gemm_act_descriptors(a8, a8 ? (const void *)q : (const void *)x, sx, sq, m, k, ldx, mp, s);
-        if (!a.maps || !a.amaps) return cudaErrorInvalidValue;
+        if (!a.maps || !encode_gemm_act_maps(a.amaps, a8, a8 ? (const void *)q : (const void *)x, sx, sq, m, k, ldx, mp))
+            return cudaErrorInvalidValue;
         a.y = y;
         a.ldy = ldy;
         a.n = n;
