@@ -510,7 +510,7 @@ __global__ void __launch_bounds__(kStepThreads, 1) stack_step(const __grid_const
             if (kTrace) tr2 = globaltimer();
 
             // K = 2048 W4A8 linears: the lane's activation blocks are the same in every tile
-            const bool reg_act = !a16 && K2 == kChunkBytes;
+            const bool reg_act = kRounds == 2 && !a16 && K2 == kChunkBytes;   // registers: 2-round variant only
             Dp4aAct A;
             if (reg_act) A = dp4a_act_load((uint32_t)K2, L, lane);
             for (int tile = t0; tile < t1; ++tile, ++ts) {
