@@ -264,11 +264,11 @@ __device__ __forceinline__ int quant_code(float v, float s, float inv)
     const float qa = v * inv;
     const float aq = fabsf(qa);
     const float fr = aq - truncf(aq);
-    float r = roundf(qa);
-    // near a half-integer, or inv not finite (s subnormal): the IEEE division decides
-    if (fabsf(fr - 0.5f) <= 1e-4f || !(aq <= 128.0f)) r = roundf(__fdiv_rn(v, s));
-    r = fminf(fmaxf(r, -127.0f), 127.0f);
-    return (int)r;
+    // off the half-integers rint (RNE) == round-half-away; the integer is read from the
+    // bits of qa + 1.5 * 2^23 (no F2I on the quarter-rate conversion pipe)
+    int code = __float_as_int(qa + 12582912.0f) - 0x4B400000;
+    if (fabsf(fr - 0.5f) <= 1e-4f || !(aq <= 128.0f)) code = (int)roundf(__fdiv_rn(v, s));
+    return code < -127 ? -127 : (code > 127 ? 127 : code);
 }
 
 // D = A.B + C with an explicit accumulator init (C may repeat registers).
