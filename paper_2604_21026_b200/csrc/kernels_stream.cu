@@ -358,7 +358,7 @@ struct Tune {
     // step_smem_kb 120: a ~5-stage ring keeps the HBM pipe busy while bounding the
     // per-SM queue of in-flight weight data that the chain's L2 accesses wait behind
     int smem_kb = 112, max_stages = 12, nocompute = 0, pdl = 0, trace = 0, step_smem_kb = 200, step = 1,
-        step_flags = 0, step_spin_ns = 16, step_polls = 5, ctas_per_sm = 0;
+        step_flags = 0, step_spin_ns = 16, step_polls = 5, ctas_per_sm = 0, step_ep_log2 = 1;
 };
 const Tune &tune()
 {
@@ -375,6 +375,9 @@ const Tune &tune()
         if (const char *e = getenv("MCAPQ_STEP_SPIN_NS")) v.step_spin_ns = atoi(e);
         if (const char *e = getenv("MCAPQ_STEP_POLLS")) v.step_polls = atoi(e);
         if (const char *e = getenv("MCAPQ_STREAM_CTAS_PER_SM")) v.ctas_per_sm = atoi(e);
+        if (const char *e = getenv("MCAPQ_STEP_EP_LOG2")) v.step_ep_log2 = atoi(e);
+        if (v.step_ep_log2 < 1) v.step_ep_log2 = 1;
+        if (v.step_ep_log2 > 3) v.step_ep_log2 = 3;
         if (v.ctas_per_sm < 0 || v.ctas_per_sm > 2) v.ctas_per_sm = 0;
         if (v.step_smem_kb < 60) v.step_smem_kb = 60;
         if (v.step_smem_kb > 226) v.step_smem_kb = 226;
@@ -745,6 +748,7 @@ bool stack_fill_op(void *host_op, int route, const StreamGroup &g, const uint16_
         tiles += (int)((g.n[i] + kTileRows - 1) / kTileRows);
     }
     op.tile_start[g.count] = tiles;
+    if (tiles > (1 << 20)) return false;   // the kernel's 32-bit tile partition (T * grid < 2^32)
     op.count = g.count;
     op.route = route;
     op.ydt = ydt;
@@ -783,6 +787,7 @@ cudaError_t launch_stack_step(const void *ops_dev, int nops, unsigned int *count
     a.flags = tune().step_flags;
     a.spin_ns = tune().step_spin_ns;
     a.polls = tune().step_polls;
+    a.ep_log2 = tune().step_ep_log2;
     // one CTA per SM: activations for the largest K under either route, the rest is ring
     const size_t act = round_up(act_bytes(HMMA1, max_k, 1) > act_bytes(DP4A, max_k, 1) ? act_bytes(HMMA1, max_k, 1)
                                                                                            : act_bytes(DP4A, max_k, 1),

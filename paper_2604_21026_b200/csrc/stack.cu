@@ -277,9 +277,12 @@ static mcapq_status build_program(mcapq_stack *st)
         if (src_op[i] >= 0) {
             deps[i].xt = st->tags + tag_off[src_op[i]][src_m[i]];
             deps[i].xt_op = src_op[i];
-            deps[src_op[i]].publish = 1;   // the consumer's slow path waits on its counter
+            // the consumer's slow path waits on its counter only as a hint (the tags
+            // decide): a relaxed add, no release fence on the epilogue warp's path
+            if (deps[src_op[i]].publish < 1) deps[src_op[i]].publish = 1;
         }
-        if (deps[i].wait_op >= 0) deps[deps[i].wait_op].publish = 1;
+        // a barrier dependency orders memory through the counter: release
+        if (deps[i].wait_op >= 0) deps[deps[i].wait_op].publish = 2;
     }
 
     const size_t ob = stack_op_bytes();

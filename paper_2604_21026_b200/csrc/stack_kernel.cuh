@@ -41,7 +41,7 @@ struct StackOp {
     const uint32_t *xt;   // dataflow source: tagged y of the producing linear (then x is not read)
     int xt_op;            // the producing linear (its counter is the slow-path wait), or -1
     int wait_op;          // barrier dependency: linear index, or -1
-    int publish;          // a later linear waits on this one's counter
+    int publish;          // a later linear waits on this one's counter: 2 release (barrier), 1 relaxed (hint)
     int pad_[3];
 };
 static_assert(sizeof(StackOp) % 16 == 0, "StackOp is copied to shared memory in 16-byte pieces");
@@ -56,8 +56,10 @@ struct StackArgs {
     unsigned long long *trace;   // debug: [nops][grid][8] or null
     int flags;                   // debug (MCAPQ_STEP_FLAGS): 1 no compute, 2 no barrier polls, 4 no staging,
                                  // 8 no waits at all (barriers skipped, tags not checked),
+                                 // 16 no publishing (only with 8), 32 no epilogue stores
     int spin_ns;                 // first back-off between re-reads of stale tagged words (doubles, <= 1 us)
     int polls;                   // CTA-wide re-read rounds before waiting on the producer's counter
+    int ep_log2;                 // log2 of the tile slots between the consumers and the epilogue warp (1..3)
 };
 
 __device__ __forceinline__ unsigned int ld_acquire_gpu(const unsigned int *p)
@@ -149,7 +151,7 @@ __device__ __forceinline__ void stage_step_a8_oct(const StackOp &op, const ActSm
                 bar_consumers();
                 if (!ok) {
                     ra = ld_relaxed_128(op.xt + e0);
-                    while (!tags_ok(ra, t16)) {   // the producer published: current now
+                    while (!tags_ok(ra, t16)) {   // the producer published (a hint): re-read until current
                         __nanosleep(spin_ns);
                         ra = ld_relaxed_128(op.xt + e0);
                     }
@@ -320,10 +322,12 @@ __global__ void __launch_bounds__(kStepThreads, 1) stack_step(const __grid_const
     const uint32_t full = sb + (uint32_t)S * kStageBytes;
     const uint32_t empty = full + 8u * S;
     const uint32_t go = empty + 8u * S;   // phase j: the j-th barrier-waiting linear may start
-    const uint32_t epf = go + 8u;         // [2] tile slot written by every consumer warp
-    const uint32_t epe = go + 24u;        // [2] tile slot stored out by the epilogue warp
+    const int EL = a.ep_log2;
+    const uint32_t EN = 1u << EL;         // tile slots (<= 8)
+    const uint32_t epf = go + 8u;         // [EN] tile slot written by every consumer warp
+    const uint32_t epe = go + 72u;        // [EN] tile slot stored out by the epilogue warp
     const uint32_t act = sb + a.act_off;
-    const uint32_t red = sb + a.red_off;  // [2] tile slots: [16 warps][16 rows] fp32
+    const uint32_t red = sb + a.red_off;  // [EN] tile slots: [16 warps][16 rows] fp32
     // this launch's tag (epoch + 1, never 0): the epoch only changes after every CTA left
     const uint32_t epoch = *reinterpret_cast<volatile unsigned int *>(a.counters + a.nops + 1);
     const uint32_t t16 = ((epoch % 65535u) + 1u) << 16;
@@ -334,7 +338,7 @@ __global__ void __launch_bounds__(kStepThreads, 1) stack_step(const __grid_const
             mbar_init(empty + 8u * s, kConsumerWarps);
         }
         mbar_init(go, 1);
-        for (int j = 0; j < 2; ++j) {
+        for (int j = 0; j < (int)EN; ++j) {
             mbar_init(epf + 8u * j, kConsumerWarps);
             mbar_init(epe + 8u * j, 1);
         }
@@ -353,8 +357,9 @@ __global__ void __launch_bounds__(kStepThreads, 1) stack_step(const __grid_const
 
     auto cta_tiles = [&](const StackOp &op, int &t0, int &t1) {
         const int T = op.tile_start[op.count];
-        t0 = (int)(((int64_t)T * blockIdx.x) / gridDim.x);
-        t1 = (int)(((int64_t)T * (blockIdx.x + 1)) / gridDim.x);
+        // 32-bit: T * gridDim < 2^32 (T <= 2^20 tiles, checked by the program builder)
+        t0 = (int)(((uint32_t)T * blockIdx.x) / gridDim.x);
+        t1 = (int)(((uint32_t)T * (blockIdx.x + 1)) / gridDim.x);
     };
 
     if (warp == kConsumerWarps + 1) {
@@ -386,26 +391,44 @@ __global__ void __launch_bounds__(kStepThreads, 1) stack_step(const __grid_const
             int li = 0;
             for (int tile = t0; tile < t1; ++tile, ++ts) {
                 while (li + 1 < op.count && tile >= op.tile_start[li + 1]) ++li;
-                const uint32_t slot = ts & 1u;
-                mbar_wait(epf + 8u * slot, (ts >> 1) & 1u);
+                const uint32_t slot = ts & (EN - 1u);
+                mbar_wait(epf + 8u * slot, (ts >> EL) & 1u);
                 const uint32_t sl = red + 1024u * slot;
                 if (lane < kTileRows) {
                     float v;
-                    if (a16) {
-                        v = __uint_as_float(lds32(sl + 4u * lane));
+                    float x[kConsumerWarps];
 #pragma unroll
-                        for (int w = 1; w < kConsumerWarps; ++w) v += __uint_as_float(lds32(sl + 64u * w + 4u * lane));
+                    for (int w = 0; w < kConsumerWarps; ++w) x[w] = __uint_as_float(lds32(sl + 64u * w + 4u * lane));
+                    if (a16) {
+                        // HMMA1 partials: the stream kernel's linear order over the warps
+                        v = x[0];
+#pragma unroll
+                        for (int w = 1; w < kConsumerWarps; ++w) v += x[w];
                     } else {
-                        v = __uint_as_float(lds32(sl + 4u * lane));
+                        // row-lane DP4A: warp w holds level 1 of stream_linear's butterfly
+                        // (lanes w, w + 16); levels 2..5 pair w with w + 8, + 4, + 2, + 1
+#pragma unroll
+                        for (int h = kConsumerWarps / 2; h > 0; h >>= 1)
+#pragma unroll
+                            for (int w = 0; w < h; ++w) x[w] += x[w + h];
+                        v = x[0];
                     }
                     const int64_t row = (int64_t)(tile - op.tile_start[li]) * kTileRows + lane;
-                    if (row < op.n[li]) store_step(op, li, row, v, t16);
+                    if (row < op.n[li] && !(a.flags & 32)) store_step(op, li, row, v, t16);
                 }
                 __syncwarp();
                 if (lane == 0) mbar_arrive(epe + 8u * slot);
             }
-            if (op.publish && lane == 0)
-                asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(a.counters + i) : "memory");
+            // publish: 2 = release (a barrier dependency reads through this counter),
+            // 1 = relaxed (dataflow consumers only take it as a hint to re-read their tags;
+            // a release here would hold this warp in a GPU-scope fence behind the SM's
+            // in-flight weight traffic, 0.2 us per linear)
+            if (op.publish && lane == 0 && !(a.flags & 16)) {
+                if (op.publish == 2)
+                    asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(a.counters + i) : "memory");
+                else
+                    asm volatile("red.relaxed.gpu.global.add.u32 [%0], 1;" ::"l"(a.counters + i) : "memory");
+            }
         }
         if (lane == 0) {
             unsigned int prev;
@@ -509,58 +532,106 @@ __global__ void __launch_bounds__(kStepThreads, 1) stack_step(const __grid_const
             bar_consumers();
             if (kTrace) tr2 = globaltimer();
 
-            // K = 2048 W4A8 linears: the lane's activation blocks are the same in every tile
-            const bool reg_act = kRounds == 2 && !a16 && K2 == kChunkBytes;   // registers: 2-round variant only
-            Dp4aAct A;
-            if (reg_act) A = dp4a_act_load((uint32_t)K2, L, lane);
-            for (int tile = t0; tile < t1; ++tile, ++ts) {
-                float acc[4] = {0.f, 0.f, 0.f, 0.f};
-                for (int ch = 0; ch < nchunks; ++ch) {
-                    const int rem = K2 - ch * kChunkBytes;
-                    const int nblk = (rem < kChunkBytes ? rem : kChunkBytes) / 16;
-                    const int blk0 = ch * kChunkBlocks;
-                    if (kTrace) {
-                        ++nstages;
-                        if (!mbar_test(full + 8u * s, ph)) ++stalls;   // stage not resident yet
+            if (!a16) {
+                // ---- W4A8, row-lane DP4A: lane -> row r = lane & 15 of the tile, and
+                // lambda = warp + 16 (lane >> 4) -> blocks lambda and lambda + 32 of every
+                // chunk.  The (warp, half) slots are exactly the 32 lanes of stream_linear's
+                // warp-per-row engine (lane lambda holds blocks lambda, lambda + 32, same
+                // fmaf order over chunks); one shuffle (xor 16) makes that engine's first
+                // butterfly level and the epilogue warp finishes its tree over the 16
+                // warps -- bit-identical outputs, one shuffle per tile instead of five.
+                const int r = lane & 15, lam = warp + 16 * (lane >> 4);
+                const uint32_t o0 = nib_off(r, lam), o1 = nib_off(r, lam + 32);
+                const uint32_t os0 = scale_off(r, lam), os1 = scale_off(r, lam + 32);
+                // K = 2048 (one chunk): the lane's two activation blocks are the same in
+                // every tile: registers (2-round variant only: the 96-register cap)
+                const bool reg_act = kRounds == 2 && K2 == kChunkBytes;
+                Dp4aAct A;
+                if (reg_act) A = dp4a_act_load_pair(L, lam, lam + 32, (uint32_t)K2);
+                for (int tile = t0; tile < t1; ++tile, ++ts) {
+                    float acc = 0.f;
+                    for (int ch = 0; ch < nchunks; ++ch) {
+                        const int rem = K2 - ch * kChunkBytes;
+                        const int nblk = (rem < kChunkBytes ? rem : kChunkBytes) / 16;
+                        const int blk0 = ch * kChunkBlocks;
+                        if (kTrace) {
+                            ++nstages;
+                            if (!mbar_test(full + 8u * s, ph)) ++stalls;   // stage not resident yet
+                        }
+                        mbar_wait(full + 8u * s, ph);
+                        if (kTrace && tile == t0 && ch == 0) tr3 = globaltimer();
+                        const uint32_t st = ring + (uint32_t)s * kStageBytes;
+                        const bool on0 = lam < nblk, on1 = lam + 32 < nblk;
+                        uint4 w0 = make_uint4(0, 0, 0, 0), w1 = w0;
+                        uint32_t h0 = 0, h1 = 0;
+                        if (on0) {
+                            w0 = lds128(st + o0);
+                            h0 = lds16(st + os0);
+                        }
+                        if (on1) {
+                            w1 = lds128(st + o1);
+                            h1 = lds16(st + os1);
+                        }
+                        if (!reg_act) A = dp4a_act_load_pair(L, blk0 + lam, blk0 + lam + 32, (uint32_t)K2);
+                        const Dp4aAct &X = A;
+                        __syncwarp();
+                        if (lane == 0) mbar_arrive(empty + 8u * s);   // release: the stage's reads are done
+                        if (++s == S) {
+                            s = 0;
+                            ph ^= 1u;
+                        }
+                        if (!(a.flags & 1)) {
+                            if (on0) acc = fmaf(h2f((uint16_t)h0) * __uint_as_float(X.p0.x),
+                                                (float)block_D(w0, X.qa0, X.qb0, (int)X.p0.y), acc);
+                            if (on1) acc = fmaf(h2f((uint16_t)h1) * __uint_as_float(X.p1.x),
+                                                (float)block_D(w1, X.qa1, X.qb1, (int)X.p1.y), acc);
+                        }
                     }
-                    mbar_wait(full + 8u * s, ph);
-                    if (kTrace && tile == t0 && ch == 0) tr3 = globaltimer();
-                    const uint32_t st = ring + (uint32_t)s * kStageBytes;
-                    if (a.flags & 1) {
-                        // debug: drain only
-                    } else if (a16) {
-                        chunk_mma<HMMA1>(st, nblk, blk0, (uint32_t)K2, L, G, 1, warp, lane, kNib2, kMagic, acc);
-                    } else if (reg_act) {
-                        chunk_dp4a_reg(st, A, warp, lane, acc[0]);
-                    } else {
-                        chunk_dp4a(st, nblk, blk0, (uint32_t)K2, L, warp, lane, acc[0]);
-                    }
+                    if (kTrace) tr4 = globaltimer();
+                    acc += __shfl_xor_sync(0xffffffffu, acc, 16);
+                    const uint32_t slot = ts & (EN - 1u);
+                    if (ts >= EN) mbar_wait(epe + 8u * slot, ((ts >> EL) - 1u) & 1u);
+                    if (lane < 16) sts32(red + 1024u * slot + 64u * warp + 4u * lane, __float_as_uint(acc));
                     __syncwarp();
-                    if (lane == 0) mbar_arrive(empty + 8u * s);
-                    if (++s == S) {
-                        s = 0;
-                        ph ^= 1u;
-                    }
+                    if (lane == 0) mbar_arrive(epf + 8u * slot);
                 }
-                if (kTrace) tr4 = globaltimer();
-                // ---- hand the tile's partials to the epilogue warp (slot by tile parity)
-                const uint32_t slot = ts & 1u;
-                if (ts >= 2) mbar_wait(epe + 8u * slot, ((ts >> 1) - 1u) & 1u);
-                const uint32_t sl = red + 1024u * slot;
-                if (a16) {
+            } else {
+                // ---- W4A16, HMMA1 engine (warp w owns blocks 4w..4w+3 for all 16 rows)
+                for (int tile = t0; tile < t1; ++tile, ++ts) {
+                    float acc[4] = {0.f, 0.f, 0.f, 0.f};
+                    for (int ch = 0; ch < nchunks; ++ch) {
+                        const int rem = K2 - ch * kChunkBytes;
+                        const int nblk = (rem < kChunkBytes ? rem : kChunkBytes) / 16;
+                        const int blk0 = ch * kChunkBlocks;
+                        if (kTrace) {
+                            ++nstages;
+                            if (!mbar_test(full + 8u * s, ph)) ++stalls;   // stage not resident yet
+                        }
+                        mbar_wait(full + 8u * s, ph);
+                        if (kTrace && tile == t0 && ch == 0) tr3 = globaltimer();
+                        const uint32_t st = ring + (uint32_t)s * kStageBytes;
+                        if (!(a.flags & 1))
+                            chunk_mma<HMMA1>(st, nblk, blk0, (uint32_t)K2, L, G, 1, warp, lane, kNib2, kMagic, acc);
+                        __syncwarp();
+                        if (lane == 0) mbar_arrive(empty + 8u * s);
+                        if (++s == S) {
+                            s = 0;
+                            ph ^= 1u;
+                        }
+                    }
+                    if (kTrace) tr4 = globaltimer();
+                    // ---- hand the tile's partials to the epilogue warp (slot ts mod EN)
+                    const uint32_t slot = ts & (EN - 1u);
+                    if (ts >= EN) mbar_wait(epe + 8u * slot, ((ts >> EL) - 1u) & 1u);
+                    const uint32_t sl = red + 1024u * slot;
                     // HMMA1: lanes t == 0 hold rows gid (acc[0]) and gid + 8 (acc[2]) of token 0
                     if ((lane & 3) == 0) {
                         sts32(sl + 64u * warp + 4u * (lane >> 2), __float_as_uint(acc[0]));
                         sts32(sl + 64u * warp + 4u * ((lane >> 2) + 8), __float_as_uint(acc[2]));
                     }
-                } else {
-                    float v = acc[0];
-#pragma unroll
-                    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-                    if (lane == 0) sts32(sl + 4u * warp, __float_as_uint(v));
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(epf + 8u * slot);
                 }
-                __syncwarp();
-                if (lane == 0) mbar_arrive(epf + 8u * slot);
             }
         }
         if (kTrace && threadIdx.x == 0) {

@@ -279,39 +279,24 @@ __device__ __forceinline__ void chunk_dp4a(uint32_t st, int nblk, int blk0, uint
     }
 }
 
-// DP4A with the activations held in registers: when K fits one chunk (K <= 2048) lane l
-// meets the same blocks (l, l + 32) in every tile of the linear, so their q words and
-// {s, 8 sum q} pairs are loaded once per linear (dp4a_act_load) instead of once per stage
-// by each of the 16 row warps (16x redundant shared-memory reads).
+// One lane's activation operands for two Q4_0 blocks (q words, {s, 8 sum q} pairs).
 struct Dp4aAct {
     uint4 qa0, qb0, qa1, qb1;
     uint2 p0, p1;
 };
-__device__ __forceinline__ Dp4aAct dp4a_act_load(uint32_t K2, const ActSmem &L, int lane)
+// the two blocks (b0, b1) a lane of the step kernel's row-lane DP4A mapping meets in a
+// chunk: q words and the {s, 8 sum q} pairs
+__device__ __forceinline__ Dp4aAct dp4a_act_load_pair(const ActSmem &L, int b0, int b1, uint32_t K2)
 {
     Dp4aAct r;
-    const int g0 = lane, g1 = lane + 32;
-    r.qa0 = lds128(L.act + 16u * g0);
-    r.qb0 = lds128(L.act + K2 + 16u * g0);
-    r.qa1 = lds128(L.act + 16u * g1);
-    r.qb1 = lds128(L.act + K2 + 16u * g1);
-    r.p0 = lds64(L.ssq + 8u * g0);
-    r.p1 = lds64(L.ssq + 8u * g1);
+    r.qa0 = lds128(L.act + 16u * b0);
+    r.qb0 = lds128(L.act + K2 + 16u * b0);
+    r.qa1 = lds128(L.act + 16u * b1);
+    r.qb1 = lds128(L.act + K2 + 16u * b1);
+    r.p0 = lds64(L.ssq + 8u * b0);
+    r.p1 = lds64(L.ssq + 8u * b1);
     return r;
 }
-__device__ __forceinline__ void chunk_dp4a_reg(uint32_t st, const Dp4aAct &A, int warp, int lane, float &acc)
-{
-    const int r = warp;
-    const uint4 w0 = lds128(st + nib_off(r, lane));
-    const uint4 w1 = lds128(st + nib_off(r, lane + 32));
-    const float d0 = h2f(lds16(st + scale_off(r, lane)));
-    const float d1 = h2f(lds16(st + scale_off(r, lane + 32)));
-    const int D0 = block_D(w0, A.qa0, A.qb0, (int)A.p0.y);
-    const int D1 = block_D(w1, A.qa1, A.qb1, (int)A.p1.y);
-    acc = fmaf(d0 * __uint_as_float(A.p0.x), (float)D0, acc);
-    acc = fmaf(d1 * __uint_as_float(A.p1.x), (float)D1, acc);
-}
-
 // MMA engines: warp w owns blocks 4w..4w+3 of the chunk (contiguous, in that order)
 // for all 16 rows; ldmatrix.x4 hands lane (gid, t) word t of rows gid / gid+8 of two
 // blocks -- the m16n8k32.s8 / m16n8k16.bf16 A fragment of the split nibble layout.
