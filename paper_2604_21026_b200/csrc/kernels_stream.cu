@@ -255,9 +255,9 @@ __device__ __forceinline__ void magic_bf16(uint32_t w, uint32_t mask, uint32_t m
 }
 
 // Exact per-token activation code q = clamp(round_half_away(fl(v / s)), -127, 127)
-// from a per-group reciprocal: v * fl(1/s) is within 2.3e-5 of fl(v/s) for
-// |v/s| <= 127.01, so both round to the same integer unless v * inv lies within
-// 1e-4 of a half-integer; those rare cases take the IEEE division.  Bit-identical to
+// from a per-group reciprocal: with inv within 1 ulp of 1/s, v * inv is within
+// 3.1e-5 of fl(v/s) for |v/s| <= 127.01, so both round to the same integer unless
+// v * inv lies within 1e-4 of a half-integer; those rare cases take the IEEE division.  Bit-identical to
 // roundf(__fdiv_rn(v, s)) clamped (test_gpu_parity: quantiser bit-exact vs oracle).
 __device__ __forceinline__ int quant_code(float v, float s, float inv)
 {

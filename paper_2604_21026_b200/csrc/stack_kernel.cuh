@@ -56,7 +56,7 @@ struct StackArgs {
     unsigned long long *trace;   // debug: [nops][grid][8] or null
     int flags;                   // debug (MCAPQ_STEP_FLAGS): 1 no compute, 2 no barrier polls, 4 no staging,
                                  // 8 no waits at all (barriers skipped, tags not checked),
-                                 // 16 no publishing (only with 8), 32 no epilogue stores
+                                 // 16 no publishing (only with 8), 32 no epilogue stores, 128 no W4A8 quantiser (loads only)
     int spin_ns;                 // first back-off between re-reads of stale tagged words (doubles, <= 1 us)
     int polls;                   // CTA-wide re-read rounds before waiting on the producer's counter
     int ep_log2;                 // log2 of the tile slots between the consumers and the epilogue warp (1..3)
@@ -122,8 +122,9 @@ __device__ __forceinline__ bool bar_consumers_and(bool v)
 // data re-reads) and the stale words are re-read once.
 // W4A8 with K <= 2048: one group per 8 threads (all 512 consumer threads busy at
 // K = 2048, half the per-thread quantiser work of the quad layout).
-__device__ __forceinline__ void stage_step_a8_oct(const StackOp &op, const ActSmem &L, int tid, uint32_t t16,
-                                                  bool check, int spin_ns, int polls, const unsigned int *counters)
+__device__ __forceinline__ void stage_step_a8_oct(unsigned long long *tmid, const StackOp &op, const ActSmem &L, int tid, uint32_t t16,
+                                                  bool check, int spin_ns, int polls, const unsigned int *counters,
+                                                  bool quant)
 {
     const int G = (int)(op.k / 32);
     const uint32_t K2 = (uint32_t)(op.k / 2);
@@ -165,23 +166,20 @@ __device__ __forceinline__ void stage_step_a8_oct(const StackOp &op, const ActSm
             backoff = backoff < 1024 ? 2 * backoff : 1024;
         }
     }
+    if (tmid) *tmid = globaltimer();
     uint2 w2;
     if (tagged) w2 = untag(ra);
     else w2 = make_uint2(ra.x, ra.y);
-    float v[4];
-    v[0] = __uint_as_float(w2.x << 16);
-    v[1] = __uint_as_float(w2.x & 0xffff0000u);
-    v[2] = __uint_as_float(w2.y << 16);
-    v[3] = __uint_as_float(w2.y & 0xffff0000u);
-    a8_oct_store(v, on, g, sub8, K2, L);
+    if (quant) a8_oct_store(w2, on, g, sub8, K2, L);
 }
 
 template <int kRounds>
-__device__ __forceinline__ void stage_step(const StackOp &op, bool a16, const ActSmem &L, int tid, uint32_t t16,
-                                           bool check, int spin_ns, int polls, const unsigned int *counters)
+__device__ __forceinline__ void stage_step(unsigned long long *tmid, const StackOp &op, bool a16, const ActSmem &L, int tid, uint32_t t16,
+                                           bool check, int spin_ns, int polls, const unsigned int *counters,
+                                           bool quant)
 {
     if (!a16 && op.k <= 2048) {
-        stage_step_a8_oct(op, L, tid, t16, check, spin_ns, polls, counters);
+        stage_step_a8_oct(tmid, op, L, tid, t16, check, spin_ns, polls, counters, quant);
         return;
     }
     const int G = (int)(op.k / 32);
@@ -266,6 +264,7 @@ __device__ __forceinline__ void stage_step(const StackOp &op, bool a16, const Ac
     }
 #pragma unroll
     for (int r = 0; r < kRounds; ++r) {
+        if (r == 0 && tmid) *tmid = globaltimer();
         if (r * NT >= nq) break;   // CTA-uniform
         const int idx = r * NT + tid;
         const bool on = idx < nq;
@@ -291,9 +290,7 @@ __device__ __forceinline__ void stage_step(const StackOp &op, bool a16, const Ac
         if (a16) {
             a16_quad_store(make_uint2(w4[0], w4[1]), make_uint2(w4[2], w4[3]), on, 0, g, sub, L);
         } else {
-            float v[8];
-            bf16x8_to_f32(w4, v);
-            a8_quad_store(v, on, 0, g, sub, G, K2, L);
+            if (quant) a8_quad_store(w4, on, 0, g, sub, G, K2, L);
         }
     }
 }
@@ -515,7 +512,7 @@ __global__ void __launch_bounds__(kStepThreads, 1) stack_step(const __grid_const
         const int nchunks = (K2 + kChunkBytes - 1) / kChunkBytes;
         int t0, t1;
         cta_tiles(op, t0, t1);
-        unsigned long long tr0 = 0, tr1 = 0, tr2 = 0, tr3 = 0, tr4 = 0;
+        unsigned long long tr0 = 0, tr1 = 0, tr2 = 0, tr3 = 0, tr4 = 0, trm = 0;
         unsigned int stalls = 0, nstages = 0;
         if (kTrace) tr0 = globaltimer();
         if (t1 > t0) {
@@ -528,7 +525,8 @@ __global__ void __launch_bounds__(kStepThreads, 1) stack_step(const __grid_const
             const bool a16 = route == MCAPQ_W4A16;
             const ActSmem L = act_layout(a16, act, k, 1);
             bar_consumers();   // every warp is done reading the previous linear's activations
-            if (!(a.flags & 4)) stage_step<kRounds>(op, a16, L, threadIdx.x, t16, !(a.flags & 8), a.spin_ns, a.polls, a.counters);
+            if (!(a.flags & 4)) stage_step<kRounds>(kTrace ? &trm : nullptr, op, a16, L, threadIdx.x, t16, !(a.flags & 8), a.spin_ns, a.polls, a.counters,
+                                                         !(a.flags & 128));
             bar_consumers();
             if (kTrace) tr2 = globaltimer();
 
@@ -637,7 +635,9 @@ __global__ void __launch_bounds__(kStepThreads, 1) stack_step(const __grid_const
         if (kTrace && threadIdx.x == 0) {
             unsigned long long *r = a.trace + 8ull * ((unsigned long long)i * gridDim.x + blockIdx.x);
             r[0] = (unsigned long long)i;
-            r[1] = ((unsigned long long)blockIdx.x << 32) | ((unsigned long long)stalls << 16) | nstages;
+            // CTA | staging split (ns from the go point to loads checked, 16 bits) | stalls | stages
+            const unsigned long long mid = trm > tr1 ? (trm - tr1 < 65535ull ? trm - tr1 : 65535ull) : 0ull;
+            r[1] = ((unsigned long long)blockIdx.x << 48) | (mid << 32) | ((unsigned long long)stalls << 16) | nstages;
             r[2] = tr0;
             r[3] = tr1;
             r[4] = tr2;

@@ -92,31 +92,90 @@ __device__ __forceinline__ void bf16x8_to_f32(const uint32_t w4[4], float v[8])
     }
 }
 
-// Quantise group (i, g): quad member `sub` holds elements 8 sub .. 8 sub + 7 in v.
-// Stores its 8 codes and (sub 0) the group's {s, 8 sum q}.  All 32 lanes call it
-// (quad shuffles); `on` masks the stores of lanes past the end.
-__device__ __forceinline__ void a8_quad_store(const float v[8], bool on, int i, int g, int sub, int G, uint32_t K2,
-                                              const ActSmem &L)
+// s = fl(a / 127) (IEEE round-to-nearest) without the division: one
+// correction step from r = fl(1/127) (q0 = a r, e = a - 127 q0 exactly by FMA,
+// s = q0 + e r).  Exact for every finite bf16 magnitude a -- checked exhaustively
+// against rational arithmetic by tests/test_quant_identities.py.
+__device__ __forceinline__ float div127_rn(float a)
 {
-    float amax = 0.0f;
-    int fin = 1;
+    const float r = 0x1.020408p-7f;
+    const float q0 = __fmul_rn(a, r);
+    const float e = __fmaf_rn(-q0, 127.0f, a);
+    return __fmaf_rn(e, r, q0);
+}
+
+// 1/s for quant_code: MUFU.RCP (<= 1 ulp), inside quant_code's half-integer margin;
+// a subnormal s (amax < 127 * 2^-126) takes the IEEE reciprocal.
+__device__ __forceinline__ float rcp_group(float s)
+{
+    float r;
+    asm("rcp.approx.f32 %0, %1;" : "=f"(r) : "f"(s));
+    if (s < 1.17549435e-38f) r = __frcp_rn(s);
+    return r;
+}
+
+// max |x| over packed bf16 words as the bits of a bf16 magnitude (integer max of
+// the sign-cleared bits == fp max for finite values; >= 0x7f80 <=> some x is inf/NaN)
+__device__ __forceinline__ uint32_t absmax_bits(uint32_t acc, uint32_t w)
+{
+    return __vmaxu2(acc, w & 0x7fff7fffu);
+}
+__device__ __forceinline__ uint32_t absmax_fold(uint32_t m)
+{
+    return max(m & 0xffffu, m >> 16);
+}
+
+// Codes of N elements of one group, branch-free: q = rint(v * inv) read from the bits
+// of fl(v * inv) + 1.5 * 2^23.  Off the half-integers rint == round_half_away(fl(v / s))
+// (quant_code's margin argument); |fl(v / s)| <= 127.00003 for every element of a live
+// group (|v| <= amax, s = fl(amax / 127)), so no clamp is needed.  Returns false when
+// some element lies within 1e-4 of a half-integer or is not finite after the multiply
+// (inv = inf for a subnormal s): the caller then recomputes the whole group with
+// quant_code (IEEE division), so the codes are bit-identical to quant_a8_kernel.
+template <int N>
+__device__ __forceinline__ bool quant_codes_fast(const float *v, float inv, int *c)
+{
+    bool ok = true;
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
-        fin &= isfinite(v[j]) ? 1 : 0;
-        amax = fmaxf(amax, fabsf(v[j]));
+    for (int j = 0; j < N; ++j) {
+        const float qa = __fmul_rn(v[j], inv);
+        const float t = __fadd_rn(qa, 12582912.0f);
+        const float r = __fsub_rn(qa, __fsub_rn(t, 12582912.0f));
+        ok = ok && fabsf(r) < 0.4999f;
+        c[j] = __float_as_int(t) - 0x4B400000;
     }
-    amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, 1));
-    amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, 2));
-    fin &= __shfl_xor_sync(0xffffffffu, fin, 1);
-    fin &= __shfl_xor_sync(0xffffffffu, fin, 2);
-    const float s = __fdiv_rn(amax, 127.0f);
-    const bool live = fin && s != 0.0f;
-    const float inv = __frcp_rn(s);
+    return ok;
+}
+
+// Quantise group (i, g): quad member `sub` holds elements 8 sub .. 8 sub + 7 as the
+// packed bf16 words w4.  Stores its 8 codes and (sub 0) the group's {s, 8 sum q}.
+// All 32 lanes call it (quad shuffles); `on` masks the stores of lanes past the end.
+// q = clamp(round_half_away(fl(x / s)), -127, 127) with s = fl(amax / 127),
+// bit-identical to quant_a8_kernel.
+__device__ __forceinline__ void a8_quad_store(const uint32_t w4[4], bool on, int i, int g, int sub, int G,
+                                              uint32_t K2, const ActSmem &L)
+{
+    uint32_t m = 0;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) m = absmax_bits(m, w4[e]);
+    m = absmax_fold(m);
+    m = max(m, __shfl_xor_sync(0xffffffffu, m, 1));
+    m = max(m, __shfl_xor_sync(0xffffffffu, m, 2));
+    const float s = div127_rn(__uint_as_float(m << 16));
+    const bool live = m < 0x7f80u && s != 0.0f;
+    const float inv = rcp_group(s);
+    float v[8];
+    bf16x8_to_f32(w4, v);
+    int c[8];
+    if (!quant_codes_fast<8>(v, inv, c) && live) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) c[j] = quant_code(v[j], s, inv);
+    }
     uint32_t lo = 0, hi = 0;
     int sum = 0;
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
-        const int code = live ? quant_code(v[j], s, inv) : 0;
+        const int code = live ? c[j] : 0;
         sum += code;
         if (j < 4)
             lo |= ((uint32_t)code & 0xffu) << (8 * j);
@@ -137,30 +196,28 @@ __device__ __forceinline__ void a8_quad_store(const float v[8], bool on, int i, 
 }
 
 // Octet variant (one token): 8 threads per group, 4 elements each (elements 4 sub8 ..
-// 4 sub8 + 3); the same per-element arithmetic as a8_quad_store, so the codes, s and
-// sum q are bit-identical -- only the reduction tree spans 8 lanes instead of 4.
-__device__ __forceinline__ void a8_oct_store(const float v[4], bool on, int g, int sub8, uint32_t K2, const ActSmem &L)
+// 4 sub8 + 3, packed bf16 words w2); the same per-element arithmetic as a8_quad_store,
+// so the codes, s and sum q are bit-identical -- only the reduction tree spans 8 lanes.
+__device__ __forceinline__ void a8_oct_store(uint2 w2, bool on, int g, int sub8, uint32_t K2, const ActSmem &L)
 {
-    float amax = 0.0f;
-    int fin = 1;
+    uint32_t m = absmax_fold(absmax_bits(w2.x & 0x7fff7fffu, w2.y));
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-        fin &= isfinite(v[j]) ? 1 : 0;
-        amax = fmaxf(amax, fabsf(v[j]));
-    }
+    for (int o = 1; o < 8; o <<= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+    const float s = div127_rn(__uint_as_float(m << 16));
+    const bool live = m < 0x7f80u && s != 0.0f;
+    const float inv = rcp_group(s);
+    const float v[4] = {__uint_as_float(w2.x << 16), __uint_as_float(w2.x & 0xffff0000u),
+                        __uint_as_float(w2.y << 16), __uint_as_float(w2.y & 0xffff0000u)};
+    int c[4];
+    if (!quant_codes_fast<4>(v, inv, c) && live) {
 #pragma unroll
-    for (int o = 1; o < 8; o <<= 1) {
-        amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, o));
-        fin &= __shfl_xor_sync(0xffffffffu, fin, o);
+        for (int j = 0; j < 4; ++j) c[j] = quant_code(v[j], s, inv);
     }
-    const float s = __fdiv_rn(amax, 127.0f);
-    const bool live = fin && s != 0.0f;
-    const float inv = __frcp_rn(s);
     uint32_t w = 0;
     int sum = 0;
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
-        const int code = live ? quant_code(v[j], s, inv) : 0;
+        const int code = live ? c[j] : 0;
         sum += code;
         w |= ((uint32_t)code & 0xffu) << (8 * j);
     }
@@ -189,9 +246,7 @@ __device__ __forceinline__ void stage_a8(const uint16_t *xg, int64_t ldx, int nt
         const int i = grp / G, g = grp - i * G;
         const uint4 u = ldg_x128<kCoherent>(xg + i * ldx + 32 * g + 8 * sub);
         const uint32_t w4[4] = {u.x, u.y, u.z, u.w};
-        float v[8];
-        bf16x8_to_f32(w4, v);
-        a8_quad_store(v, on, i, g, sub, G, K2, L);
+        a8_quad_store(w4, on, i, g, sub, G, K2, L);
     }
 }
 

@@ -65,7 +65,7 @@ def main():
     rec = buf[:n].astype(np.int64)
     t0 = rec[rec[:, 2] > 0, 2].min()
     print(f"{'op':>3} {'ctas':>4} {'start':>8} {'go':>6} {'stage':>6} {'wfirst':>6} {'compute':>7} {'epi':>6} "
-          f"{'end_med':>8} {'end_max':>8} {'stages':>6} {'stalled':>7}")
+          f"{'end_med':>8} {'end_max':>8} {'stages':>6} {'stalled':>7} {'load':>6}")
     tot = np.zeros(5)
     for op in range(min(args.ops, int(rec[:, 0].max()) + 1)):
         r = rec[(rec[:, 0] == op) & (rec[:, 6] > 0)]
@@ -73,10 +73,11 @@ def main():
             continue
         d = np.median(np.stack([r[:, 3] - r[:, 2], r[:, 4] - r[:, 3], r[:, 6] - r[:, 4], r[:, 7] - r[:, 6],
                                 r[:, 5] - r[:, 7]], 1), 0) / 1000
+        load = np.median((r[:, 1] >> 32) & 0xFFFF) / 1000   # go -> input loaded and checked
         tot += d
         print(f"{op:3d} {len(r):4d} {(np.median(r[:, 2]) - t0) / 1000:8.2f} {d[0]:6.2f} {d[1]:6.2f} {d[2]:6.2f} "
               f"{d[3]:7.2f} {d[4]:6.2f} {(np.median(r[:, 5]) - t0) / 1000:8.2f} {(r[:, 5].max() - t0) / 1000:8.2f} "
-              f"{np.mean(r[:, 1] & 0xFFFF):6.2f} {np.mean((r[:, 1] >> 16) & 0xFFFF):7.2f}")
+              f"{np.mean(r[:, 1] & 0xFFFF):6.2f} {np.mean((r[:, 1] >> 16) & 0xFFFF):7.2f} {load:6.2f}")
     print("sum of medians (go, stage, wfirst, compute, epi):", np.round(tot, 2))
     print("total span us:", (rec[:, 5].max() - t0) / 1000)
 
