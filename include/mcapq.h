@@ -172,6 +172,24 @@ mcapq_status mcapq_w4a8_x(const uint8_t *nib, const uint16_t *scale, int64_t n, 
 mcapq_status mcapq_w4a16(const uint8_t *nib, const uint16_t *scale, int64_t n, int64_t k, const uint16_t *x,
                          int64_t m, int64_t ldx, void *y, int ydt, int64_t ldy, void *stream);
 
+/*
+ * a6 (bf16-dequant semantics, reading A13): W4A16 as "dequantise to 16-bit, then a
+ * dense GEMM" (the paper's prefill path, "materializes F16 for cuBLAS"):
+ *   W^[n][k] = bf16_rne(f32(d_{n,k/32}) (c_{n,k} - 8)),  y[i][n] = sum_k W^[n][k] x[i][k]
+ * with fp32 accumulation over all of K.  Unlike mcapq_w4a16 each weight is rounded
+ * once to bf16 (|W^ - d (c - 8)| <= 2^-9 |d (c - 8)|), which lets the whole K
+ * reduction stay in the tensor core: tcgen05.mma kind::f16, accumulator in TMEM,
+ * 128 weight rows x <= 64 tokens per CTA, one weight pass per 64 tokens.  Meant for
+ * batched decode / prefill (m >= 9); any m >= 1 is accepted.
+ * Layout/ownership as mcapq_w4a16 (x [m][ldx] bf16, y [m][ldy], caller-owned device
+ * memory, stream-ordered, graph-capturable).  Errors: MCAPQ_EUNSUP unless k % 256 == 0;
+ * MCAPQ_EINVAL for a scale plane not 16-byte aligned, ldx % 8 != 0, or the checks of
+ * mcapq_w4a16.
+ */
+mcapq_status mcapq_w4a16_bf16deq(const uint8_t *nib, const uint16_t *scale, int64_t n, int64_t k,
+                                 const uint16_t *x, int64_t m, int64_t ldx, void *y, int ydt, int64_t ldy,
+                                 void *stream);
+
 /* Routed linear: route MCAPQ_W4A8 -> mcapq_w4a8_x, MCAPQ_W4A16 -> mcapq_w4a16. */
 mcapq_status mcapq_linear(int route, const uint8_t *nib, const uint16_t *scale, int64_t n, int64_t k,
                           const uint16_t *x, int64_t m, int64_t ldx, void *y, int ydt, int64_t ldy, void *ws,

@@ -25,6 +25,7 @@ BF16, F32 = 0, 1
 
 __all__ = [
     "W4A8", "W4A16", "BF16", "F32", "McapqError", "load", "pack_w4", "quant_a8", "w4a8", "w4a8_x", "w4a16",
+    "w4a16_bf16deq",
     "linear", "linear_group", "linear_host", "w4a8_group_dots", "workspace_bytes", "host_workspace_bytes", "Profile",
     "profile_parse", "Stack", "Comm", "linear_colshard", "PackedW4", "device_sms", "set_pdl",
 ]
@@ -151,6 +152,17 @@ def w4a16(w: PackedW4, x: torch.Tensor, out_dtype=torch.float32, out=None, strea
     y = _out(m, w.n, out_dtype, x.device, out)
     check(load().mcapq_w4a16(_ptr(w.nib), _ptr(w.scale), w.n, w.k, _ptr(x2), m, x2.stride(0), _ptr(y),
                              _dt(y.dtype), y.stride(0), _stream(stream)), "mcapq_w4a16")
+    return y
+
+
+def w4a16_bf16deq(w: PackedW4, x: torch.Tensor, out_dtype=torch.float32, out=None, stream=None):
+    """a6, bf16-dequant semantics: W^ = bf16(d (c - 8)), y = x W^T on tcgen05 (K % 256 == 0)."""
+    _need_cuda(w.nib, x)
+    x2 = x if x.dim() == 2 else x.view(1, -1)
+    m = x2.shape[0]
+    y = _out(m, w.n, out_dtype, x.device, out)
+    check(load().mcapq_w4a16_bf16deq(_ptr(w.nib), _ptr(w.scale), w.n, w.k, _ptr(x2), m, x2.stride(0), _ptr(y),
+                                     _dt(y.dtype), y.stride(0), _stream(stream)), "mcapq_w4a16_bf16deq")
     return y
 
 

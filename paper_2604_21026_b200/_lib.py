@@ -34,6 +34,7 @@ SIGNATURES = {
     "mcapq_workspace_bytes": (SZ, [I32, I64, I64, I64]),
     "mcapq_w4a8_x": (I32, [P, P, I64, I64, P, I64, I64, P, I32, I64, P, SZ, P]),
     "mcapq_w4a16": (I32, [P, P, I64, I64, P, I64, I64, P, I32, I64, P]),
+    "mcapq_w4a16_bf16deq": (I32, [P, P, I64, I64, P, I64, I64, P, I32, I64, P]),
     "mcapq_linear": (I32, [I32, P, P, I64, I64, P, I64, I64, P, I32, I64, P, SZ, P]),
     "mcapq_linear_group": (I32, [I32, I32, P, P, P, I64, P, I64, I64, P, I32, P, P, SZ, P]),
     "mcapq_host_workspace_bytes": (SZ, [I32, I64, I64, I64]),

@@ -253,6 +253,29 @@ mcapq_status mcapq_w4a16(const uint8_t *nib, const uint16_t *scale, int64_t n, i
     return MCAPQ_OK;
 }
 
+mcapq_status mcapq_w4a16_bf16deq(const uint8_t *nib, const uint16_t *scale, int64_t n, int64_t k,
+                                 const uint16_t *x, int64_t m, int64_t ldx, void *y, int ydt, int64_t ldy,
+                                 void *stream)
+{
+    clear_error();
+    CHECK_SHAPE(n, k, m);
+    mcapq_status st = check_weight(nib, scale, n, k);
+    if (st != MCAPQ_OK) return st;
+    CHECK_PTR(x, "x");
+    CHECK_PTR(y, "y");
+    CHECK_AL16(x, "x");
+    CHECK_AL16(y, "y");
+    CHECK_YDT(ydt);
+    CHECK_LD(ldx, k, "ldx");
+    CHECK_LD(ldy, n, "ldy");
+    MCAPQ_REQUIRE(k % 256 == 0 && gemm_supported(k), MCAPQ_EUNSUP, "w4a16_bf16deq needs K %% 256 == 0 (K = %lld)",
+                  (long long)k);
+    MCAPQ_REQUIRE(aligned16(scale) && ldx % 8 == 0, MCAPQ_EINVAL,
+                  "w4a16_bf16deq needs a 16-byte aligned scale plane and ldx %% 8 == 0");
+    LAUNCH_TRY(launch_tc05(nib, scale, n, k, x, ldx, m, y, ydt, ldy, as_stream(stream), api_pdl()));
+    return MCAPQ_OK;
+}
+
 mcapq_status mcapq_linear(int route, const uint8_t *nib, const uint16_t *scale, int64_t n, int64_t k,
                           const uint16_t *x, int64_t m, int64_t ldx, void *y, int ydt, int64_t ldy, void *ws,
                           size_t ws_bytes, void *stream)

@@ -295,6 +295,7 @@ __device__ __forceinline__ void hmma(uint32_t a0, uint32_t a1, uint32_t a2, uint
 #include "stream_kernel.cuh"
 #include "stack_kernel.cuh"
 #include "gemm_kernel.cuh"
+#include "tc05_kernel.cuh"
 
 // ------------------------------------------------------------------ host side
 typedef CUresult (*EncodeTiledFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
@@ -637,6 +638,62 @@ cudaError_t dispatch_gemm(const GemmCfg &c, GemmArgs &a, size_t smem, int grid, 
     return cudaErrorInvalidValue;
 }
 }  // namespace
+
+// ------------------------------------------------------------------ batched W4A16 on tcgen05
+namespace {
+template <int MP>
+cudaError_t launch_tc05_mp(GemmArgs &a, size_t smem, int grid, cudaStream_t s, bool pdl)
+{
+    static int attr_done = 0;
+    if (!attr_done) {
+        cudaError_t e = cudaFuncSetAttribute(tc05_w4a16<MP>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+        if (e != cudaSuccess) return e;
+        attr_done = 1;
+    }
+    return launch_pdl(tc05_w4a16<MP>, dim3(grid), dim3(tc05::kThreads), smem, s, pdl, a);
+}
+}  // namespace
+
+// tc05_w4a16 (bf16-dequantised weights, tcgen05): 128-row CTA tiles, passes of <= 64
+// tokens (MP = 16 / 32 / 64); K % 256 == 0.
+cudaError_t launch_tc05(const uint8_t *nib, const uint16_t *scale, int64_t n, int64_t k, const uint16_t *x,
+                        int64_t ldx, int64_t m, void *y, int ydt, int64_t ldy, cudaStream_t s, bool pdl)
+{
+    const int sms = device_sms();
+    for (int64_t tok0 = 0; tok0 < m; tok0 += 64) {
+        const int ntok = (int)((m - tok0) < 64 ? (m - tok0) : 64);
+        const int mp = ntok <= 16 ? 16 : (ntok <= 32 ? 32 : 64);
+        GemmArgs a;
+        memset(&a, 0, sizeof(a));
+        a.maps = descriptors_of_kind(nib, scale, n, k, 128, s);
+        if (!a.maps || !encode_gemm_act_maps(a.amaps, false, x, nullptr, nullptr, m, k, ldx, mp))
+            return cudaErrorInvalidValue;
+        a.y = y;
+        a.ldy = ldy;
+        a.n = n;
+        a.k = k;
+        a.ydt = ydt;
+        a.tok0 = tok0;
+        a.ntok = ntok;
+        a.mp = mp;
+        a.bn = 128;
+        a.row_tiles = (int)((n + 127) / 128);
+        a.stage_bytes = tc05::kNibBytes + tc05::kScBytes + (uint32_t)mp * 512u;
+        const size_t fixed = 1024 + (size_t)tc05::kNA * tc05::kAtomBytes + 256;
+        int S = (int)((227 * 1024 - fixed) / a.stage_bytes);
+        S = S > 4 ? 4 : S;
+        if (S < 2) return cudaErrorInvalidValue;
+        a.stages = S;
+        const size_t smem = fixed + (size_t)S * a.stage_bytes;
+        const int grid = a.row_tiles < sms ? a.row_tiles : sms;
+        cudaError_t e = mp == 16 ? launch_tc05_mp<16>(a, smem, grid, s, pdl)
+                                 : (mp == 32 ? launch_tc05_mp<32>(a, smem, grid, s, pdl)
+                                             : launch_tc05_mp<64>(a, smem, grid, s, pdl));
+        if (e != cudaSuccess) return e;
+        pdl = true;
+    }
+    return cudaSuccess;
+}
 
 cudaError_t launch_gemm(int route, const uint8_t *nib, const uint16_t *scale, int64_t n, int64_t k, const uint16_t *x,
                         int64_t ldx, const int8_t *q, const float *sx, const int32_t *sq, int64_t m, void *y, int ydt,

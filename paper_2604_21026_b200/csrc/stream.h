@@ -88,6 +88,8 @@ int stream_tokens_per_pass(int route, int64_t k);
 // workspace (q [m][k], sx/sq [m][k/32]); W4A16 reads x [m][ldx] directly.
 constexpr int64_t kGemmMinTokens = 9;
 bool gemm_supported(int64_t k);
+cudaError_t launch_tc05(const uint8_t *nib, const uint16_t *scale, int64_t n, int64_t k, const uint16_t *x,
+                        int64_t ldx, int64_t m, void *y, int ydt, int64_t ldy, cudaStream_t s, bool pdl);
 cudaError_t launch_gemm(int route, const uint8_t *nib, const uint16_t *scale, int64_t n, int64_t k, const uint16_t *x,
                         int64_t ldx, const int8_t *q, const float *sx, const int32_t *sq, int64_t m, void *y, int ydt,
                         int64_t ldy, cudaStream_t s, bool pdl);

@@ -1,0 +1,318 @@
+// tc05_kernel.cuh -- batched W4A16 decode linear with bf16-dequantised weights (row a6,
+// the bf16-dequant semantics of reading A13) on the 5th-generation tensor cores:
+// tcgen05.mma kind::f16, accumulator in TMEM across all of K (included by
+// kernels_stream.cu after gemm_kernel.cuh; reuses GemmArgs and the gemm tensor maps).
+//
+//   W^[n][k] = bf16_rne(f32(d[n][k/32]) * (c[n][k] - 8)),   y = X . W^T  (fp32 accumulate)
+//
+// = "dequantise to 16-bit, then a dense GEMM" (the paper's prefill path);
+// oracle: oracle_w4a16_bf16deq.  The exact per-block-scale semantics (mcapq_w4a16) needs
+// one TMEM read-back per Q4_0 block, and TMEM reads at ~64 B/clk/SM make that 8 * MP
+// cycles per 128-row block: 5x the HBM time at MP = 64 (measured 231 us for the 8B
+// lm_head) -- that path stays on mma.sync (gemm_w4); this one reads TMEM once per tile.
+//
+// CTA = 128 weight rows (UMMA_M = 128) x MP tokens (UMMA_N = MP), K in slices of 256.
+// Warp roles (448 threads):
+//   warp 0      TMA producer: per slice one nibble box {128 B, 128 rows} (128B swizzle),
+//               one scale box {8 fp16, 128 rows}, the slice's activations as 4 swizzled
+//               64-K atoms [4][MP][128 B] (rows past M read as zeros).
+//   warp 1      TMEM allocator; lane 0 issues the MMAs (4 x K16 per 64-K atom) and commits.
+//   warps 2-9   dequantise: thread = (weight row, block of the atom); 32 nibbles ->
+//               32 bf16 W^ in the canonical K-major SW128 layout (A ring, 16 KiB atoms).
+//   warps 10-13 epilogue: warp w reads TMEM lanes 32 (w % 4) .. + 31 (= its rows) once per
+//               tile (MP fp32 columns) and stores y[t][row].
+#pragma once
+
+namespace tc05 {
+constexpr int kThreads = 448;
+constexpr int kDqWarps = 8;
+constexpr int kNA = 4;                        // A ring slots (one 64-K atom = 16 KiB each)
+constexpr int kNB = 2;                        // TMEM accumulators (tile t computes while t-1 drains)
+constexpr uint32_t kNibBytes = 128u * 128u;   // nibble box
+constexpr uint32_t kScBytes = 128u * 16u;     // scale box
+constexpr uint32_t kAtomBytes = 128u * 128u;  // A atom: 128 rows x 64 bf16
+
+__device__ __forceinline__ void fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+
+// UMMA shared-memory descriptor: K-major, 128B swizzle (8-row x 128 B atoms, SBO = 1024 B,
+// LBO unused = 1), start address in 16-B units, version 1 (sm_100).
+__device__ __forceinline__ uint64_t smem_desc(uint32_t addr)
+{
+    return (uint64_t)((addr & 0x3FFFFu) >> 4) | (1ull << 16) | ((uint64_t)(1024 >> 4) << 32) | (1ull << 46) |
+           (2ull << 61);
+}
+// Instruction descriptor kind::f16: D f32, A/B bf16, both K-major, N = MP, M = 128.
+template <int MP>
+__device__ __forceinline__ constexpr uint32_t idesc()
+{
+    return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(MP >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+}
+__device__ __forceinline__ void mma_bf16(uint32_t dtmem, uint64_t adesc, uint64_t bdesc, uint32_t id, uint32_t acc)
+{
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(dtmem),
+        "l"(adesc), "l"(bdesc), "r"(id), "r"(acc)
+        : "memory");
+}
+// arrive on an mbarrier when every tcgen05 op this thread issued so far has completed
+__device__ __forceinline__ void commit(uint32_t bar)
+{
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar) : "memory");
+}
+// 32 lanes x 16 columns of fp32 from TMEM (lane quarter of the calling warp)
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float *v)
+{
+    uint32_t r[16];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+        : "r"(taddr)
+        : "memory");
+#pragma unroll
+    for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+
+// Scale d split for the bf16 dequantiser: d = hi + lo with hi = bf16_rne(d) and lo the
+// rest (<= 3 significant bits of the fp16 d: exact in bf16), both broadcast to bf16x2.
+__device__ __forceinline__ void split_scale(float d, uint32_t &hi2, uint32_t &lo2)
+{
+    const uint32_t hb = (uint32_t)dev::float_to_bf16_bits(d);
+    const float hi = __uint_as_float(hb << 16);
+    const uint32_t lb = (uint32_t)dev::float_to_bf16_bits(d - hi);   // exact
+    hi2 = hb | (hb << 16);
+    lo2 = lb | (lb << 16);
+}
+// One bf16x2 pair of W^ from two codes placed as bf16 bits 0x43cc (= 128 + c):
+//   cm8 = c - 8 (exact), e = lo (c - 8) (exact: <= 3 x 4 bits), W^ = rn(hi (c - 8) + e)
+// -- one rounding of the exact d (c - 8): bf16_rne(f32(d) (c - 8)).
+__device__ __forceinline__ uint32_t dq_pair(uint32_t m, uint32_t hi2, uint32_t lo2)
+{
+    const uint32_t one = 0x3F803F80u, m136 = 0xC308C308u, zero = 0x80008000u;   // {1,1}, {-136,-136}, {-0,-0}
+    uint32_t cm8, e, r;
+    asm("fma.rn.bf16x2 %0, %1, %2, %3;" : "=r"(cm8) : "r"(m), "r"(one), "r"(m136));
+    asm("fma.rn.bf16x2 %0, %1, %2, %3;" : "=r"(e) : "r"(lo2), "r"(cm8), "r"(zero));
+    asm("fma.rn.bf16x2 %0, %1, %2, %3;" : "=r"(r) : "r"(hi2), "r"(cm8), "r"(e));
+    return r;
+}
+// 4 nibble bytes of a block (bytes t..t+3) -> W^ of elements t..t+3 (low nibbles: lo01,
+// lo23) and t+16..t+19 (high nibbles: hi01, hi23) as bf16 pairs.
+__device__ __forceinline__ void dq4(uint32_t w, uint32_t hi2s, uint32_t lo2s, uint32_t &lo01, uint32_t &lo23,
+                                    uint32_t &hi01, uint32_t &hi23)
+{
+    const uint32_t l = w & 0x0F0F0F0Fu, h = (w >> 4) & 0x0F0F0F0Fu;
+    // byte_perm with 0x43 as the second source's byte 0: {c_a, 0x43, c_b, 0x43} = bf16 (128 + c_a, 128 + c_b)
+    lo01 = dq_pair(__byte_perm(l, 0x43u, 0x4140), hi2s, lo2s);
+    lo23 = dq_pair(__byte_perm(l, 0x43u, 0x4342), hi2s, lo2s);
+    hi01 = dq_pair(__byte_perm(h, 0x43u, 0x4140), hi2s, lo2s);
+    hi23 = dq_pair(__byte_perm(h, 0x43u, 0x4342), hi2s, lo2s);
+}
+}  // namespace tc05
+
+template <int MP>
+__global__ void __launch_bounds__(tc05::kThreads, 1) tc05_w4a16(const __grid_constant__ GemmArgs a)
+{
+    using namespace tc05;
+    extern __shared__ __align__(16) uint8_t smem_raw[];
+    const uint32_t sb = (smem_addr(smem_raw) + 1023u) & ~1023u;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int S = a.stages;
+    const int G8 = (int)(a.k / 256);   // K slices
+    const uint32_t stage_bytes = a.stage_bytes;
+    const uint32_t ring = sb;
+    const uint32_t aring = sb + (uint32_t)S * stage_bytes;
+    const uint32_t bars = aring + (uint32_t)kNA * kAtomBytes;
+    const uint32_t sfull = bars, sempty = bars + 8u * S;
+    const uint32_t afull = sempty + 8u * S, aempty = afull + 8u * kNA;
+    const uint32_t dfull = aempty + 8u * kNA, dempty = dfull + 8u * kNB;
+    const uint32_t tslot = dempty + 8u * kNB;   // TMEM base address written by tcgen05.alloc
+    constexpr uint32_t kCols = (kNB * MP) < 32 ? 32 : (kNB * MP);   // a power of two for MP in {16, 32, 64}
+
+    const int T = a.row_tiles;
+    const int t0 = (int)(((uint32_t)T * blockIdx.x) / gridDim.x);
+    const int t1 = (int)(((uint32_t)T * (blockIdx.x + 1)) / gridDim.x);
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < S; ++s) {
+            mbar_init(sfull + 8u * s, 1);
+            mbar_init(sempty + 8u * s, 1 + kDqWarps);   // MMA commit + the dequantise warps
+        }
+        for (int s = 0; s < kNA; ++s) {
+            mbar_init(afull + 8u * s, kDqWarps);
+            mbar_init(aempty + 8u * s, 1);
+        }
+        for (int s = 0; s < kNB; ++s) {
+            mbar_init(dfull + 8u * s, 1);
+            mbar_init(dempty + 8u * s, 4);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(tslot), "r"(kCols)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    dev::griddep_launch();
+    fence_before();
+    __syncthreads();
+    fence_after();
+    const uint32_t tbase = lds32(tslot);
+    dev::griddep_wait();   // activations and outputs are ordered after the predecessor
+
+    if (warp == 0) {
+        // ================= TMA producer =================
+        if (lane == 0) {
+            const uint64_t pol = evict_first_policy();
+            int s = 0;
+            uint32_t ph = 0;
+            const uint32_t tx = kNibBytes + kScBytes + (uint32_t)MP * 512u;
+            for (int rt = t0; rt < t1; ++rt) {
+                const int row0 = rt * 128;
+                for (int sl = 0; sl < G8; ++sl) {
+                    mbar_wait(sempty + 8u * s, ph ^ 1u);
+                    const uint32_t st = ring + (uint32_t)s * stage_bytes;
+                    const uint32_t fb = sfull + 8u * s;
+                    mbar_expect_tx(fb, tx);
+                    tma_2d(st, a.maps, sl * 128, row0, fb, pol);
+                    tma_2d(st + kNibBytes, a.maps + 1, sl * 8, row0, fb, pol);
+                    tma_3d(st + kNibBytes + kScBytes, a.amaps, 0, (int)a.tok0, sl * 4, fb, 0);
+                    if (++s == S) {
+                        s = 0;
+                        ph ^= 1u;
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ================= MMA issuer: D[buf] = sum over K of W^ . X^T =================
+        if (lane == 0) {
+            constexpr uint32_t id = idesc<MP>();
+            int s = 0, sa = 0, bf = 0;
+            uint32_t ph = 0, pha = 0, phb = 0;
+            for (int rt = t0; rt < t1; ++rt) {
+                mbar_wait(dempty + 8u * bf, phb ^ 1u);   // the epilogue drained this accumulator
+                fence_after();
+                const uint32_t d = tbase + (uint32_t)bf * MP;
+                for (int sl = 0; sl < G8; ++sl) {
+                    mbar_wait(sfull + 8u * s, ph);
+                    fence_after();
+                    const uint32_t xs = ring + (uint32_t)s * stage_bytes + kNibBytes + kScBytes;
+                    for (int at = 0; at < 4; ++at) {
+                        mbar_wait(afull + 8u * sa, pha);
+                        fence_after();
+                        const uint32_t aa = aring + (uint32_t)sa * kAtomBytes;
+                        const uint32_t xa = xs + (uint32_t)at * (uint32_t)MP * 128u;
+#pragma unroll
+                        for (int kk = 0; kk < 4; ++kk)   // K16 steps of the atom: 32 B apart
+                            mma_bf16(d, smem_desc(aa + 32u * kk), smem_desc(xa + 32u * kk), id,
+                                     (sl | at | kk) != 0 ? 1u : 0u);
+                        commit(aempty + 8u * sa);
+                        if (++sa == kNA) {
+                            sa = 0;
+                            pha ^= 1u;
+                        }
+                    }
+                    commit(sempty + 8u * s);
+                    if (++s == S) {
+                        s = 0;
+                        ph ^= 1u;
+                    }
+                }
+                commit(dfull + 8u * bf);
+                if (++bf == kNB) {
+                    bf = 0;
+                    phb ^= 1u;
+                }
+            }
+        }
+    } else if (warp < 2 + kDqWarps) {
+        // ================= dequantise: thread = (row r, block bb of each 64-K atom) =================
+        const int tq = threadIdx.x - 64;
+        const int r = tq & 127, bb = tq >> 7;
+        const uint32_t sw = (uint32_t)(r & 7);
+        int s = 0, sa = 0;
+        uint32_t ph = 0, pha = 0;
+        for (int rt = t0; rt < t1; ++rt) {
+            for (int sl = 0; sl < G8; ++sl) {
+                mbar_wait(sfull + 8u * s, ph);
+                const uint32_t st = ring + (uint32_t)s * stage_bytes;
+                const uint4 scw = lds128(st + kNibBytes + (uint32_t)r * 16u);   // the row's 8 block scales
+                const uint32_t sc[4] = {scw.x, scw.y, scw.z, scw.w};
+                for (int at = 0; at < 4; ++at) {
+                    const int blk = 2 * at + bb;   // block of the slice
+                    const uint4 w = lds128(st + (uint32_t)r * 128u + (((uint32_t)blk ^ sw) << 4));
+                    uint32_t dh, dl;
+                    split_scale(h2f((uint16_t)(bb ? sc[at] >> 16 : sc[at] & 0xffffu)), dh, dl);
+                    uint32_t lo[8], hi[8];
+                    dq4(w.x, dh, dl, lo[0], lo[1], hi[0], hi[1]);
+                    dq4(w.y, dh, dl, lo[2], lo[3], hi[2], hi[3]);
+                    dq4(w.z, dh, dl, lo[4], lo[5], hi[4], hi[5]);
+                    dq4(w.w, dh, dl, lo[6], lo[7], hi[6], hi[7]);
+                    mbar_wait(aempty + 8u * sa, pha ^ 1u);
+                    // atom row r, 16-B chunks 4 bb + {0: K 0-7, 1: K 8-15, 2: K 16-23, 3: K 24-31}
+                    const uint32_t ar = aring + (uint32_t)sa * kAtomBytes + (uint32_t)r * 128u;
+                    const uint32_t c0 = 4u * (uint32_t)bb;
+                    asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(ar + (((c0 + 0) ^ sw) << 4)),
+                                 "r"(lo[0]), "r"(lo[1]), "r"(lo[2]), "r"(lo[3]) : "memory");
+                    asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(ar + (((c0 + 1) ^ sw) << 4)),
+                                 "r"(lo[4]), "r"(lo[5]), "r"(lo[6]), "r"(lo[7]) : "memory");
+                    asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(ar + (((c0 + 2) ^ sw) << 4)),
+                                 "r"(hi[0]), "r"(hi[1]), "r"(hi[2]), "r"(hi[3]) : "memory");
+                    asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(ar + (((c0 + 3) ^ sw) << 4)),
+                                 "r"(hi[4]), "r"(hi[5]), "r"(hi[6]), "r"(hi[7]) : "memory");
+                    // generic-proxy stores -> visible to the tensor core's async proxy
+                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(afull + 8u * sa);
+                    if (++sa == kNA) {
+                        sa = 0;
+                        pha ^= 1u;
+                    }
+                }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(sempty + 8u * s);
+                if (++s == S) {
+                    s = 0;
+                    ph ^= 1u;
+                }
+            }
+        }
+    } else {
+        // ================= epilogue: TMEM -> registers -> y, once per tile =================
+        const int quarter = warp & 3;
+        const int r = quarter * 32 + lane;   // weight row within the tile = TMEM lane
+        const uint32_t tl = tbase + ((uint32_t)(quarter * 32) << 16);
+        int bf = 0;
+        uint32_t phb = 0;
+        for (int rt = t0; rt < t1; ++rt) {
+            mbar_wait(dfull + 8u * bf, phb);
+            fence_after();
+            float D[MP];
+#pragma unroll
+            for (int c = 0; c < MP; c += 16) tmem_ld16(tl + (uint32_t)bf * MP + (uint32_t)c, D + c);
+            tmem_wait_ld();
+            fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(dempty + 8u * bf);
+            if (++bf == kNB) {
+                bf = 0;
+                phb ^= 1u;
+            }
+            const int64_t row = (int64_t)rt * 128 + r;
+            if (row < a.n) {
+#pragma unroll
+                for (int t = 0; t < MP; ++t)
+                    if (t < a.ntok) dev::store_out(a.y, a.ydt, (a.tok0 + t) * a.ldy + row, D[t]);
+            }
+        }
+    }
+    fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tbase), "r"(kCols) : "memory");
+    }
+}

@@ -32,6 +32,8 @@ CASES = {
     "up_3b_m16": ([(8192, 3072)], 16),
     "q_3b_m64": ([(3072, 3072)], 64),
     "lmhead_8b_m64": ([(128256, 4096)], 64),
+    "lmhead_8b_m16": ([(128256, 4096)], 16),
+    "up_3b_m64": ([(8192, 3072)], 64),
 }
 
 
@@ -60,11 +62,15 @@ def main():
         outs = [torch.empty(m, n, dtype=torch.bfloat16, device=dev) for n, _ in shapes]
         for route in [int(r) for r in args.routes.split(",")]:
             reps = args.reps or max(copies, 32)
-            ws = torch.empty(max(256, mq.workspace_bytes(route, m, max(n for n, _ in shapes), k)), dtype=torch.uint8,
+            ws = torch.empty(max(256, mq.workspace_bytes(min(route, 1), m, max(n for n, _ in shapes), k)), dtype=torch.uint8,
                              device=dev)
 
             def call(i):
-                mq.linear_group(route, sets[i % copies], x, outs=outs, ws=ws, stream=stream)
+                if route == 2:   # a6 with bf16-dequantised weights (tcgen05 kernel)
+                    for w_, y_ in zip(sets[i % copies], outs):
+                        mq.w4a16_bf16deq(w_, x, out=y_, stream=stream)
+                else:
+                    mq.linear_group(route, sets[i % copies], x, outs=outs, ws=ws, stream=stream)
 
             with torch.cuda.stream(stream):
                 for i in range(copies):     # descriptors of every copy encoded outside the capture
@@ -84,7 +90,7 @@ def main():
                     e1.record(stream)
                     e1.synchronize()
                     best = min(best, e0.elapsed_time(e1) * 1000 / reps)
-            print(json.dumps({"tag": args.tag, "case": name, "route": "w4a8" if route == 0 else "w4a16", "m": m,
+            print(json.dumps({"tag": args.tag, "case": name, "route": ["w4a8", "w4a16", "w4a16_bf16deq"][route], "m": m,
                               "us": round(best, 3), "GBps": round(wbytes / best / 1e3, 1), "weight_bytes": wbytes,
                               "copies": copies, "reps": reps, "env": env}), flush=True)
         del sets, base

@@ -224,6 +224,69 @@ def test_batched_ldx_ldy_and_rows_beyond_n(mq, orc, route):
     assert torch.all(yd[:, n:] == 7.0)
 
 
+# ---------------------------------------------------------------- a6, bf16-dequant semantics (tcgen05)
+@pytest.mark.parametrize("n,k", GEMM_SHAPES)
+@pytest.mark.parametrize("m", [1, 9, 16, 33, 64, 100])
+def test_bf16deq_vs_oracle(mq, orc, m, n, k):
+    """tcgen05 kernel vs oracle_w4a16_bf16deq (W^ = bf16_rne(d (c - 8)), fp32 accumulation):
+    ragged row tiles over 128-row CTAs, token passes of 16/32/64 (+ a second pass at 100),
+    K from one 256-slice up; reading T."""
+    w = si.weight(n, k, 1451 + n + k)
+    x = si.activation(m, k, 1452 + m + k)
+    pw, nib, sc = _pack_both(mq, orc, w)
+    y = mq.w4a16_bf16deq(pw, x.to(DEV), out_dtype=torch.float32)
+    _, y64 = orc.w4a16_bf16deq(nib, sc, _f32(x))
+    _assert_close(y, y64, 1e-3)
+
+
+def test_bf16deq_rounds_the_weights(mq, orc):
+    """The kernel really applies the bf16 rounding of d (c - 8): its distance to the
+    bf16-dequant oracle is far below the distance between the two semantics."""
+    n, k, m = 1024, 2048, 32
+    w = si.weight(n, k, 1461)
+    x = si.activation(m, k, 1462)
+    pw, nib, sc = _pack_both(mq, orc, w)
+    y = mq.w4a16_bf16deq(pw, x.to(DEV)).cpu().numpy().astype(np.float64)
+    _, yb = orc.w4a16_bf16deq(nib, sc, _f32(x))
+    _, ye = orc.w4a16(nib, sc, _f32(x))
+    gap = np.linalg.norm(yb - ye)
+    assert gap > 0
+    assert np.linalg.norm(y - yb) < 0.05 * gap
+
+
+def test_bf16deq_strides_bf16_out_rows_beyond_n(mq, orc):
+    """Strided x / y, bf16 output, last row tile mostly out of bounds (never stored)."""
+    n, k, m = 40, 1024, 20
+    w = si.weight(n, k, 1471)
+    xs = si.activation(m, k + 64, 1472)
+    pw, nib, sc = _pack_both(mq, orc, w)
+    yd = torch.full((m, n + 24), 7.0, dtype=torch.bfloat16, device=DEV)
+    mq.w4a16_bf16deq(pw, xs.to(DEV)[:, :k], out=yd[:, :n])
+    _, y64 = orc.w4a16_bf16deq(nib, sc, _f32(xs[:, :k].contiguous()))
+    _assert_close(yd[:, :n], y64, 2e-3)
+    assert torch.all(yd[:, n:] == 7.0)
+
+
+def test_bf16deq_full_size_lm_head_sampled_rows(mq, orc):
+    """Config 5 at its full size (8B lm_head 128256 x 4096, M = 64), in the launch
+    configuration bench.py times; sampled rows (incl. the last) against the oracle."""
+    n, k, m = 128256, 4096, 64
+    w = si.weight(n, k, 1481)
+    x = si.activation(m, k, 1482)
+    pw = mq.pack_w4(w.to(DEV))
+    y = mq.w4a16_bf16deq(pw, x.to(DEV), out_dtype=torch.float32)
+    rows = np.unique(np.concatenate([np.linspace(0, n - 1, 48).astype(np.int64), [127, 128, n - 128, n - 1]]))
+    nib, sc = orc.pack_w4(_f32(w[rows]))
+    _, y64 = orc.w4a16_bf16deq(nib, sc, _f32(x))
+    _assert_close(y[:, rows], y64, 1e-3)
+
+
+def test_bf16deq_rejects_k_not_multiple_of_256(mq):
+    pw = mq.pack_w4(si.weight(64, 288, 1491).to(DEV))
+    with pytest.raises(mq.McapqError):
+        mq.w4a16_bf16deq(pw, si.activation(16, 288, 1492).to(DEV))
+
+
 def test_zero_activation_and_impulse_rows(mq, orc):
     # S:315 / S:324-325 special cases through the GPU path
     k = 256
