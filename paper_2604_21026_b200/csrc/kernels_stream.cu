@@ -681,7 +681,7 @@ cudaError_t launch_tc05(const uint8_t *nib, const uint16_t *scale, int64_t n, in
         a.stage_bytes = tc05::kNibBytes + tc05::kScBytes + (uint32_t)mp * 512u;
         const size_t fixed = 1024 + (size_t)tc05::kNA * tc05::kAtomBytes + 256;
         int S = (int)((227 * 1024 - fixed) / a.stage_bytes);
-        S = S > 4 ? 4 : S;
+        S = S > 8 ? 8 : S;   // weight ring: as deep as shared memory allows (<= 8 slices)
         if (S < 2) return cudaErrorInvalidValue;
         a.stages = S;
         const size_t smem = fixed + (size_t)S * a.stage_bytes;

@@ -26,7 +26,7 @@
 namespace tc05 {
 constexpr int kThreads = 448;
 constexpr int kDqWarps = 8;
-constexpr int kNA = 4;                        // A ring slots (one 64-K atom = 16 KiB each)
+constexpr int kNA = 4;                        // A ring slots (one 64-K atom = 16 KiB each; even)
 constexpr int kNB = 2;                        // TMEM accumulators (tile t computes while t-1 drains)
 constexpr uint32_t kNibBytes = 128u * 128u;   // nibble box
 constexpr uint32_t kScBytes = 128u * 16u;     // scale box
@@ -241,33 +241,43 @@ __global__ void __launch_bounds__(tc05::kThreads, 1) tc05_w4a16(const __grid_con
                 const uint32_t st = ring + (uint32_t)s * stage_bytes;
                 const uint4 scw = lds128(st + kNibBytes + (uint32_t)r * 16u);   // the row's 8 block scales
                 const uint32_t sc[4] = {scw.x, scw.y, scw.z, scw.w};
-                for (int at = 0; at < 4; ++at) {
-                    const int blk = 2 * at + bb;   // block of the slice
-                    const uint4 w = lds128(st + (uint32_t)r * 128u + (((uint32_t)blk ^ sw) << 4));
-                    uint32_t dh, dl;
-                    split_scale(h2f((uint16_t)(bb ? sc[at] >> 16 : sc[at] & 0xffffu)), dh, dl);
-                    uint32_t lo[8], hi[8];
-                    dq4(w.x, dh, dl, lo[0], lo[1], hi[0], hi[1]);
-                    dq4(w.y, dh, dl, lo[2], lo[3], hi[2], hi[3]);
-                    dq4(w.z, dh, dl, lo[4], lo[5], hi[4], hi[5]);
-                    dq4(w.w, dh, dl, lo[6], lo[7], hi[6], hi[7]);
-                    mbar_wait(aempty + 8u * sa, pha ^ 1u);
-                    // atom row r, 16-B chunks 4 bb + {0: K 0-7, 1: K 8-15, 2: K 16-23, 3: K 24-31}
-                    const uint32_t ar = aring + (uint32_t)sa * kAtomBytes + (uint32_t)r * 128u;
-                    const uint32_t c0 = 4u * (uint32_t)bb;
-                    asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(ar + (((c0 + 0) ^ sw) << 4)),
-                                 "r"(lo[0]), "r"(lo[1]), "r"(lo[2]), "r"(lo[3]) : "memory");
-                    asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(ar + (((c0 + 1) ^ sw) << 4)),
-                                 "r"(lo[4]), "r"(lo[5]), "r"(lo[6]), "r"(lo[7]) : "memory");
-                    asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(ar + (((c0 + 2) ^ sw) << 4)),
-                                 "r"(hi[0]), "r"(hi[1]), "r"(hi[2]), "r"(hi[3]) : "memory");
-                    asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(ar + (((c0 + 3) ^ sw) << 4)),
-                                 "r"(hi[4]), "r"(hi[5]), "r"(hi[6]), "r"(hi[7]) : "memory");
+                // two atoms per proxy fence (the fence waits for this thread's stores; one
+                // wait per 128 K instead of per 64 K); kNA is even, so slots sa, sa + 1
+                for (int ap = 0; ap < 4; ap += 2) {
+#pragma unroll
+                    for (int j = 0; j < 2; ++j) {
+                        const int at = ap + j;
+                        const int blk = 2 * at + bb;   // block of the slice
+                        const uint4 w = lds128(st + (uint32_t)r * 128u + (((uint32_t)blk ^ sw) << 4));
+                        uint32_t dh, dl;
+                        split_scale(h2f((uint16_t)(bb ? sc[at] >> 16 : sc[at] & 0xffffu)), dh, dl);
+                        uint32_t lo[8], hi[8];
+                        dq4(w.x, dh, dl, lo[0], lo[1], hi[0], hi[1]);
+                        dq4(w.y, dh, dl, lo[2], lo[3], hi[2], hi[3]);
+                        dq4(w.z, dh, dl, lo[4], lo[5], hi[4], hi[5]);
+                        dq4(w.w, dh, dl, lo[6], lo[7], hi[6], hi[7]);
+                        mbar_wait(aempty + 8u * (sa + j), pha ^ 1u);
+                        // atom row r, 16-B chunks 4 bb + {0: K 0-7, 1: K 8-15, 2: K 16-23, 3: K 24-31}
+                        const uint32_t ar = aring + (uint32_t)(sa + j) * kAtomBytes + (uint32_t)r * 128u;
+                        const uint32_t c0 = 4u * (uint32_t)bb;
+                        asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(ar + (((c0 + 0) ^ sw) << 4)),
+                                     "r"(lo[0]), "r"(lo[1]), "r"(lo[2]), "r"(lo[3]) : "memory");
+                        asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(ar + (((c0 + 1) ^ sw) << 4)),
+                                     "r"(lo[4]), "r"(lo[5]), "r"(lo[6]), "r"(lo[7]) : "memory");
+                        asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(ar + (((c0 + 2) ^ sw) << 4)),
+                                     "r"(hi[0]), "r"(hi[1]), "r"(hi[2]), "r"(hi[3]) : "memory");
+                        asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(ar + (((c0 + 3) ^ sw) << 4)),
+                                     "r"(hi[4]), "r"(hi[5]), "r"(hi[6]), "r"(hi[7]) : "memory");
+                    }
                     // generic-proxy stores -> visible to the tensor core's async proxy
                     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                     __syncwarp();
-                    if (lane == 0) mbar_arrive(afull + 8u * sa);
-                    if (++sa == kNA) {
+                    if (lane == 0) {
+                        mbar_arrive(afull + 8u * sa);
+                        mbar_arrive(afull + 8u * (sa + 1));
+                    }
+                    sa += 2;
+                    if (sa == kNA) {
                         sa = 0;
                         pha ^= 1u;
                     }
