@@ -68,6 +68,16 @@ def peaks():
     return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
+def bf16_peak_tflops():
+    """Dense bf16 tensor peak: MEASURED_PEAKS.json bf16_tflops (cuBLAS burst), else 2250."""
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        if "bf16_tflops" in d:
+            return float(d["bf16_tflops"])
+    return 2250.0
+
+
 # ---------------------------------------------------------------- clocks
 class ClockSampler:
     """NVML sampling of SM clock + throttle reasons during the timed region."""
@@ -324,7 +334,10 @@ def time_single_linears(mq, dev, stream):
         row = {"config": cfg, "model": model, "slot": slot, "N": n, "K": k, "M": m, "weight_bytes": wbytes}
         with torch.cuda.stream(stream):
             wsp = torch.empty(mq.workspace_bytes(0, m, n, k), dtype=torch.uint8, device=dev)
-            for (route, name), pdl in itertools.product(((0, "w4a8"), (1, "w4a16")), (True, False)):
+            combos = list(itertools.product(((0, "w4a8"), (1, "w4a16")), (True, False)))
+            if m > 1:   # a6 with bf16-dequantised weights on tcgen05 (mcapq_w4a16_bf16deq)
+                combos.append(((2, "w4a16_bf16deq"), True))
+            for (route, name), pdl in combos:
                 # pdl: back-to-back linears as a decode engine launches them (mcapq_set_pdl: the
                 # next weight stream starts under the previous kernel's tail); also without
                 prev = mq.set_pdl(pdl)
@@ -333,8 +346,10 @@ def time_single_linears(mq, dev, stream):
                 def call(pw):
                     if route == 0:
                         mq.linear(0, pw, x, out=y, ws=wsp, stream=stream)
-                    else:
+                    elif route == 1:
                         mq.w4a16(pw, x, out=y, stream=stream)
+                    else:
+                        mq.w4a16_bf16deq(pw, x, out=y, stream=stream)
                 for pw in ws:        # every copy once: TMA descriptors are encoded outside the capture
                     call(pw)
                 reps = max(copies, 20)
@@ -359,6 +374,8 @@ def time_single_linears(mq, dev, stream):
                     row[f"{name_}_frac"] = round(wbytes / us / 1e3 / peaks()[0], 4)
                 if m > 1 and pdl:   # batched rows are judged on the tensor pipe too: int8 / bf16 MMA ops per second
                     row[f"{name_}_tops"] = round(2 * m * n * k / (us * 1e-6) / 1e12, 1)
+                    if route == 2:   # useful bf16 FLOP/s against the measured dense bf16 peak
+                        row[f"{name_}_tensor_frac"] = round(2 * m * n * k / (us * 1e-6) / 1e12 / bf16_peak_tflops(), 4)
         row["w4a8_over_w4a16"] = round(row["w4a16_us"] / row["w4a8_us"], 3)
         out.append(row)
         del ws, pw0

@@ -10,9 +10,10 @@ timeout 1200 python -m pytest tests -m gpu -x -q > $OUT/pytest_gpu.log 2>&1; ech
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $OUT/smoke.log 2>&1; echo "smoke exit $?" >> $OUT/smoke.log
 timeout 900 python bench.py > $OUT/bench.json 2> $OUT/bench.err; echo "bench exit $?" >> $OUT/bench.err
 timeout 400 python scripts/kbench.py --cases o_1b,qkv_1b,gateup_1b,down_1b,gate_8b,down_8b,lmhead_8b,up_3b_m16,q_3b_m64,lmhead_8b_m64 > $OUT/kbench.jsonl 2>&1
+timeout 300 python scripts/kbench.py --cases up_3b_m16,up_3b_m64,q_3b_m64,lmhead_8b_m16,lmhead_8b_m64 --routes 2 >> $OUT/kbench.jsonl 2>&1
 if [ "${NCU:-1}" = "1" ]; then
   # every launch of a short bench run with its device time (cold-cache, serialised: compare shares)
-  timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:'stack_step|stream_linear|gemv|tc_linear|quant_a8|gemm_w4' \
+  timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:'stack_step|stream_linear|gemv|tc_linear|quant_a8|gemm_w4|tc05' \
      -c 400 --csv --log-file $OUT/launches.csv python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-extras > $OUT/ncu_launch.log 2>&1
   # the headline step kernel (whole 16-layer step in one launch)
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:stack_step -s 3 -c 1 \
@@ -28,5 +29,8 @@ if [ "${NCU:-1}" = "1" ]; then
      -o $OUT/prof_gemm_a8 python scripts/kbench.py --cases lmhead_8b_m64 --routes 0 --reps 2 > $OUT/ncu_gemm_a8.log 2>&1
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:gemm_w4 -s 2 -c 1 \
      -o $OUT/prof_gemm_a16 python scripts/kbench.py --cases lmhead_8b_m64 --routes 1 --reps 2 > $OUT/ncu_gemm_a16.log 2>&1
+  # batched W4A16 with bf16-dequantised weights on tcgen05 (8B lm_head, M = 64)
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:tc05 -s 2 -c 1 \
+     -o $OUT/prof_tc05 python scripts/kbench.py --cases lmhead_8b_m64 --routes 2 --reps 2 > $OUT/ncu_tc05.log 2>&1
 fi
 echo done > $OUT/DONE
