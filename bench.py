@@ -56,7 +56,7 @@ def traffic_from_profiles(kernel_prefix):
             continue
         for cap, e in json.load(open(p)).get("captures", {}).items():
             if kernel_prefix in e.get("kernel", "") and e.get("dram_read_bytes") is not None:
-                return int(e["dram_read_bytes"] + (e.get("dram_write_bytes") or 0)), f"profiles/{sub}/{cap}"
+                return int(e["dram_read_bytes"] + (e.get("dram_write_bytes") or 0)), f"profiles/{sub}/summary.json:{cap}"
     return None, None
 
 
