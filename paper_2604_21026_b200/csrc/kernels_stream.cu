@@ -359,13 +359,16 @@ struct Tune {
     // step_smem_kb 120: a ~5-stage ring keeps the HBM pipe busy while bounding the
     // per-SM queue of in-flight weight data that the chain's L2 accesses wait behind
     int smem_kb = 112, max_stages = 12, nocompute = 0, pdl = 0, trace = 0, step_smem_kb = 200, step = 1,
-        step_flags = 0, step_spin_ns = 16, step_polls = 5, ctas_per_sm = 0, step_ep_log2 = 1;
+        step_flags = 0, step_spin_ns = 16, step_polls = 5, ctas_per_sm = 0, step_ep_log2 = 1, smem_kb_env = 0;
 };
 const Tune &tune()
 {
     static Tune t = [] {
         Tune v;
-        if (const char *e = getenv("MCAPQ_STREAM_SMEM_KB")) v.smem_kb = atoi(e);
+        if (const char *e = getenv("MCAPQ_STREAM_SMEM_KB")) {
+            v.smem_kb = atoi(e);
+            v.smem_kb_env = 1;
+        }
         if (const char *e = getenv("MCAPQ_STREAM_STAGES")) v.max_stages = atoi(e);
         if (const char *e = getenv("MCAPQ_STREAM_NOCOMPUTE")) v.nocompute = atoi(e);
         if (const char *e = getenv("MCAPQ_STREAM_PDL")) v.pdl = atoi(e);
@@ -400,7 +403,7 @@ size_t plan_smem(int engine, int64_t k, int ntok, StreamArgs &a)
     (void)ntok;
     const size_t act = round_up(act_bytes(engine, k, ntok), 128);
     const size_t fixed = kBarBytes + xraw + act + kRedBytes;
-    const size_t budget = (size_t)tune().smem_kb * 1024;
+    const size_t budget = (size_t)(a.smem_kb ? a.smem_kb : tune().smem_kb) * 1024;
     int S = (int)(((long)budget - (long)fixed - 1024) / kStageBytes);
     S = S < 2 ? 2 : (S > tune().max_stages ? tune().max_stages : S);
     S = S > kMaxStages ? kMaxStages : S;
@@ -936,6 +939,12 @@ cudaError_t launch_stream_group(int route, const StreamGroup &g, const uint16_t 
     // (8B lm_head: 6.08 -> 6.47 TB/s).  MCAPQ_STREAM_CTAS_PER_SM forces 1 or 2.
     const int per_sm = tune().ctas_per_sm ? tune().ctas_per_sm : (tiles >= 16 * device_sms() ? 2 : 1);
     const int sms = device_sms() * per_sm;
+    // shared-memory plan: ~112 KB (two CTAs per SM: the next linear's CTA co-resides under
+    // PDL); a wide input (K >= 8192: a 9-15 KB activation area) at one CTA per SM takes
+    // 130 KB instead -- two more ring stages beat the PDL overlap there (1B down 6.2 ->
+    // 4.8 us, 8B down 11.3 -> 10.6 us; 8B gate at K = 4096 stays faster at 112 KB).
+    // MCAPQ_STREAM_SMEM_KB overrides both.
+    a.smem_kb = (!tune().smem_kb_env && per_sm == 1 && g.k >= 8192) ? 130 : 0;
     const int tp = stream_tokens_per_pass(route, g.k);
     pdl = pdl || tune().pdl || api_pdl();
     for (int64_t tok0 = 0; tok0 < m; tok0 += tp) {

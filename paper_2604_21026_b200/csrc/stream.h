@@ -43,6 +43,7 @@ struct StreamArgs {
     int xraw_off;    // byte offset of the raw x staging area
     unsigned long long *trace;   // debug timeline (MCAPQ_STREAM_TRACE): 8 u64 per CTA, or null
     int launch_id;
+    int smem_kb;     // host side: shared-memory plan of this launch (plan_smem)
 };
 
 // Debug timeline (MCAPQ_STREAM_TRACE=1): per CTA {launch, block, t_start, t_wait,
