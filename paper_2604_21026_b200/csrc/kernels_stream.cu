@@ -359,7 +359,7 @@ struct Tune {
     // step_smem_kb 120: a ~5-stage ring keeps the HBM pipe busy while bounding the
     // per-SM queue of in-flight weight data that the chain's L2 accesses wait behind
     int smem_kb = 112, max_stages = 12, nocompute = 0, pdl = 0, trace = 0, step_smem_kb = 200, step = 1,
-        step_flags = 0, step_spin_ns = 16, step_polls = 5, ctas_per_sm = 0, step_ep_log2 = 1, smem_kb_env = 0;
+        step_flags = 0, step_spin_ns = 16, step_polls = 1, ctas_per_sm = 0, step_ep_log2 = 1, smem_kb_env = 0;
 };
 const Tune &tune()
 {
