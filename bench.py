@@ -318,7 +318,8 @@ def time_single_linears(mq, dev, stream):
     l2 = torch.cuda.get_device_properties(dev).L2_cache_size
     for cfg, model, slot, m in ((1, "llama-3.2-1b", "q", 1), (4, "llama-3.1-8b", "gate", 1),
                                 (4, "llama-3.1-8b", "down", 1), (5, "llama-3.1-8b", "lm_head", 1),
-                                (3, "llama-3.2-3b", "up", 16), (3, "llama-3.2-3b", "q", 64),
+                                (3, "llama-3.2-3b", "up", 1), (3, "llama-3.2-3b", "up", 16),
+                                (3, "llama-3.2-3b", "up", 64), (3, "llama-3.2-3b", "q", 64),
                                 (5, "llama-3.1-8b", "lm_head", 64)):
         n, k = si.linear_shape(model, slot)
         wbytes = n * k // 2 + n * (k // 32) * 2
