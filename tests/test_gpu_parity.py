@@ -466,6 +466,38 @@ def _step_stack(mq, mode, L=4, routes=(0, 1, 0, 1)):
     return st, ops
 
 
+def test_bench_step_full_size_sampled(mq, orc):
+    """Row a9 at BASELINE's full size, in the launch configuration bench.py times: the
+    16-layer Llama-3.2-1B chained stack under the golden MCAP mask (tab:per_layer_scores,
+    layer 15 W4A16), one stack_step launch captured in a graph.  Sampled rows of every
+    linear of layers 0, 7, 14 (W4A8) and 15 (W4A16) against the oracle on the linear's
+    actual input (the same per-linear check as the small step tests)."""
+    import bench
+    routes = mq.profile_parse(open(bench.GOLDEN_PROFILE).read()).routes()
+    assert list(routes) == [0] * 15 + [1]
+    st, _, xs, ys = bench.build_stack(mq, torch.device(DEV), routes)
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        st.capture(1, stream=s)
+        st.replay(stream=s)
+    s.synchronize()
+    assert st.launches(1) == 1
+    rng = np.random.default_rng(260421026)
+    for l in (0, 7, 14, 15):
+        for slot in bench.SLOTS:
+            n, k = si.linear_shape(bench.MODEL, slot)
+            rows = np.sort(rng.choice(n, size=16, replace=False))
+            rows[-1] = n - 1
+            w = si.weight(n, k, si.seed_for(bench.CONFIG_ID, l, slot))
+            nib, sc = orc.pack_w4(_f32(w[rows]))
+            x = _f32(xs[(l, bench.INPUT_ID[slot])])
+            if routes[l] == 0:
+                _, y64 = orc.w4a8_from_x(nib, sc, x)
+            else:
+                _, y64 = orc.w4a16(nib, sc, x)
+            _assert_close(ys[(l, slot)][:, rows], y64, 2e-3)
+
+
 @pytest.mark.parametrize("mode", ["independent", "dataflow", "barrier"])
 def test_step_kernel_m1_vs_oracle(mq, orc, mode):
     routes = (0, 1, 0, 1)
