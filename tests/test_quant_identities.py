@@ -65,3 +65,49 @@ def test_div127_one_correction_step_is_exact_for_every_bf16_magnitude():
 def test_scale_never_underflows_to_zero(amax_bits):
     # live <=> amax != 0: the smallest bf16 subnormal / 127 is still a nonzero fp32
     assert _rnd32(_bf16(amax_bits) / 127) != 0
+
+
+# ---------------------------------------------------------------------------
+# tcgen05 bf16-dequant path (mcapq_w4a16_bf16deq, reading A13'): the kernel forms
+# W^ = bf16_rne(f32(d) (c - 8)) in bf16x2 arithmetic as rn(hi (c - 8) + lo (c - 8)) with
+# hi = bf16_rne(d), lo = d - hi.  That is one rounding of the exact product iff lo and
+# lo (c - 8) are exact in bf16 (8 significant bits) -- checked here for every finite fp16 d
+# and every code, in exact binary arithmetic (float64 holds all these values exactly).
+def _sig_bits(v):
+    """Significant bits of each (exactly float64-representable) value; 0 for zero."""
+    import numpy as np
+    v = np.abs(np.asarray(v, np.float64))
+    m, _ = np.frexp(v)                       # v = m 2^e, m in [0.5, 1)
+    bits = np.zeros(v.shape, np.int64)
+    nz = v != 0
+    mant = (m[nz] * 2.0 ** 53).astype(np.uint64)
+    tz = np.zeros(mant.shape, np.int64)
+    x = mant.copy()
+    for _ in range(53):
+        z = (x & np.uint64(1)) == 0
+        tz += z & (x != 0)
+        x = np.where(z, x >> np.uint64(1), x)
+    bits[nz] = 53 - tz
+    return bits
+
+
+def _bf16_rne(v):
+    import numpy as np
+    import torch
+    return torch.from_numpy(np.asarray(v, np.float32)).to(torch.bfloat16).float().numpy().astype(np.float64)
+
+
+def test_bf16deq_split_scale_is_one_rounding():
+    import numpy as np
+    h = np.arange(0, 0x10000, dtype=np.uint32).astype(np.uint16)
+    d = h.view(np.float16).astype(np.float64)
+    d = d[np.isfinite(d)]
+    hi = _bf16_rne(d)
+    lo = d - hi                                        # exact in float64
+    assert (_sig_bits(lo) <= 8).all()                  # lo is a bf16 value
+    assert (np.abs(hi) < 3.0e38).all()
+    for c in range(16):
+        e = lo * (c - 8)
+        assert (_sig_bits(e) <= 8).all(), c            # lo (c - 8) is exact in bf16
+        exact = d * (c - 8)                            # = hi (c - 8) + e, exactly
+        assert np.array_equal(hi * (c - 8) + e, exact)
