@@ -317,26 +317,38 @@ def time_single_linears(mq, dev, stream):
     out = []
     l2 = torch.cuda.get_device_properties(dev).L2_cache_size
     for cfg, model, slot, m in ((1, "llama-3.2-1b", "q", 1), (4, "llama-3.1-8b", "gate", 1),
+                                (4, "llama-3.1-8b", "gate+up", 1),
                                 (4, "llama-3.1-8b", "down", 1), (5, "llama-3.1-8b", "lm_head", 1),
                                 (3, "llama-3.2-3b", "up", 1), (3, "llama-3.2-3b", "up", 16),
                                 (3, "llama-3.2-3b", "up", 64), (3, "llama-3.2-3b", "q", 64),
                                 (5, "llama-3.1-8b", "lm_head", 64)):
-        n, k = si.linear_shape(model, slot)
-        wbytes = n * k // 2 + n * (k // 32) * 2
+        # "a+b": the linears sharing one input in ONE grouped launch (mcapq_linear_group: the
+        # fused gate/up of P:977), as the framework launches the 8B MLP up-projections
+        members = slot.split("+")
+        dims = [si.linear_shape(model, s_) for s_ in members]
+        n, k = dims[0]
+        wbytes = sum(n_ * k_ // 2 + n_ * (k_ // 32) * 2 for n_, k_ in dims)
         copies = max(2, min(32, math.ceil(4 * l2 / wbytes)))
         ws = []
-        base = si.weight(n, k, si.seed_for(cfg, 0, slot)).to(dev)
-        pw0 = mq.pack_w4(base)
-        del base
+        pw0s = []
+        for s_, (n_, k_) in zip(members, dims):
+            base = si.weight(n_, k_, si.seed_for(cfg, 0, s_)).to(dev)
+            pw0s.append(mq.pack_w4(base))
+            del base
         for c in range(copies):
-            ws.append(mq.PackedW4(pw0.nib.clone(), pw0.scale.clone()))
-        x = si.activation(m, k, si.seed_for(cfg, 0, slot, True), si.activation_kind(slot)).to(dev)
-        y = torch.empty(m, n, dtype=torch.bfloat16, device=dev)
-        row = {"config": cfg, "model": model, "slot": slot, "N": n, "K": k, "M": m, "weight_bytes": wbytes}
+            ws.append([mq.PackedW4(p_.nib.clone(), p_.scale.clone()) for p_ in pw0s])
+        x = si.activation(m, k, si.seed_for(cfg, 0, members[0], True), si.activation_kind(members[0])).to(dev)
+        ys_ = [torch.empty(m, n_, dtype=torch.bfloat16, device=dev) for n_, _ in dims]
+        y = ys_[0]
+        grouped = len(members) > 1
+        row = {"config": cfg, "model": model, "slot": slot, "N": sum(n_ for n_, _ in dims) if grouped else n, "K": k,
+               "M": m, "weight_bytes": wbytes}
+        if grouped:
+            row["launch"] = "one grouped launch (mcapq_linear_group)"
         with torch.cuda.stream(stream):
-            wsp = torch.empty(mq.workspace_bytes(0, m, n, k), dtype=torch.uint8, device=dev)
+            wsp = torch.empty(mq.workspace_bytes(0, m, max(n_ for n_, _ in dims), k), dtype=torch.uint8, device=dev)
             combos = list(itertools.product(((0, "w4a8"), (1, "w4a16")), (True, False)))
-            if m > 1:   # a6 with bf16-dequantised weights on tcgen05 (mcapq_w4a16_bf16deq)
+            if m > 1 and not grouped:   # a6 with bf16-dequantised weights on tcgen05 (mcapq_w4a16_bf16deq)
                 combos.append(((2, "w4a16_bf16deq"), True))
             for (route, name), pdl in combos:
                 # pdl: back-to-back linears as a decode engine launches them (mcapq_set_pdl: the
@@ -344,7 +356,11 @@ def time_single_linears(mq, dev, stream):
                 prev = mq.set_pdl(pdl)
                 name_ = name if pdl else name + "_nopdl"
 
-                def call(pw):
+                def call(pws):
+                    if grouped:
+                        mq.linear_group(route, pws, x, outs=ys_, ws=wsp, stream=stream)
+                        return
+                    pw = pws[0]
                     if route == 0:
                         mq.linear(0, pw, x, out=y, ws=wsp, stream=stream)
                     elif route == 1:
@@ -379,7 +395,7 @@ def time_single_linears(mq, dev, stream):
                         row[f"{name_}_tensor_frac"] = round(2 * m * n * k / (us * 1e-6) / 1e12 / bf16_peak_tflops(), 4)
         row["w4a8_over_w4a16"] = round(row["w4a16_us"] / row["w4a8_us"], 3)
         out.append(row)
-        del ws, pw0
+        del ws, pw0s
         torch.cuda.empty_cache()
     return out
 

@@ -27,6 +27,7 @@ CASES = {
     "o_1b": ([(2048, 2048)], 1),
     "down_1b": ([(2048, 8192)], 1),
     "gate_8b": ([(14336, 4096)], 1),
+    "gateup_8b": ([(14336, 4096), (14336, 4096)], 1),
     "down_8b": ([(4096, 14336)], 1),
     "lmhead_8b": ([(128256, 4096)], 1),
     "up_3b_m16": ([(8192, 3072)], 16),
