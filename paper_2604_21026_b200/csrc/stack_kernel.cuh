@@ -173,28 +173,22 @@ __device__ __forceinline__ void stage_step_a8_oct(unsigned long long *tmid, cons
     if (quant) a8_oct_store(w2, on, g, sub8, K2, L);
 }
 
+// Rounds q0 / NT .. q0 / NT + kRounds - 1 of the quad staging (one phase; see stage_step).
 template <int kRounds>
-__device__ __forceinline__ void stage_step(unsigned long long *tmid, const StackOp &op, bool a16, const ActSmem &L, int tid, uint32_t t16,
-                                           bool check, int spin_ns, int polls, const unsigned int *counters,
-                                           bool quant)
+__device__ __forceinline__ void stage_step_phase(unsigned long long *tmid, const StackOp &op, bool a16, const ActSmem &L,
+                                                 int tid, uint32_t t16, bool check, int spin_ns, int polls,
+                                                 const unsigned int *counters, bool quant, int q0)
 {
-    if (!a16 && op.k <= 2048) {
-        stage_step_a8_oct(tmid, op, L, tid, t16, check, spin_ns, polls, counters, quant);
-        return;
-    }
     const int G = (int)(op.k / 32);
     const uint32_t K2 = (uint32_t)(op.k / 2);
     const int nq = G * 4;
     const bool tagged = op.xt != nullptr;
     constexpr int NT = kConsumerWarps * 32;
-    if (a16)
-        for (int idx = tid; idx < G * 8; idx += NT)     // tokens 1..7 of corr: zero
-            if ((idx & 7) != 0) sts32(L.corr + 4u * (uint32_t)idx, 0u);
     uint4 ra[kRounds], rb[kRounds];
 #pragma unroll
     for (int r = 0; r < kRounds; ++r) {
-        const int idx = r * NT + tid;
-        if (r * NT < nq && idx < nq) {
+        const int idx = q0 + r * NT + tid;
+        if (q0 + r * NT < nq && idx < nq) {
             const int g = idx >> 2, sub = idx & 3;
             // element offsets: W4A8 quad member sub holds 8 sub .. 8 sub + 7; W4A16 4t..4t+3, 4t+16..4t+19
             const int e0 = 32 * g + (a16 ? 4 * sub : 8 * sub);
@@ -216,8 +210,8 @@ __device__ __forceinline__ void stage_step(unsigned long long *tmid, const Stack
         auto reload_stale = [&]() {
 #pragma unroll
             for (int r = 0; r < kRounds; ++r) {
-                const int idx = r * NT + tid;
-                if (r * NT < nq && idx < nq && !(tags_ok(ra[r], t16) && tags_ok(rb[r], t16))) {
+                const int idx = q0 + r * NT + tid;
+                if (q0 + r * NT < nq && idx < nq && !(tags_ok(ra[r], t16) && tags_ok(rb[r], t16))) {
                     const int g = idx >> 2, sub = idx & 3;
                     const int e0 = 32 * g + (a16 ? 4 * sub : 8 * sub);
                     const int e1 = a16 ? e0 + 16 : e0 + 4;
@@ -235,7 +229,7 @@ __device__ __forceinline__ void stage_step(unsigned long long *tmid, const Stack
                 bool ok = true;
 #pragma unroll
                 for (int r = 0; r < kRounds; ++r)
-                    if (r * NT + tid < nq) ok = ok && tags_ok(ra[r], t16) && tags_ok(rb[r], t16);
+                    if (q0 + r * NT + tid < nq) ok = ok && tags_ok(ra[r], t16) && tags_ok(rb[r], t16);
                 if (ok) break;
                 __nanosleep(backoff);
                 reload_stale();
@@ -246,7 +240,7 @@ __device__ __forceinline__ void stage_step(unsigned long long *tmid, const Stack
             bool ok = true;
 #pragma unroll
             for (int r = 0; r < kRounds; ++r)
-                if (r * NT + tid < nq) ok = ok && tags_ok(ra[r], t16) && tags_ok(rb[r], t16);
+                if (q0 + r * NT + tid < nq) ok = ok && tags_ok(ra[r], t16) && tags_ok(rb[r], t16);
             if (bar_consumers_and(ok)) break;
             if (p >= polls) {
                 if (tid == 0)
@@ -264,9 +258,9 @@ __device__ __forceinline__ void stage_step(unsigned long long *tmid, const Stack
     }
 #pragma unroll
     for (int r = 0; r < kRounds; ++r) {
-        if (r == 0 && tmid) *tmid = globaltimer();
-        if (r * NT >= nq) break;   // CTA-uniform
-        const int idx = r * NT + tid;
+        if (r == 0 && q0 == 0 && tmid) *tmid = globaltimer();
+        if (q0 + r * NT >= nq) break;   // CTA-uniform
+        const int idx = q0 + r * NT + tid;
         const bool on = idx < nq;
         const int q = on ? idx : 0;
         const int g = q >> 2, sub = q & 3;
@@ -291,6 +285,35 @@ __device__ __forceinline__ void stage_step(unsigned long long *tmid, const Stack
             a16_quad_store(make_uint2(w4[0], w4[1]), make_uint2(w4[2], w4[3]), on, 0, g, sub, L);
         } else {
             if (quant) a8_quad_store(w4, on, 0, g, sub, G, K2, L);
+        }
+    }
+}
+
+// Stage one linear's input (M = 1) into shared memory, quads of threads per 32-group.
+// At most two rounds of 512 quads are held in registers at a time: a K > 8192 input
+// (kRounds = 4) is staged in two phases, so the K = 14336 variant of the step kernel has
+// the register profile of the K <= 8192 one (the whole kernel shares the 96-register cap).
+template <int kRounds>
+__device__ __forceinline__ void stage_step(unsigned long long *tmid, const StackOp &op, bool a16, const ActSmem &L, int tid, uint32_t t16,
+                                           bool check, int spin_ns, int polls, const unsigned int *counters,
+                                           bool quant)
+{
+    if (!a16 && op.k <= 2048) {
+        stage_step_a8_oct(tmid, op, L, tid, t16, check, spin_ns, polls, counters, quant);
+        return;
+    }
+    constexpr int NT = kConsumerWarps * 32;
+    const int G = (int)(op.k / 32);
+    if (a16)
+        for (int idx = tid; idx < G * 8; idx += NT)     // tokens 1..7 of corr: zero
+            if ((idx & 7) != 0) sts32(L.corr + 4u * (uint32_t)idx, 0u);
+    if constexpr (kRounds <= 2) {
+        stage_step_phase<kRounds>(tmid, op, a16, L, tid, t16, check, spin_ns, polls, counters, quant, 0);
+    } else {
+#pragma unroll 1
+        for (int q0 = 0; q0 < kRounds * NT; q0 += 2 * NT) {
+            if (q0 >= G * 4) break;   // CTA-uniform
+            stage_step_phase<2>(tmid, op, a16, L, tid, t16, check, spin_ns, polls, counters, quant, q0);
         }
     }
 }
