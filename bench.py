@@ -348,6 +348,14 @@ def time_single_linears(mq, dev, stream):
         with torch.cuda.stream(stream):
             wsp = torch.empty(mq.workspace_bytes(0, m, max(n_ for n_, _ in dims), k), dtype=torch.uint8, device=dev)
             combos = list(itertools.product(((0, "w4a8"), (1, "w4a16")), (True, False)))
+            if m == 1 and not grouped:
+                # the paper's two-kernel W4A8 design on this GPU (app:kernels): a separate
+                # quantisation kernel (mcapq_quant_a8) + a warp-per-row dp4a GEMV on the pre-quantised
+                # activations (mcapq_w4a8), PDL-chained -- the baseline the fused TMA path replaces
+                combos.append(((3, "w4a8_twokernel"), True))
+                qbuf = (torch.empty((m, k), dtype=torch.int8, device=dev),
+                        torch.empty((m, k // 32), dtype=torch.float32, device=dev),
+                        torch.empty((m, k // 32), dtype=torch.int32, device=dev))
             if m > 1 and not grouped:   # a6 with bf16-dequantised weights on tcgen05 (mcapq_w4a16_bf16deq)
                 combos.append(((2, "w4a16_bf16deq"), True))
             for (route, name), pdl in combos:
@@ -365,8 +373,11 @@ def time_single_linears(mq, dev, stream):
                         mq.linear(0, pw, x, out=y, ws=wsp, stream=stream)
                     elif route == 1:
                         mq.w4a16(pw, x, out=y, stream=stream)
-                    else:
+                    elif route == 2:
                         mq.w4a16_bf16deq(pw, x, out=y, stream=stream)
+                    else:
+                        mq.quant_a8(x, stream=stream, out=qbuf)
+                        mq.w4a8(pw, *qbuf, out=y, stream=stream)
                 for pw in ws:        # every copy once: TMA descriptors are encoded outside the capture
                     call(pw)
                 reps = max(copies, 20)

@@ -88,14 +88,18 @@ def pack_w4(w: torch.Tensor, dev_err: torch.Tensor | None = None, stream=None) -
     return PackedW4(nib, scale)
 
 
-def quant_a8(x: torch.Tensor, stream=None):
-    """a2: x [M, K] bf16 -> (q int8 [M, K], sx fp32 [M, K/32], sq int32 [M, K/32])."""
+def quant_a8(x: torch.Tensor, stream=None, out=None):
+    """a2: x [M, K] bf16 -> (q int8 [M, K], sx fp32 [M, K/32], sq int32 [M, K/32]);
+    out: optional preallocated (q, sx, sq)."""
     _need_cuda(x)
     x2 = x if x.dim() == 2 else x.view(1, -1)
     m, k = x2.shape
-    q = torch.empty((m, k), dtype=torch.int8, device=x.device)
-    sx = torch.empty((m, k // 32), dtype=torch.float32, device=x.device)
-    sq = torch.empty((m, k // 32), dtype=torch.int32, device=x.device)
+    if out is not None:
+        q, sx, sq = out
+    else:
+        q = torch.empty((m, k), dtype=torch.int8, device=x.device)
+        sx = torch.empty((m, k // 32), dtype=torch.float32, device=x.device)
+        sq = torch.empty((m, k // 32), dtype=torch.int32, device=x.device)
     check(load().mcapq_quant_a8(_ptr(x2), m, k, x2.stride(0), _ptr(q), _ptr(sx), _ptr(sq), _stream(stream)),
           "mcapq_quant_a8")
     return q, sx, sq
