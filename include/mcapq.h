@@ -264,6 +264,32 @@ mcapq_status mcapq_profile_scores(const mcapq_profile *p, double *scores_host, i
 mcapq_status mcapq_profile_routes(const mcapq_profile *p, uint8_t *routes_host, int n);
 void mcapq_profile_free(mcapq_profile *p);
 
+/*
+ * NEXT-3: the MCAP profile artifact from raw per-layer scores s_i (Alg. 1 line 10,
+ * P:547-549): writes {"format_version":1,"num_layers":L,"prompt_count":k,"epsilon":1e-09,
+ * "raw_scores":[...],"tau":tau} (NUL-terminated) into buf (host, cap bytes); *len = length
+ * without the NUL.  mcapq_profile_parse of it min-max normalises (lines 11-15) and routes
+ * (line 16).  MCAPQ_ENOSPACE if cap < *len + 1; MCAPQ_EINVAL for NULL / non-finite input.
+ */
+mcapq_status mcapq_profile_write_json(const double *raw_scores_host, int layers, int prompts, double tau, char *buf,
+                                      size_t cap, size_t *len);
+
+/*
+ * NEXT-3: MCAP profiling on the GPU (Alg. 1 lines 3-10).  For one layer and one
+ * prompt of m tokens, given that layer's linear outputs as bf16 rows (Q x_t in yq [m][ldq],
+ * first nq used; V x_t in yv; FFN(x_t) in yffn):
+ *   a_t = || [Q x_t, V x_t] ||_2 + || FFN(x_t) ||_2      (fp64 from the exact bf16 values)
+ *   *score += weight * sum_t a_t                          (fixed order: deterministic)
+ * score: one device fp64 accumulator per layer (caller-owned, caller-initialised);
+ * weight = 1 / (k m) gives Alg. 1's mean over prompts and tokens.  ws: device workspace of
+ * >= mcapq_mcap_workspace_bytes(m) bytes.  Stream-ordered, no allocation, graph-capturable.
+ * Errors: MCAPQ_EINVAL (NULL, m/n < 1, ld < n, non-finite weight), MCAPQ_ENOSPACE.
+ */
+size_t mcapq_mcap_workspace_bytes(int64_t m);
+mcapq_status mcapq_mcap_accumulate(const uint16_t *yq, int64_t ldq, int64_t nq, const uint16_t *yv, int64_t ldv,
+                                   int64_t nv, const uint16_t *yffn, int64_t ldf, int64_t nf, int64_t m,
+                                   double weight, double *score, void *ws, size_t ws_bytes, void *stream);
+
 /* ------------------------------------------------ decode linear stack (a9) */
 /*
  * A routed stack of decode linears: L layers x S slots, each slot a packed

@@ -265,6 +265,34 @@ def w4a16_bf16deq(nib, scale, x):
 
 
 # --------------------------------------------------------------------------
+# NEXT-3: MCAP raw scores (Alg. 1 lines 1-10)
+# --------------------------------------------------------------------------
+def mcap_raw_scores(prompts):
+    """Alg. 1 lines 1-10 written out.  prompts: k prompts, each a list over the L layers
+    of (q, v, ffn) arrays [|p_j|, n] (the layer's Q x_t, V x_t and FFN(x_t) rows).
+        a_attn = || [Q x_t, V x_t] ||_2          (line 5)
+        a_ffn  = || FFN(x_t) ||_2                (line 6)
+        s_i    = 1/k sum_j 1/|p_j| sum_t (a_attn + a_ffn)     (line 10)
+    in fp64.  -> [s_1 .. s_L]."""
+    k = len(prompts)
+    L = len(prompts[0])
+    s = [0.0] * L
+    for layers in prompts:
+        for i, (q, v, f) in enumerate(layers):
+            q = np.asarray(q, np.float64)
+            v = np.asarray(v, np.float64)
+            f = np.asarray(f, np.float64)
+            m = q.shape[0]
+            total = 0.0
+            for t in range(m):
+                a_attn = math.sqrt(float(np.sum(q[t] * q[t])) + float(np.sum(v[t] * v[t])))
+                a_ffn = math.sqrt(float(np.sum(f[t] * f[t])))
+                total += a_attn + a_ffn
+            s[i] += total / m / k
+    return s
+
+
+# --------------------------------------------------------------------------
 # a7: profile -> routes (Alg. 1 lines 8-13, P:550-557; P:840-842; A14)
 # --------------------------------------------------------------------------
 def minmax_normalize(scores, eps: float = EPS_DEFAULT):

@@ -27,7 +27,8 @@ __all__ = [
     "W4A8", "W4A16", "BF16", "F32", "McapqError", "load", "pack_w4", "quant_a8", "w4a8", "w4a8_x", "w4a16",
     "w4a16_bf16deq",
     "linear", "linear_group", "linear_host", "w4a8_group_dots", "workspace_bytes", "host_workspace_bytes", "Profile",
-    "profile_parse", "Stack", "Comm", "linear_colshard", "PackedW4", "device_sms", "set_pdl",
+    "profile_parse", "profile_write_json", "mcap_accumulate", "Stack", "Comm", "linear_colshard", "PackedW4",
+    "device_sms", "set_pdl",
 ]
 
 
@@ -267,6 +268,37 @@ def profile_parse(text: str | bytes, tau: float | None = None) -> Profile:
     check(load().mcapq_profile_parse(b, len(b), float("nan") if tau is None else float(tau), ctypes.byref(h)),
           "mcapq_profile_parse")
     return Profile(h)
+
+
+def profile_write_json(raw_scores, prompts: int, tau: float = 0.7) -> str:
+    """NEXT-3: the profile artifact (JSON) from raw per-layer scores (mcapq_profile_write_json)."""
+    L = len(raw_scores)
+    arr = (ctypes.c_double * L)(*[float(v) for v in raw_scores])
+    n = ctypes.c_size_t(0)
+    cap = 64 + 32 * L
+    buf = ctypes.create_string_buffer(cap)
+    check(load().mcapq_profile_write_json(ctypes.cast(arr, ctypes.c_void_p), L, int(prompts), float(tau), buf, cap,
+                                          ctypes.byref(n)), "mcapq_profile_write_json")
+    return buf.value.decode()
+
+
+def mcap_accumulate(yq: torch.Tensor, yv: torch.Tensor, yffn: torch.Tensor, weight: float, score: torch.Tensor,
+                    ws: torch.Tensor | None = None, stream=None):
+    """NEXT-3 (Alg. 1 lines 3-10): score (fp64 device scalar) += weight * sum_t (||[q_t, v_t]|| + ||ffn_t||)
+    over the m token rows of one layer's bf16 linear outputs."""
+    _need_cuda(yq, yv, yffn, score)
+    for t in (yq, yv, yffn):
+        if t.dtype != torch.bfloat16 or t.dim() != 2 or t.stride(1) != 1:
+            raise McapqError(1, "binding", "mcap_accumulate: bf16 [m, n] row-major tensors expected")
+    if score.dtype != torch.float64:
+        raise McapqError(2, "dtype", "score must be float64")
+    m = yq.shape[0]
+    if ws is None:
+        ws = torch.empty(max(8, load().mcapq_mcap_workspace_bytes(m)), dtype=torch.uint8, device=yq.device)
+    check(load().mcapq_mcap_accumulate(_ptr(yq), yq.stride(0), yq.shape[1], _ptr(yv), yv.stride(0), yv.shape[1],
+                                       _ptr(yffn), yffn.stride(0), yffn.shape[1], m, float(weight), _ptr(score),
+                                       _ptr(ws), ws.numel(), _stream(stream)), "mcapq_mcap_accumulate")
+    return score
 
 
 # ------------------------------------------------------------------ stack

@@ -46,6 +46,9 @@ SIGNATURES = {
     "mcapq_profile_scores": (I32, [P, P, I32]),
     "mcapq_profile_routes": (I32, [P, P, I32]),
     "mcapq_profile_free": (None, [P]),
+    "mcapq_profile_write_json": (I32, [P, I32, I32, DBL, ctypes.c_char_p, SZ, ctypes.POINTER(SZ)]),
+    "mcapq_mcap_workspace_bytes": (SZ, [I64]),
+    "mcapq_mcap_accumulate": (I32, [P, I64, I64, P, I64, I64, P, I64, I64, I64, DBL, P, P, SZ, P]),
     "mcapq_stack_create": (I32, [I32, P, I64, ctypes.POINTER(P)]),
     "mcapq_stack_set": (I32, [P, I32, I32, I32, P, P, I64, I64, P, P, I32]),
     "mcapq_stack_run": (I32, [P, I64, P]),

@@ -265,4 +265,30 @@ mcapq_status mcapq_profile_routes(const mcapq_profile *p, uint8_t *routes_host, 
 
 void mcapq_profile_free(mcapq_profile *p) { delete p; }
 
+// The profile artifact from raw per-layer scores (Alg. 1 line 10 output, e.g. accumulated by
+// mcapq_mcap_accumulate): the same JSON form mcapq_profile_parse reads ("raw_scores" are
+// min-max normalised there, Alg. 1 lines 11-15).  %.17g keeps every double exact.
+mcapq_status mcapq_profile_write_json(const double *raw_scores_host, int layers, int prompts, double tau, char *buf,
+                                      size_t cap, size_t *len)
+{
+    clear_error();
+    MCAPQ_REQUIRE(raw_scores_host && buf && len, MCAPQ_EINVAL, "NULL argument");
+    MCAPQ_REQUIRE(layers >= 1 && prompts >= 1, MCAPQ_EINVAL, "layers=%d prompts=%d", layers, prompts);
+    MCAPQ_REQUIRE(std::isfinite(tau), MCAPQ_EINVAL, "tau is not finite");
+    std::string s = "{\"format_version\":1,\"num_layers\":" + std::to_string(layers) +
+                    ",\"prompt_count\":" + std::to_string(prompts) + ",\"epsilon\":1e-09,\"raw_scores\":[";
+    char num[64];
+    for (int i = 0; i < layers; ++i) {
+        MCAPQ_REQUIRE(std::isfinite(raw_scores_host[i]), MCAPQ_EINVAL, "raw score %d is not finite", i);
+        snprintf(num, sizeof(num), "%s%.17g", i ? "," : "", raw_scores_host[i]);
+        s += num;
+    }
+    snprintf(num, sizeof(num), "],\"tau\":%.17g}", tau);
+    s += num;
+    *len = s.size();
+    MCAPQ_REQUIRE(cap >= s.size() + 1, MCAPQ_ENOSPACE, "buffer %zu < %zu bytes", cap, s.size() + 1);
+    memcpy(buf, s.c_str(), s.size() + 1);
+    return MCAPQ_OK;
+}
+
 }  // extern "C"
