@@ -190,6 +190,27 @@ mcapq_status mcapq_w4a16_bf16deq(const uint8_t *nib, const uint16_t *scale, int6
                                  const uint16_t *x, int64_t m, int64_t ldx, void *y, int ydt, int64_t ldy,
                                  void *stream);
 
+/*
+ * NEXT-4 (prefill / large M; the paper's "dequantise to 16-bit, then GEMM"): the
+ * bf16-dequant semantics of mcapq_w4a16_bf16deq with the weights materialised ONCE:
+ *   mcapq_dequant_w4_bf16: W^[n][k] = bf16_rne(f32(d) (c - 8)), bf16 row-major, caller's w
+ *     (16-byte aligned, n*k*2 bytes; = mcapq_prefill_workspace_bytes(n, k)); load time or per
+ *     prefill; bandwidth-bound (0.5625 B read + 2 B written per weight).
+ *   mcapq_bf16w_gemm: y[i][n] = sum_k W^[n][k] x[i][k], fp32 accumulation: tcgen05.mma
+ *     kind::f16 with the accumulator in TMEM, 128 weight rows x <= 256 tokens per CTA,
+ *     W^ and x by TMA; K % 64 == 0 (else MCAPQ_EUNSUP), ldx % 8 == 0.
+ *   mcapq_w4a16_bf16deq_prefill: both, W^ in ws (>= mcapq_prefill_workspace_bytes).
+ * Layouts/ownership as mcapq_w4a16; stream-ordered, graph-capturable, no allocation.
+ */
+size_t mcapq_prefill_workspace_bytes(int64_t n, int64_t k);
+mcapq_status mcapq_dequant_w4_bf16(const uint8_t *nib, const uint16_t *scale, int64_t n, int64_t k, uint16_t *w,
+                                   void *stream);
+mcapq_status mcapq_bf16w_gemm(const uint16_t *w, int64_t n, int64_t k, const uint16_t *x, int64_t m, int64_t ldx,
+                              void *y, int ydt, int64_t ldy, void *stream);
+mcapq_status mcapq_w4a16_bf16deq_prefill(const uint8_t *nib, const uint16_t *scale, int64_t n, int64_t k,
+                                         const uint16_t *x, int64_t m, int64_t ldx, void *y, int ydt, int64_t ldy,
+                                         void *ws, size_t ws_bytes, void *stream);
+
 /* Routed linear: route MCAPQ_W4A8 -> mcapq_w4a8_x, MCAPQ_W4A16 -> mcapq_w4a16. */
 mcapq_status mcapq_linear(int route, const uint8_t *nib, const uint16_t *scale, int64_t n, int64_t k,
                           const uint16_t *x, int64_t m, int64_t ldx, void *y, int ydt, int64_t ldy, void *ws,

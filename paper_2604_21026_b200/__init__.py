@@ -25,7 +25,7 @@ BF16, F32 = 0, 1
 
 __all__ = [
     "W4A8", "W4A16", "BF16", "F32", "McapqError", "load", "pack_w4", "quant_a8", "w4a8", "w4a8_x", "w4a16",
-    "w4a16_bf16deq",
+    "w4a16_bf16deq", "dequant_w4_bf16", "bf16w_gemm", "w4a16_bf16deq_prefill",
     "linear", "linear_group", "linear_host", "w4a8_group_dots", "workspace_bytes", "host_workspace_bytes", "Profile",
     "profile_parse", "profile_write_json", "mcap_accumulate", "Stack", "Comm", "linear_colshard", "PackedW4",
     "device_sms", "set_pdl",
@@ -168,6 +168,41 @@ def w4a16_bf16deq(w: PackedW4, x: torch.Tensor, out_dtype=torch.float32, out=Non
     y = _out(m, w.n, out_dtype, x.device, out)
     check(load().mcapq_w4a16_bf16deq(_ptr(w.nib), _ptr(w.scale), w.n, w.k, _ptr(x2), m, x2.stride(0), _ptr(y),
                                      _dt(y.dtype), y.stride(0), _stream(stream)), "mcapq_w4a16_bf16deq")
+    return y
+
+
+def dequant_w4_bf16(w: PackedW4, out=None, stream=None) -> torch.Tensor:
+    """NEXT-4: W^ = bf16_rne(d (c - 8)) as a bf16 [N, K] tensor (mcapq_dequant_w4_bf16)."""
+    _need_cuda(w.nib)
+    y = out if out is not None else torch.empty((w.n, w.k), dtype=torch.bfloat16, device=w.nib.device)
+    check(load().mcapq_dequant_w4_bf16(_ptr(w.nib), _ptr(w.scale), w.n, w.k, _ptr(y), _stream(stream)),
+          "mcapq_dequant_w4_bf16")
+    return y
+
+
+def bf16w_gemm(wdq: torch.Tensor, x: torch.Tensor, out_dtype=torch.float32, out=None, stream=None):
+    """NEXT-4: y = x W^T for a resident bf16 W^ [N, K] on tcgen05 (mcapq_bf16w_gemm)."""
+    _need_cuda(wdq, x)
+    x2 = x if x.dim() == 2 else x.view(1, -1)
+    m = x2.shape[0]
+    n, k = wdq.shape
+    y = _out(m, n, out_dtype, x.device, out)
+    check(load().mcapq_bf16w_gemm(_ptr(wdq), n, k, _ptr(x2), m, x2.stride(0), _ptr(y), _dt(y.dtype), y.stride(0),
+                                  _stream(stream)), "mcapq_bf16w_gemm")
+    return y
+
+
+def w4a16_bf16deq_prefill(w: PackedW4, x: torch.Tensor, out_dtype=torch.float32, out=None, ws=None, stream=None):
+    """NEXT-4: dequantise once into ws, then the tcgen05 GEMM (mcapq_w4a16_bf16deq_prefill)."""
+    _need_cuda(w.nib, x)
+    x2 = x if x.dim() == 2 else x.view(1, -1)
+    m = x2.shape[0]
+    y = _out(m, w.n, out_dtype, x.device, out)
+    if ws is None:
+        ws = torch.empty(load().mcapq_prefill_workspace_bytes(w.n, w.k), dtype=torch.uint8, device=x.device)
+    check(load().mcapq_w4a16_bf16deq_prefill(_ptr(w.nib), _ptr(w.scale), w.n, w.k, _ptr(x2), m, x2.stride(0),
+                                             _ptr(y), _dt(y.dtype), y.stride(0), _ptr(ws), ws.numel(),
+                                             _stream(stream)), "mcapq_w4a16_bf16deq_prefill")
     return y
 
 

@@ -35,6 +35,10 @@ SIGNATURES = {
     "mcapq_w4a8_x": (I32, [P, P, I64, I64, P, I64, I64, P, I32, I64, P, SZ, P]),
     "mcapq_w4a16": (I32, [P, P, I64, I64, P, I64, I64, P, I32, I64, P]),
     "mcapq_w4a16_bf16deq": (I32, [P, P, I64, I64, P, I64, I64, P, I32, I64, P]),
+    "mcapq_prefill_workspace_bytes": (SZ, [I64, I64]),
+    "mcapq_dequant_w4_bf16": (I32, [P, P, I64, I64, P, P]),
+    "mcapq_bf16w_gemm": (I32, [P, I64, I64, P, I64, I64, P, I32, I64, P]),
+    "mcapq_w4a16_bf16deq_prefill": (I32, [P, P, I64, I64, P, I64, I64, P, I32, I64, P, SZ, P]),
     "mcapq_linear": (I32, [I32, P, P, I64, I64, P, I64, I64, P, I32, I64, P, SZ, P]),
     "mcapq_linear_group": (I32, [I32, I32, P, P, P, I64, P, I64, I64, P, I32, P, P, SZ, P]),
     "mcapq_host_workspace_bytes": (SZ, [I32, I64, I64, I64]),

@@ -276,6 +276,54 @@ mcapq_status mcapq_w4a16_bf16deq(const uint8_t *nib, const uint16_t *scale, int6
     return MCAPQ_OK;
 }
 
+size_t mcapq_prefill_workspace_bytes(int64_t n, int64_t k) { return n > 0 && k > 0 ? (size_t)(2 * n * k) : 0; }
+
+mcapq_status mcapq_dequant_w4_bf16(const uint8_t *nib, const uint16_t *scale, int64_t n, int64_t k, uint16_t *w,
+                                   void *stream)
+{
+    clear_error();
+    CHECK_SHAPE(n, k, 1);
+    mcapq_status st = check_weight(nib, scale, n, k);
+    if (st != MCAPQ_OK) return st;
+    CHECK_PTR(w, "w");
+    CHECK_AL16(w, "w");
+    CHECK_AL16(nib, "nib");
+    LAUNCH_TRY(launch_dequant_w4_bf16(nib, scale, n, k, w, as_stream(stream)));
+    return MCAPQ_OK;
+}
+
+mcapq_status mcapq_bf16w_gemm(const uint16_t *w, int64_t n, int64_t k, const uint16_t *x, int64_t m, int64_t ldx,
+                              void *y, int ydt, int64_t ldy, void *stream)
+{
+    clear_error();
+    CHECK_SHAPE(n, k, m);
+    CHECK_PTR(w, "w");
+    CHECK_PTR(x, "x");
+    CHECK_PTR(y, "y");
+    CHECK_AL16(w, "w");
+    CHECK_AL16(x, "x");
+    CHECK_AL16(y, "y");
+    CHECK_YDT(ydt);
+    CHECK_LD(ldx, k, "ldx");
+    CHECK_LD(ldy, n, "ldy");
+    MCAPQ_REQUIRE(k % 64 == 0, MCAPQ_EUNSUP, "bf16w_gemm needs K %% 64 == 0 (K = %lld)", (long long)k);
+    MCAPQ_REQUIRE(ldx % 8 == 0, MCAPQ_EINVAL, "ldx %% 8 != 0");
+    LAUNCH_TRY(launch_prefill(w, n, k, x, ldx, m, y, ydt, ldy, as_stream(stream), api_pdl()));
+    return MCAPQ_OK;
+}
+
+mcapq_status mcapq_w4a16_bf16deq_prefill(const uint8_t *nib, const uint16_t *scale, int64_t n, int64_t k,
+                                         const uint16_t *x, int64_t m, int64_t ldx, void *y, int ydt, int64_t ldy,
+                                         void *ws, size_t ws_bytes, void *stream)
+{
+    clear_error();
+    MCAPQ_REQUIRE(ws && ws_bytes >= mcapq_prefill_workspace_bytes(n, k), MCAPQ_ENOSPACE,
+                  "prefill workspace %zu < %zu bytes", ws_bytes, mcapq_prefill_workspace_bytes(n, k));
+    mcapq_status st = mcapq_dequant_w4_bf16(nib, scale, n, k, reinterpret_cast<uint16_t *>(ws), stream);
+    if (st != MCAPQ_OK) return st;
+    return mcapq_bf16w_gemm(reinterpret_cast<const uint16_t *>(ws), n, k, x, m, ldx, y, ydt, ldy, stream);
+}
+
 mcapq_status mcapq_linear(int route, const uint8_t *nib, const uint16_t *scale, int64_t n, int64_t k,
                           const uint16_t *x, int64_t m, int64_t ldx, void *y, int ydt, int64_t ldy, void *ws,
                           size_t ws_bytes, void *stream)

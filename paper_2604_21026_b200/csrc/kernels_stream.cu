@@ -698,6 +698,74 @@ cudaError_t launch_tc05(const uint8_t *nib, const uint16_t *scale, int64_t n, in
     return cudaSuccess;
 }
 
+// ------------------------------------------------------------------ NEXT-4 prefill
+cudaError_t launch_dequant_w4_bf16(const uint8_t *nib, const uint16_t *scale, int64_t n, int64_t k, uint16_t *w,
+                                   cudaStream_t s)
+{
+    const int64_t nb = n * (k / 32);
+    dequant_w4_bf16_kernel<<<(unsigned)((nb + 255) / 256), 256, 0, s>>>(nib, scale, nb, w);
+    return cudaGetLastError();
+}
+
+namespace {
+bool encode_bf16_rows(CUtensorMap *m, const void *base, int64_t rows, int64_t k, int64_t ld, int box_rows)
+{
+    EncodeTiledFn fn = encode_fn();
+    if (!fn) return false;
+    const cuuint64_t d[2] = {(cuuint64_t)k, (cuuint64_t)rows};
+    const cuuint64_t st[1] = {(cuuint64_t)ld * 2};
+    const cuuint32_t box[2] = {64, (cuuint32_t)box_rows};
+    const cuuint32_t es[2] = {1, 1};
+    return fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void *>(base), d, st, box, es,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+template <int MP>
+cudaError_t launch_prefill_mp(PrefillArgs &a, size_t smem, int grid, cudaStream_t s, bool pdl)
+{
+    static int attr_done = 0;
+    if (!attr_done) {
+        cudaError_t e = cudaFuncSetAttribute(tc05_prefill<MP>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+        if (e != cudaSuccess) return e;
+        attr_done = 1;
+    }
+    return launch_pdl(tc05_prefill<MP>, dim3(grid), dim3(192), smem, s, pdl, a);
+}
+}  // namespace
+
+// y = X . W^T for a bf16 W^ [n][k] (k % 64 == 0), ONE launch: work units = (token pass of
+// MP = 64 / 128 / 256 tokens, 128-row tile) pairs spread over the persistent CTAs.
+cudaError_t launch_prefill(const uint16_t *w, int64_t n, int64_t k, const uint16_t *x, int64_t ldx, int64_t m, void *y,
+                           int ydt, int64_t ldy, cudaStream_t s, bool pdl)
+{
+    const int sms = device_sms();
+    const int mp = m <= 64 ? 64 : (m <= 128 ? 128 : 256);
+    PrefillArgs a;
+    memset(&a, 0, sizeof(a));
+    if (!encode_bf16_rows(&a.amap, w, n, k, k, 128) || !encode_bf16_rows(&a.xmap, x, m, k, ldx, mp))
+        return cudaErrorInvalidValue;
+    a.y = y;
+    a.ldy = ldy;
+    a.n = n;
+    a.k = k;
+    a.ydt = ydt;
+    a.m = m;
+    a.passes = (int)((m + mp - 1) / mp);
+    a.row_tiles = (int)((n + 127) / 128);
+    if ((int64_t)a.row_tiles * a.passes > (1 << 20)) return cudaErrorInvalidValue;   // 32-bit unit partition
+    a.stage_bytes = 128u * 128u + (uint32_t)mp * 128u;
+    const size_t fixed = 1024 + 256;
+    int S = (int)((227 * 1024 - fixed) / a.stage_bytes);
+    S = S > 8 ? 8 : S;
+    if (S < 2) return cudaErrorInvalidValue;
+    a.stages = S;
+    const size_t smem = fixed + (size_t)S * a.stage_bytes;
+    const int units = a.row_tiles * a.passes;
+    const int grid = units < sms ? units : sms;
+    return mp == 64 ? launch_prefill_mp<64>(a, smem, grid, s, pdl)
+                    : (mp == 128 ? launch_prefill_mp<128>(a, smem, grid, s, pdl) : launch_prefill_mp<256>(a, smem, grid, s, pdl));
+}
+
 cudaError_t launch_gemm(int route, const uint8_t *nib, const uint16_t *scale, int64_t n, int64_t k, const uint16_t *x,
                         int64_t ldx, const int8_t *q, const float *sx, const int32_t *sq, int64_t m, void *y, int ydt,
                         int64_t ldy, cudaStream_t s, bool pdl)

@@ -91,6 +91,10 @@ constexpr int64_t kGemmMinTokens = 9;
 bool gemm_supported(int64_t k);
 cudaError_t launch_tc05(const uint8_t *nib, const uint16_t *scale, int64_t n, int64_t k, const uint16_t *x,
                         int64_t ldx, int64_t m, void *y, int ydt, int64_t ldy, cudaStream_t s, bool pdl);
+cudaError_t launch_dequant_w4_bf16(const uint8_t *nib, const uint16_t *scale, int64_t n, int64_t k, uint16_t *w,
+                                   cudaStream_t s);
+cudaError_t launch_prefill(const uint16_t *w, int64_t n, int64_t k, const uint16_t *x, int64_t ldx, int64_t m, void *y,
+                           int ydt, int64_t ldy, cudaStream_t s, bool pdl);
 cudaError_t launch_gemm(int route, const uint8_t *nib, const uint16_t *scale, int64_t n, int64_t k, const uint16_t *x,
                         int64_t ldx, const int8_t *q, const float *sx, const int32_t *sq, int64_t m, void *y, int ydt,
                         int64_t ldy, cudaStream_t s, bool pdl);

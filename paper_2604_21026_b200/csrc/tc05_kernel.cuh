@@ -100,15 +100,17 @@ __device__ __forceinline__ uint32_t dq_pair(uint32_t m, uint32_t hi2, uint32_t l
 }
 // 4 nibble bytes of a block (bytes t..t+3) -> W^ of elements t..t+3 (low nibbles: lo01,
 // lo23) and t+16..t+19 (high nibbles: hi01, hi23) as bf16 pairs.
+// sgn2: 0, or 0x80008000 with hi2s / lo2s split from |d| (mcapq_dequant_w4_bf16: exact IEEE
+// signs of zero, bf16_rne(d (c - 8)) = sign(d) bf16_rne(|d| (c - 8)); the GEMM paths pass 0).
 __device__ __forceinline__ void dq4(uint32_t w, uint32_t hi2s, uint32_t lo2s, uint32_t &lo01, uint32_t &lo23,
-                                    uint32_t &hi01, uint32_t &hi23)
+                                    uint32_t &hi01, uint32_t &hi23, uint32_t sgn2 = 0u)
 {
     const uint32_t l = w & 0x0F0F0F0Fu, h = (w >> 4) & 0x0F0F0F0Fu;
     // byte_perm with 0x43 as the second source's byte 0: {c_a, 0x43, c_b, 0x43} = bf16 (128 + c_a, 128 + c_b)
-    lo01 = dq_pair(__byte_perm(l, 0x43u, 0x4140), hi2s, lo2s);
-    lo23 = dq_pair(__byte_perm(l, 0x43u, 0x4342), hi2s, lo2s);
-    hi01 = dq_pair(__byte_perm(h, 0x43u, 0x4140), hi2s, lo2s);
-    hi23 = dq_pair(__byte_perm(h, 0x43u, 0x4342), hi2s, lo2s);
+    lo01 = dq_pair(__byte_perm(l, 0x43u, 0x4140), hi2s, lo2s) ^ sgn2;
+    lo23 = dq_pair(__byte_perm(l, 0x43u, 0x4342), hi2s, lo2s) ^ sgn2;
+    hi01 = dq_pair(__byte_perm(h, 0x43u, 0x4140), hi2s, lo2s) ^ sgn2;
+    hi23 = dq_pair(__byte_perm(h, 0x43u, 0x4342), hi2s, lo2s) ^ sgn2;
 }
 }  // namespace tc05
 
@@ -316,6 +318,183 @@ __global__ void __launch_bounds__(tc05::kThreads, 1) tc05_w4a16(const __grid_con
 #pragma unroll
                 for (int t = 0; t < MP; ++t)
                     if (t < a.ntok) dev::store_out(a.y, a.ydt, (a.tok0 + t) * a.ldy + row, D[t]);
+            }
+        }
+    }
+    fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tbase), "r"(kCols) : "memory");
+    }
+}
+
+// ============================================================================ NEXT-4: prefill
+// W^ materialised once (mcapq_dequant_w4_bf16: bf16_rne(d (c - 8)) in [N][K], the same
+// exact split-scale arithmetic as the batched kernel's dequantiser), then a plain bf16
+// GEMM on tcgen05 -- the paper's prefill path ("materializes F16 for cuBLAS").
+
+// one thread per Q4_0 block: 16 nibble bytes -> 32 bf16 of W^ (64 B of output)
+__global__ void __launch_bounds__(256) dequant_w4_bf16_kernel(const uint8_t *__restrict__ nib,
+                                                              const uint16_t *__restrict__ scale, int64_t nblocks,
+                                                              uint16_t *__restrict__ w)
+{
+    const int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= nblocks) return;
+    const uint4 q = *reinterpret_cast<const uint4 *>(nib + 16 * b);
+    uint32_t dh, dl;
+    const uint16_t d16 = scale[b];
+    tc05::split_scale(h2f((uint16_t)(d16 & 0x7fffu)), dh, dl);   // |d|; the sign goes on last (exact zeros)
+    const uint32_t sg = (d16 & 0x8000u) ? 0x80008000u : 0u;
+    uint32_t lo[8], hi[8];
+    tc05::dq4(q.x, dh, dl, lo[0], lo[1], hi[0], hi[1], sg);
+    tc05::dq4(q.y, dh, dl, lo[2], lo[3], hi[2], hi[3], sg);
+    tc05::dq4(q.z, dh, dl, lo[4], lo[5], hi[4], hi[5], sg);
+    tc05::dq4(q.w, dh, dl, lo[6], lo[7], hi[6], hi[7], sg);
+    uint4 *o = reinterpret_cast<uint4 *>(w + 32 * b);   // elements 32 g .. 32 g + 31 of the row
+    o[0] = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+    o[1] = make_uint4(lo[4], lo[5], lo[6], lo[7]);
+    o[2] = make_uint4(hi[0], hi[1], hi[2], hi[3]);
+    o[3] = make_uint4(hi[4], hi[5], hi[6], hi[7]);
+}
+
+struct PrefillArgs {
+    alignas(64) CUtensorMap amap;   // W^ [N][K] bf16, box {64, 128 rows}, 128B swizzle
+    alignas(64) CUtensorMap xmap;   // X [M][K] bf16, box {64, MP rows}, 128B swizzle (rows past M: 0)
+    void *y;
+    int64_t ldy, n, k;
+    int ydt;
+    int64_t m;             // tokens; work unit u = (token pass u / row_tiles, row tile u % row_tiles)
+    int passes;            // ceil(m / MP)
+    int row_tiles, stages;
+    uint32_t stage_bytes;
+};
+
+// D[128 rows][MP tokens] = sum over K of W^ . X^T: warp 0 TMA (A box + X box per 64-K
+// block), warp 1 TMEM + MMA (4 x K16 per block), warps 2-5 epilogue (lane quarter = warp % 4).
+template <int MP>
+__global__ void __launch_bounds__(192, 1) tc05_prefill(const __grid_constant__ PrefillArgs a)
+{
+    using namespace tc05;
+    extern __shared__ __align__(16) uint8_t smem_raw[];
+    const uint32_t sb = (smem_addr(smem_raw) + 1023u) & ~1023u;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int S = a.stages;
+    const int KB = (int)(a.k / 64);
+    const uint32_t ring = sb;
+    const uint32_t bars = sb + (uint32_t)S * a.stage_bytes;
+    const uint32_t sfull = bars, sempty = bars + 8u * S;
+    const uint32_t dfull = sempty + 8u * S, dempty = dfull + 16u;
+    const uint32_t tslot = dempty + 16u;
+    constexpr uint32_t kCols = 2 * MP < 32 ? 32 : 2 * MP;
+    constexpr uint32_t kABytes = 128u * 128u;
+    const int T = a.row_tiles * a.passes;   // work units: every (token pass, row tile) pair
+    const int t0 = (int)(((uint32_t)T * blockIdx.x) / gridDim.x);
+    const int t1 = (int)(((uint32_t)T * (blockIdx.x + 1)) / gridDim.x);
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < S; ++s) {
+            mbar_init(sfull + 8u * s, 1);
+            mbar_init(sempty + 8u * s, 1);
+        }
+        for (int s = 0; s < 2; ++s) {
+            mbar_init(dfull + 8u * s, 1);
+            mbar_init(dempty + 8u * s, 4);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(tslot), "r"(kCols)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    dev::griddep_launch();
+    fence_before();
+    __syncthreads();
+    fence_after();
+    const uint32_t tbase = lds32(tslot);
+    dev::griddep_wait();
+
+    if (warp == 0) {
+        if (lane == 0) {
+            int s = 0;
+            uint32_t ph = 0;
+            const uint32_t tx = kABytes + (uint32_t)MP * 128u;
+            for (int u = t0; u < t1; ++u) {
+                const int rt = u % a.row_tiles, pass = u / a.row_tiles;
+                for (int kb = 0; kb < KB; ++kb) {
+                    mbar_wait(sempty + 8u * s, ph ^ 1u);
+                    const uint32_t st = ring + (uint32_t)s * a.stage_bytes;
+                    mbar_expect_tx(sfull + 8u * s, tx);
+                    tma_2d(st, &a.amap, kb * 64, rt * 128, sfull + 8u * s, 0);
+                    tma_2d(st + kABytes, &a.xmap, kb * 64, pass * MP, sfull + 8u * s, 0);
+                    if (++s == S) {
+                        s = 0;
+                        ph ^= 1u;
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            constexpr uint32_t id = idesc<MP>();
+            int s = 0, bf = 0;
+            uint32_t ph = 0, phb = 0;
+            for (int u = t0; u < t1; ++u) {
+                mbar_wait(dempty + 8u * bf, phb ^ 1u);
+                fence_after();
+                const uint32_t d = tbase + (uint32_t)bf * MP;
+                for (int kb = 0; kb < KB; ++kb) {
+                    mbar_wait(sfull + 8u * s, ph);
+                    fence_after();
+                    const uint32_t st = ring + (uint32_t)s * a.stage_bytes;
+#pragma unroll
+                    for (int kk = 0; kk < 4; ++kk)
+                        mma_bf16(d, smem_desc(st + 32u * kk), smem_desc(st + kABytes + 32u * kk), id,
+                                 (kb | kk) != 0 ? 1u : 0u);
+                    commit(sempty + 8u * s);
+                    if (++s == S) {
+                        s = 0;
+                        ph ^= 1u;
+                    }
+                }
+                commit(dfull + 8u * bf);
+                if (++bf == 2) {
+                    bf = 0;
+                    phb ^= 1u;
+                }
+            }
+        }
+    } else {
+        const int quarter = warp & 3;
+        const int r = quarter * 32 + lane;
+        const uint32_t tl = tbase + ((uint32_t)(quarter * 32) << 16);
+        int bf = 0;
+        uint32_t phb = 0;
+        for (int u = t0; u < t1; ++u) {
+            const int rt = u % a.row_tiles, pass = u / a.row_tiles;
+            const int64_t tok0 = (int64_t)pass * MP;
+            mbar_wait(dfull + 8u * bf, phb);
+            fence_after();
+            const int64_t row = (int64_t)rt * 128 + r;
+#pragma unroll 1
+            for (int c = 0; c < MP; c += 16) {
+                if (tok0 + c >= a.m) break;   // warp-uniform
+                float D[16];
+                tmem_ld16(tl + (uint32_t)bf * MP + (uint32_t)c, D);
+                tmem_wait_ld();
+                if (row < a.n) {
+#pragma unroll
+                    for (int j = 0; j < 16; ++j)
+                        if (tok0 + c + j < a.m) dev::store_out(a.y, a.ydt, (tok0 + c + j) * a.ldy + row, D[j]);
+                }
+            }
+            fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(dempty + 8u * bf);
+            if (++bf == 2) {
+                bf = 0;
+                phb ^= 1u;
             }
         }
     }

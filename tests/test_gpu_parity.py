@@ -287,6 +287,50 @@ def test_bf16deq_rejects_k_not_multiple_of_256(mq):
         mq.w4a16_bf16deq(pw, si.activation(16, 288, 1492).to(DEV))
 
 
+# ---------------------------------------------------------------- NEXT-4 prefill (dequantise once + tcgen05 GEMM)
+@pytest.mark.parametrize("n,k", [(200, 256), (37, 4096), (1000, 2048)])
+def test_dequant_w4_bf16_bit_exact(mq, orc, n, k):
+    """W^ = bf16_rne(f32(d) (c - 8)) bit-for-bit: the oracle's exact dequantisation
+    (oracle_dequant_w4) rounded by the oracle's RNE fp32 -> bf16."""
+    w = si.weight(n, k, 1521 + n)
+    pw, nib, sc = _pack_both(mq, orc, w)
+    got = mq.dequant_w4_bf16(pw).cpu().view(torch.int16).numpy().view(np.uint16)
+    ref = orc.f32_to_bf16_bits(orc.dequant_w4(nib, sc))
+    assert np.array_equal(got, ref)
+
+
+@pytest.mark.parametrize("n,k", [(200, 256), (1000, 2048), (4000, 512)])
+@pytest.mark.parametrize("m", [64, 100, 256, 300])
+def test_prefill_vs_oracle(mq, orc, m, n, k):
+    """Dequantise once + tcgen05 GEMM vs oracle_w4a16_bf16deq: token passes of 64/128/256
+    (300 = 256 + 44), ragged 128-row tiles; reading T."""
+    w = si.weight(n, k, 1531 + n + k)
+    x = si.activation(m, k, 1532 + m + k)
+    pw, nib, sc = _pack_both(mq, orc, w)
+    y = mq.w4a16_bf16deq_prefill(pw, x.to(DEV), out_dtype=torch.float32)
+    _, y64 = orc.w4a16_bf16deq(nib, sc, _f32(x))
+    _assert_close(y, y64, 1e-3)
+
+
+def test_bf16w_gemm_strides_bf16_out_rows_beyond_n(mq, orc):
+    n, k, m = 40, 1024, 70
+    w = si.weight(n, k, 1541)
+    xs = si.activation(m, k + 64, 1542)
+    pw, nib, sc = _pack_both(mq, orc, w)
+    wdq = mq.dequant_w4_bf16(pw)
+    yd = torch.full((m, n + 24), 7.0, dtype=torch.bfloat16, device=DEV)
+    mq.bf16w_gemm(wdq, xs.to(DEV)[:, :k], out=yd[:, :n])
+    _, y64 = orc.w4a16_bf16deq(nib, sc, _f32(xs[:, :k].contiguous()))
+    _assert_close(yd[:, :n], y64, 2e-3)
+    assert torch.all(yd[:, n:] == 7.0)
+
+
+def test_bf16w_gemm_rejects_k_not_multiple_of_64(mq):
+    pw = mq.pack_w4(si.weight(64, 288, 1551).to(DEV))
+    with pytest.raises(mq.McapqError):
+        mq.w4a16_bf16deq_prefill(pw, si.activation(64, 288, 1552).to(DEV))
+
+
 def test_zero_activation_and_impulse_rows(mq, orc):
     # S:315 / S:324-325 special cases through the GPU path
     k = 256
