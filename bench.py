@@ -411,6 +411,47 @@ def time_single_linears(mq, dev, stream):
     return out
 
 
+def time_prefill(mq, dev, stream):
+    """NEXT-4 rows: the 8B gate (14336 x 4096) and down at prefill sizes -- dequantise once
+    (mcapq_dequant_w4_bf16) + the tcgen05 bf16 GEMM (mcapq_bf16w_gemm), CUDA-graph timed;
+    useful bf16 FLOP/s against MEASURED_PEAKS.json bf16_tflops."""
+    out = []
+    for slot, m in (("gate", 1024), ("gate", 4096), ("down", 1024)):
+        n, k = si.linear_shape("llama-3.1-8b", slot)
+        pw = mq.pack_w4(si.weight(n, k, si.seed_for(4, 0, slot)).to(dev))
+        x = si.activation(m, k, si.seed_for(4, 0, slot, True), si.activation_kind(slot)).to(dev)
+        y = torch.empty(m, n, dtype=torch.bfloat16, device=dev)
+        wdq = mq.dequant_w4_bf16(pw)
+        res = {}
+        with torch.cuda.stream(stream):
+            for name, fn in (("dequant", lambda: mq.dequant_w4_bf16(pw, out=wdq, stream=stream)),
+                             ("gemm", lambda: mq.bf16w_gemm(wdq, x, out=y, stream=stream))):
+                fn()
+                stream.synchronize()
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g, stream=stream):
+                    for _ in range(10):
+                        fn()
+                g.replay()
+                stream.synchronize()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                for _ in range(3):
+                    g.replay()
+                e1.record(stream)
+                e1.synchronize()
+                res[name] = e0.elapsed_time(e1) * 1000 / 30
+        fl = 2.0 * m * n * k
+        out.append({"model": "llama-3.1-8b", "slot": slot, "N": n, "K": k, "M": m,
+                    "dequant_us": round(res["dequant"], 2), "gemm_us": round(res["gemm"], 2),
+                    "gemm_tflops": round(fl / res["gemm"] / 1e6, 1),
+                    "gemm_tensor_frac": round(fl / res["gemm"] / 1e6 / bf16_peak_tflops(), 4),
+                    "prefill_tflops": round(fl / (res["gemm"] + res["dequant"]) / 1e6, 1)})
+        del pw, x, y, wdq
+        torch.cuda.empty_cache()
+    return out
+
+
 # ---------------------------------------------------------------- CPU oracle
 def oracle_prepare(layers=(0, 15)):
     """Pack (outside any timing) the sample layers of the stack for the oracle:
@@ -594,6 +635,7 @@ def main():
 
     extras = [] if args.no_extras or rank != 0 else time_single_linears(mq, dev, stream)
     mlp8b = None if args.no_extras or rank != 0 else time_mlp8b_stack(mq, dev, stream)
+    prefill = None if args.no_extras or rank != 0 else time_prefill(mq, dev, stream)
     colshard = None
     if world > 1 and not args.no_extras:
         try:
@@ -645,6 +687,7 @@ def main():
             "clocks": clk.report(),
             "single_linears": extras,
             "mlp_8b_stack": mlp8b,
+            "prefill_8b": prefill,
             "lm_head_colshard": colshard,
         }
         if cpu is not None:
