@@ -341,7 +341,7 @@ __global__ void __launch_bounds__(256) dequant_w4_bf16_kernel(const uint8_t *__r
 {
     const int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (b >= nblocks) return;
-    const uint4 q = *reinterpret_cast<const uint4 *>(nib + 16 * b);
+    const uint4 q = __ldcs(reinterpret_cast<const uint4 *>(nib + 16 * b));
     uint32_t dh, dl;
     const uint16_t d16 = scale[b];
     tc05::split_scale(h2f((uint16_t)(d16 & 0x7fffu)), dh, dl);   // |d|; the sign goes on last (exact zeros)
@@ -352,10 +352,11 @@ __global__ void __launch_bounds__(256) dequant_w4_bf16_kernel(const uint8_t *__r
     tc05::dq4(q.z, dh, dl, lo[4], lo[5], hi[4], hi[5], sg);
     tc05::dq4(q.w, dh, dl, lo[6], lo[7], hi[6], hi[7], sg);
     uint4 *o = reinterpret_cast<uint4 *>(w + 32 * b);   // elements 32 g .. 32 g + 31 of the row
-    o[0] = make_uint4(lo[0], lo[1], lo[2], lo[3]);
-    o[1] = make_uint4(lo[4], lo[5], lo[6], lo[7]);
-    o[2] = make_uint4(hi[0], hi[1], hi[2], hi[3]);
-    o[3] = make_uint4(hi[4], hi[5], hi[6], hi[7]);
+    // streaming stores (evict-first): W^ is written once and read back by the GEMM's TMA
+    __stcs(o + 0, make_uint4(lo[0], lo[1], lo[2], lo[3]));
+    __stcs(o + 1, make_uint4(lo[4], lo[5], lo[6], lo[7]));
+    __stcs(o + 2, make_uint4(hi[0], hi[1], hi[2], hi[3]));
+    __stcs(o + 3, make_uint4(hi[4], hi[5], hi[6], hi[7]));
 }
 
 struct PrefillArgs {
