@@ -325,6 +325,38 @@ def test_bf16w_gemm_strides_bf16_out_rows_beyond_n(mq, orc):
     assert torch.all(yd[:, n:] == 7.0)
 
 
+def test_prefill_and_bf16deq_graph_capture_and_pdl(mq):
+    """Both tcgen05 paths are stream-ordered and capturable: a CUDA graph of
+    prefill + batched bf16-dequant calls (with programmatic dependent launch on) replays
+    to the same bits as eager launches."""
+    n, k, m = 1000, 2048, 96
+    pw = mq.pack_w4(si.weight(n, k, 1561).to(DEV))
+    x = si.activation(m, k, 1562).to(DEV)
+    ref_p = mq.w4a16_bf16deq_prefill(pw, x)
+    ref_b = mq.w4a16_bf16deq(pw, x)
+    yp = torch.empty_like(ref_p)
+    yb = torch.empty_like(ref_b)
+    ws = torch.empty(mq.load().mcapq_prefill_workspace_bytes(n, k), dtype=torch.uint8, device=DEV)
+    prev = mq.set_pdl(True)
+    try:
+        s = torch.cuda.Stream()
+        with torch.cuda.stream(s):
+            mq.w4a16_bf16deq_prefill(pw, x, out=yp, ws=ws, stream=s)
+            mq.w4a16_bf16deq(pw, x, out=yb, stream=s)
+            s.synchronize()
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=s):
+                mq.w4a16_bf16deq_prefill(pw, x, out=yp, ws=ws, stream=s)
+                mq.w4a16_bf16deq(pw, x, out=yb, stream=s)
+            yp.zero_()
+            yb.zero_()
+            g.replay()
+            s.synchronize()
+    finally:
+        mq.set_pdl(prev)
+    assert torch.equal(yp, ref_p) and torch.equal(yb, ref_b)
+
+
 def test_bf16w_gemm_rejects_k_not_multiple_of_64(mq):
     pw = mq.pack_w4(si.weight(64, 288, 1551).to(DEV))
     with pytest.raises(mq.McapqError):
