@@ -252,6 +252,20 @@ mcapq_status mcapq_w4a8_group_dots(const uint8_t *nib, int64_t n, int64_t k, con
                                    int64_t m, int32_t *D, int mode, void *stream);
 
 /*
+ * TEST ENTRY: the persistent TMA stream kernel's W4A8 engine (the batch-1 DP4A path of
+ * mcapq_linear, K % 256 == 0, K >= 2048) with its outputs replaced by its integer
+ * stages: the fused in-kernel quantiser's codes for the one token x [k] bf16 (q [k]
+ * int8, sx [k/32] fp32, sq [k/32] int32 -- a2's definition) and every
+ * block's exact D [n][k/32] int32 = sum_j c q - 8 sq, computed by the
+ * production staging and block_D code.  ws: >= mcapq_debug_stream_dump_workspace_bytes(k)
+ * device bytes.  MCAPQ_EUNSUP off the stream path.
+ */
+size_t mcapq_debug_stream_dump_workspace_bytes(int64_t k);
+mcapq_status mcapq_debug_stream_w4a8_dump(const uint8_t *nib, const uint16_t *scale, int64_t n, int64_t k,
+                                          const uint16_t *x, int8_t *q, float *sx, int32_t *sq, int32_t *D,
+                                          void *ws, size_t ws_bytes, void *stream);
+
+/*
  * DEBUG: per-CTA timeline of the stream kernels, recorded only when the
  * environment has MCAPQ_STREAM_TRACE=1 at library load.  Copies up to
  * max_records records of 8 uint64 into host memory (%globaltimer ns) and
@@ -377,6 +391,15 @@ void mcapq_stack_destroy(mcapq_stack *st);
  * process group); mcapq_comm_init: collective over the `world` ranks, binds the
  * communicator to the current CUDA device.  Not graph-capturable: init/destroy.
  * ws: >= mcapq_colshard_workspace_bytes(route, m, n_full, k, world).
+ * Data path: M == 1 -- the local rows are written straight into y_full + r N/P and
+ * the all-gather runs in place; M > 1 -- they go to slot r of a rank-major
+ * [P][M][N/P] workspace, the all-gather fills it in place, and
+ * mcapq_colshard_assemble writes y_full.
+ *
+ * mcapq_colshard_assemble: y_full[i][r N/P + j] = rank_major[r][i][j] for a rank-major
+ * [world][m][n_full/world] buffer of ydt elements (device, caller-owned, no overlap).
+ * The M > 1 assembly step of mcapq_linear_colshard; also a test entry (P shards
+ * computed by mcapq_linear on one GPU, assembled, compared with the unsharded call).
  */
 typedef struct mcapq_comm mcapq_comm;
 mcapq_status mcapq_comm_unique_id(uint8_t *id_host_128);
@@ -387,6 +410,8 @@ size_t mcapq_colshard_workspace_bytes(int route, int64_t m, int64_t n_full, int6
 mcapq_status mcapq_linear_colshard(const mcapq_comm *c, int route, const uint8_t *nib_shard,
                                    const uint16_t *scale_shard, int64_t n_full, int64_t k, const uint16_t *x,
                                    int64_t m, void *y_full, int ydt, void *ws, size_t ws_bytes, void *stream);
+mcapq_status mcapq_colshard_assemble(const void *rank_major, void *y_full, int64_t m, int64_t n_full, int world,
+                                     int ydt, void *stream);
 void mcapq_comm_destroy(mcapq_comm *c);
 
 #ifdef __cplusplus

@@ -28,6 +28,7 @@ __all__ = [
     "w4a16_bf16deq", "dequant_w4_bf16", "bf16w_gemm", "w4a16_bf16deq_prefill",
     "linear", "linear_group", "linear_host", "w4a8_group_dots", "workspace_bytes", "host_workspace_bytes", "Profile",
     "profile_parse", "profile_write_json", "mcap_accumulate", "Stack", "Comm", "linear_colshard", "PackedW4",
+    "colshard_assemble", "stream_w4a8_dump",
     "device_sms", "set_pdl",
 ]
 
@@ -53,6 +54,27 @@ def _need_cuda(*ts):
     for t in ts:
         if t is not None and not t.is_cuda:
             raise McapqError(1, "binding", "tensor is not on a CUDA device (no CPU path exists)")
+
+
+def _act(x: torch.Tensor, k: int, what: str = "x") -> torch.Tensor:
+    """Activations as a [M, K] bf16 row-major view (the C ABI reads raw bf16 bits)."""
+    _need_cuda(x)
+    if x.dtype != torch.bfloat16:
+        raise McapqError(2, "binding", f"{what} must be bfloat16, got {x.dtype}")
+    x2 = x if x.dim() == 2 else x.view(1, -1)
+    if x2.dim() != 2 or x2.shape[1] != k or x2.stride(1) != 1:
+        raise McapqError(1, "binding", f"{what} must be a row-major [M, {k}] tensor, got shape "
+                                       f"{tuple(x.shape)} strides {tuple(x.stride())}")
+    return x2
+
+
+def _scratch(nbytes: int, device, stream=None) -> torch.Tensor:
+    """Library workspace allocated on the stream the call runs on, so the caching
+    allocator cannot hand it to other work before that stream's kernels finish."""
+    if stream is None:
+        return torch.empty(max(int(nbytes), 256), dtype=torch.uint8, device=device)
+    with torch.cuda.stream(stream):
+        return torch.empty(max(int(nbytes), 256), dtype=torch.uint8, device=device)
 
 
 def device_sms() -> int:
@@ -92,8 +114,7 @@ def pack_w4(w: torch.Tensor, dev_err: torch.Tensor | None = None, stream=None) -
 def quant_a8(x: torch.Tensor, stream=None, out=None):
     """a2: x [M, K] bf16 -> (q int8 [M, K], sx fp32 [M, K/32], sq int32 [M, K/32]);
     out: optional preallocated (q, sx, sq)."""
-    _need_cuda(x)
-    x2 = x if x.dim() == 2 else x.view(1, -1)
+    x2 = _act(x, x.shape[-1])
     m, k = x2.shape
     if out is not None:
         q, sx, sq = out
@@ -113,9 +134,13 @@ def _out(m, n, dtype, device, out):
 
 
 def w4a8(w: PackedW4, q, sx, sq, out_dtype=torch.float32, out=None, stream=None):
-    """a3/a5 on pre-quantised activations."""
-    _need_cuda(w.nib, q)
+    """a3/a5 on pre-quantised activations (q int8 [M, K], sx fp32 / sq int32 [M, K/32])."""
+    _need_cuda(w.nib, q, sx, sq)
     m = q.shape[0]
+    for t, dt, cols, name in ((q, torch.int8, w.k, "q"), (sx, torch.float32, w.k // 32, "sx"),
+                              (sq, torch.int32, w.k // 32, "sq")):
+        if t.dtype != dt or tuple(t.shape) != (m, cols) or not t.is_contiguous():
+            raise McapqError(1, "binding", f"{name} must be a contiguous {dt} [{m}, {cols}] tensor")
     y = _out(m, w.n, out_dtype, q.device, out)
     check(load().mcapq_w4a8(_ptr(w.nib), _ptr(w.scale), w.n, w.k, _ptr(q), _ptr(sx), _ptr(sq), m, _ptr(y),
                             _dt(y.dtype), y.stride(0), _stream(stream)), "mcapq_w4a8")
@@ -130,20 +155,19 @@ def host_workspace_bytes(route: int, m: int, n: int, k: int) -> int:
     return load().mcapq_host_workspace_bytes(route, m, n, k)
 
 
-def _ws(route, m, n, k, device, ws):
-    need = workspace_bytes(route, m, n, k)
+def _ws(route, m, n, k, device, ws, stream=None):
     if ws is not None:
         return ws
-    return torch.empty(max(need, 256), dtype=torch.uint8, device=device)
+    return _scratch(workspace_bytes(route, m, n, k), device, stream)
 
 
 def w4a8_x(w: PackedW4, x: torch.Tensor, out_dtype=torch.float32, out=None, ws=None, stream=None):
     """a2+a3/a5: quantise x then W4A8 (two PDL-chained launches)."""
-    _need_cuda(w.nib, x)
-    x2 = x if x.dim() == 2 else x.view(1, -1)
+    _need_cuda(w.nib)
+    x2 = _act(x, w.k)
     m = x2.shape[0]
     y = _out(m, w.n, out_dtype, x.device, out)
-    ws = _ws(W4A8, m, w.n, w.k, x.device, ws)
+    ws = _ws(W4A8, m, w.n, w.k, x.device, ws, stream)
     check(load().mcapq_w4a8_x(_ptr(w.nib), _ptr(w.scale), w.n, w.k, _ptr(x2), m, x2.stride(0), _ptr(y),
                               _dt(y.dtype), y.stride(0), _ptr(ws), ws.numel(), _stream(stream)), "mcapq_w4a8_x")
     return y
@@ -151,8 +175,8 @@ def w4a8_x(w: PackedW4, x: torch.Tensor, out_dtype=torch.float32, out=None, ws=N
 
 def w4a16(w: PackedW4, x: torch.Tensor, out_dtype=torch.float32, out=None, stream=None):
     """a4/a6: exact-dequant W4A16 on bf16 tensor cores."""
-    _need_cuda(w.nib, x)
-    x2 = x if x.dim() == 2 else x.view(1, -1)
+    _need_cuda(w.nib)
+    x2 = _act(x, w.k)
     m = x2.shape[0]
     y = _out(m, w.n, out_dtype, x.device, out)
     check(load().mcapq_w4a16(_ptr(w.nib), _ptr(w.scale), w.n, w.k, _ptr(x2), m, x2.stride(0), _ptr(y),
@@ -162,8 +186,8 @@ def w4a16(w: PackedW4, x: torch.Tensor, out_dtype=torch.float32, out=None, strea
 
 def w4a16_bf16deq(w: PackedW4, x: torch.Tensor, out_dtype=torch.float32, out=None, stream=None):
     """a6, bf16-dequant semantics: W^ = bf16(d (c - 8)), y = x W^T on tcgen05 (K % 256 == 0)."""
-    _need_cuda(w.nib, x)
-    x2 = x if x.dim() == 2 else x.view(1, -1)
+    _need_cuda(w.nib)
+    x2 = _act(x, w.k)
     m = x2.shape[0]
     y = _out(m, w.n, out_dtype, x.device, out)
     check(load().mcapq_w4a16_bf16deq(_ptr(w.nib), _ptr(w.scale), w.n, w.k, _ptr(x2), m, x2.stride(0), _ptr(y),
@@ -182,10 +206,10 @@ def dequant_w4_bf16(w: PackedW4, out=None, stream=None) -> torch.Tensor:
 
 def bf16w_gemm(wdq: torch.Tensor, x: torch.Tensor, out_dtype=torch.float32, out=None, stream=None):
     """NEXT-4: y = x W^T for a resident bf16 W^ [N, K] on tcgen05 (mcapq_bf16w_gemm)."""
-    _need_cuda(wdq, x)
-    x2 = x if x.dim() == 2 else x.view(1, -1)
-    m = x2.shape[0]
+    _need_cuda(wdq)
     n, k = wdq.shape
+    x2 = _act(x, k)
+    m = x2.shape[0]
     y = _out(m, n, out_dtype, x.device, out)
     check(load().mcapq_bf16w_gemm(_ptr(wdq), n, k, _ptr(x2), m, x2.stride(0), _ptr(y), _dt(y.dtype), y.stride(0),
                                   _stream(stream)), "mcapq_bf16w_gemm")
@@ -194,12 +218,12 @@ def bf16w_gemm(wdq: torch.Tensor, x: torch.Tensor, out_dtype=torch.float32, out=
 
 def w4a16_bf16deq_prefill(w: PackedW4, x: torch.Tensor, out_dtype=torch.float32, out=None, ws=None, stream=None):
     """NEXT-4: dequantise once into ws, then the tcgen05 GEMM (mcapq_w4a16_bf16deq_prefill)."""
-    _need_cuda(w.nib, x)
-    x2 = x if x.dim() == 2 else x.view(1, -1)
+    _need_cuda(w.nib)
+    x2 = _act(x, w.k)
     m = x2.shape[0]
     y = _out(m, w.n, out_dtype, x.device, out)
     if ws is None:
-        ws = torch.empty(load().mcapq_prefill_workspace_bytes(w.n, w.k), dtype=torch.uint8, device=x.device)
+        ws = _scratch(load().mcapq_prefill_workspace_bytes(w.n, w.k), x.device, stream)
     check(load().mcapq_w4a16_bf16deq_prefill(_ptr(w.nib), _ptr(w.scale), w.n, w.k, _ptr(x2), m, x2.stride(0),
                                              _ptr(y), _dt(y.dtype), y.stride(0), _ptr(ws), ws.numel(),
                                              _stream(stream)), "mcapq_w4a16_bf16deq_prefill")
@@ -214,11 +238,11 @@ def set_pdl(enable: bool) -> bool:
 
 def linear(route: int, w: PackedW4, x: torch.Tensor, out_dtype=torch.float32, out=None, ws=None, stream=None):
     """Routed linear (a3-a6 by route)."""
-    _need_cuda(w.nib, x)
-    x2 = x if x.dim() == 2 else x.view(1, -1)
+    _need_cuda(w.nib)
+    x2 = _act(x, w.k)
     m = x2.shape[0]
     y = _out(m, w.n, out_dtype, x.device, out)
-    ws = _ws(route, m, w.n, w.k, x.device, ws)
+    ws = _ws(route, m, w.n, w.k, x.device, ws, stream)
     check(load().mcapq_linear(route, _ptr(w.nib), _ptr(w.scale), w.n, w.k, _ptr(x2), m, x2.stride(0), _ptr(y),
                               _dt(y.dtype), y.stride(0), _ptr(ws), ws.numel(), _stream(stream)), "mcapq_linear")
     return y
@@ -227,8 +251,11 @@ def linear(route: int, w: PackedW4, x: torch.Tensor, out_dtype=torch.float32, ou
 def linear_group(route: int, ws_list, x: torch.Tensor, out_dtype=torch.float32, outs=None, ws=None, stream=None):
     """Grouped routed linear: several PackedW4 sharing the same input x in one launch."""
     ws_list = list(ws_list)
-    x2 = x if x.dim() == 2 else x.view(1, -1)
-    m, k = x2.shape
+    k = ws_list[0].k
+    if any(w.k != k for w in ws_list):
+        raise McapqError(1, "binding", "linear_group: every weight must have the same K")
+    x2 = _act(x, k)
+    m = x2.shape[0]
     cnt = len(ws_list)
     outs = outs if outs is not None else [torch.empty((m, w.n), dtype=out_dtype, device=x.device) for w in ws_list]
     arr = lambda T, vals: (T * cnt)(*vals)  # noqa: E731
@@ -237,7 +264,7 @@ def linear_group(route: int, ws_list, x: torch.Tensor, out_dtype=torch.float32, 
     ns = arr(ctypes.c_int64, [w.n for w in ws_list])
     ys = arr(ctypes.c_void_p, [y.data_ptr() for y in outs])
     lds = arr(ctypes.c_int64, [y.stride(0) for y in outs])
-    ws = _ws(route, m, max(w.n for w in ws_list), k, x.device, ws)
+    ws = _ws(route, m, max(w.n for w in ws_list), k, x.device, ws, stream)
     check(load().mcapq_linear_group(route, cnt, ctypes.cast(nibs, ctypes.c_void_p), ctypes.cast(scs, ctypes.c_void_p),
                                     ctypes.cast(ns, ctypes.c_void_p), k, _ptr(x2), m, x2.stride(0),
                                     ctypes.cast(ys, ctypes.c_void_p), _dt(outs[0].dtype),
@@ -262,6 +289,24 @@ def w4a8_group_dots(w: PackedW4, q, sq, mode: int = 1, stream=None):
     check(load().mcapq_w4a8_group_dots(_ptr(w.nib), w.n, w.k, _ptr(q), _ptr(sq), m, _ptr(D), mode,
                                        _stream(stream)), "mcapq_w4a8_group_dots")
     return D
+
+
+def stream_w4a8_dump(w: PackedW4, x: torch.Tensor, stream=None):
+    """Test entry: the stream kernel's fused quantiser output (q, sx, sq) for one token
+    and every block's exact D [N, K/32] (mcapq_debug_stream_w4a8_dump)."""
+    _need_cuda(w.nib)
+    x2 = _act(x, w.k)
+    assert x2.shape[0] == 1
+    dev = x.device
+    q = torch.empty(w.k, dtype=torch.int8, device=dev)
+    sx = torch.empty(w.k // 32, dtype=torch.float32, device=dev)
+    sq = torch.empty(w.k // 32, dtype=torch.int32, device=dev)
+    D = torch.empty((w.n, w.k // 32), dtype=torch.int32, device=dev)
+    ws = _scratch(load().mcapq_debug_stream_dump_workspace_bytes(w.k), dev, stream)
+    check(load().mcapq_debug_stream_w4a8_dump(_ptr(w.nib), _ptr(w.scale), w.n, w.k, _ptr(x2), _ptr(q), _ptr(sx),
+                                              _ptr(sq), _ptr(D), _ptr(ws), ws.numel(), _stream(stream)),
+          "mcapq_debug_stream_w4a8_dump")
+    return q, sx, sq, D
 
 
 # ------------------------------------------------------------------ profile
@@ -329,7 +374,7 @@ def mcap_accumulate(yq: torch.Tensor, yv: torch.Tensor, yffn: torch.Tensor, weig
         raise McapqError(2, "dtype", "score must be float64")
     m = yq.shape[0]
     if ws is None:
-        ws = torch.empty(max(8, load().mcapq_mcap_workspace_bytes(m)), dtype=torch.uint8, device=yq.device)
+        ws = _scratch(load().mcapq_mcap_workspace_bytes(m), yq.device, stream)
     check(load().mcapq_mcap_accumulate(_ptr(yq), yq.stride(0), yq.shape[1], _ptr(yv), yv.stride(0), yv.shape[1],
                                        _ptr(yffn), yffn.stride(0), yffn.shape[1], m, float(weight), _ptr(score),
                                        _ptr(ws), ws.numel(), _stream(stream)), "mcapq_mcap_accumulate")
@@ -355,6 +400,9 @@ class Stack:
             self._h = None
 
     def set(self, layer: int, slot: int, input_id: int, w: PackedW4, x: torch.Tensor, y: torch.Tensor):
+        _act(x, w.k)
+        if y.shape[-1] != w.n or y.stride(-1) != 1 or not y.is_contiguous():
+            raise McapqError(1, "binding", f"y must be a contiguous [M, {w.n}] tensor")
         self._keep.append((w, x, y))
         check(load().mcapq_stack_set(self._h, layer, slot, input_id, _ptr(w.nib), _ptr(w.scale), w.n, w.k, _ptr(x),
                                      _ptr(y), _dt(y.dtype)), "mcapq_stack_set")
@@ -423,14 +471,24 @@ class Comm:
         return load().mcapq_colshard_workspace_bytes(route, m, n_full, k, self.world)
 
 
+def colshard_assemble(rank_major: torch.Tensor, world: int, out=None, stream=None) -> torch.Tensor:
+    """a8 assembly: rank-major [P, M, N/P] -> y_full [M, N] (mcapq_colshard_assemble)."""
+    _need_cuda(rank_major)
+    P, m, per = rank_major.shape
+    assert P == world and rank_major.is_contiguous()
+    y = _out(m, P * per, rank_major.dtype, rank_major.device, out)
+    check(load().mcapq_colshard_assemble(_ptr(rank_major), _ptr(y), m, P * per, world, _dt(y.dtype),
+                                         _stream(stream)), "mcapq_colshard_assemble")
+    return y
+
+
 def linear_colshard(comm: Comm, route: int, w_shard: PackedW4, n_full: int, x: torch.Tensor,
                     out_dtype=torch.bfloat16, out=None, ws=None, stream=None):
     """a8: column-sharded routed linear + NCCL all-gather into y_full [M, n_full]."""
-    x2 = x if x.dim() == 2 else x.view(1, -1)
+    x2 = _act(x, w_shard.k)
     m = x2.shape[0]
     y = _out(m, n_full, out_dtype, x.device, out)
-    need = comm.workspace_bytes(route, m, n_full, w_shard.k)
-    ws = ws if ws is not None else torch.empty(max(need, 256), dtype=torch.uint8, device=x.device)
+    ws = ws if ws is not None else _scratch(comm.workspace_bytes(route, m, n_full, w_shard.k), x.device, stream)
     check(load().mcapq_linear_colshard(comm._h, route, _ptr(w_shard.nib), _ptr(w_shard.scale), n_full, w_shard.k,
                                        _ptr(x2), m, _ptr(y), _dt(y.dtype), _ptr(ws), ws.numel(), _stream(stream)),
           "mcapq_linear_colshard")

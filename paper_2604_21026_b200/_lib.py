@@ -44,6 +44,8 @@ SIGNATURES = {
     "mcapq_host_workspace_bytes": (SZ, [I32, I64, I64, I64]),
     "mcapq_linear_host": (I32, [I32, P, P, I64, I64, P, I64, P, I32, P, SZ, P]),
     "mcapq_w4a8_group_dots": (I32, [P, I64, I64, P, P, I64, P, I32, P]),
+    "mcapq_debug_stream_dump_workspace_bytes": (SZ, [I64]),
+    "mcapq_debug_stream_w4a8_dump": (I32, [P, P, I64, I64, P, P, P, P, P, P, SZ, P]),
     "mcapq_profile_parse": (I32, [ctypes.c_char_p, SZ, DBL, ctypes.POINTER(P)]),
     "mcapq_profile_layers": (I32, [P]),
     "mcapq_profile_tau": (DBL, [P]),
@@ -69,6 +71,7 @@ SIGNATURES = {
     "mcapq_comm_rank": (I32, [P]),
     "mcapq_colshard_workspace_bytes": (SZ, [I32, I64, I64, I64, I32]),
     "mcapq_linear_colshard": (I32, [P, I32, P, P, I64, I64, P, I64, P, I32, P, SZ, P]),
+    "mcapq_colshard_assemble": (I32, [P, P, I64, I64, I32, I32, P]),
     "mcapq_comm_destroy": (None, [P]),
 }
 

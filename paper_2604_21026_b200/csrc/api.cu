@@ -3,6 +3,9 @@
 // arithmetic step runs in the kernels of kernels_*.cu.
 #include <cmath>
 #include <cstring>
+#include <mutex>
+#include <set>
+#include <utility>
 
 #include "internal.h"
 #include "stream.h"
@@ -26,6 +29,22 @@ int device_sms()
     if (cudaGetDevice(&dev) != cudaSuccess) return 0;
     if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return 0;
     return sms;
+}
+
+cudaError_t kernel_smem_attr(const void *kernel, int smem_bytes, int carveout)
+{
+    static std::mutex mu;
+    static std::set<std::pair<const void *, int>> done;   // (kernel, device ordinal)
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    std::lock_guard<std::mutex> lock(mu);
+    if (done.count({kernel, dev})) return cudaSuccess;
+    e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes);
+    if (e == cudaSuccess && carveout >= 0)
+        e = cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout, carveout);
+    if (e == cudaSuccess) done.insert({kernel, dev});
+    return e;
 }
 
 static size_t align256(size_t b) { return (b + 255) & ~(size_t)255; }
@@ -418,6 +437,31 @@ mcapq_status mcapq_linear_host(int route, const uint8_t *nib, const uint16_t *sc
     if (st != MCAPQ_OK) return st;
     MCAPQ_CUDA_TRY(cudaMemcpyAsync(y_host, yd, (size_t)(m * n) * (ydt == MCAPQ_F32 ? 4 : 2),
                                    cudaMemcpyDeviceToHost, s));
+    return MCAPQ_OK;
+}
+
+size_t mcapq_debug_stream_dump_workspace_bytes(int64_t k) { return k >= 32 ? stream_dump_workspace_bytes(k) : 0; }
+
+mcapq_status mcapq_debug_stream_w4a8_dump(const uint8_t *nib, const uint16_t *scale, int64_t n, int64_t k,
+                                          const uint16_t *x, int8_t *q, float *sx, int32_t *sq, int32_t *D,
+                                          void *ws, size_t ws_bytes, void *stream)
+{
+    clear_error();
+    CHECK_SHAPE(n, k, 1);
+    mcapq_status st = check_weight(nib, scale, n, k);
+    if (st != MCAPQ_OK) return st;
+    CHECK_PTR(x, "x");
+    CHECK_PTR(q, "q");
+    CHECK_PTR(sx, "sx");
+    CHECK_PTR(sq, "sq");
+    CHECK_PTR(D, "D");
+    CHECK_PTR(ws, "ws");
+    CHECK_AL16(x, "x");
+    CHECK_AL16(ws, "ws");
+    MCAPQ_REQUIRE(stream_supported(k) && aligned16(scale), MCAPQ_EUNSUP, "not on the stream path (K=%lld)",
+                  (long long)k);
+    MCAPQ_REQUIRE(ws_bytes >= stream_dump_workspace_bytes(k), MCAPQ_ENOSPACE, "workspace too small");
+    LAUNCH_TRY(launch_stream_dump(nib, scale, n, k, x, q, sx, sq, D, ws, as_stream(stream)));
     return MCAPQ_OK;
 }
 

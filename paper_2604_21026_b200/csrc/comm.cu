@@ -6,10 +6,12 @@
 // the packed weight (reading A22); every rank holds the full x.  Each rank runs
 // the routed linear on its shard; the per-row arithmetic depends on K only, so
 // the gathered y is bit-identical to the single-GPU result.
-//   M == 1 : the rank-major gather is already the row order of y -> gather in
-//            place into y_full.
-//   M  > 1 : gather [P][M][N/P] into the workspace, then one permute kernel
-//            writes y_full[m][r N/P + j].
+//   M == 1 : the rank-major gather is already the row order of y: the linear writes
+//            its rows straight into y_full + r N/P and the all-gather runs in place.
+//   M  > 1 : the linear writes slot r of a rank-major [P][M][N/P] workspace, the
+//            all-gather fills the other slots in place, and one assemble (permute)
+//            kernel writes y_full[m][r N/P + j] (mcapq_colshard_assemble, also a test
+//            entry: P-way shard emulation on one GPU).
 #include <nccl.h>
 
 #include "internal.h"
@@ -93,11 +95,26 @@ int mcapq_comm_rank(const mcapq_comm *c) { return c ? c->rank : -1; }
 size_t mcapq_colshard_workspace_bytes(int route, int64_t m, int64_t n_full, int64_t k, int world)
 {
     if (world < 1 || m < 1 || n_full < 1 || k < 32 || n_full % world) return 0;
-    const int64_t per = n_full / world;
-    size_t b = align256((size_t)(m * per) * 4);               // local slice (fp32 worst case)
-    if (m > 1) b += align256((size_t)(m * n_full) * 4);        // rank-major gather
+    size_t b = 256;
+    if (m > 1) b += align256((size_t)(m * n_full) * 4);        // rank-major gather (fp32 worst case)
     if (route == MCAPQ_W4A8) b += a8_workspace_bytes(m, k);
     return b;
+}
+
+mcapq_status mcapq_colshard_assemble(const void *rank_major, void *y_full, int64_t m, int64_t n_full, int world,
+                                     int ydt, void *stream)
+{
+    clear_error();
+    MCAPQ_REQUIRE(rank_major && y_full && m >= 1 && n_full >= 1 && world >= 1 && n_full % world == 0, MCAPQ_EINVAL,
+                  "bad colshard_assemble arguments");
+    MCAPQ_REQUIRE(ydt == MCAPQ_BF16 || ydt == MCAPQ_F32, MCAPQ_EDTYPE, "bad ydt");
+    const int64_t total = m * n_full;
+    const int grid = (int)((total + 255) / 256 < 4096 ? (total + 255) / 256 : 4096);
+    permute_rank_major<<<grid, 256, 0, as_stream(stream)>>>(reinterpret_cast<const uint8_t *>(rank_major),
+                                                            reinterpret_cast<uint8_t *>(y_full), m, n_full, world,
+                                                            ydt == MCAPQ_F32 ? 4 : 2);
+    MCAPQ_CUDA_TRY(cudaGetLastError());
+    return MCAPQ_OK;
 }
 
 mcapq_status mcapq_linear_colshard(const mcapq_comm *c, int route, const uint8_t *nib_shard,
@@ -115,9 +132,7 @@ mcapq_status mcapq_linear_colshard(const mcapq_comm *c, int route, const uint8_t
     const int64_t per = n_full / c->world;
     MCAPQ_REQUIRE(per % 8 == 0, MCAPQ_EINVAL, "N/P=%lld must be a multiple of 8", (long long)per);
     const int es = ydt == MCAPQ_F32 ? 4 : 2;
-    uint8_t *p = reinterpret_cast<uint8_t *>(ws);
-    uint8_t *local = p;
-    p += align256((size_t)(m * per) * 4);
+    uint8_t *p = reinterpret_cast<uint8_t *>(ws) + 256;
     uint8_t *gathered = nullptr;
     if (m > 1) {
         gathered = p;
@@ -126,21 +141,16 @@ mcapq_status mcapq_linear_colshard(const mcapq_comm *c, int route, const uint8_t
     void *rest = p;
     const size_t rest_bytes = ws_bytes - (size_t)(p - reinterpret_cast<uint8_t *>(ws));
     cudaStream_t s = as_stream(stream);
-
-    mcapq_status st = mcapq_linear(route, nib_shard, scale_shard, per, k, x, m, k, local, ydt, per, rest, rest_bytes,
+    const ncclDataType_t dt = ydt == MCAPQ_F32 ? ncclFloat32 : ncclBfloat16;
+    // the local rows go straight to their place in the gather buffer (in-place all-gather:
+    // sendbuff = recvbuff + rank * count)
+    uint8_t *dst = m == 1 ? reinterpret_cast<uint8_t *>(y_full) : gathered;
+    uint8_t *mine = dst + (size_t)c->rank * (size_t)(m * per) * es;
+    mcapq_status st = mcapq_linear(route, nib_shard, scale_shard, per, k, x, m, k, mine, ydt, per, rest, rest_bytes,
                                    stream);
     if (st != MCAPQ_OK) return st;
-    const ncclDataType_t dt = ydt == MCAPQ_F32 ? ncclFloat32 : ncclBfloat16;
-    if (m == 1) {
-        NCCL_TRY(ncclAllGather(local, y_full, (size_t)per, dt, c->comm, s));
-    } else {
-        NCCL_TRY(ncclAllGather(local, gathered, (size_t)(m * per), dt, c->comm, s));
-        const int64_t total = m * n_full;
-        const int grid = (int)((total + 255) / 256 < 4096 ? (total + 255) / 256 : 4096);
-        permute_rank_major<<<grid, 256, 0, s>>>(gathered, reinterpret_cast<uint8_t *>(y_full), m, n_full, c->world,
-                                                es);
-        MCAPQ_CUDA_TRY(cudaGetLastError());
-    }
+    NCCL_TRY(ncclAllGather(mine, dst, (size_t)(m * per), dt, c->comm, s));
+    if (m > 1) return mcapq_colshard_assemble(gathered, y_full, m, n_full, c->world, ydt, stream);
     return MCAPQ_OK;
 }
 

@@ -27,7 +27,9 @@ struct GemmArgs {
     // activation maps as kernel parameters (encoded per launch; nothing cached per buffer):
     // W4A8 {q, sx, sq}, W4A16 {x} (encode_gemm_act_maps)
     alignas(64) CUtensorMap amaps[3];
-    const CUtensorMap *maps;    // weights {nib box {128 B, bn}, scale box {8, bn}} (device table)
+    // weight maps, also kernel parameters (encoded per launch, never cached or allocated):
+    // {nib box {128 B, bn}, scale box {8, bn}} (encode_gemm_maps)
+    alignas(64) CUtensorMap maps[2];
     void *y;
     int64_t ldy;
     int64_t n, k;

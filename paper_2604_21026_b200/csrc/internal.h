@@ -64,6 +64,9 @@ cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t s
 
 // Per-process device facts (cached per device ordinal).
 int device_sms();
+// cudaFuncSetAttribute(kernel, MaxDynamicSharedMemorySize = smem_bytes [, preferred
+// carveout]) once per (kernel, current device): host-side, thread-safe, no stream work.
+cudaError_t kernel_smem_attr(const void *kernel, int smem_bytes, int carveout = -1);
 
 // Kernel launchers (kernels_*.cu).  All return cudaError_t of the launch.
 cudaError_t launch_pack_w4(const void *w, int wdt, int64_t n, int64_t k, int64_t ldw, uint8_t *nib,

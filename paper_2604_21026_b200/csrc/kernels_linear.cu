@@ -411,12 +411,8 @@ cudaError_t launch_tc(const TcArgs &a0, cudaStream_t s, bool pdl)
     TcArgs a = a0;
     a.tokens_per_pass = tokens_per_pass<A8>(a.m, a.k);
     const size_t smem = kRedBytes + (size_t)a.tokens_per_pass * act_bytes_per_token<A8>(a.k);
-    static bool attr_set = false;
-    if (!attr_set) {
-        cudaError_t e = cudaFuncSetAttribute(tc_linear<A8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMaxSmem);
-        if (e != cudaSuccess) return e;
-        attr_set = true;
-    }
+    cudaError_t e = kernel_smem_attr(reinterpret_cast<const void *>(tc_linear<A8>), (int)kMaxSmem);
+    if (e != cudaSuccess) return e;
     const unsigned grid = (unsigned)((a.n + 15) / 16);
     return launch_pdl(tc_linear<A8>, dim3(grid), dim3(kThreads), smem, s, pdl, a);
 }
@@ -428,13 +424,9 @@ cudaError_t launch_w4a8(const uint8_t *nib, const uint16_t *scale, int64_t n, in
                         cudaStream_t s, bool pdl)
 {
     if (m == 1) {
-        static bool attr_set = false;
         const size_t smem = (size_t)k + 8 * (size_t)(k / 32);
-        if (!attr_set) {
-            cudaError_t e = cudaFuncSetAttribute(w4a8_gemv_dp4a, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMaxSmem);
-            if (e != cudaSuccess) return e;
-            attr_set = true;
-        }
+        cudaError_t e = kernel_smem_attr(reinterpret_cast<const void *>(w4a8_gemv_dp4a), (int)kMaxSmem);
+        if (e != cudaSuccess) return e;
         if (smem <= kMaxSmem) {
             const unsigned grid = (unsigned)((n + kWarps - 1) / kWarps);
             return launch_pdl(w4a8_gemv_dp4a, dim3(grid), dim3(kThreads), smem, s, pdl, nib, scale, n, k, q, sx, sq,

@@ -34,10 +34,6 @@
 // all reductions have a fixed order, so an output row is bit-identical whatever
 // N, the group, the grid or the column shard (reading A22).
 #include <cstdlib>
-#include <mutex>
-#include <unordered_map>
-#include <utility>
-#include <vector>
 
 #include "internal.h"
 #include "stream.h"
@@ -57,7 +53,9 @@ constexpr int kMaxStages = 16;
 constexpr int kBarBytes = 512;                     // mbarriers: full[S] + empty[S] + done + go <= 16*16 + 16
 
 // HMMA1: W4A16 with a single token (only MMA column 0 is computed);  NONE: bandwidth probe
-enum Engine { DP4A = 0, IMMA = 1, HMMA = 2, NONE = 3, HMMA1 = 4 };
+// DUMP: the DP4A engine (same staging, same fused quantiser, same block_D) writing the
+// staged activation codes and every block's exact int32 D instead of y (test entry)
+enum Engine { DP4A = 0, IMMA = 1, HMMA = 2, NONE = 3, HMMA1 = 4, DUMP = 5 };
 
 // ------------------------------------------------------------------ PTX helpers
 // All shared-memory traffic uses explicit 32-bit shared-window addresses
@@ -298,6 +296,8 @@ __device__ __forceinline__ void hmma(uint32_t a0, uint32_t a1, uint32_t a2, uint
 #include "tc05_kernel.cuh"
 
 // ------------------------------------------------------------------ host side
+}  // namespace
+
 typedef CUresult (*EncodeTiledFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
                                   const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
@@ -338,6 +338,7 @@ bool encode_maps(CUtensorMap *tn, CUtensorMap *ts, const uint8_t *nib, const uin
               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+namespace {
 size_t act_bytes(int engine, int64_t k, int ntok)
 {
     const int64_t G = k / 32;
@@ -418,16 +419,10 @@ template <int E>
 cudaError_t launch_one(StreamArgs &a, cudaStream_t s, bool pdl, int sms)
 {
     const size_t smem = plan_smem(E, a.k, a.ntok, a);
-    static int attr_done = 0;
-    if (!attr_done) {
-        cudaError_t e = cudaFuncSetAttribute(stream_linear<E>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-        if (e != cudaSuccess) return e;
-        // one L1/shared carveout for every linear: consecutive (PDL-overlapped) kernels
-        // never force an SM to drain for a carveout change
-        e = cudaFuncSetAttribute(stream_linear<E>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-        if (e != cudaSuccess) return e;
-        attr_done = 1;
-    }
+    // one L1/shared carveout for every linear: consecutive (PDL-overlapped) kernels
+    // never force an SM to drain for a carveout change
+    cudaError_t e = kernel_smem_attr(reinterpret_cast<const void *>(stream_linear<E>), 227 * 1024, 100);
+    if (e != cudaSuccess) return e;
     const int T = a.tile_start[a.count];
     const int grid = T < sms ? T : sms;
     if (grid == 0) return cudaSuccess;
@@ -451,74 +446,6 @@ cudaError_t launch_one(StreamArgs &a, cudaStream_t s, bool pdl, int sms)
 
 }  // namespace
 
-// ------------------------------------------------------------------ descriptor table
-// Device-resident groups of tensor maps (4 slots each), keyed by what they describe.
-// Entries are written once (pinned staging -> cudaMemcpyAsync, capturable) and never
-// reused, so a kernel in flight or a captured graph always sees its own.
-//   kind 0        : stream maps {nib, scale} of a packed weight (16-row x 2048-K stages)
-//   kind BN > 0   : gemm maps {nib, scale} (BN rows x 256 K)
-// (activation maps are not cached: they travel as kernel parameters, see GemmArgs)
-namespace {
-struct DescKey {
-    const void *p0, *p1;
-    int64_t n, k, ld;
-    int kind;
-    bool operator==(const DescKey &o) const
-    {
-        return p0 == o.p0 && p1 == o.p1 && n == o.n && k == o.k && ld == o.ld && kind == o.kind;
-    }
-};
-struct DescKeyHash {
-    size_t operator()(const DescKey &d) const
-    {
-        return std::hash<const void *>()(d.p0) ^ (std::hash<const void *>()(d.p1) << 1) ^
-               (size_t)(d.n * 31 + d.k * 7 + d.ld * 13 + d.kind);
-    }
-};
-constexpr int kDescSlots = 4;
-struct DescTable {
-    std::mutex mu;
-    std::unordered_map<DescKey, const CUtensorMap *, DescKeyHash> map;
-    std::vector<std::pair<CUtensorMap *, CUtensorMap *>> blocks;   // (device, pinned host)
-    int used = 0;                                                   // groups used in the last block
-    static constexpr int kGroups = 2048;
-};
-DescTable &desc_table()
-{
-    static DescTable t;
-    return t;
-}
-
-// Look the group up, or encode it (enc fills up to kDescSlots host maps) and upload it.
-template <typename Enc>
-const CUtensorMap *desc_group(const DescKey &key, Enc enc, cudaStream_t s)
-{
-    DescTable &t = desc_table();
-    std::lock_guard<std::mutex> lock(t.mu);
-    auto it = t.map.find(key);
-    if (it != t.map.end()) return it->second;
-    if (t.blocks.empty() || t.used == DescTable::kGroups) {
-        CUtensorMap *d = nullptr, *h = nullptr;
-        if (cudaMalloc(&d, sizeof(CUtensorMap) * kDescSlots * DescTable::kGroups) != cudaSuccess) return nullptr;
-        if (cudaMallocHost(&h, sizeof(CUtensorMap) * kDescSlots * DescTable::kGroups) != cudaSuccess) {
-            cudaFree(d);
-            return nullptr;
-        }
-        t.blocks.emplace_back(d, h);
-        t.used = 0;
-    }
-    CUtensorMap *dg = t.blocks.back().first + kDescSlots * t.used;
-    CUtensorMap *hg = t.blocks.back().second + kDescSlots * t.used;
-    memset(hg, 0, sizeof(CUtensorMap) * kDescSlots);
-    if (!enc(hg)) return nullptr;
-    if (cudaMemcpyAsync(dg, hg, kDescSlots * sizeof(CUtensorMap), cudaMemcpyHostToDevice, s) != cudaSuccess)
-        return nullptr;
-    ++t.used;
-    t.map.emplace(key, dg);
-    return dg;
-}
-}  // namespace
-
 // gemm maps: nibbles 2-D {K/2, N}, box {128 B, bn rows}, 128B swizzle (row r's 16-B
 // chunk c at c ^ (r & 7)); scales 2-D {K/32, N}, box {8, bn rows}, no swizzle (16 B/row).
 bool encode_gemm_maps(CUtensorMap *tn, CUtensorMap *ts, const uint8_t *nib, const uint16_t *scale, int64_t n,
@@ -540,19 +467,6 @@ bool encode_gemm_maps(CUtensorMap *tn, CUtensorMap *ts, const uint8_t *nib, cons
     return fn(ts, CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, const_cast<uint16_t *>(scale), sd, ss, sbox, es,
               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
-}
-
-const CUtensorMap *descriptors_of_kind(const uint8_t *nib, const uint16_t *scale, int64_t n, int64_t k, int kind,
-                                       cudaStream_t s)
-{
-    const DescKey key{nib, scale, n, k, 0, kind};
-    return desc_group(
-        key,
-        [&](CUtensorMap *h) {
-            return kind == 0 ? encode_maps(&h[0], &h[1], nib, scale, n, k)
-                             : encode_gemm_maps(&h[0], &h[1], nib, scale, n, k, kind);
-        },
-        s);
 }
 
 // gemm activation maps, boxes of mp token rows (rows past m read as zeros):
@@ -594,12 +508,6 @@ bool encode_gemm_act_maps(CUtensorMap *h, bool a8, const void *x_or_q, const flo
               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-const CUtensorMap *stream_descriptors(const uint8_t *nib, const uint16_t *scale, int64_t n, int64_t k,
-                                      cudaStream_t s)
-{
-    return descriptors_of_kind(nib, scale, n, k, 0, s);
-}
-
 // ------------------------------------------------------------------ batched decode (gemm_w4)
 bool gemm_supported(int64_t k) { return k >= 256 && k % 256 == 0 && encode_fn() != nullptr; }
 
@@ -619,12 +527,8 @@ constexpr GemmCfg kCfg64h[] = {{2, 4, 2}, {1, 4, 2}, {1, 2, 4}};
 template <bool A8, int MT, int NT>
 cudaError_t launch_gemm_cfg(GemmArgs &a, size_t smem, int grid, cudaStream_t s, bool pdl)
 {
-    static int attr_done = 0;
-    if (!attr_done) {
-        cudaError_t e = cudaFuncSetAttribute(gemm_w4<A8, MT, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-        if (e != cudaSuccess) return e;
-        attr_done = 1;
-    }
+    cudaError_t e = kernel_smem_attr(reinterpret_cast<const void *>(gemm_w4<A8, MT, NT>), 227 * 1024);
+    if (e != cudaSuccess) return e;
     return launch_pdl(gemm_w4<A8, MT, NT>, dim3(grid), dim3(kGemmThreads), smem, s, pdl, a);
 }
 
@@ -647,12 +551,8 @@ namespace {
 template <int MP>
 cudaError_t launch_tc05_mp(GemmArgs &a, size_t smem, int grid, cudaStream_t s, bool pdl)
 {
-    static int attr_done = 0;
-    if (!attr_done) {
-        cudaError_t e = cudaFuncSetAttribute(tc05_w4a16<MP>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-        if (e != cudaSuccess) return e;
-        attr_done = 1;
-    }
+    cudaError_t e = kernel_smem_attr(reinterpret_cast<const void *>(tc05_w4a16<MP>), 227 * 1024);
+    if (e != cudaSuccess) return e;
     return launch_pdl(tc05_w4a16<MP>, dim3(grid), dim3(tc05::kThreads), smem, s, pdl, a);
 }
 }  // namespace
@@ -668,8 +568,7 @@ cudaError_t launch_tc05(const uint8_t *nib, const uint16_t *scale, int64_t n, in
         const int mp = ntok <= 16 ? 16 : (ntok <= 32 ? 32 : 64);
         GemmArgs a;
         memset(&a, 0, sizeof(a));
-        a.maps = descriptors_of_kind(nib, scale, n, k, 128, s);
-        if (!a.maps || !encode_gemm_act_maps(a.amaps, false, x, nullptr, nullptr, m, k, ldx, mp))
+        if (!encode_gemm_maps(&a.maps[0], &a.maps[1], nib, scale, n, k, 128) || !encode_gemm_act_maps(a.amaps, false, x, nullptr, nullptr, m, k, ldx, mp))
             return cudaErrorInvalidValue;
         a.y = y;
         a.ldy = ldy;
@@ -723,12 +622,8 @@ bool encode_bf16_rows(CUtensorMap *m, const void *base, int64_t rows, int64_t k,
 template <int MP>
 cudaError_t launch_prefill_mp(PrefillArgs &a, size_t smem, int grid, cudaStream_t s, bool pdl)
 {
-    static int attr_done = 0;
-    if (!attr_done) {
-        cudaError_t e = cudaFuncSetAttribute(tc05_prefill<MP>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-        if (e != cudaSuccess) return e;
-        attr_done = 1;
-    }
+    cudaError_t e = kernel_smem_attr(reinterpret_cast<const void *>(tc05_prefill<MP>), 227 * 1024);
+    if (e != cudaSuccess) return e;
     return launch_pdl(tc05_prefill<MP>, dim3(grid), dim3(192), smem, s, pdl, a);
 }
 }  // namespace
@@ -786,8 +681,7 @@ cudaError_t launch_gemm(int route, const uint8_t *nib, const uint16_t *scale, in
         const int bn = c.bn(), mp = c.mp();
         GemmArgs a;
         memset(&a, 0, sizeof(a));
-        a.maps = descriptors_of_kind(nib, scale, n, k, bn, s);
-        if (!a.maps || !encode_gemm_act_maps(a.amaps, a8, a8 ? (const void *)q : (const void *)x, sx, sq, m, k, ldx, mp))
+        if (!encode_gemm_maps(&a.maps[0], &a.maps[1], nib, scale, n, k, bn) || !encode_gemm_act_maps(a.amaps, a8, a8 ? (const void *)q : (const void *)x, sx, sq, m, k, ldx, mp))
             return cudaErrorInvalidValue;
         a.y = y;
         a.ldy = ldy;
@@ -862,14 +756,15 @@ size_t stack_op_bytes() { return sizeof(StackOp); }
 bool stack_step_enabled() { return tune().step != 0 && encode_fn() != nullptr; }
 
 bool stack_fill_op(void *host_op, int route, const StreamGroup &g, const uint16_t *x, int ydt, const StackDeps &d,
-                   cudaStream_t s)
+                   CUtensorMap *host_maps, const CUtensorMap *dev_maps)
 {
     StackOp op;
     memset(&op, 0, sizeof(op));
     int tiles = 0;
     for (int i = 0; i < g.count; ++i) {
-        op.maps[i] = stream_descriptors(g.nib[i], g.scale[i], g.n[i], g.k, s);
-        if (!op.maps[i]) return false;
+        memset(host_maps + 2 * i, 0, 2 * sizeof(CUtensorMap));
+        if (!encode_maps(host_maps + 2 * i, host_maps + 2 * i + 1, g.nib[i], g.scale[i], g.n[i], g.k)) return false;
+        op.maps[i] = dev_maps + 2 * i;
         op.y[i] = g.y[i];
         op.n[i] = (int)g.n[i];
         op.tile_start[i] = tiles;
@@ -894,18 +789,12 @@ bool stack_fill_op(void *host_op, int route, const StreamGroup &g, const uint16_
 cudaError_t launch_stack_step(const void *ops_dev, int nops, unsigned int *counters_dev, int64_t max_k,
                               cudaStream_t s)
 {
-    static int attr_done = 0;
-    if (!attr_done) {
-        cudaError_t e = cudaFuncSetAttribute(stack_step<false, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             227 * 1024);
-        if (e == cudaSuccess)
-            e = cudaFuncSetAttribute(stack_step<true, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-        if (e == cudaSuccess)
-            e = cudaFuncSetAttribute(stack_step<false, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-        if (e == cudaSuccess)
-            e = cudaFuncSetAttribute(stack_step<true, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    for (const void *f : {reinterpret_cast<const void *>(stack_step<false, 2>),
+                          reinterpret_cast<const void *>(stack_step<true, 2>),
+                          reinterpret_cast<const void *>(stack_step<false, 4>),
+                          reinterpret_cast<const void *>(stack_step<true, 4>)}) {
+        cudaError_t e = kernel_smem_attr(f, 227 * 1024);
         if (e != cudaSuccess) return e;
-        attr_done = 1;
     }
     StackArgs a;
     memset(&a, 0, sizeof(a));
@@ -964,6 +853,52 @@ size_t stream_trace_read(unsigned long long *host_out, size_t max_records)
     return n;
 }
 
+namespace {
+// q [k] int8, sx / sq [G] from the DUMP engine's copy of the staged activations
+__global__ void unpack_stream_dump(const uint32_t *act, int64_t k, int8_t *q, float *sx, int32_t *sq)
+{
+    const int G = (int)(k / 32);
+    const uint8_t *b = reinterpret_cast<const uint8_t *>(act);
+    const uint32_t *ssq = act + k / 4;
+    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < k; j += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t g = j / 32, t = j % 32;
+        q[j] = (int8_t)b[(t < 16 ? 0 : k / 2) + 16 * g + (t & 15)];
+        if (t == 0) {
+            sx[g] = __uint_as_float(ssq[2 * g]);
+            sq[g] = (int32_t)ssq[2 * g + 1] / 8;
+        }
+    }
+    (void)G;
+}
+}  // namespace
+
+size_t stream_dump_workspace_bytes(int64_t k) { return (size_t)(k / 4 + 2 * (k / 32)) * 4; }
+
+cudaError_t launch_stream_dump(const uint8_t *nib, const uint16_t *scale, int64_t n, int64_t k, const uint16_t *x,
+                               int8_t *q, float *sx, int32_t *sq, int32_t *D, void *ws, cudaStream_t s)
+{
+    StreamArgs a;
+    memset(&a, 0, sizeof(a));
+    a.count = 1;
+    if (!encode_maps(&a.maps[0][0], &a.maps[0][1], nib, scale, n, k)) return cudaErrorInvalidValue;
+    a.n[0] = n;
+    a.y[0] = nullptr;
+    a.ldy[0] = n;
+    a.tile_start[0] = 0;
+    a.tile_start[1] = (int)((n + kTileRows - 1) / kTileRows);
+    a.k = k;
+    a.x = x;
+    a.ldx = k;
+    a.ntok = 1;
+    a.ydt = MCAPQ_F32;
+    a.dump_d = D;
+    a.dump_act = reinterpret_cast<uint32_t *>(ws);
+    cudaError_t e = launch_one<DUMP>(a, s, false, device_sms());
+    if (e != cudaSuccess) return e;
+    unpack_stream_dump<<<(unsigned)((k + 255) / 256), 256, 0, s>>>(a.dump_act, k, q, sx, sq);
+    return cudaGetLastError();
+}
+
 bool stream_supported(int64_t k) { return k >= 2048 && k % 256 == 0 && encode_fn() != nullptr; }
 
 int stream_tokens_per_pass(int route, int64_t k)
@@ -988,8 +923,8 @@ cudaError_t launch_stream_group(int route, const StreamGroup &g, const uint16_t 
     a.count = g.count;
     int tiles = 0;
     for (int i = 0; i < g.count; ++i) {
-        a.maps[i] = stream_descriptors(g.nib[i], g.scale[i], g.n[i], g.k, s);
-        if (!a.maps[i]) return cudaErrorInvalidValue;
+        if (!encode_maps(&a.maps[i][0], &a.maps[i][1], g.nib[i], g.scale[i], g.n[i], g.k))
+            return cudaErrorInvalidValue;
         a.n[i] = g.n[i];
         a.y[i] = g.y[i];
         a.ldy[i] = g.ldy[i];

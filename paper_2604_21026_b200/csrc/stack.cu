@@ -12,6 +12,8 @@
 // for its predecessor's completion before touching activations.
 #include <vector>
 
+#include <cuda.h>
+
 #include "internal.h"
 #include "stream.h"
 
@@ -43,6 +45,7 @@ struct mcapq_stack {
     bool prog_dirty = true, prog_ok = false;
     void *ops_dev = nullptr, *ops_host = nullptr;
     unsigned int *counters = nullptr;   // [nops] + exit count + epoch
+    CUtensorMap *descs = nullptr;       // [nops][kMaxGroup][2] TMA descriptors the ops point at
     uint32_t *tags = nullptr;           // tagged copies of outputs consumed inside the step
     int nops = 0;
     int64_t max_k = 0;
@@ -56,11 +59,24 @@ static void free_program(mcapq_stack *st)
     if (st->ops_host) cudaFreeHost(st->ops_host);
     if (st->counters) cudaFree(st->counters);
     if (st->tags) cudaFree(st->tags);
+    if (st->descs) cudaFree(st->descs);
+    st->descs = nullptr;
     st->ops_dev = st->ops_host = nullptr;
     st->counters = nullptr;
     st->tags = nullptr;
     st->nops = 0;
     st->prog_ok = false;
+}
+
+// A registration change invalidates the captured graph (it points at the old
+// program / workspace): destroy it; replay then refuses until the next capture.
+static void drop_graph(mcapq_stack *st)
+{
+    if (st->exec) cudaGraphExecDestroy(st->exec);
+    if (st->graph) cudaGraphDestroy(st->graph);
+    st->exec = nullptr;
+    st->graph = nullptr;
+    st->graph_m = 0;
 }
 
 static mcapq_status ensure_ws(mcapq_stack *st, int64_t k)
@@ -116,12 +132,7 @@ mcapq_status mcapq_stack_set(mcapq_stack *st, int layer, int slot, int input_id,
     s.y = y;
     s.ydt = ydt;
     st->prog_dirty = true;
-    if (stream_supported(k) && aligned16(scale)) {
-        // encode + upload this weight's TMA descriptors now, outside any graph capture
-        MCAPQ_REQUIRE(stream_descriptors(nib, scale, n, k, nullptr) != nullptr, MCAPQ_ECUDA,
-                      "TMA descriptor encode/upload failed");
-        MCAPQ_CUDA_TRY(cudaStreamSynchronize(nullptr));
-    }
+    drop_graph(st);
     if (st->routes[layer] == MCAPQ_W4A8) return ensure_ws(st, k);
     return MCAPQ_OK;
 }
@@ -291,12 +302,19 @@ static mcapq_status build_program(mcapq_stack *st)
     MCAPQ_CUDA_TRY(cudaMalloc(&st->ops_dev, ob * nops));
     MCAPQ_CUDA_TRY(cudaMalloc(&st->counters, sizeof(unsigned int) * (nops + 2)));
     MCAPQ_CUDA_TRY(cudaMemset(st->counters, 0, sizeof(unsigned int) * (nops + 2)));
+    // the program's TMA descriptors: library-owned, uploaded once here (host-synchronous,
+    // outside any capture), freed with the program
+    const size_t nmaps = (size_t)nops * kMaxGroup * 2;
+    std::vector<CUtensorMap> hmaps(nmaps);
+    MCAPQ_CUDA_TRY(cudaMalloc(&st->descs, nmaps * sizeof(CUtensorMap)));
     for (int i = 0; i < nops; ++i) {
         const int l = groups[i].first;
+        const size_t off = (size_t)i * kMaxGroup * 2;
         MCAPQ_REQUIRE(stack_fill_op(reinterpret_cast<uint8_t *>(st->ops_host) + ob * i, st->routes[l], gs[i],
-                                    heads[i]->x, heads[i]->ydt, deps[i], nullptr),
+                                    heads[i]->x, heads[i]->ydt, deps[i], hmaps.data() + off, st->descs + off),
                       MCAPQ_ECUDA, "stack op %d: TMA descriptor encode failed", i);
     }
+    MCAPQ_CUDA_TRY(cudaMemcpy(st->descs, hmaps.data(), nmaps * sizeof(CUtensorMap), cudaMemcpyHostToDevice));
     MCAPQ_CUDA_TRY(cudaMemcpy(st->ops_dev, st->ops_host, ob * nops, cudaMemcpyHostToDevice));
     st->prog_ok = true;
     return MCAPQ_OK;
@@ -377,10 +395,7 @@ mcapq_status mcapq_stack_capture(mcapq_stack *st, int64_t m, void *stream)
         mcapq_status r = build_program(st);   // allocations happen before the capture
         if (r != MCAPQ_OK) return r;
     }
-    if (st->exec) cudaGraphExecDestroy(st->exec);
-    if (st->graph) cudaGraphDestroy(st->graph);
-    st->exec = nullptr;
-    st->graph = nullptr;
+    drop_graph(st);
     MCAPQ_CUDA_TRY(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
     mcapq_status r = mcapq_stack_run(st, m, stream);
     cudaGraph_t g = nullptr;
@@ -536,8 +551,7 @@ mcapq_status mcapq_stack_step_host(mcapq_stack *st, int64_t m, const void *x_hos
 void mcapq_stack_destroy(mcapq_stack *st)
 {
     if (!st) return;
-    if (st->exec) cudaGraphExecDestroy(st->exec);
-    if (st->graph) cudaGraphDestroy(st->graph);
+    drop_graph(st);
     if (st->ws) cudaFree(st->ws);
     free_program(st);
     delete st;

@@ -19,13 +19,14 @@ struct StreamGroup {
     int64_t ldy[kMaxGroup];
 };
 
-// Kernel parameters (small: the launch rate of graph kernel nodes drops with the
-// parameter block size).  The TMA descriptors live in a device-resident table,
-// encoded once per packed weight: maps[i] -> {nib map, scale map}.
+// Kernel parameters.  The TMA descriptors travel IN the parameter block
+// (__grid_constant__), encoded on the host per launch: a hot-path call never
+// allocates, never uploads and holds no per-weight cache, so it is capturable at any
+// time (maps[i] = {nib map, scale map} of linear i of the group):
 //   nib  : uint8 3-D view {128 B, N rows, K/256 columns}, box {128, 16, 8}, 128B swizzle
 //   scale: uint16 [N][K/32], box {64, 16 rows}, 128B swizzle
 struct StreamArgs {
-    const CUtensorMap *maps[kMaxGroup];
+    alignas(64) CUtensorMap maps[kMaxGroup][2];
     void *y[kMaxGroup];
     int64_t n[kMaxGroup];
     int64_t ldy[kMaxGroup];
@@ -44,6 +45,8 @@ struct StreamArgs {
     unsigned long long *trace;   // debug timeline (MCAPQ_STREAM_TRACE): 8 u64 per CTA, or null
     int launch_id;
     int smem_kb;     // host side: shared-memory plan of this launch (plan_smem)
+    int32_t *dump_d;     // DUMP engine: D [n][k/32] int32
+    uint32_t *dump_act;  // DUMP engine: CTA 0's staged activations (q_lo|q_hi bytes, then {s, 8 sum q} pairs)
 };
 
 // Debug timeline (MCAPQ_STREAM_TRACE=1): per CTA {launch, block, t_start, t_wait,
@@ -69,20 +72,26 @@ struct StackDeps {
 constexpr int64_t kStepMaxK = 16384;
 // Fill one op (host memory, stack_op_bytes() bytes) for `route` over group g with
 // input x [k] bf16 and outputs g.y (ydt); encodes/uploads descriptors on `s`.
+// The op's TMA descriptors are encoded into host_maps[2 * count] (copied by the caller
+// to dev_maps, the stack's own device array; op.maps point there).
 bool stack_fill_op(void *host_op, int route, const StreamGroup &g, const uint16_t *x, int ydt, const StackDeps &d,
-                   cudaStream_t s);
+                   CUtensorMap *host_maps, const CUtensorMap *dev_maps);
 // Launch the step: ops_dev = nops filled ops in device memory; counters_dev = nops + 2
 // uint32 (zeroed once at allocation; the kernel's last CTA resets them and advances
 // the epoch at [nops + 1]); max_k = the largest K of the program.
 cudaError_t launch_stack_step(const void *ops_dev, int nops, unsigned int *counters_dev, int64_t max_k,
                               cudaStream_t s);
 
-// Device pointer to the {nib, scale} tensor-map pair of a packed weight, encoding
-// and uploading it on first use (stream-ordered; capturable once the table exists).
-// Returns null on failure.
-const CUtensorMap *stream_descriptors(const uint8_t *nib, const uint16_t *scale, int64_t n, int64_t k,
-                                      cudaStream_t s);
+// Encode the {nib, scale} tensor-map pair of a packed weight for the stream / step
+// kernels (host only; false if the driver entry point is missing or encoding fails).
+bool encode_maps(CUtensorMap *tn, CUtensorMap *ts, const uint8_t *nib, const uint16_t *scale, int64_t n, int64_t k);
 int stream_tokens_per_pass(int route, int64_t k);
+// TEST ENTRY (DUMP engine, one token, W4A8): the stream kernel's fused quantiser output
+// (q [k] int8, sx/sq [k/32]) and every block's exact D [n][k/32] -- the production staging
+// and block_D code, with the fp32 scale-accumulate replaced by stores.
+size_t stream_dump_workspace_bytes(int64_t k);
+cudaError_t launch_stream_dump(const uint8_t *nib, const uint16_t *scale, int64_t n, int64_t k, const uint16_t *x,
+                               int8_t *q, float *sx, int32_t *sq, int32_t *D, void *ws, cudaStream_t s);
 
 // Batched decode (rows a5/a6): one weight pass per 64 tokens (gemm_kernel.cuh).
 // Used for m >= kGemmMinTokens when K % 256 == 0.  W4A8 reads the quant_a8

@@ -334,6 +334,24 @@ __device__ __forceinline__ void chunk_dp4a(uint32_t st, int nblk, int blk0, uint
     }
 }
 
+// DUMP engine (test entry): chunk_dp4a's blocks and block_D, storing each block's D.
+__device__ __forceinline__ void chunk_dump(uint32_t st, int nblk, int blk0, uint32_t K2, const ActSmem &L, int warp,
+                                           int lane, int64_t row0, int64_t n, int G, int32_t *dump_d)
+{
+    const int r = warp;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        const int b = lane + 32 * h;
+        if (b < nblk && row0 + r < n) {
+            const int g = blk0 + b;
+            const uint4 qa = lds128(L.act + 16u * g), qb = lds128(L.act + K2 + 16u * g);
+            const uint4 w = lds128(st + nib_off(r, b));
+            const uint2 p = lds64(L.ssq + 8u * g);
+            dump_d[(row0 + r) * G + g] = block_D(w, qa, qb, (int)p.y);
+        }
+    }
+}
+
 // One lane's activation operands for two Q4_0 blocks (q words, {s, 8 sum q} pairs).
 struct Dp4aAct {
     uint4 qa0, qb0, qa1, qb1;

@@ -86,6 +86,14 @@ __global__ void __launch_bounds__(kThreads, 2) stream_linear(const __grid_consta
         stage_a8<false>(xg, a.ldx, ntok, k, L, threadIdx.x, kConsumerWarps * 32);
     bar_consumers();
     if (a.trace) tr_ready = globaltimer();
+    if constexpr (E == DUMP) {
+        // test entry: CTA 0 copies the staged activations (q_lo | q_hi, then the {s, 8 sum q} pairs)
+        if (blockIdx.x == 0) {
+            const int nq = (int)(k / 4);   // q_lo | q_hi words of the one token
+            for (int w = threadIdx.x; w < nq + 2 * G; w += kConsumerWarps * 32)
+                a.dump_act[w] = w < nq ? lds32(L.act + 4u * (uint32_t)w) : lds32(L.ssq + 4u * (uint32_t)(w - nq));
+        }
+    }
 
     // ================= consumers: main loop =================
     uint32_t kNib2 = 0x000F000Fu, kMagic = 0x43004300u;      // in registers: one LOP3 per bf16 pair
@@ -105,6 +113,9 @@ __global__ void __launch_bounds__(kThreads, 2) stream_linear(const __grid_consta
             const uint32_t st = ring + (uint32_t)s * kStageBytes;
             if constexpr (E == DP4A)
                 chunk_dp4a(st, nblk, blk0, (uint32_t)K2, L, warp, lane, acc[0]);
+            else if constexpr (E == DUMP)
+                chunk_dump(st, nblk, blk0, (uint32_t)K2, L, warp, lane,
+                           (int64_t)(tile - a.tile_start[li]) * kTileRows, a.n[li], G, a.dump_d);
             else if constexpr (E != NONE)
                 chunk_mma<E>(st, nblk, blk0, (uint32_t)K2, L, G, ntok, warp, lane, kNib2, kMagic, acc);
             __syncwarp();
@@ -115,7 +126,9 @@ __global__ void __launch_bounds__(kThreads, 2) stream_linear(const __grid_consta
             }
         }
         const int64_t row0 = (int64_t)(tile - a.tile_start[li]) * kTileRows;
-        if constexpr (E == DP4A)
+        if constexpr (E == DUMP)
+            continue;
+        else if constexpr (E == DP4A)
             epilogue_dp4a(acc[0], row0, a.n[li], a.y[li], a.ydt, a.tok0 * a.ldy[li], warp, lane);
         else
             epilogue_mma(acc, red, row0, a.n[li], a.y[li], a.ydt, a.ldy[li], a.tok0, ntok, warp, lane);

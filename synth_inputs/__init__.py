@@ -140,6 +140,18 @@ def adversarial_activation(m: int, k: int, seed: int) -> torch.Tensor:
     return x.to(torch.bfloat16)
 
 
+def wide_range_activation(m: int, k: int, seed: int) -> torch.Tensor:
+    """Every 32-group spans ~14 binades (|x| from 2^-14 to 1, random signs) plus one x100
+    outlier: stresses fp32 cancellation in offset-code W4A16 accumulation."""
+    g = _gen(seed)
+    mag = torch.exp2(-14.0 * torch.rand(m, k, generator=g))
+    sgn = torch.where(torch.rand(m, k, generator=g) < 0.5, -1.0, 1.0)
+    x = (mag * sgn).view(m, k // 32, 32)
+    idx = torch.randint(0, 32, (m, k // 32, 1), generator=g)
+    x.scatter_(2, idx, x.gather(2, idx) * 100.0)
+    return x.view(m, k).to(torch.bfloat16)
+
+
 def bf16_to_f32_numpy(t: torch.Tensor):
     """Exact widening for the oracle (bf16 -> fp32 is exact)."""
     return t.float().numpy()

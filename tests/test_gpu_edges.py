@@ -1,0 +1,155 @@
+"""GPU parity on the inputs most likely to break the production engines (SURVEY §8(c)
+"Adversarial inputs"), and the column-shard data path (row a8) emulated P ways on one
+GPU.  Every check is against the CPU oracle on identical seeded inputs: integer stages
+bit-exact, outputs within reading T:
+    |y - y*| <= rtol * max(|y*_n|, rms(y*)),  y* = oracle fp64, rtol 1e-3 (fp32 out).
+
+Engines reached (K % 256 == 0, K >= 2048 unless noted):
+    M = 1 W4A8  -> stream_linear<DP4A> (fused quantiser a8_quad_store)
+    M = 1 W4A16 -> stream_linear<HMMA1>
+    M = 4       -> stream_linear<IMMA> / <HMMA>
+    M = 16, 64  -> gemm_w4<A8> / <A16>  (quant_a8 kernel + TMA-fed mma.sync)
+    bf16deq     -> tc05_w4a16 (tcgen05, reading A13')
+    stack       -> stack_step (row-lane DP4A, octet/quad quantisers, HMMA1)
+"""
+import numpy as np
+import pytest
+import torch
+
+import synth_inputs as si
+from test_gpu_parity import DEV, _assert_close, _f32, _pack_both, mq  # noqa: F401
+
+pytestmark = pytest.mark.gpu
+
+
+def _oracle_y64(orc, route, nib, sc, x):
+    if route == 0:
+        return orc.w4a8_from_x(nib, sc, _f32(x))[1]
+    return orc.w4a16(nib, sc, _f32(x))[1]
+
+
+# ---------------------------------------------------------------- adversarial inputs, every engine
+ENGINES = [(1, 0), (1, 1), (4, 0), (4, 1), (16, 0), (16, 1), (64, 0), (64, 1)]
+
+
+@pytest.mark.parametrize("k", [2048, 4096])
+@pytest.mark.parametrize("m,route", ENGINES)
+def test_adversarial_through_engines(mq, orc, m, route, k):
+    n = 176                                   # 11 row tiles of 16: ragged against every CTA tile
+    w = si.adversarial_weight(n, k, 2000 + k + m)
+    x = si.adversarial_activation(m, k, 2001 + k + m)
+    pw, nib, sc = _pack_both(mq, orc, w)
+    for out_dtype, rtol in ((torch.float32, 1e-3), (torch.bfloat16, 2e-3)):
+        y = mq.linear(route, pw, x.to(DEV), out_dtype=out_dtype)
+        _assert_close(y, _oracle_y64(orc, route, nib, sc, x), rtol)
+
+
+@pytest.mark.parametrize("m", [1, 4, 16, 64])
+def test_wide_range_activations_w4a16(mq, orc, m):
+    """W4A16 engines that accumulate (128 + c) x and add -136 sum x (HMMA1 / HMMA): groups
+    spanning ~14 binades with x100 outliers, where that correction cancels the most."""
+    n, k = 176, 4096
+    w = si.weight(n, k, 2101)
+    x = si.wide_range_activation(m, k, 2102 + m)
+    pw, nib, sc = _pack_both(mq, orc, w)
+    y = mq.linear(1, pw, x.to(DEV), out_dtype=torch.float32)
+    _assert_close(y, _oracle_y64(orc, 1, nib, sc, x), 1e-3)
+
+
+@pytest.mark.parametrize("m", [1, 16, 64])
+def test_adversarial_bf16deq(mq, orc, m):
+    n, k = 176, 2048
+    w = si.adversarial_weight(n, k, 2201 + m)
+    x = si.adversarial_activation(m, k, 2202 + m)
+    pw, nib, sc = _pack_both(mq, orc, w)
+    y = mq.w4a16_bf16deq(pw, x.to(DEV), out_dtype=torch.float32)
+    _, y64 = orc.w4a16_bf16deq(nib, sc, _f32(x))
+    _assert_close(y, y64, 1e-3)
+
+
+@pytest.mark.parametrize("k", [2048, 4096, 14336])
+def test_stream_quantiser_and_group_dots_bit_exact(mq, orc, k):
+    """The stream kernel's fused quantiser (a8_quad_store, its IEEE-division fallback near
+    half-integers, amax = 0 groups) and its block_D: q, sx, sq and every D bit-exact."""
+    n = 48
+    w = si.adversarial_weight(n, k, 2300 + k)
+    x = si.adversarial_activation(1, k, 2301 + k)
+    pw, nib, sc = _pack_both(mq, orc, w)
+    q, sx, sq, D = mq.stream_w4a8_dump(pw, x.to(DEV))
+    oq, os_, osq = orc.quant_a8(_f32(x))
+    torch.cuda.synchronize()
+    assert np.array_equal(q.cpu().numpy(), oq.reshape(-1))
+    assert np.array_equal(sx.cpu().numpy().view(np.uint32), os_.reshape(-1).view(np.uint32))
+    assert np.array_equal(sq.cpu().numpy(), osq.reshape(-1))
+    oD = orc.w4a8_group_dots(nib, oq, osq)
+    assert np.array_equal(D.cpu().numpy(), oD.reshape(n, k // 32))
+
+
+# ---------------------------------------------------------------- the persistent step on adversarial data
+ADV_STEP = {"q": (256, 2048), "k": (64, 2048), "v": (64, 2048), "o": (256, 2048), "gate": (512, 2048),
+            "up": (512, 2048), "down": (256, 4096)}
+ADV_INPUT = {"q": 0, "k": 0, "v": 0, "o": 1, "gate": 2, "up": 2, "down": 3}
+
+
+def test_step_kernel_adversarial(mq, orc):
+    """stack_step with adversarial weights and adversarial step inputs (every input a step
+    input: K = 2048 takes the octet quantiser, K = 4096 the quad quantiser), routes W4A8 and
+    W4A16; each linear against the oracle."""
+    routes = (0, 1)
+    st = mq.Stack(list(routes), max_m=1)
+    ops, xs = [], {}
+    for l in range(len(routes)):
+        for sid, (slot, (n, k)) in enumerate(ADV_STEP.items()):
+            key = (l, ADV_INPUT[slot])
+            if key not in xs:
+                xs[key] = si.adversarial_activation(1, k, 2400 + 16 * l + sid)
+                xs[key] = (xs[key], xs[key].to(DEV))
+            w = si.adversarial_weight(n, k, 2450 + 16 * l + sid)
+            pw = mq.pack_w4(w.to(DEV))
+            y = torch.empty(1, n, dtype=torch.float32, device=DEV)
+            st.set(l, sid, ADV_INPUT[slot], pw, xs[key][1], y)
+            ops.append((l, w, xs[key][0], y))
+    st.run(1)
+    torch.cuda.synchronize()
+    assert st.launches(1) == 1
+    for (l, w, x, y) in ops:
+        nib, sc = orc.pack_w4(_f32(w))
+        _assert_close(y, _oracle_y64(orc, routes[l], nib, sc, x), 1e-3)
+
+
+# ---------------------------------------------------------------- a8: P-way column shards on one GPU
+@pytest.mark.parametrize("P", [2, 4, 8])
+@pytest.mark.parametrize("m", [1, 64])
+@pytest.mark.parametrize("route", [0, 1])
+def test_colshard_emulated_vs_oracle(mq, orc, P, m, route):
+    """Rank r's linear on rows [r N/P, (r+1) N/P) into slot r of the rank-major buffer
+    (what mcapq_linear_colshard computes before the all-gather fills the other slots),
+    then mcapq_colshard_assemble: equal to the oracle's sharded linear (reading A22) and
+    bit-identical to the unsharded GPU call."""
+    n, k = 2048, 2048
+    w = si.weight(n, k, 2500 + P)
+    x = si.activation(m, k, 2501 + m)
+    pw, nib, sc = _pack_both(mq, orc, w)
+    xd = x.to(DEV)
+    per = n // P
+    y64 = _oracle_y64(orc, route, nib, sc, x)
+    for dt, rtol in ((torch.float32, 1e-3), (torch.bfloat16, 2e-3)):
+        rank_major = torch.empty(P, m, per, dtype=dt, device=DEV)
+        for r in range(P):
+            mq.linear(route, pw.shard(P, r), xd, out=rank_major[r])
+        y = mq.colshard_assemble(rank_major, P)
+        full = mq.linear(route, pw, xd, out_dtype=dt)
+        torch.cuda.synchronize()
+        assert torch.equal(y, full)
+        if dt == torch.float32:
+            _assert_close(y, y64, rtol)
+    y32c = orc.colshard_linear(route, nib, sc, _f32(x), P)
+    y32 = (orc.w4a8_from_x(nib, sc, _f32(x)) if route == 0 else orc.w4a16(nib, sc, _f32(x)))[0]
+    assert np.array_equal(y32c, y32)          # the oracle's own shard invariant
+
+
+def test_colshard_assemble_f32_ragged_m(mq):
+    P, m, per = 4, 5, 24
+    src = torch.randn(P, m, per, device=DEV)
+    y = mq.colshard_assemble(src, P)
+    assert torch.equal(y, src.permute(1, 0, 2).reshape(m, P * per))
