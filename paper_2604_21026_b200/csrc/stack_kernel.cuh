@@ -60,6 +60,7 @@ struct StackArgs {
     int spin_ns;                 // first back-off between re-reads of stale tagged words (doubles, <= 1 us)
     int polls;                   // CTA-wide re-read rounds before waiting on the producer's counter
     int ep_log2;                 // log2 of the tile slots between the consumers and the epilogue warp (1..3)
+    int hold;                    // 1: the producer holds ring refills while this CTA stages an input (see `hold`)
 };
 
 __device__ __forceinline__ unsigned int ld_acquire_gpu(const unsigned int *p)
@@ -75,6 +76,12 @@ __device__ __forceinline__ uint4 ld_relaxed_128(const void *p)
                  : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
                  : "l"(p)
                  : "memory");
+    return v;
+}
+__device__ __forceinline__ uint32_t lds32_volatile(uint32_t addr)
+{
+    uint32_t v;
+    asm volatile("ld.volatile.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr) : "memory");
     return v;
 }
 __device__ __forceinline__ bool tags_ok(uint4 a, uint32_t t16)
@@ -346,6 +353,11 @@ __global__ void __launch_bounds__(kStepThreads, 1) stack_step(const __grid_const
     const uint32_t EN = 1u << EL;         // tile slots (<= 8)
     const uint32_t epf = go + 8u;         // [EN] tile slot written by every consumer warp
     const uint32_t epe = go + 72u;        // [EN] tile slot stored out by the epilogue warp
+    // refill hold: set by the consumers from the last stage of a linear until the next
+    // linear's input is staged; the producer issues no ring refill meanwhile, so the
+    // latency-critical activation loads do not queue behind this SM's in-flight weight
+    // data (the refills it holds are for later linears: the current one is resident)
+    const uint32_t hold = go + 136u;
     const uint32_t act = sb + a.act_off;
     const uint32_t red = sb + a.red_off;  // [EN] tile slots: [16 warps][16 rows] fp32
     // this launch's tag (epoch + 1, never 0): the epoch only changes after every CTA left
@@ -358,6 +370,7 @@ __global__ void __launch_bounds__(kStepThreads, 1) stack_step(const __grid_const
             mbar_init(empty + 8u * s, kConsumerWarps);
         }
         mbar_init(go, 1);
+        sts32(hold, 0u);
         for (int j = 0; j < (int)EN; ++j) {
             mbar_init(epf + 8u * j, kConsumerWarps);
             mbar_init(epe + 8u * j, 1);
@@ -505,6 +518,8 @@ __global__ void __launch_bounds__(kStepThreads, 1) stack_step(const __grid_const
                     const int row0 = (tile - op.tile_start[li]) * kTileRows;
                     for (int ch = 0; ch < nchunks; ++ch) {
                         mbar_wait(empty + 8u * s, ph ^ 1u);
+                        if (a.hold)
+                            while (lds32_volatile(hold) != 0u) __nanosleep(32);
                         const uint32_t st = ring + (uint32_t)s * kStageBytes;
                         const uint32_t fb = full + 8u * s;
                         mbar_expect_tx(fb, (uint32_t)kStageBytes);
@@ -526,6 +541,9 @@ __global__ void __launch_bounds__(kStepThreads, 1) stack_step(const __grid_const
     asm volatile("" : "+r"(kNib2), "+r"(kMagic));
     int s = 0;
     uint32_t ph = 0, goph = 0, ts = 0;
+    auto hold_set = [&](uint32_t v) {
+        if (a.hold && threadIdx.x == 0) sts32(hold, v);
+    };
     for (int i = 0; i < a.nops; ++i) {
         const StackOp &op = ops[i];
         const int count = op.count, route = op.route;
@@ -547,10 +565,12 @@ __global__ void __launch_bounds__(kStepThreads, 1) stack_step(const __grid_const
             if (kTrace) tr1 = globaltimer();
             const bool a16 = route == MCAPQ_W4A16;
             const ActSmem L = act_layout(a16, act, k, 1);
+            hold_set(1u);
             bar_consumers();   // every warp is done reading the previous linear's activations
             if (!(a.flags & 4)) stage_step<kRounds>(kTrace ? &trm : nullptr, op, a16, L, threadIdx.x, t16, !(a.flags & 8), a.spin_ns, a.polls, a.counters,
                                                          !(a.flags & 128));
             bar_consumers();
+            hold_set(0u);
             if (kTrace) tr2 = globaltimer();
 
             if (!a16) {
@@ -580,6 +600,7 @@ __global__ void __launch_bounds__(kStepThreads, 1) stack_step(const __grid_const
                             if (!mbar_test(full + 8u * s, ph)) ++stalls;   // stage not resident yet
                         }
                         mbar_wait(full + 8u * s, ph);
+                        if (tile == t1 - 1 && ch == nchunks - 1) hold_set(1u);   // the linear's last stage is resident
                         if (kTrace && tile == t0 && ch == 0) tr3 = globaltimer();
                         const uint32_t st = ring + (uint32_t)s * kStageBytes;
                         const bool on0 = lam < nblk, on1 = lam + 32 < nblk;
@@ -629,6 +650,7 @@ __global__ void __launch_bounds__(kStepThreads, 1) stack_step(const __grid_const
                             if (!mbar_test(full + 8u * s, ph)) ++stalls;   // stage not resident yet
                         }
                         mbar_wait(full + 8u * s, ph);
+                        if (tile == t1 - 1 && ch == nchunks - 1) hold_set(1u);   // the linear's last stage is resident
                         if (kTrace && tile == t0 && ch == 0) tr3 = globaltimer();
                         const uint32_t st = ring + (uint32_t)s * kStageBytes;
                         if (!(a.flags & 1))
@@ -669,4 +691,5 @@ __global__ void __launch_bounds__(kStepThreads, 1) stack_step(const __grid_const
             r[7] = tr4;
         }
     }
+    hold_set(0u);   // never leave the producer held
 }
