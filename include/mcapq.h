@@ -211,6 +211,32 @@ mcapq_status mcapq_w4a16_bf16deq_prefill(const uint8_t *nib, const uint16_t *sca
                                          const uint16_t *x, int64_t m, int64_t ldx, void *y, int ydt, int64_t ldy,
                                          void *ws, size_t ws_bytes, void *stream);
 
+/*
+ * NEXT-2: greedy decode on the lm_head ("decode uses greedy (argmax) sampling
+ * throughout").  idx[i] = argmax_n y[i][n] of the routed linear's fp32
+ * outputs (exactly the values mcapq_linear writes with ydt = MCAPQ_F32), ties -> the
+ * lowest n (-0.0 == +0.0); val[i] = y[i][idx[i]] (val nullable).  idx: device [m] int64.
+ * M = 1 with K % 256 == 0, K >= 2048 fuses the reduction into the linear's epilogue (the
+ * logits never reach memory); otherwise the fp32 logits go to ws and a row reduction
+ * follows.  Non-finite logits give an unspecified index.  ws: >=
+ * mcapq_argmax_workspace_bytes(route, m, n, k, 1) device bytes, 16-byte aligned.
+ *
+ * mcapq_argmax_keys: the building block -- keys[i] (device uint64, [m], 8-byte aligned)
+ * = the largest of key(y[i][n], row_offset + n) over the n rows of this (shard of the)
+ * weight, key(v, j) = (the IEEE bits of v in unsigned total order) << 32 |
+ * (0xffffffff - j): unsigned max of keys = larger value, then smaller index, so shards
+ * combine in any order.  row_offset + n <= 2^32 - 1.  ws as above (unused on the fused
+ * path).  mcapq_argmax_combine: idx / val of the largest key over keys[p][i], p < parts.
+ */
+size_t mcapq_argmax_workspace_bytes(int route, int64_t m, int64_t n, int64_t k, int parts);
+mcapq_status mcapq_linear_argmax(int route, const uint8_t *nib, const uint16_t *scale, int64_t n, int64_t k,
+                                 const uint16_t *x, int64_t m, int64_t ldx, int64_t *idx, float *val, void *ws,
+                                 size_t ws_bytes, void *stream);
+mcapq_status mcapq_argmax_keys(int route, const uint8_t *nib, const uint16_t *scale, int64_t n, int64_t k,
+                               const uint16_t *x, int64_t m, int64_t ldx, int64_t row_offset, uint64_t *keys,
+                               void *ws, size_t ws_bytes, void *stream);
+mcapq_status mcapq_argmax_combine(const uint64_t *keys, int parts, int64_t m, int64_t *idx, float *val, void *stream);
+
 /* Routed linear: route MCAPQ_W4A8 -> mcapq_w4a8_x, MCAPQ_W4A16 -> mcapq_w4a16. */
 mcapq_status mcapq_linear(int route, const uint8_t *nib, const uint16_t *scale, int64_t n, int64_t k,
                           const uint16_t *x, int64_t m, int64_t ldx, void *y, int ydt, int64_t ldy, void *ws,
@@ -412,6 +438,18 @@ mcapq_status mcapq_linear_colshard(const mcapq_comm *c, int route, const uint8_t
                                    int64_t m, void *y_full, int ydt, void *ws, size_t ws_bytes, void *stream);
 mcapq_status mcapq_colshard_assemble(const void *rank_major, void *y_full, int64_t m, int64_t n_full, int world,
                                      int ydt, void *stream);
+/*
+ * a8 + NEXT-2: the column-sharded lm_head with a LOCAL argmax (greedy decode): rank r
+ * reduces its N/P rows to m argmax keys (global row indices, mcapq_argmax_keys), an
+ * all-gather moves P x m 8-byte keys instead of the m x N logits (M = 64, 8B lm_head:
+ * 4 KB instead of 16.4 MB), and every rank combines them: idx / val exactly as
+ * mcapq_linear_argmax on the unsharded weight.  ws: >= mcapq_argmax_workspace_bytes(route,
+ * m, n_full / world, k, world).
+ */
+mcapq_status mcapq_linear_colshard_argmax(const mcapq_comm *c, int route, const uint8_t *nib_shard,
+                                          const uint16_t *scale_shard, int64_t n_full, int64_t k, const uint16_t *x,
+                                          int64_t m, int64_t *idx, float *val, void *ws, size_t ws_bytes,
+                                          void *stream);
 void mcapq_comm_destroy(mcapq_comm *c);
 
 #ifdef __cplusplus

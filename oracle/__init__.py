@@ -356,3 +356,40 @@ def colshard_linear(route: int, nib, scale, x, world: int):
             y32, _ = w4a16(nib[a:b], scale[a:b], x)
         outs.append(y32)
     return np.concatenate(outs, axis=1)
+
+
+# --------------------------------------------------------------------------
+# NEXT-2: greedy decode ("decode uses greedy (argmax) sampling")
+def argmax_first(y):
+    """Per row of y: the index of the largest value, the FIRST such index on ties
+    (a plain left-to-right scan with IEEE '>' -- so -0.0 == +0.0 ties too).  y: [n]
+    or [m, n] float; returns an int64 array [m] (or a scalar for 1-D y)."""
+    a = np.asarray(y)
+    rows = a.reshape(1, -1) if a.ndim == 1 else a
+    out = np.empty(rows.shape[0], dtype=np.int64)
+    for i in range(rows.shape[0]):
+        r = rows[i].tolist()
+        best, bi = r[0], 0
+        for j in range(1, len(r)):
+            if r[j] > best:
+                best, bi = r[j], j
+        out[i] = bi
+    return int(out[0]) if a.ndim == 1 else out
+
+
+def colshard_argmax(y, world: int):
+    """The sharded greedy decode: each of `world` contiguous row shards (A22) takes its
+    local argmax_first, then the winner is the largest local maximum, the lowest rank on
+    ties (== the first global index).  y: [m, n] logits."""
+    a = np.asarray(y)
+    m, n = a.shape
+    out = np.empty(m, dtype=np.int64)
+    for i in range(m):
+        best_v, best_j = None, -1
+        for r in range(world):
+            lo, hi = colshard_rows(n, world, r)
+            j = lo + argmax_first(a[i, lo:hi])
+            if best_v is None or a[i, j] > best_v:
+                best_v, best_j = a[i, j], j
+        out[i] = best_j
+    return out

@@ -28,7 +28,8 @@ __all__ = [
     "w4a16_bf16deq", "dequant_w4_bf16", "bf16w_gemm", "w4a16_bf16deq_prefill",
     "linear", "linear_group", "linear_host", "w4a8_group_dots", "workspace_bytes", "host_workspace_bytes", "Profile",
     "profile_parse", "profile_write_json", "mcap_accumulate", "Stack", "Comm", "linear_colshard", "PackedW4",
-    "colshard_assemble", "stream_w4a8_dump",
+    "colshard_assemble", "stream_w4a8_dump", "linear_argmax", "argmax_keys", "argmax_combine",
+    "argmax_workspace_bytes", "linear_colshard_argmax",
     "device_sms", "set_pdl",
 ]
 
@@ -246,6 +247,51 @@ def linear(route: int, w: PackedW4, x: torch.Tensor, out_dtype=torch.float32, ou
     check(load().mcapq_linear(route, _ptr(w.nib), _ptr(w.scale), w.n, w.k, _ptr(x2), m, x2.stride(0), _ptr(y),
                               _dt(y.dtype), y.stride(0), _ptr(ws), ws.numel(), _stream(stream)), "mcapq_linear")
     return y
+
+
+def argmax_workspace_bytes(route: int, m: int, n: int, k: int, parts: int = 1) -> int:
+    return load().mcapq_argmax_workspace_bytes(route, m, n, k, parts)
+
+
+def linear_argmax(route: int, w: PackedW4, x: torch.Tensor, ws=None, stream=None):
+    """NEXT-2 greedy decode: (idx int64 [M], val fp32 [M]) = argmax over the N outputs of the
+    routed linear's fp32 logits, ties -> lowest index (mcapq_linear_argmax)."""
+    _need_cuda(w.nib)
+    x2 = _act(x, w.k)
+    m = x2.shape[0]
+    idx = torch.empty(m, dtype=torch.int64, device=x.device)
+    val = torch.empty(m, dtype=torch.float32, device=x.device)
+    ws = ws if ws is not None else _scratch(argmax_workspace_bytes(route, m, w.n, w.k), x.device, stream)
+    check(load().mcapq_linear_argmax(route, _ptr(w.nib), _ptr(w.scale), w.n, w.k, _ptr(x2), m, x2.stride(0), _ptr(idx),
+                                     _ptr(val), _ptr(ws), ws.numel(), _stream(stream)), "mcapq_linear_argmax")
+    return idx, val
+
+
+def argmax_keys(route: int, w: PackedW4, x: torch.Tensor, row_offset: int = 0, out=None, ws=None, stream=None):
+    """NEXT-2 building block: per-token 64-bit argmax keys (as int64 bits) of this (shard of
+    the) weight, global row index = row_offset + n (mcapq_argmax_keys)."""
+    _need_cuda(w.nib)
+    x2 = _act(x, w.k)
+    m = x2.shape[0]
+    keys = out if out is not None else torch.empty(m, dtype=torch.int64, device=x.device)
+    ws = ws if ws is not None else _scratch(argmax_workspace_bytes(route, m, w.n, w.k), x.device, stream)
+    check(load().mcapq_argmax_keys(route, _ptr(w.nib), _ptr(w.scale), w.n, w.k, _ptr(x2), m, x2.stride(0),
+                                   int(row_offset), _ptr(keys), _ptr(ws), ws.numel(), _stream(stream)),
+          "mcapq_argmax_keys")
+    return keys
+
+
+def argmax_combine(keys: torch.Tensor, stream=None):
+    """(idx, val) of the largest key over the parts: keys int64 [P, M] (mcapq_argmax_combine)."""
+    _need_cuda(keys)
+    k2 = keys if keys.dim() == 2 else keys.view(1, -1)
+    assert k2.dtype == torch.int64 and k2.is_contiguous()
+    parts, m = k2.shape
+    idx = torch.empty(m, dtype=torch.int64, device=keys.device)
+    val = torch.empty(m, dtype=torch.float32, device=keys.device)
+    check(load().mcapq_argmax_combine(_ptr(k2), parts, m, _ptr(idx), _ptr(val), _stream(stream)),
+          "mcapq_argmax_combine")
+    return idx, val
 
 
 def linear_group(route: int, ws_list, x: torch.Tensor, out_dtype=torch.float32, outs=None, ws=None, stream=None):
@@ -480,6 +526,21 @@ def colshard_assemble(rank_major: torch.Tensor, world: int, out=None, stream=Non
     check(load().mcapq_colshard_assemble(_ptr(rank_major), _ptr(y), m, P * per, world, _dt(y.dtype),
                                          _stream(stream)), "mcapq_colshard_assemble")
     return y
+
+
+def linear_colshard_argmax(comm: Comm, route: int, w_shard: PackedW4, n_full: int, x: torch.Tensor, ws=None,
+                           stream=None):
+    """a8 + NEXT-2: column-sharded lm_head with a local argmax and a P x M key all-gather."""
+    x2 = _act(x, w_shard.k)
+    m = x2.shape[0]
+    idx = torch.empty(m, dtype=torch.int64, device=x.device)
+    val = torch.empty(m, dtype=torch.float32, device=x.device)
+    ws = ws if ws is not None else _scratch(
+        argmax_workspace_bytes(route, m, n_full // comm.world, w_shard.k, comm.world), x.device, stream)
+    check(load().mcapq_linear_colshard_argmax(comm._h, route, _ptr(w_shard.nib), _ptr(w_shard.scale), n_full,
+                                              w_shard.k, _ptr(x2), m, _ptr(idx), _ptr(val), _ptr(ws), ws.numel(),
+                                              _stream(stream)), "mcapq_linear_colshard_argmax")
+    return idx, val
 
 
 def linear_colshard(comm: Comm, route: int, w_shard: PackedW4, n_full: int, x: torch.Tensor,

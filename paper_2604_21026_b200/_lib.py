@@ -39,6 +39,10 @@ SIGNATURES = {
     "mcapq_dequant_w4_bf16": (I32, [P, P, I64, I64, P, P]),
     "mcapq_bf16w_gemm": (I32, [P, I64, I64, P, I64, I64, P, I32, I64, P]),
     "mcapq_w4a16_bf16deq_prefill": (I32, [P, P, I64, I64, P, I64, I64, P, I32, I64, P, SZ, P]),
+    "mcapq_argmax_workspace_bytes": (SZ, [I32, I64, I64, I64, I32]),
+    "mcapq_linear_argmax": (I32, [I32, P, P, I64, I64, P, I64, I64, P, P, P, SZ, P]),
+    "mcapq_argmax_keys": (I32, [I32, P, P, I64, I64, P, I64, I64, I64, P, P, SZ, P]),
+    "mcapq_argmax_combine": (I32, [P, I32, I64, P, P, P]),
     "mcapq_linear": (I32, [I32, P, P, I64, I64, P, I64, I64, P, I32, I64, P, SZ, P]),
     "mcapq_linear_group": (I32, [I32, I32, P, P, P, I64, P, I64, I64, P, I32, P, P, SZ, P]),
     "mcapq_host_workspace_bytes": (SZ, [I32, I64, I64, I64]),
@@ -72,6 +76,7 @@ SIGNATURES = {
     "mcapq_colshard_workspace_bytes": (SZ, [I32, I64, I64, I64, I32]),
     "mcapq_linear_colshard": (I32, [P, I32, P, P, I64, I64, P, I64, P, I32, P, SZ, P]),
     "mcapq_colshard_assemble": (I32, [P, P, I64, I64, I32, I32, P]),
+    "mcapq_linear_colshard_argmax": (I32, [P, I32, P, P, I64, I64, P, I64, P, P, P, SZ, P]),
     "mcapq_comm_destroy": (None, [P]),
 }
 

@@ -405,6 +405,77 @@ mcapq_status mcapq_linear_group(int route, int count, const uint8_t *const *nibs
     return MCAPQ_OK;
 }
 
+// ------------------------------------------------------------------ NEXT-2 greedy decode
+static bool argmax_fused_path(int64_t m, int64_t k, const uint16_t *scale)
+{
+    return m == 1 && stream_supported(k) && aligned16(scale);
+}
+
+size_t mcapq_argmax_workspace_bytes(int route, int64_t m, int64_t n, int64_t k, int parts)
+{
+    if (m < 1 || n < 1 || k < 32 || parts < 1) return 0;
+    // keys [parts][m] | fp32 logits [m][n] (off the fused path) | the routed linear's workspace
+    return align256((size_t)(parts * m) * 8) + align256((size_t)(m * n) * 4) + mcapq_workspace_bytes(route, m, n, k);
+}
+
+mcapq_status mcapq_argmax_keys(int route, const uint8_t *nib, const uint16_t *scale, int64_t n, int64_t k,
+                               const uint16_t *x, int64_t m, int64_t ldx, int64_t row_offset, uint64_t *keys,
+                               void *ws, size_t ws_bytes, void *stream)
+{
+    clear_error();
+    CHECK_SHAPE(n, k, m);
+    mcapq_status st = check_weight(nib, scale, n, k);
+    if (st != MCAPQ_OK) return st;
+    CHECK_PTR(x, "x");
+    CHECK_PTR(keys, "keys");
+    CHECK_AL16(x, "x");
+    CHECK_LD(ldx, k, "ldx");
+    MCAPQ_REQUIRE(route == MCAPQ_W4A8 || route == MCAPQ_W4A16, MCAPQ_EINVAL, "bad route %d", route);
+    MCAPQ_REQUIRE(row_offset >= 0 && row_offset + n <= 0xffffffffll, MCAPQ_ERANGE, "row indices must fit 32 bits");
+    MCAPQ_REQUIRE((reinterpret_cast<uintptr_t>(keys) & 7u) == 0, MCAPQ_EINVAL, "keys is not 8-byte aligned");
+    cudaStream_t s = as_stream(stream);
+    unsigned long long *k64 = reinterpret_cast<unsigned long long *>(keys);
+    if (argmax_fused_path(m, k, scale) && ldx == k) {
+        LAUNCH_TRY(launch_argmax_fused(route, nib, scale, n, k, x, row_offset, k64, s));
+        return MCAPQ_OK;
+    }
+    CHECK_PTR(ws, "ws");
+    CHECK_AL16(ws, "ws");
+    const size_t lb = align256((size_t)(m * n) * 4);
+    MCAPQ_REQUIRE(ws_bytes >= lb + mcapq_workspace_bytes(route, m, n, k), MCAPQ_ENOSPACE, "workspace too small");
+    float *logits = reinterpret_cast<float *>(ws);
+    st = mcapq_linear(route, nib, scale, n, k, x, m, ldx, logits, MCAPQ_F32, n, reinterpret_cast<uint8_t *>(ws) + lb,
+                      ws_bytes - lb, stream);
+    if (st != MCAPQ_OK) return st;
+    LAUNCH_TRY(launch_argmax_rows(logits, m, n, n, row_offset, k64, s));
+    return MCAPQ_OK;
+}
+
+mcapq_status mcapq_argmax_combine(const uint64_t *keys, int parts, int64_t m, int64_t *idx, float *val, void *stream)
+{
+    clear_error();
+    MCAPQ_REQUIRE(keys && idx && parts >= 1 && m >= 1, MCAPQ_EINVAL, "bad argmax_combine arguments");
+    LAUNCH_TRY(launch_argmax_combine(reinterpret_cast<const unsigned long long *>(keys), parts, m, idx, val,
+                                     as_stream(stream)));
+    return MCAPQ_OK;
+}
+
+mcapq_status mcapq_linear_argmax(int route, const uint8_t *nib, const uint16_t *scale, int64_t n, int64_t k,
+                                 const uint16_t *x, int64_t m, int64_t ldx, int64_t *idx, float *val, void *ws,
+                                 size_t ws_bytes, void *stream)
+{
+    clear_error();
+    CHECK_PTR(ws, "ws");
+    CHECK_AL16(ws, "ws");
+    MCAPQ_REQUIRE(ws_bytes >= mcapq_argmax_workspace_bytes(route, m, n, k, 1), MCAPQ_ENOSPACE, "workspace too small");
+    uint64_t *keys = reinterpret_cast<uint64_t *>(ws);
+    const size_t kb = align256((size_t)m * 8);
+    mcapq_status st = mcapq_argmax_keys(route, nib, scale, n, k, x, m, ldx, 0, keys, reinterpret_cast<uint8_t *>(ws) + kb,
+                                        ws_bytes - kb, stream);
+    if (st != MCAPQ_OK) return st;
+    return mcapq_argmax_combine(keys, 1, m, idx, val, stream);
+}
+
 size_t mcapq_host_workspace_bytes(int route, int64_t m, int64_t n, int64_t k)
 {
     if (m < 1 || n < 1 || k < 32) return 0;

@@ -154,6 +154,29 @@ mcapq_status mcapq_linear_colshard(const mcapq_comm *c, int route, const uint8_t
     return MCAPQ_OK;
 }
 
+mcapq_status mcapq_linear_colshard_argmax(const mcapq_comm *c, int route, const uint8_t *nib_shard,
+                                          const uint16_t *scale_shard, int64_t n_full, int64_t k, const uint16_t *x,
+                                          int64_t m, int64_t *idx, float *val, void *ws, size_t ws_bytes, void *stream)
+{
+    clear_error();
+    MCAPQ_REQUIRE(c && c->comm, MCAPQ_EINVAL, "communicator is NULL");
+    MCAPQ_REQUIRE(n_full % c->world == 0, MCAPQ_EINVAL, "N=%lld not divisible by P=%d", (long long)n_full, c->world);
+    MCAPQ_REQUIRE(ws && aligned16(ws), MCAPQ_EINVAL, "NULL/misaligned ws");
+    const int64_t per = n_full / c->world;
+    MCAPQ_REQUIRE(ws_bytes >= mcapq_argmax_workspace_bytes(route, m, per, k, c->world), MCAPQ_ENOSPACE,
+                  "workspace too small");
+    // rank r's keys (global row indices r N/P + n) into slot r of [P][m]; the all-gather of
+    // P x m 8-byte keys replaces the m x N logit gather; every rank combines the same keys
+    uint64_t *keys = reinterpret_cast<uint64_t *>(ws);
+    const size_t kb = align256((size_t)(c->world * m) * 8);
+    mcapq_status st = mcapq_argmax_keys(route, nib_shard, scale_shard, per, k, x, m, k, (int64_t)c->rank * per,
+                                        keys + (size_t)c->rank * m, reinterpret_cast<uint8_t *>(ws) + kb, ws_bytes - kb,
+                                        stream);
+    if (st != MCAPQ_OK) return st;
+    NCCL_TRY(ncclAllGather(keys + (size_t)c->rank * m, keys, (size_t)m, ncclUint64, c->comm, as_stream(stream)));
+    return mcapq_argmax_combine(keys, c->world, m, idx, val, stream);
+}
+
 void mcapq_comm_destroy(mcapq_comm *c)
 {
     if (!c) return;

@@ -856,6 +856,93 @@ size_t stream_trace_read(unsigned long long *host_out, size_t max_records)
     return n;
 }
 
+// ------------------------------------------------------------------ NEXT-2 greedy decode
+namespace {
+// keys[i] = max_n argmax_key(logits[i][n], row_off + n): one CTA per token row
+__global__ void argmax_rows_kernel(const float *__restrict__ logits, int64_t n, int64_t ld, int64_t row_off,
+                                   unsigned long long *keys)
+{
+    __shared__ unsigned long long wbest[32];
+    const float *row = logits + (int64_t)blockIdx.x * ld;
+    unsigned long long best = 0ull;
+    for (int64_t j = threadIdx.x; j < n; j += blockDim.x) {
+        const unsigned long long key = argmax_key(row[j], row_off + j);
+        best = key > best ? key : best;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const unsigned long long v = __shfl_xor_sync(0xffffffffu, best, o);
+        best = v > best ? v : best;
+    }
+    if ((threadIdx.x & 31) == 0) wbest[threadIdx.x >> 5] = best;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        best = threadIdx.x < blockDim.x / 32 ? wbest[threadIdx.x] : 0ull;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const unsigned long long v = __shfl_xor_sync(0xffffffffu, best, o);
+            best = v > best ? v : best;
+        }
+        if (threadIdx.x == 0) keys[blockIdx.x] = best;
+    }
+}
+
+__global__ void argmax_combine_kernel(const unsigned long long *keys, int parts, int64_t m, int64_t *idx, float *val)
+{
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) {
+        unsigned long long best = 0ull;
+        for (int p = 0; p < parts; ++p) {
+            const unsigned long long v = keys[(int64_t)p * m + i];
+            best = v > best ? v : best;
+        }
+        idx[i] = (int64_t)(0xffffffffu - (uint32_t)(best & 0xffffffffull));
+        if (val) val[i] = argmax_key_value(best);
+    }
+}
+}  // namespace
+
+cudaError_t launch_argmax_rows(const float *logits, int64_t m, int64_t n, int64_t ld, int64_t row_off,
+                               unsigned long long *keys, cudaStream_t s)
+{
+    argmax_rows_kernel<<<(unsigned)m, 512, 0, s>>>(logits, n, ld, row_off, keys);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_argmax_combine(const unsigned long long *keys, int parts, int64_t m, int64_t *idx, float *val,
+                                  cudaStream_t s)
+{
+    argmax_combine_kernel<<<(unsigned)((m + 255) / 256), 256, 0, s>>>(keys, parts, m, idx, val);
+    return cudaGetLastError();
+}
+
+// M = 1 on the stream path: the linear's epilogue folds every row into the argmax key
+cudaError_t launch_argmax_fused(int route, const uint8_t *nib, const uint16_t *scale, int64_t n, int64_t k,
+                                const uint16_t *x, int64_t row_off, unsigned long long *key, cudaStream_t s)
+{
+    cudaError_t e = cudaMemsetAsync(key, 0, sizeof(unsigned long long), s);
+    if (e != cudaSuccess) return e;
+    StreamArgs a;
+    memset(&a, 0, sizeof(a));
+    a.count = 1;
+    if (!encode_maps(&a.maps[0][0], &a.maps[0][1], nib, scale, n, k)) return cudaErrorInvalidValue;
+    a.n[0] = n;
+    a.ldy[0] = n;
+    a.tile_start[0] = 0;
+    a.tile_start[1] = (int)((n + kTileRows - 1) / kTileRows);
+    a.k = k;
+    a.x = x;
+    a.ldx = k;
+    a.ntok = 1;
+    a.ydt = MCAPQ_F32;
+    a.amax_key = key;
+    a.amax_off = row_off;
+    const int per_sm = tune().ctas_per_sm ? tune().ctas_per_sm : (a.tile_start[1] >= 16 * device_sms() ? 2 : 1);
+    a.smem_kb = (!tune().smem_kb_env && per_sm == 1 && k >= 8192) ? 130 : 0;
+    const bool pdl = tune().pdl || api_pdl();
+    return route == MCAPQ_W4A16 ? launch_one<HMMA1>(a, s, pdl, device_sms() * per_sm)
+                                : launch_one<DP4A>(a, s, pdl, device_sms() * per_sm);
+}
+
 namespace {
 // q [k] int8, sx / sq [G] from the DUMP engine's copy of the staged activations
 __global__ void unpack_stream_dump(const uint32_t *act, int64_t k, int8_t *q, float *sx, int32_t *sq)

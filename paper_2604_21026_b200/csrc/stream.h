@@ -47,6 +47,11 @@ struct StreamArgs {
     int smem_kb;     // host side: shared-memory plan of this launch (plan_smem)
     int32_t *dump_d;     // DUMP engine: D [n][k/32] int32
     uint32_t *dump_act;  // DUMP engine: CTA 0's staged activations (q_lo|q_hi bytes, then {s, 8 sum q} pairs)
+    // NEXT-2 greedy-decode mode (one linear, one token): no y is stored; each row's fp32
+    // output y_n becomes the key argmax_key(y_n, amax_off + n) and the largest key of
+    // the launch is atomicMax-ed into *amax_key (zeroed by the launcher first)
+    unsigned long long *amax_key;
+    int64_t amax_off;
 };
 
 // Debug timeline (MCAPQ_STREAM_TRACE=1): per CTA {launch, block, t_start, t_wait,
@@ -86,6 +91,17 @@ cudaError_t launch_stack_step(const void *ops_dev, int nops, unsigned int *count
 // kernels (host only; false if the driver entry point is missing or encoding fails).
 bool encode_maps(CUtensorMap *tn, CUtensorMap *ts, const uint8_t *nib, const uint16_t *scale, int64_t n, int64_t k);
 int stream_tokens_per_pass(int route, int64_t k);
+// NEXT-2: per-token argmax keys of a routed linear's fp32 outputs, row indices offset by
+// row_off: keys[i] = max_n argmax_key(y[i][n], row_off + n).  M = 1 on the stream path:
+// fused into the linear's epilogue (the logits never reach memory); otherwise the fp32
+// logits go to ws (argmax_logits_bytes) and a row-reduction kernel takes the keys.
+cudaError_t launch_argmax_fused(int route, const uint8_t *nib, const uint16_t *scale, int64_t n, int64_t k,
+                                const uint16_t *x, int64_t row_off, unsigned long long *key, cudaStream_t s);
+cudaError_t launch_argmax_rows(const float *logits, int64_t m, int64_t n, int64_t ld, int64_t row_off,
+                               unsigned long long *keys, cudaStream_t s);
+// idx[i] / val[i] from the largest of keys[p][i] over p < parts (any order: max is exact)
+cudaError_t launch_argmax_combine(const unsigned long long *keys, int parts, int64_t m, int64_t *idx, float *val,
+                                  cudaStream_t s);
 // TEST ENTRY (DUMP engine, one token, W4A8): the stream kernel's fused quantiser output
 // (q [k] int8, sx/sq [k/32]) and every block's exact D [n][k/32] -- the production staging
 // and block_D code, with the fp32 scale-accumulate replaced by stores.

@@ -442,6 +442,24 @@ __device__ __forceinline__ void chunk_mma(uint32_t st, int nblk, int blk0, uint3
     }
 }
 
+// ---------------------------------------------------------------- argmax keys (NEXT-2)
+// A 64-bit key whose unsigned order is "larger fp32 value first, then smaller index":
+// high word = the IEEE bits mapped to an unsigned total order (-0 folded onto +0, so
+// equal values tie), low word = 0xffffffff - index.  max() over keys is exact and
+// order-independent: any reduction tree gives the same argmax (first index on ties).
+__device__ __forceinline__ unsigned long long argmax_key(float v, int64_t idx)
+{
+    uint32_t b = __float_as_uint(v);
+    if (b == 0x80000000u) b = 0u;
+    const uint32_t ord = (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+    return ((unsigned long long)ord << 32) | (unsigned long long)(0xffffffffu - (uint32_t)idx);
+}
+__device__ __forceinline__ float argmax_key_value(unsigned long long key)
+{
+    const uint32_t ord = (uint32_t)(key >> 32);
+    return __uint_as_float((ord & 0x80000000u) ? (ord & 0x7fffffffu) : ~ord);
+}
+
 // ---------------------------------------------------------------- tile epilogues
 // DP4A: fixed xor butterfly; lane 0 of warp w stores row row0 + w.
 __device__ __forceinline__ void epilogue_dp4a(float acc, int64_t row0, int64_t n, void *y, int ydt, int64_t off, int warp,
@@ -455,9 +473,25 @@ __device__ __forceinline__ void epilogue_dp4a(float acc, int64_t row0, int64_t n
     }
 }
 
+// DP4A epilogue in greedy-decode mode: the same butterfly, the row's value folded into
+// lane 0's running argmax key instead of stored
+__device__ __forceinline__ void epilogue_dp4a_amax(float acc, int64_t row0, int64_t n, int64_t off, int warp, int lane,
+                                                   unsigned long long &best)
+{
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    const int64_t row = row0 + warp;
+    if (lane == 0 && row < n) {
+        const unsigned long long key = argmax_key(acc, off + row);
+        best = key > best ? key : best;
+    }
+}
+
 // MMA: fixed-order cross-warp reduction through shared memory (red: 16 warps x 512 B).
+// best != nullptr: greedy-decode mode (token 0's rows folded into a running argmax key).
 __device__ __forceinline__ void epilogue_mma(const float acc[4], uint32_t red, int64_t row0, int64_t n, void *y,
-                                             int ydt, int64_t ldy, int64_t tok0, int ntok, int warp, int lane)
+                                             int ydt, int64_t ldy, int64_t tok0, int ntok, int warp, int lane,
+                                             unsigned long long *best = nullptr, int64_t amax_off = 0)
 {
     const int gid = lane >> 2, t = lane & 3;
     const uint32_t rw = red + 512u * warp;
@@ -474,7 +508,14 @@ __device__ __forceinline__ void epilogue_mma(const float acc[4], uint32_t red, i
 #pragma unroll
         for (int w = 1; w < kConsumerWarps; ++w) sum += __uint_as_float(lds32(red + 512u * w + 4u * tid));
         const int64_t row = row0 + r;
-        if (row < n && tk < ntok) dev::store_out(y, ydt, (tok0 + tk) * ldy + row, sum);
+        if (best) {
+            if (row < n && tk == 0) {
+                const unsigned long long key = argmax_key(sum, amax_off + row);
+                *best = key > *best ? key : *best;
+            }
+        } else if (row < n && tk < ntok) {
+            dev::store_out(y, ydt, (tok0 + tk) * ldy + row, sum);
+        }
     }
     bar_consumers();
 }

@@ -29,11 +29,13 @@ __global__ void __launch_bounds__(kThreads, 2) stream_linear(const __grid_consta
     const int t0 = (int)(((int64_t)T * blockIdx.x) / gridDim.x);
     const int t1 = (int)(((int64_t)T * (blockIdx.x + 1)) / gridDim.x);
 
+    const uint32_t amax_slot = full + 480u;                      // greedy-decode mode: the CTA's best key
     if (threadIdx.x == 0) {
         for (int s = 0; s < S; ++s) {
             mbar_init(full + 8u * s, 1);
             mbar_init(empty + 8u * s, kConsumerWarps);
         }
+        asm volatile("st.shared.u64 [%0], %1;" ::"r"(amax_slot), "l"(0ull) : "memory");
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
@@ -101,6 +103,7 @@ __global__ void __launch_bounds__(kThreads, 2) stream_linear(const __grid_consta
     int s = 0;
     uint32_t ph = 0;
     int li = 0;
+    unsigned long long best = 0ull;   // greedy-decode mode: this thread's running argmax key
     for (int tile = t0; tile < t1; ++tile) {
         while (li + 1 < a.count && tile >= a.tile_start[li + 1]) ++li;
         float acc[4] = {0.f, 0.f, 0.f, 0.f};
@@ -126,12 +129,27 @@ __global__ void __launch_bounds__(kThreads, 2) stream_linear(const __grid_consta
             }
         }
         const int64_t row0 = (int64_t)(tile - a.tile_start[li]) * kTileRows;
-        if constexpr (E == DUMP)
+        if constexpr (E == DUMP) {
             continue;
-        else if constexpr (E == DP4A)
-            epilogue_dp4a(acc[0], row0, a.n[li], a.y[li], a.ydt, a.tok0 * a.ldy[li], warp, lane);
-        else
-            epilogue_mma(acc, red, row0, a.n[li], a.y[li], a.ydt, a.ldy[li], a.tok0, ntok, warp, lane);
+        } else if constexpr (E == DP4A) {
+            if (a.amax_key)
+                epilogue_dp4a_amax(acc[0], row0, a.n[li], a.amax_off, warp, lane, best);
+            else
+                epilogue_dp4a(acc[0], row0, a.n[li], a.y[li], a.ydt, a.tok0 * a.ldy[li], warp, lane);
+        } else {
+            epilogue_mma(acc, red, row0, a.n[li], a.y[li], a.ydt, a.ldy[li], a.tok0, ntok, warp, lane,
+                         a.amax_key ? &best : nullptr, a.amax_off);
+        }
+    }
+    if (a.amax_key) {
+        // greedy decode: CTA maximum in shared memory, then one global atomic per CTA
+        if (best) asm volatile("atom.shared.max.u64 %0, [%1], %2;" : "=l"(best) : "r"(amax_slot), "l"(best) : "memory");
+        bar_consumers();
+        if (threadIdx.x == 0) {
+            unsigned long long v;
+            asm volatile("ld.shared.u64 %0, [%1];" : "=l"(v) : "r"(amax_slot) : "memory");
+            if (v) atomicMax(a.amax_key, v);
+        }
     }
     if (a.trace && threadIdx.x == 0) {
         unsigned long long *r = a.trace + 8ull * (unsigned long long)blockIdx.x;
