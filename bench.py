@@ -10,9 +10,12 @@ weights/activations (synth_inputs), random-init, no checkpoints.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
-N > 1 (torchrun): every rank runs its own replica of the stack (independent
-decode streams; "scaling": "weak"); the column-sharded lm_head/MLP with its
-NCCL all-gather is measured by `--workload lmhead`.  One JSON line on rank 0.
+N > 1 (torchrun, or self-launched when --gpus N is given without a launcher): every
+rank runs its own replica of the stack (independent decode streams; "scaling":
+"weak": the 1B step does not shard), and the line's `sharded`
+object carries the column-sharded Llama-3.1-8B lm_head (M = 1, 64) and MLP gate /
+down with their NCCL all-gather: T(1), T(P), comm us and E(P) = T(1) / (P T(P)).
+One JSON line on rank 0.
 """
 from __future__ import annotations
 
@@ -237,44 +240,101 @@ def time_dominant_kernel(mq, weights, xs, stream, reps_per_layer=4):
     return per_launch_ms, alg_bytes, len(seq)
 
 
-def time_colshard_lm_head(mq, dev, stream, dist, world, rank, m=1, reps=20):
-    """cfg5 a8: the 8B lm_head (128256 x 4096) column-sharded over the job's ranks, each
-    rank computing its N/P rows and all-gathering y over NCCL (mcapq_linear_colshard),
-    captured in a CUDA graph.  Per-call time = max over ranks (CUDA events)."""
-    n, k = si.linear_shape("llama-3.1-8b", "lm_head")
-    per = n // world
-    w = si.weight(n, k, si.seed_for(5, 0, "lm_head"))[rank * per:(rank + 1) * per].contiguous().to(dev)
-    pw = mq.pack_w4(w)
-    del w
-    x = si.activation(m, k, si.seed_for(5, 0, "lm_head", True)).to(dev)
-    comm = mq.Comm()
-    out = {}
-    for route, name in ((0, "w4a8"), (1, "w4a16")):
-        y = torch.empty(m, n, dtype=torch.bfloat16, device=dev)
-        ws = torch.empty(max(256, comm.workspace_bytes(route, m, n, k)), dtype=torch.uint8, device=dev)
-        with torch.cuda.stream(stream):
-            mq.linear_colshard(comm, route, pw, n, x, out=y, ws=ws, stream=stream)
-            stream.synchronize()
-            g = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(g, stream=stream):
-                for _ in range(reps):
-                    mq.linear_colshard(comm, route, pw, n, x, out=y, ws=ws, stream=stream)
-            g.replay()
-            stream.synchronize()
+def _graph_us(fns, stream, reps, dist=None):
+    """Per-call us of `reps` calls captured in one CUDA graph, call r = fns[r % len(fns)]
+    (rotating weight copies, so repeated calls stream from HBM, not L2); CUDA events on
+    the launching stream after one warm replay; max over ranks when dist is given."""
+    dev = torch.device("cuda", torch.cuda.current_device())
+    with torch.cuda.stream(stream):
+        for f in fns:
+            f()
+        stream.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=stream):
+            for r in range(reps):
+                fns[r % len(fns)]()
+        g.replay()
+        stream.synchronize()
+        if dist is not None:
             dist.barrier()
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record(stream)
-            g.replay()
-            e1.record(stream)
-            e1.synchronize()
-        t = torch.tensor([e0.elapsed_time(e1) * 1000 / reps], device=dev)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        g.replay()
+        e1.record(stream)
+        e1.synchronize()
+    t = torch.tensor([e0.elapsed_time(e1) * 1000 / reps], device=dev)
+    if dist is not None:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        us = float(t.item())
-        out[f"{name}_us"] = round(us, 3)
-        out[f"{name}_gbs_total"] = round((n * k // 2 + n * (k // 32) * 2) / us / 1e3, 1)
+    del g
+    return float(t.item())
+
+
+def _copies(pw, l2):
+    """Distinct HBM copies of a packed weight, together >= 4 x L2 (at most 16)."""
+    c = max(1, min(16, -(-4 * l2 // pw.nbytes)))
+    return [pw] + [type(pw)(pw.nib.clone(), pw.scale.clone()) for _ in range(c - 1)]
+
+
+# the sharded layers of north_star (configs 4 and 5): (slot, M, graph reps)
+SHARDED = (("lm_head", 1, 20), ("lm_head", 64, 4), ("gate", 1, 64), ("down", 1, 64))
+
+
+def time_sharded(mq, dev, stream, dist, world, rank):
+    """Rows a8 / NEXT-2 at P = world: the Llama-3.1-8B lm_head
+    (M = 1, 64) and MLP gate / down column-sharded over the job's ranks.  Per layer and
+    route: T(1) = the unsharded linear on one GPU (no collective), T(P) = the sharded
+    linear + NCCL all-gather into the replicated y (mcapq_linear_colshard), t_local = the
+    rank's shard alone, comm = T(P) - t_local, E(P) = T(1) / (P T(P)); for the lm_head
+    also greedy decode (local argmax + P x M key gather, mcapq_linear_colshard_argmax).
+    Every time is a CUDA graph of repeated calls over rotating weight copies (>= 4 x L2
+    together), CUDA events, max over ranks."""
+    comm = mq.Comm() if world > 1 else None
+    l2 = torch.cuda.get_device_properties(dev).L2_cache_size
+    rows = []
+    for slot, m, reps in SHARDED:
+        n, k = si.linear_shape("llama-3.1-8b", slot)
+        per = n // world
+        w = si.weight(n, k, si.seed_for(5 if slot == "lm_head" else 4, 0, slot))
+        pw_full = mq.pack_w4(w.to(dev))
+        del w
+        pw = pw_full.shard(world, rank) if world > 1 else pw_full
+        x = si.activation(m, k, si.seed_for(5 if slot == "lm_head" else 4, 0, slot, True)).to(dev)
+        wbytes = n * k // 2 + n * (k // 32) * 2
+        full_c, shard_c = _copies(pw_full, l2), (_copies(pw, l2) if world > 1 else None)
+        for route, name in ((0, "w4a8"), (1, "w4a16")):
+            y = torch.empty(m, n, dtype=torch.bfloat16, device=dev)
+            yl = torch.empty(m, per, dtype=torch.bfloat16, device=dev)
+            ws = torch.empty(max(256, mq.workspace_bytes(route, m, n, k)), dtype=torch.uint8, device=dev)
+            t1 = _graph_us([lambda c=c: mq.linear(route, c, x, out=y, ws=ws, stream=stream) for c in full_c],
+                           stream, reps, dist)
+            row = {"model": "llama-3.1-8b", "slot": slot, "N": n, "K": k, "M": m, "route": name, "P": world,
+                   "rows_per_rank": per, "T1_us": round(t1, 3), "T1_gbs": round(wbytes / t1 / 1e3, 1),
+                   "weight_copies": [len(full_c), len(shard_c) if shard_c else 0]}
+            if comm is not None:
+                tl = _graph_us([lambda c=c: mq.linear(route, c, x, out=yl, ws=ws, stream=stream) for c in shard_c],
+                               stream, reps, dist)
+                wsc = torch.empty(max(256, comm.workspace_bytes(route, m, n, k)), dtype=torch.uint8, device=dev)
+                tp = _graph_us([lambda c=c: mq.linear_colshard(comm, route, c, n, x, out=y, ws=wsc, stream=stream)
+                                for c in shard_c], stream, reps, dist)
+                row.update({"t_local_us": round(tl, 3), "TP_us": round(tp, 3), "comm_us": round(tp - tl, 3),
+                            "E": round(t1 / (world * tp), 3), "gbs_total": round(wbytes / tp / 1e3, 1)})
+                if slot == "lm_head":
+                    wsa = torch.empty(max(256, mq.argmax_workspace_bytes(route, m, per, k, world)),
+                                      dtype=torch.uint8, device=dev)
+                    ws1 = torch.empty(max(256, mq.argmax_workspace_bytes(route, m, n, k)), dtype=torch.uint8,
+                                      device=dev)
+                    ta = _graph_us([lambda c=c: mq.linear_colshard_argmax(comm, route, c, n, x, ws=wsa, stream=stream)
+                                    for c in shard_c], stream, reps, dist)
+                    t1a = _graph_us([lambda c=c: mq.linear_argmax(route, c, x, ws=ws1, stream=stream) for c in full_c],
+                                    stream, reps, dist)
+                    row.update({"greedy_T1_us": round(t1a, 3), "greedy_TP_us": round(ta, 3),
+                                "greedy_E": round(t1a / (world * ta), 3)})
+            rows.append(row)
+        del pw_full, pw, full_c, shard_c
     del comm
-    return {"N": n, "K": k, "M": m, "P": world, "rows_per_rank": per, **out,
-            "timing": "graph of 20 calls, CUDA events, max over ranks; includes the NCCL all-gather"}
+    return {"timing": "CUDA graph of repeated calls over rotating weight copies (>= 4 x L2), CUDA events, max "
+                      "over ranks; T(1) unsharded on one GPU, "
+                      "T(P) sharded + NCCL all-gather (E = T(1) / (P T(P)))", "rows": rows}
 
 
 def time_mlp8b_stack(mq, dev, stream, layers=8, steps=20):
@@ -551,8 +611,21 @@ def main():
     args.warmup = max(3, args.warmup)
     if args.impl == "reference":
         return run_reference(args)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # `python bench.py --gpus N` without a launcher: start the N ranks ourselves
+        # (one process per GPU, NCCL over 127.0.0.1), rank 0 prints the line
+        import socket
+        import subprocess
+        with socket.socket() as sk:
+            sk.bind(("127.0.0.1", 0))
+            port = sk.getsockname()[1]
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *sys.argv[1:]]
+        return subprocess.call(cmd)
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world != args.gpus:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}; timing {world} rank(s)", file=sys.stderr)
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     dist = None
@@ -636,12 +709,12 @@ def main():
     extras = [] if args.no_extras or rank != 0 else time_single_linears(mq, dev, stream)
     mlp8b = None if args.no_extras or rank != 0 else time_mlp8b_stack(mq, dev, stream)
     prefill = None if args.no_extras or rank != 0 else time_prefill(mq, dev, stream)
-    colshard = None
+    sharded = None
     if world > 1 and not args.no_extras:
         try:
-            colshard = time_colshard_lm_head(mq, dev, stream, dist, world, rank)
+            sharded = time_sharded(mq, dev, stream, dist, world, rank)
         except Exception as e:   # the headline line must still print
-            colshard = {"error": f"{type(e).__name__}: {e}"[:200]}
+            sharded = {"error": f"{type(e).__name__}: {e}"[:200]}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -688,7 +761,7 @@ def main():
             "single_linears": extras,
             "mlp_8b_stack": mlp8b,
             "prefill_8b": prefill,
-            "lm_head_colshard": colshard,
+            "sharded": sharded,
         }
         if cpu is not None:
             line["cpu_baseline"] = cpu

@@ -10,7 +10,8 @@ import os
 from pathlib import Path
 
 _PKG = Path(__file__).resolve().parent
-LIB_PATH = _PKG / "lib" / "libmcapq.so"
+# MCAPQ_LIB: diagnostic A/B runs only (another build of the same sources, e.g. under _ab/)
+LIB_PATH = Path(os.environ.get("MCAPQ_LIB") or (_PKG / "lib" / "libmcapq.so"))
 
 P = ctypes.c_void_p
 I64 = ctypes.c_int64

@@ -43,44 +43,6 @@ struct GemmArgs {
     uint32_t nib_bytes, sc_off, act_off, ss_off, sq_off, stage_bytes;   // per-stage layout
 };
 
-// fp32 pairs in one 64-bit register (FFMA2 / FADD2 / FMUL2: two independent IEEE ops)
-typedef unsigned long long f2_t;
-__device__ __forceinline__ f2_t f2_pack(float a, float b)
-{
-    f2_t r;
-    asm("mov.b64 %0, {%1,%2};" : "=l"(r) : "f"(a), "f"(b));
-    return r;
-}
-__device__ __forceinline__ f2_t f2_pack_bits(uint32_t a, uint32_t b)
-{
-    f2_t r;
-    asm("mov.b64 %0, {%1,%2};" : "=l"(r) : "r"(a), "r"(b));
-    return r;
-}
-__device__ __forceinline__ float2 f2_unpack(f2_t r)
-{
-    float2 v;
-    asm("mov.b64 {%0,%1}, %2;" : "=f"(v.x), "=f"(v.y) : "l"(r));
-    return v;
-}
-__device__ __forceinline__ f2_t f2_fma(f2_t a, f2_t b, f2_t c)
-{
-    f2_t d;
-    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
-    return d;
-}
-__device__ __forceinline__ f2_t f2_add(f2_t a, f2_t b)
-{
-    f2_t d;
-    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
-    return d;
-}
-__device__ __forceinline__ f2_t f2_mul(f2_t a, f2_t b)
-{
-    f2_t d;
-    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
-    return d;
-}
 // IMMA m16n8k32 with an explicit int32 accumulator init (C may repeat registers)
 __device__ __forceinline__ void imma_c(uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3, uint32_t b0, uint32_t b1,
                                        int c0, int c1, int d[4])

@@ -361,7 +361,7 @@ struct Tune {
     // per-SM queue of in-flight weight data that the chain's L2 accesses wait behind
     int smem_kb = 112, max_stages = 12, nocompute = 0, pdl = 0, trace = 0, step_smem_kb = 200, step = 1,
         step_flags = 0, step_spin_ns = 16, step_polls = 1, ctas_per_sm = 0, step_ep_log2 = 1, smem_kb_env = 0,
-        step_hold = 1;
+        step_hold = 1, step_inflight = 0;
 };
 const Tune &tune()
 {
@@ -383,6 +383,7 @@ const Tune &tune()
         if (const char *e = getenv("MCAPQ_STREAM_CTAS_PER_SM")) v.ctas_per_sm = atoi(e);
         if (const char *e = getenv("MCAPQ_STEP_EP_LOG2")) v.step_ep_log2 = atoi(e);
         if (const char *e = getenv("MCAPQ_STEP_HOLD")) v.step_hold = atoi(e);
+        if (const char *e = getenv("MCAPQ_STEP_INFLIGHT")) v.step_inflight = atoi(e);
         if (v.step_ep_log2 < 1) v.step_ep_log2 = 1;
         if (v.step_ep_log2 > 3) v.step_ep_log2 = 3;
         if (v.ctas_per_sm < 0 || v.ctas_per_sm > 2) v.ctas_per_sm = 0;
@@ -808,6 +809,7 @@ cudaError_t launch_stack_step(const void *ops_dev, int nops, unsigned int *count
     a.polls = tune().step_polls;
     a.ep_log2 = tune().step_ep_log2;
     a.hold = tune().step_hold;
+    a.inflight = tune().step_inflight;
     // one CTA per SM: activations for the largest K under either route, the rest is ring
     const size_t act = round_up(act_bytes(HMMA1, max_k, 1) > act_bytes(DP4A, max_k, 1) ? act_bytes(HMMA1, max_k, 1)
                                                                                            : act_bytes(DP4A, max_k, 1),

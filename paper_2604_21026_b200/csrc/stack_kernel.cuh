@@ -56,11 +56,13 @@ struct StackArgs {
     unsigned long long *trace;   // debug: [nops][grid][8] or null
     int flags;                   // debug (MCAPQ_STEP_FLAGS): 1 no compute, 2 no barrier polls, 4 no staging,
                                  // 8 no waits at all (barriers skipped, tags not checked),
-                                 // 16 no publishing (only with 8), 32 no epilogue stores, 128 no W4A8 quantiser (loads only)
+                                 // 16 no publishing (only with 8), 32 no epilogue stores, 128 no W4A8 quantiser (loads only),
+                                 // 256 no weight loads (the chain alone on stale ring data), 512 no epilogue work (handshake only)
     int spin_ns;                 // first back-off between re-reads of stale tagged words (doubles, <= 1 us)
     int polls;                   // CTA-wide re-read rounds before waiting on the producer's counter
     int ep_log2;                 // log2 of the tile slots between the consumers and the epilogue warp (1..3)
     int hold;                    // 1: the producer holds ring refills while this CTA stages an input (see `hold`)
+    int inflight;                // > 0: at most this many stages issued by the producer and not yet landed
 };
 
 __device__ __forceinline__ unsigned int ld_acquire_gpu(const unsigned int *p)
@@ -427,7 +429,7 @@ __global__ void __launch_bounds__(kStepThreads, 1) stack_step(const __grid_const
                 const uint32_t slot = ts & (EN - 1u);
                 mbar_wait(epf + 8u * slot, (ts >> EL) & 1u);
                 const uint32_t sl = red + 1024u * slot;
-                if (lane < kTileRows) {
+                if (lane < kTileRows && !(a.flags & 512)) {
                     float v;
                     float x[kConsumerWarps];
 #pragma unroll
@@ -483,8 +485,8 @@ __global__ void __launch_bounds__(kStepThreads, 1) stack_step(const __grid_const
         // ================= producer: the whole step's weights, in op order =================
         if (lane == 0) {
             const uint64_t pol = evict_first_policy();
-            int s = 0;
-            uint32_t ph = 0;
+            int s = 0, ls = 0, inflight = 0;
+            uint32_t ph = 0, lph = 0;
             auto prefetch_maps = [&](int j) {
                 // TMA descriptors of linear j into the TMA unit's cache before first use
                 if (j >= a.nops) return;
@@ -520,11 +522,27 @@ __global__ void __launch_bounds__(kStepThreads, 1) stack_step(const __grid_const
                         mbar_wait(empty + 8u * s, ph ^ 1u);
                         if (a.hold)
                             while (lds32_volatile(hold) != 0u) __nanosleep(32);
+                        // in-flight cap: at most a.inflight stages issued and not landed, so
+                        // this SM's weight requests never queue deep in front of the chain's
+                        // latency-critical L2 accesses while the ring still refills continuously
+                        while (a.inflight > 0 && inflight >= a.inflight) {
+                            mbar_wait(full + 8u * ls, lph);
+                            --inflight;
+                            if (++ls == S) {
+                                ls = 0;
+                                lph ^= 1u;
+                            }
+                        }
+                        ++inflight;
                         const uint32_t st = ring + (uint32_t)s * kStageBytes;
                         const uint32_t fb = full + 8u * s;
-                        mbar_expect_tx(fb, (uint32_t)kStageBytes);
-                        tma_3d(st, map, 0, row0, ch * 8, fb, pol);
-                        tma_2d(st + 8 * kBox, map + 1, ch * kChunkBlocks, row0, fb, pol);
+                        if (a.flags & 256) {
+                            mbar_arrive(fb);   // debug: no weight traffic (the chain alone, garbage results)
+                        } else {
+                            mbar_expect_tx(fb, (uint32_t)kStageBytes);
+                            tma_3d(st, map, 0, row0, ch * 8, fb, pol);
+                            tma_2d(st + 8 * kBox, map + 1, ch * kChunkBlocks, row0, fb, pol);
+                        }
                         if (++s == S) {
                             s = 0;
                             ph ^= 1u;
@@ -589,6 +607,66 @@ __global__ void __launch_bounds__(kStepThreads, 1) stack_step(const __grid_const
                 const bool reg_act = kRounds == 2 && K2 == kChunkBytes;
                 Dp4aAct A;
                 if (reg_act) A = dp4a_act_load_pair(L, lam, lam + 32, (uint32_t)K2);
+                if ((K2 & (kChunkBytes - 1)) == 0) {
+                    // lean path (every chunk full: K % 2048 == 0, all the configs' step
+                    // linears): no per-stage predicates, the stage address advanced
+                    // incrementally, the activation mode a compile-time branch; the same
+                    // loads, block order and fmaf chain as below, so the outputs are
+                    // bit-identical
+                    auto lean = [&](auto reg_c) {
+                        constexpr bool kReg = decltype(reg_c)::value;
+                        uint32_t st = ring + (uint32_t)s * kStageBytes;
+                        uint32_t xa = L.act + 16u * (uint32_t)lam, xs = L.ssq + 8u * (uint32_t)lam;
+                        for (int tile = t0; tile < t1; ++tile, ++ts) {
+                            float acc = 0.f;
+                            const int hold_ch = tile == t1 - 1 ? nchunks - 1 : -1;
+                            for (int ch = 0; ch < nchunks; ++ch) {
+                                if (kTrace) {
+                                    ++nstages;
+                                    if (!mbar_test(full + 8u * s, ph)) ++stalls;
+                                }
+                                mbar_wait(full + 8u * s, ph);
+                                if (kTrace && tile == t0 && ch == 0) tr3 = globaltimer();
+                                const uint4 w0 = lds128(st + o0), w1 = lds128(st + o1);
+                                const uint32_t h0 = lds16(st + os0), h1 = lds16(st + os1);
+                                if constexpr (!kReg) {
+                                    const uint32_t xo = 16u * kChunkBlocks * (uint32_t)ch;
+                                    A.qa0 = lds128(xa + xo);
+                                    A.qb0 = lds128(xa + xo + (uint32_t)K2);
+                                    A.qa1 = lds128(xa + xo + 512u);
+                                    A.qb1 = lds128(xa + xo + 512u + (uint32_t)K2);
+                                    A.p0 = lds64(xs + xo / 2u);
+                                    A.p1 = lds64(xs + xo / 2u + 256u);
+                                }
+                                __syncwarp();
+                                if (lane == 0) mbar_arrive(empty + 8u * s);
+                                if (ch == hold_ch) hold_set(1u);   // the linear's last stage is resident
+                                if (++s == S) {
+                                    s = 0;
+                                    ph ^= 1u;
+                                    st = ring;
+                                } else {
+                                    st += (uint32_t)kStageBytes;
+                                }
+                                const int D0 = block_D(w0, A.qa0, A.qb0, (int)A.p0.y);
+                                const int D1 = block_D(w1, A.qa1, A.qb1, (int)A.p1.y);
+                                acc = fmaf(h2f((uint16_t)h0) * __uint_as_float(A.p0.x), (float)D0, acc);
+                                acc = fmaf(h2f((uint16_t)h1) * __uint_as_float(A.p1.x), (float)D1, acc);
+                            }
+                            if (kTrace) tr4 = globaltimer();
+                            acc += __shfl_xor_sync(0xffffffffu, acc, 16);
+                            const uint32_t slot = ts & (EN - 1u);
+                            if (ts >= EN) mbar_wait(epe + 8u * slot, ((ts >> EL) - 1u) & 1u);
+                            if (lane < 16) sts32(red + 1024u * slot + 64u * warp + 4u * lane, __float_as_uint(acc));
+                            __syncwarp();
+                            if (lane == 0) mbar_arrive(epf + 8u * slot);
+                        }
+                    };
+                    if (reg_act)
+                        lean(std::true_type{});
+                    else
+                        lean(std::false_type{});
+                } else
                 for (int tile = t0; tile < t1; ++tile, ++ts) {
                     float acc = 0.f;
                     for (int ch = 0; ch < nchunks; ++ch) {

@@ -11,6 +11,44 @@
 //         then corr [G][8 tokens] fp32 = -136 * sum_j x_j of the group.
 #pragma once
 
+// fp32 pairs in one 64-bit register (FFMA2 / FADD2 / FMUL2: two independent IEEE ops)
+typedef unsigned long long f2_t;
+__device__ __forceinline__ f2_t f2_pack(float a, float b)
+{
+    f2_t r;
+    asm("mov.b64 %0, {%1,%2};" : "=l"(r) : "f"(a), "f"(b));
+    return r;
+}
+__device__ __forceinline__ f2_t f2_pack_bits(uint32_t a, uint32_t b)
+{
+    f2_t r;
+    asm("mov.b64 %0, {%1,%2};" : "=l"(r) : "r"(a), "r"(b));
+    return r;
+}
+__device__ __forceinline__ float2 f2_unpack(f2_t r)
+{
+    float2 v;
+    asm("mov.b64 {%0,%1}, %2;" : "=f"(v.x), "=f"(v.y) : "l"(r));
+    return v;
+}
+__device__ __forceinline__ f2_t f2_fma(f2_t a, f2_t b, f2_t c)
+{
+    f2_t d;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+    return d;
+}
+__device__ __forceinline__ f2_t f2_add(f2_t a, f2_t b)
+{
+    f2_t d;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+    return d;
+}
+__device__ __forceinline__ f2_t f2_mul(f2_t a, f2_t b)
+{
+    f2_t d;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+    return d;
+}
 struct ActSmem {
     uint32_t act, tsz, ssq, corr;
 };
@@ -109,7 +147,7 @@ __device__ __forceinline__ float div127_rn(float a)
 __device__ __forceinline__ float rcp_group(float s)
 {
     float r;
-    asm("rcp.approx.f32 %0, %1;" : "=f"(r) : "f"(s));
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(s));
     if (s < 1.17549435e-38f) r = __frcp_rn(s);
     return r;
 }
@@ -147,6 +185,80 @@ __device__ __forceinline__ bool quant_codes_fast(const float *v, float inv, int 
     return ok;
 }
 
+// Codes of the elements of packed bf16 words w[0..NW) (element 2e = low half of w[e]),
+// packed four per word in element order into out[0..NW/2), branch-free on the f32x2
+// pipe: q = rint(v * inv) is the low byte of fl(fl(v * inv) + 1.5 * 2^23) (the magic
+// sum is M + rint exactly for |v * inv| < 2^22), packed by three PRMTs per four codes.
+// Off the half-integers rint == round_half_away(fl(v / s)) (quant_code's margin
+// argument; |fl(v / s)| <= 127.00003 in a live group, so no clamp).  Returns false when
+// some element lies within 1e-4 of a half-integer: the caller then takes quant_code
+// (IEEE division) for every element, so the codes stay bit-identical to quant_a8_kernel.
+// For a live group with a finite inv every v * inv is finite (|v| <= amax), so the
+// NaN-ignoring max below never hides a non-finite residual.
+template <int NW>
+__device__ __forceinline__ bool quant_words_fast(const uint32_t *w, float inv, uint32_t *out)
+{
+    const f2_t I = f2_pack(inv, inv), Mp = f2_pack(12582912.0f, 12582912.0f), Mn = f2_pack(-12582912.0f, -12582912.0f),
+               N1 = f2_pack(-1.0f, -1.0f);
+    uint32_t tb[2 * NW];
+    float worst = 0.0f;
+#pragma unroll
+    for (int e = 0; e < NW; ++e) {
+        const f2_t v = f2_pack_bits(w[e] << 16, w[e] & 0xffff0000u);
+        const f2_t qa = f2_mul(v, I);
+        const f2_t t = f2_add(qa, Mp);
+        const f2_t d = f2_fma(f2_add(t, Mn), N1, qa);   // qa - rint(qa), exact
+        const float2 dd = f2_unpack(d), tt = f2_unpack(t);
+        worst = fmaxf(worst, fmaxf(fabsf(dd.x), fabsf(dd.y)));
+        tb[2 * e] = __float_as_uint(tt.x);
+        tb[2 * e + 1] = __float_as_uint(tt.y);
+    }
+#pragma unroll
+    for (int o = 0; o < NW / 2; ++o)
+        out[o] = __byte_perm(__byte_perm(tb[4 * o], tb[4 * o + 1], 0x0040), __byte_perm(tb[4 * o + 2], tb[4 * o + 3], 0x0040),
+                             0x5410);
+    // inv = inf (a live group with s < 2^-128: 1/s overflows) makes residuals NaN, which
+    // fmaxf drops: such groups always take the IEEE path
+    return worst < 0.4999f && inv < __int_as_float(0x7f800000);
+}
+
+// Slow path of quant_words_fast (a group with an element near a half-integer): every
+// code by quant_code (IEEE division), packed four per word.
+template <int NW>
+__device__ __forceinline__ void quant_words_ieee(const uint32_t *w, float s, float inv, uint32_t *out)
+{
+#pragma unroll
+    for (int o = 0; o < NW / 2; ++o) {
+        uint32_t p = 0;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const uint32_t b = w[2 * o + (j >> 1)];
+            const float v = __uint_as_float((j & 1) ? (b & 0xffff0000u) : (b << 16));
+            p |= ((uint32_t)quant_code(v, s, inv) & 0xffu) << (8 * j);
+        }
+        out[o] = p;
+    }
+}
+
+// Codes of NW packed bf16 words of a group whose abs-max bits are m (reduced over the
+// group): s = fl(amax / 127), codes packed four per word, sum of the codes (dp4a
+// against 0x01010101) -- the per-thread part of the per-token quantiser.
+template <int NW>
+__device__ __forceinline__ float quant_group_part(const uint32_t *w, uint32_t m, uint32_t *out, int &sum)
+{
+    const float s = div127_rn(__uint_as_float(m << 16));
+    const bool live = m < 0x7f80u && s != 0.0f;
+    const float inv = rcp_group(s);
+    if (!quant_words_fast<NW>(w, inv, out) && live) quant_words_ieee<NW>(w, s, inv, out);
+    sum = 0;
+#pragma unroll
+    for (int o = 0; o < NW / 2; ++o) {
+        if (!live) out[o] = 0u;
+        sum = __dp4a((int)out[o], 0x01010101, sum);
+    }
+    return live ? s : 0.0f;
+}
+
 // Quantise group (i, g): quad member `sub` holds elements 8 sub .. 8 sub + 7 as the
 // packed bf16 words w4.  Stores its 8 codes and (sub 0) the group's {s, 8 sum q}.
 // All 32 lanes call it (quad shuffles); `on` masks the stores of lanes past the end.
@@ -161,36 +273,18 @@ __device__ __forceinline__ void a8_quad_store(const uint32_t w4[4], bool on, int
     m = absmax_fold(m);
     m = max(m, __shfl_xor_sync(0xffffffffu, m, 1));
     m = max(m, __shfl_xor_sync(0xffffffffu, m, 2));
-    const float s = div127_rn(__uint_as_float(m << 16));
-    const bool live = m < 0x7f80u && s != 0.0f;
-    const float inv = rcp_group(s);
-    float v[8];
-    bf16x8_to_f32(w4, v);
-    int c[8];
-    if (!quant_codes_fast<8>(v, inv, c) && live) {
-#pragma unroll
-        for (int j = 0; j < 8; ++j) c[j] = quant_code(v[j], s, inv);
-    }
-    uint32_t lo = 0, hi = 0;
-    int sum = 0;
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-        const int code = live ? c[j] : 0;
-        sum += code;
-        if (j < 4)
-            lo |= ((uint32_t)code & 0xffu) << (8 * j);
-        else
-            hi |= ((uint32_t)code & 0xffu) << (8 * (j - 4));
-    }
+    uint32_t q[2];
+    int sum;
+    const float s = quant_group_part<4>(w4, m, q, sum);
     sum += __shfl_xor_sync(0xffffffffu, sum, 1);
     sum += __shfl_xor_sync(0xffffffffu, sum, 2);
     if (on) {
         // elements 8sub..8sub+7: sub 0/1 -> q_lo, sub 2/3 -> q_hi
         const uint32_t qt = L.act + (uint32_t)i * L.tsz + (sub < 2 ? 0u : K2) + 16u * g + 8u * (sub & 1);
-        asm volatile("st.shared.v2.u32 [%0], {%1,%2};" ::"r"(qt), "r"(lo), "r"(hi) : "memory");
+        asm volatile("st.shared.v2.u32 [%0], {%1,%2};" ::"r"(qt), "r"(q[0]), "r"(q[1]) : "memory");
         if (sub == 0)
             asm volatile("st.shared.v2.u32 [%0], {%1,%2};" ::"r"(L.ssq + 8u * (uint32_t)(i * G + g)),
-                         "r"(__float_as_uint(live ? s : 0.0f)), "r"((uint32_t)(8 * sum))
+                         "r"(__float_as_uint(s)), "r"((uint32_t)(8 * sum))
                          : "memory");
     }
 }
@@ -203,31 +297,17 @@ __device__ __forceinline__ void a8_oct_store(uint2 w2, bool on, int g, int sub8,
     uint32_t m = absmax_fold(absmax_bits(w2.x & 0x7fff7fffu, w2.y));
 #pragma unroll
     for (int o = 1; o < 8; o <<= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
-    const float s = div127_rn(__uint_as_float(m << 16));
-    const bool live = m < 0x7f80u && s != 0.0f;
-    const float inv = rcp_group(s);
-    const float v[4] = {__uint_as_float(w2.x << 16), __uint_as_float(w2.x & 0xffff0000u),
-                        __uint_as_float(w2.y << 16), __uint_as_float(w2.y & 0xffff0000u)};
-    int c[4];
-    if (!quant_codes_fast<4>(v, inv, c) && live) {
-#pragma unroll
-        for (int j = 0; j < 4; ++j) c[j] = quant_code(v[j], s, inv);
-    }
-    uint32_t w = 0;
-    int sum = 0;
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-        const int code = live ? c[j] : 0;
-        sum += code;
-        w |= ((uint32_t)code & 0xffu) << (8 * j);
-    }
+    const uint32_t w[2] = {w2.x, w2.y};
+    uint32_t q[1];
+    int sum;
+    const float s = quant_group_part<2>(w, m, q, sum);
 #pragma unroll
     for (int o = 1; o < 8; o <<= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
     if (on) {
-        sts32(L.act + (sub8 < 4 ? 0u : K2) + 16u * g + 4u * (sub8 & 3), w);
+        sts32(L.act + (sub8 < 4 ? 0u : K2) + 16u * g + 4u * (sub8 & 3), q[0]);
         if (sub8 == 0)
             asm volatile("st.shared.v2.u32 [%0], {%1,%2};" ::"r"(L.ssq + 8u * (uint32_t)g),
-                         "r"(__float_as_uint(live ? s : 0.0f)), "r"((uint32_t)(8 * sum))
+                         "r"(__float_as_uint(s)), "r"((uint32_t)(8 * sum))
                          : "memory");
     }
 }
