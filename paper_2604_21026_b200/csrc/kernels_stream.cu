@@ -361,7 +361,7 @@ struct Tune {
     // per-SM queue of in-flight weight data that the chain's L2 accesses wait behind
     int smem_kb = 112, max_stages = 12, nocompute = 0, pdl = 0, trace = 0, step_smem_kb = 200, step = 1,
         step_flags = 0, step_spin_ns = 16, step_polls = 1, ctas_per_sm = 0, step_ep_log2 = 1, smem_kb_env = 0,
-        step_hold = 1, step_inflight = 0;
+        step_hold = 1, step_inflight = 0, step_rec_spin = 64;
 };
 const Tune &tune()
 {
@@ -384,6 +384,7 @@ const Tune &tune()
         if (const char *e = getenv("MCAPQ_STEP_EP_LOG2")) v.step_ep_log2 = atoi(e);
         if (const char *e = getenv("MCAPQ_STEP_HOLD")) v.step_hold = atoi(e);
         if (const char *e = getenv("MCAPQ_STEP_INFLIGHT")) v.step_inflight = atoi(e);
+        if (const char *e = getenv("MCAPQ_STEP_REC_SPIN")) v.step_rec_spin = atoi(e);
         if (v.step_ep_log2 < 1) v.step_ep_log2 = 1;
         if (v.step_ep_log2 > 3) v.step_ep_log2 = 3;
         if (v.ctas_per_sm < 0 || v.ctas_per_sm > 2) v.ctas_per_sm = 0;
@@ -785,8 +786,57 @@ bool stack_fill_op(void *host_op, int route, const StreamGroup &g, const uint16_
     for (int i = 0; i < g.count; ++i) op.yt[i] = d.yt[i];
     op.wait_op = d.wait_op;
     op.publish = d.publish;
+    // an op whose outputs feed producer-quantised records hands its tiles out in 32-row
+    // pairs (quantisation groups; every member's N a multiple of 32, so a pair never
+    // spans two members); the other ops keep the contiguous balanced split
+    bool recs = false;
+    for (int i = 0; i < g.count; ++i) recs = recs || d.yq[i] != nullptr;
+    bool paired = recs && stack_clustered() && (tiles % 2 == 0);
+    for (int i = 0; i < g.count; ++i) paired = paired && g.n[i] % 32 == 0;
+    op.paired = paired ? 1 : 0;
+    for (int i = 0; i < g.count; ++i) op.yq[i] = paired ? d.yq[i] : nullptr;
+    op.xq = d.xq;
     memcpy(host_op, &op, sizeof(op));
     return true;
+}
+
+int64_t stack_rec_min_k()
+{
+    static const int64_t v = [] {
+        const char *e = getenv("MCAPQ_STEP_REC_MINK");
+        return e ? (int64_t)atoll(e) : (int64_t)4096;
+    }();
+    return v;
+}
+
+// One cluster of 2 per SM pair over the whole grid (1 CTA per SM: the step's shared
+// memory), checked once with the occupancy API; otherwise the plain cooperative launch.
+bool stack_clustered()
+{
+    static int v = -1;
+    if (v >= 0) return v != 0;
+    v = 0;
+    if (getenv("MCAPQ_STEP_CLUSTER") && atoi(getenv("MCAPQ_STEP_CLUSTER")) == 0) return false;
+    const void *f = reinterpret_cast<const void *>(stack_step<false, 2>);
+    if (kernel_smem_attr(f, 227 * 1024) != cudaSuccess) return false;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(device_sms());
+    cfg.blockDim = dim3(kStepThreads);
+    cfg.dynamicSmemBytes = 200 * 1024;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    int n = 0;
+    if (cudaOccupancyMaxActiveClusters(&n, f, &cfg) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    v = (2 * n >= device_sms() && device_sms() % 2 == 0) ? 1 : 0;
+    return v != 0;
 }
 
 cudaError_t launch_stack_step(const void *ops_dev, int nops, unsigned int *counters_dev, int64_t max_k,
@@ -810,6 +860,7 @@ cudaError_t launch_stack_step(const void *ops_dev, int nops, unsigned int *count
     a.ep_log2 = tune().step_ep_log2;
     a.hold = tune().step_hold;
     a.inflight = tune().step_inflight;
+    a.rec_spin = tune().step_rec_spin;
     // one CTA per SM: activations for the largest K under either route, the rest is ring
     const size_t act = round_up(act_bytes(HMMA1, max_k, 1) > act_bytes(DP4A, max_k, 1) ? act_bytes(HMMA1, max_k, 1)
                                                                                            : act_bytes(DP4A, max_k, 1),
@@ -829,9 +880,9 @@ cudaError_t launch_stack_step(const void *ops_dev, int nops, unsigned int *count
         // debug timeline: [op][cta] records at the start of the trace buffer
         constexpr size_t kCap = 1u << 20;
         if (!g_trace && cudaMalloc(&g_trace, kCap * 64) != cudaSuccess) g_trace = nullptr;
-        if (g_trace && (size_t)nops * grid <= kCap) {
+        if (g_trace && 2 * (size_t)nops * grid <= kCap) {
             a.trace = g_trace;
-            g_trace_used = (size_t)nops * grid;
+            g_trace_used = 2 * (size_t)nops * grid;   // + the epilogue records
         }
     }
     cudaLaunchConfig_t cfg = {};
@@ -840,8 +891,18 @@ cudaError_t launch_stack_step(const void *ops_dev, int nops, unsigned int *count
     cfg.dynamicSmemBytes = smem;
     cfg.stream = s;
     cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeCooperative;   // all CTAs co-resident: the grid barrier is safe
-    attr[0].val.cooperative = 1;
+    a.clustered = stack_clustered() ? 1 : 0;
+    if (a.clustered) {
+        // clusters of 2 (paired tiles); all CTAs co-resident: one per SM, and the
+        // occupancy check found room for every cluster
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = 2;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+    } else {
+        attr[0].id = cudaLaunchAttributeCooperative;   // all CTAs co-resident: the grid barrier is safe
+        attr[0].val.cooperative = 1;
+    }
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     if (max_k <= 8192)

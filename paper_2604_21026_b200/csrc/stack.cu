@@ -238,6 +238,8 @@ static mcapq_status build_program(mcapq_stack *st)
         d.xt = nullptr;
         d.xt_op = -1;
         for (int m = 0; m < kMaxGroup; ++m) d.yt[m] = nullptr;
+        for (int m = 0; m < kMaxGroup; ++m) d.yq[m] = nullptr;
+        d.xq = nullptr;
         d.wait_op = -1;
         d.publish = 0;
         // RAW on x_i: the latest earlier writer of any byte of x_i
@@ -270,23 +272,52 @@ static mcapq_status build_program(mcapq_stack *st)
             }
         }
     }
-    // tagged buffers: one per (producer op, member) that feeds a dataflow consumer
+    // per (producer op, member) feeding a dataflow consumer: a tagged bf16 copy for W4A16
+    // consumers, or -- in the clustered step, every member N a multiple of 32 -- quantised
+    // records for W4A8 consumers (the producer's epilogue quantises each group once)
+    auto rec_ok = [&](int j) {
+        if (!stack_clustered()) return false;
+        for (int m = 0; m < gs[j].count; ++m)
+            if (gs[j].n[m] % 32) return false;
+        return true;
+    };
     std::vector<std::vector<size_t>> tag_off(nops, std::vector<size_t>(kMaxGroup, (size_t)-1));
-    size_t tag_words = 0;
-    for (int i = 0; i < nops; ++i)
-        if (src_op[i] >= 0 && tag_off[src_op[i]][src_m[i]] == (size_t)-1) {
-            tag_off[src_op[i]][src_m[i]] = tag_words;
-            tag_words += (size_t)((gs[src_op[i]].n[src_m[i]] + 3) / 4 * 4);
-        }
-    if (tag_words) {
-        MCAPQ_CUDA_TRY(cudaMalloc(&st->tags, tag_words * 4));
-        MCAPQ_CUDA_TRY(cudaMemset(st->tags, 0, tag_words * 4));
-    }
+    std::vector<std::vector<size_t>> rec_off(nops, std::vector<size_t>(kMaxGroup, (size_t)-1));
+    std::vector<char> use_rec(nops, 0);
+    size_t tag_words = 0, rec_words = 0;
     for (int i = 0; i < nops; ++i) {
-        for (int m = 0; m < gs[i].count; ++m)
+        if (src_op[i] < 0) continue;
+        const int j = src_op[i], m = src_m[i];
+        if (st->routes[groups[i].first] == MCAPQ_W4A8 && rec_ok(j) && gs[i].k >= stack_rec_min_k()) {
+            use_rec[i] = 1;
+            if (rec_off[j][m] == (size_t)-1) {
+                rec_off[j][m] = rec_words;
+                rec_words += (size_t)(gs[j].n[m] / 32) * (kStackRecBytes / 8);
+            }
+        } else if (tag_off[j][m] == (size_t)-1) {
+            tag_off[j][m] = tag_words;
+            tag_words += (size_t)((gs[j].n[m] + 3) / 4 * 4);
+        }
+    }
+    // one allocation: tagged words, then the 16-B aligned records (both zero: tag 0 is
+    // never current)
+    const size_t tag_bytes = (tag_words * 4 + 15) / 16 * 16;
+    if (tag_words + rec_words) {
+        MCAPQ_CUDA_TRY(cudaMalloc(&st->tags, tag_bytes + rec_words * 8));
+        MCAPQ_CUDA_TRY(cudaMemset(st->tags, 0, tag_bytes + rec_words * 8));
+    }
+    unsigned long long *recs =
+        reinterpret_cast<unsigned long long *>(reinterpret_cast<uint8_t *>(st->tags) + tag_bytes);
+    for (int i = 0; i < nops; ++i) {
+        for (int m = 0; m < gs[i].count; ++m) {
             if (tag_off[i][m] != (size_t)-1) deps[i].yt[m] = st->tags + tag_off[i][m];
+            if (rec_off[i][m] != (size_t)-1) deps[i].yq[m] = recs + rec_off[i][m];
+        }
         if (src_op[i] >= 0) {
-            deps[i].xt = st->tags + tag_off[src_op[i]][src_m[i]];
+            if (use_rec[i])
+                deps[i].xq = recs + rec_off[src_op[i]][src_m[i]];
+            else
+                deps[i].xt = st->tags + tag_off[src_op[i]][src_m[i]];
             deps[i].xt_op = src_op[i];
             // the consumer's slow path waits on its counter only as a hint (the tags
             // decide): a relaxed add, no release fence on the epilogue warp's path

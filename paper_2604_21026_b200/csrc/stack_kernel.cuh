@@ -42,7 +42,14 @@ struct StackOp {
     int xt_op;            // the producing linear (its counter is the slow-path wait), or -1
     int wait_op;          // barrier dependency: linear index, or -1
     int publish;          // a later linear waits on this one's counter: 2 release (barrier), 1 relaxed (hint)
-    int pad_[3];
+    int paired;           // tiles are handed out in 32-row pairs per CTA pair (cluster), see cta_tiles
+    // producer-side quantisation (W4A8 consumers): the epilogue quantises every 32-row
+    // group of y[m] once and stores its record (6 tagged u64 words: 32 codes, fp32 s,
+    // int16 8 sum q) to yq[m]; a consumer with xq != null stages those records instead
+    // of quantising the bf16 words itself (148 times)
+    unsigned long long *yq[kMaxGroup];
+    const unsigned long long *xq;
+    int pad_[4];
 };
 static_assert(sizeof(StackOp) % 16 == 0, "StackOp is copied to shared memory in 16-byte pieces");
 
@@ -63,6 +70,8 @@ struct StackArgs {
     int ep_log2;                 // log2 of the tile slots between the consumers and the epilogue warp (1..3)
     int hold;                    // 1: the producer holds ring refills while this CTA stages an input (see `hold`)
     int inflight;                // > 0: at most this many stages issued by the producer and not yet landed
+    int clustered;               // launched as clusters of 2 CTAs: paired ops split their tiles per cluster
+    int rec_spin;                // > 0: record consumers spin per thread (back-off cap, ns); 0: counter scheme
 };
 
 __device__ __forceinline__ unsigned int ld_acquire_gpu(const unsigned int *p)
@@ -94,6 +103,110 @@ __device__ __forceinline__ bool tags_ok(uint4 a, uint32_t t16)
 __device__ __forceinline__ uint2 untag(uint4 a)
 {
     return make_uint2(__byte_perm(a.x, a.y, 0x5410), __byte_perm(a.z, a.w, 0x5410));
+}
+
+// ---- producer-side quantisation records and the CTA-pair exchange (clusters of 2)
+constexpr int kRecWords = 6;   // u64 per 32-group: 7 payload bytes + 1 tag byte each
+__device__ __forceinline__ uint32_t cluster_rank()
+{
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ uint32_t mapa_peer(uint32_t addr, uint32_t rank)
+{
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+    return r;
+}
+__device__ __forceinline__ void cluster_sync_all()
+{
+    asm volatile("barrier.cluster.arrive.release;\n\tbarrier.cluster.wait.acquire;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_wait_cluster(uint32_t bar, uint32_t parity)
+{
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "WAITC_%=:\n\t"
+        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAITC_%=;\n\t}" ::"r"(bar),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_remote(uint32_t cluster_bar)
+{
+    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_bar) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_remote_relaxed(uint32_t cluster_bar)
+{
+    asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_bar) : "memory");
+}
+__device__ __forceinline__ void st_async_u32(uint32_t cluster_addr, uint32_t v, uint32_t cluster_bar)
+{
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.u32 [%0], %1, [%2];" ::"r"(cluster_addr),
+                 "r"(v), "r"(cluster_bar)
+                 : "memory");
+}
+__device__ __forceinline__ void ld_relaxed_2x64(const unsigned long long *p, unsigned long long &a, unsigned long long &b)
+{
+    asm volatile("ld.relaxed.gpu.global.v2.u64 {%0,%1}, [%2];" : "=l"(a), "=l"(b) : "l"(p) : "memory");
+}
+__device__ __forceinline__ bool rec_ok(unsigned long long w, uint32_t t8) { return (uint32_t)(w >> 56) == t8; }
+
+// Quantise one 32-row group held one bf16 value per lane (lane j = element j of the
+// group) and store its record: codes, s = fl(amax / 127) and 8 sum q,
+// bit-identical to quant_a8_kernel (same fast path and IEEE fallback as a8_*_store).
+// All 32 lanes call it.
+__device__ __forceinline__ void quant_group_record(uint32_t xb, unsigned long long *rec, uint32_t t8, int lane)
+{
+    const uint32_t m = __reduce_max_sync(0xffffffffu, xb & 0x7fffu);
+    const float s = div127_rn(__uint_as_float(m << 16));
+    const bool live = m < 0x7f80u && s != 0.0f;
+    const float inv = rcp_group(s);
+    const float v = __uint_as_float(xb << 16);
+    const float qa = __fmul_rn(v, inv);
+    const float t = __fadd_rn(qa, 12582912.0f);
+    const float r = __fsub_rn(qa, __fsub_rn(t, 12582912.0f));
+    int c = __float_as_int(t) - 0x4B400000;
+    // a NaN residual (inv = inf) counts as bad: !(|r| < 0.4999)
+    if (__any_sync(0xffffffffu, !(fabsf(r) < 0.4999f)) && live) c = quant_code(v, s, inv);
+    if (!live) c = 0;
+    const int sum = __reduce_add_sync(0xffffffffu, c);
+    const uint32_t cb = (uint32_t)c & 0xffu;
+    const uint32_t sbits = __float_as_uint(live ? s : 0.0f);
+    const uint32_t sq16 = (uint32_t)(8 * sum) & 0xffffu;
+    unsigned long long word = (unsigned long long)t8 << 56;
+#pragma unroll
+    for (int k = 0; k < 7; ++k) {
+        const int idx = 7 * lane + k;
+        const uint32_t code = __shfl_sync(0xffffffffu, cb, idx & 31);
+        uint32_t byte;
+        if (idx < 32) byte = code;
+        else if (idx < 36) byte = (sbits >> (8 * (idx - 32))) & 0xffu;
+        else if (idx < 38) byte = (sq16 >> (8 * (idx - 36))) & 0xffu;
+        else byte = 0u;
+        word |= (unsigned long long)byte << (8 * k);
+    }
+    if (lane < kRecWords) asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(rec + lane), "l"(word) : "memory");
+}
+
+// A record's payload into the engine's activation layout: q_lo (codes 0..15), q_hi
+// (codes 16..31), {s, 8 sum q}.
+__device__ __forceinline__ void rec_unpack_store(const unsigned long long w[kRecWords], int g, uint32_t K2,
+                                                 const ActSmem &L)
+{
+    const unsigned long long M56 = 0x00ffffffffffffffull;
+    const unsigned long long a = w[0] & M56, b = w[1] & M56, c = w[2] & M56, d = w[3] & M56, e = w[4] & M56,
+                             f = w[5] & M56;
+    const unsigned long long lo0 = a | (b << 56), lo1 = (b >> 8) | (c << 48);
+    const unsigned long long hi0 = (c >> 16) | (d << 40), hi1 = (d >> 24) | (e << 32);
+    const uint32_t sbits = (uint32_t)((e >> 32) | (f << 24));
+    const int sq8 = (int)(int16_t)(uint16_t)((f >> 8) & 0xffffu);
+    asm volatile("st.shared.v2.u64 [%0], {%1,%2};" ::"r"(L.act + 16u * (uint32_t)g), "l"(lo0), "l"(lo1) : "memory");
+    asm volatile("st.shared.v2.u64 [%0], {%1,%2};" ::"r"(L.act + K2 + 16u * (uint32_t)g), "l"(hi0), "l"(hi1)
+                 : "memory");
+    asm volatile("st.shared.v2.u32 [%0], {%1,%2};" ::"r"(L.ssq + 8u * (uint32_t)g), "r"(sbits), "r"((uint32_t)sq8)
+                 : "memory");
 }
 
 constexpr int kStepThreads = (kConsumerWarps + 2) * 32;   // consumers + producer warp + sync warp
@@ -150,7 +263,15 @@ __device__ __forceinline__ void stage_step_a8_oct(unsigned long long *tmid, cons
             ra = make_uint4(p.x, p.y, 0, 0);
         }
     }
-    if (tagged && check) {
+    if (tagged && check && polls < 0) {
+        // per-thread re-reads of this thread's 16 B until current, back-off capped at -polls ns
+        int backoff = spin_ns;
+        while (on && !tags_ok(ra, t16)) {
+            __nanosleep(backoff);
+            ra = ld_relaxed_128(op.xt + e0);
+            backoff = backoff < -polls ? 2 * backoff : -polls;
+        }
+    } else if (tagged && check) {
         int backoff = spin_ns;
         for (int p = 0;; ++p) {
             const bool ok = !on || tags_ok(ra, t16);
@@ -180,6 +301,70 @@ __device__ __forceinline__ void stage_step_a8_oct(unsigned long long *tmid, cons
     if (tagged) w2 = untag(ra);
     else w2 = make_uint2(ra.x, ra.y);
     if (quant) a8_oct_store(w2, on, g, sub8, K2, L);
+}
+
+// Stage a W4A8 input whose producer quantised it (records, see quant_group_record): one
+// thread per 32-group loads its 6 tagged words (48 B instead of the 128 B of tagged
+// bf16 words), the same current-tag protocol as the bf16 staging (CTA-wide re-read
+// rounds, then the producer's counter, then per-thread re-reads), and unpacks codes and
+// {s, 8 sum q} into the engine's layout -- no quantiser on the consumer side.
+__device__ __forceinline__ void stage_step_rec(unsigned long long *tmid, const StackOp &op, const ActSmem &L, int tid,
+                                               uint32_t t8, bool check, int spin_ns, int polls,
+                                               const unsigned int *counters, int rec_spin)
+{
+    const int G = (int)(op.k / 32);
+    const uint32_t K2 = (uint32_t)(op.k / 2);
+    const bool on = tid < G;
+    const unsigned long long *src = op.xq + (size_t)(on ? tid : 0) * kRecWords;
+    unsigned long long w[kRecWords] = {0, 0, 0, 0, 0, 0};
+    if (on) {
+        ld_relaxed_2x64(src, w[0], w[1]);
+        ld_relaxed_2x64(src + 2, w[2], w[3]);
+        ld_relaxed_2x64(src + 4, w[4], w[5]);
+    }
+    if (check && rec_spin > 0) {
+        // records are small (48 B per group): every thread re-reads its own until current,
+        // back-off capped at rec_spin ns -- no CTA-wide rounds, no counter round trip
+        int backoff = spin_ns;
+        while (on && !(rec_ok(w[0], t8) && rec_ok(w[1], t8) && rec_ok(w[2], t8) && rec_ok(w[3], t8) &&
+                       rec_ok(w[4], t8) && rec_ok(w[5], t8))) {
+            __nanosleep(backoff);
+            ld_relaxed_2x64(src, w[0], w[1]);
+            ld_relaxed_2x64(src + 2, w[2], w[3]);
+            ld_relaxed_2x64(src + 4, w[4], w[5]);
+            backoff = backoff < rec_spin ? 2 * backoff : rec_spin;
+        }
+    } else if (check) {
+        int backoff = spin_ns;
+        for (int p = 0;; ++p) {
+            const bool ok = !on || (rec_ok(w[0], t8) && rec_ok(w[1], t8) && rec_ok(w[2], t8) && rec_ok(w[3], t8) &&
+                                    rec_ok(w[4], t8) && rec_ok(w[5], t8));
+            if (bar_consumers_and(ok)) break;
+            if (p >= polls) {
+                if (tid == 0)
+                    while (ld_acquire_gpu(counters + op.xt_op) < gridDim.x) __nanosleep(spin_ns);
+                bar_consumers();
+                // the producer published (a hint): re-read until current
+                while (on && !(rec_ok(w[0], t8) && rec_ok(w[1], t8) && rec_ok(w[2], t8) && rec_ok(w[3], t8) &&
+                               rec_ok(w[4], t8) && rec_ok(w[5], t8))) {
+                    __nanosleep(spin_ns);
+                    ld_relaxed_2x64(src, w[0], w[1]);
+                    ld_relaxed_2x64(src + 2, w[2], w[3]);
+                    ld_relaxed_2x64(src + 4, w[4], w[5]);
+                }
+                break;
+            }
+            if (!ok) {
+                __nanosleep(backoff);
+                ld_relaxed_2x64(src, w[0], w[1]);
+                ld_relaxed_2x64(src + 2, w[2], w[3]);
+                ld_relaxed_2x64(src + 4, w[4], w[5]);
+            }
+            backoff = backoff < 1024 ? 2 * backoff : 1024;
+        }
+    }
+    if (tmid) *tmid = globaltimer();
+    if (on) rec_unpack_store(w, tid, K2, L);
 }
 
 // Rounds q0 / NT .. q0 / NT + kRounds - 1 of the quad staging (one phase; see stage_step).
@@ -305,8 +490,12 @@ __device__ __forceinline__ void stage_step_phase(unsigned long long *tmid, const
 template <int kRounds>
 __device__ __forceinline__ void stage_step(unsigned long long *tmid, const StackOp &op, bool a16, const ActSmem &L, int tid, uint32_t t16,
                                            bool check, int spin_ns, int polls, const unsigned int *counters,
-                                           bool quant)
+                                           bool quant, uint32_t t8, int rec_spin)
 {
+    if (!a16 && op.xq) {
+        stage_step_rec(tmid, op, L, tid, t8, check, spin_ns, polls, counters, rec_spin);
+        return;
+    }
     if (!a16 && op.k <= 2048) {
         stage_step_a8_oct(tmid, op, L, tid, t16, check, spin_ns, polls, counters, quant);
         return;
@@ -365,6 +554,10 @@ __global__ void __launch_bounds__(kStepThreads, 1) stack_step(const __grid_const
     // this launch's tag (epoch + 1, never 0): the epoch only changes after every CTA left
     const uint32_t epoch = *reinterpret_cast<volatile unsigned int *>(a.counters + a.nops + 1);
     const uint32_t t16 = ((epoch % 65535u) + 1u) << 16;
+    const uint32_t t8 = (epoch % 255u) + 1u;   // record tag (consecutive launches differ)
+    // CTA-pair exchange of a group's first 16 rows when its two tiles sit on the two CTAs
+    // of a cluster: xfull[2] (st.async complete_tx), xempty[2] (the reader's release), xbuf[2][32 B]
+    const uint32_t xfull = go + 144u, xempty = go + 160u, xbuf = go + 176u;
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < S; ++s) {
@@ -376,6 +569,10 @@ __global__ void __launch_bounds__(kStepThreads, 1) stack_step(const __grid_const
         for (int j = 0; j < (int)EN; ++j) {
             mbar_init(epf + 8u * j, kConsumerWarps);
             mbar_init(epe + 8u * j, 1);
+        }
+        for (int j = 0; j < 2; ++j) {
+            mbar_init(xfull + 8u * j, 1);
+            mbar_init(xempty + 8u * j, 1);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -389,12 +586,36 @@ __global__ void __launch_bounds__(kStepThreads, 1) stack_step(const __grid_const
         for (int i = threadIdx.x; i < n16; i += blockDim.x) dst[i] = src[i];
     }
     __syncthreads();
+    if (a.clustered) cluster_sync_all();   // the peer's exchange barriers are initialised
 
-    auto cta_tiles = [&](const StackOp &op, int &t0, int &t1) {
+    // This CTA's tiles [t0, t1) of an op.  Paired ops (clusters of 2): 32-row pairs are
+    // split evenly over the clusters and each cluster's range in halves over its two
+    // CTAs, so a quantisation group (two tiles) lies in one CTA or, at most once per op,
+    // straddles the cluster's two CTAs (`straddle`: rank 0's last tile is its first
+    // half, rank 1's first tile its second half).  Otherwise contiguous balanced ranges.
+    auto cta_tiles = [&](const StackOp &op, int &t0, int &t1, bool &straddle) {
         const int T = op.tile_start[op.count];
+        straddle = false;
+        if (a.clustered && op.paired) {
+            const uint32_t C = gridDim.x >> 1, c = blockIdx.x >> 1, r = blockIdx.x & 1u;
+            const int P = T >> 1;
+            const int p0 = (int)(((uint32_t)P * c) / C), p1 = (int)(((uint32_t)P * (c + 1)) / C);
+            const int np = p1 - p0;
+            t0 = 2 * p0 + (r ? np : 0);
+            t1 = r ? 2 * p1 : 2 * p0 + np;
+            straddle = (np & 1) != 0;
+            return;
+        }
         // 32-bit: T * gridDim < 2^32 (T <= 2^20 tiles, checked by the program builder)
         t0 = (int)(((uint32_t)T * blockIdx.x) / gridDim.x);
         t1 = (int)(((uint32_t)T * (blockIdx.x + 1)) / gridDim.x);
+    };
+    // The order a CTA works through its tiles (the producer's stages, the epilogue's
+    // slots; the consumers just follow the ring): rank 0 of a straddling pair takes the
+    // shared group's first half FIRST, so both halves are done at the same time and the
+    // exchange never waits for the rest of rank 0's range.
+    auto tile_seq = [&](int j, int t0, int t1, bool straddle) {
+        return (straddle && (blockIdx.x & 1u) == 0) ? (j == 0 ? t1 - 1 : t0 + j - 1) : t0 + j;
     };
 
     if (warp == kConsumerWarps + 1) {
@@ -408,10 +629,12 @@ __global__ void __launch_bounds__(kStepThreads, 1) stack_step(const __grid_const
         // resets the counters and advances the epoch for the next launch.
         const bool nowait = (a.flags & 10) != 0;
         uint32_t ts = 0;   // tile sequence number of this CTA
+        uint32_t held = 0, xsend = 0, xrecv = 0;   // producer-side quantisation state
         for (int i = 0; i < a.nops; ++i) {
             const StackOp &op = ops[i];
             int t0, t1;
-            cta_tiles(op, t0, t1);
+            bool straddle;
+            cta_tiles(op, t0, t1, straddle);
             if (op.wait_op >= 0 && t1 > t0) {
                 if (lane == 0) {
                     if (!nowait)
@@ -423,14 +646,18 @@ __global__ void __launch_bounds__(kStepThreads, 1) stack_step(const __grid_const
                 __syncwarp();
             }
             const bool a16 = op.route == MCAPQ_W4A16;
-            int li = 0;
-            for (int tile = t0; tile < t1; ++tile, ++ts) {
+            for (int j = 0; j < t1 - t0; ++j, ++ts) {
+                const int tile = tile_seq(j, t0, t1, straddle);
+                int li = 0;
                 while (li + 1 < op.count && tile >= op.tile_start[li + 1]) ++li;
                 const uint32_t slot = ts & (EN - 1u);
                 mbar_wait(epf + 8u * slot, (ts >> EL) & 1u);
+                unsigned long long te0 = 0;
+                if (kTrace && lane == 0 && j == t1 - t0 - 1) te0 = globaltimer();
                 const uint32_t sl = red + 1024u * slot;
+                float v = 0.0f;
+                const int tl = tile - op.tile_start[li];
                 if (lane < kTileRows && !(a.flags & 512)) {
-                    float v;
                     float x[kConsumerWarps];
 #pragma unroll
                     for (int w = 0; w < kConsumerWarps; ++w) x[w] = __uint_as_float(lds32(sl + 64u * w + 4u * lane));
@@ -448,11 +675,60 @@ __global__ void __launch_bounds__(kStepThreads, 1) stack_step(const __grid_const
                             for (int w = 0; w < h; ++w) x[w] += x[w + h];
                         v = x[0];
                     }
-                    const int64_t row = (int64_t)(tile - op.tile_start[li]) * kTileRows + lane;
-                    if (row < op.n[li] && !(a.flags & 32)) store_step(op, li, row, v, t16);
                 }
                 __syncwarp();
-                if (lane == 0) mbar_arrive(epe + 8u * slot);
+                if (lane == 0) mbar_arrive(epe + 8u * slot);   // the slot is read: release it
+                if (lane < kTileRows && !(a.flags & 512)) {
+                    const int64_t row = (int64_t)tl * kTileRows + lane;
+                    if (row < op.n[li] && !(a.flags & 32)) store_step(op, li, row, v, t16);
+                }
+                if (op.yq[li] && !(a.flags & 512)) {
+                    // producer-side quantisation of group tl / 2 (rows 32 (tl/2) ..): this
+                    // tile's 16 bf16 values (exactly what y holds) in lanes 0..15
+                    const uint32_t b = lane < kTileRows ? (uint32_t)dev::float_to_bf16_bits(v) : 0u;
+                    if ((tl & 1) == 0) {
+                        if (straddle && tile == t1 - 1) {
+                            // first half of the group the peer (rank 1) completes: push the 16
+                            // values into its exchange slot (st.async + complete_tx)
+                            const uint32_t xs = xsend & 1u;
+                            if (lane == 0) mbar_wait_cluster(xempty + 8u * xs, ((xsend >> 1) & 1u) ^ 1u);
+                            __syncwarp();
+                            const uint32_t lo = __shfl_sync(0xffffffffu, b, (2 * lane) & 31);
+                            const uint32_t hi = __shfl_sync(0xffffffffu, b, (2 * lane + 1) & 31);
+                            if (lane < 8)
+                                st_async_u32(mapa_peer(xbuf + 32u * xs + 4u * lane, 1u), lo | (hi << 16),
+                                             mapa_peer(xfull + 8u * xs, 1u));
+                            ++xsend;
+                        } else {
+                            held = b;
+                        }
+                    } else {
+                        uint32_t first = held;
+                        if (straddle && tile == t0) {
+                            // second half here, first half from the peer (rank 0)
+                            const uint32_t xs = xrecv & 1u;
+                            if (lane == 0) mbar_expect_tx(xfull + 8u * xs, 32u);
+                            mbar_wait(xfull + 8u * xs, (xrecv >> 1) & 1u);
+                            first = lane < kTileRows ? lds16(xbuf + 32u * xs + 2u * lane) : 0u;
+                        }
+                        const uint32_t second = __shfl_sync(0xffffffffu, b, lane & 15);
+                        quant_group_record(lane < kTileRows ? first : second, op.yq[li] + (size_t)(tl >> 1) * kRecWords,
+                                           t8, lane);
+                        if (straddle && tile == t0) {
+                            // the exchange slot is free again: every lane consumed its value
+                            // (the record is built from it), so a relaxed arrive suffices
+                            __syncwarp();
+                            if (lane == 0) mbar_arrive_remote_relaxed(mapa_peer(xempty + 8u * (xrecv & 1u), 0u));
+                            ++xrecv;
+                        }
+                    }
+                }
+                if (kTrace && lane == 0 && j == t1 - t0 - 1) {
+                    // debug: the op's last tile in this epilogue (start, stores issued)
+                    unsigned long long *r = a.trace + 8ull * ((unsigned long long)(a.nops + i) * gridDim.x + blockIdx.x);
+                    r[0] = te0;
+                    r[1] = globaltimer();
+                }
             }
             // publish: 2 = release (a barrier dependency reads through this counter),
             // 1 = relaxed (dataflow consumers only take it as a hint to re-read their tags;
@@ -478,6 +754,7 @@ __global__ void __launch_bounds__(kStepThreads, 1) stack_step(const __grid_const
                 __threadfence();
             }
         }
+        if (a.clustered) cluster_sync_all();   // no CTA leaves while its peer may still address it
         return;
     }
 
@@ -506,15 +783,17 @@ __global__ void __launch_bounds__(kStepThreads, 1) stack_step(const __grid_const
                 const int K2 = (int)(op.k / 2);
                 const int nchunks = (K2 + kChunkBytes - 1) / kChunkBytes;
                 int t0, t1;
-                cta_tiles(op, t0, t1);
-                if (!op.xt) {
+                bool straddle_;
+                cta_tiles(op, t0, t1, straddle_);
+                if (!op.xt && !op.xq) {
                     // a step input: warm it in L2 (evict_last) while the weights stream
                     const int xlines = (int)((op.k * 2 + 127) / 128);
                     for (int ln = blockIdx.x; ln < xlines; ln += gridDim.x)
                         asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(op.x + 64 * ln) : "memory");
                 }
-                int li = 0;
-                for (int tile = t0; tile < t1; ++tile) {
+                for (int j = 0; j < t1 - t0; ++j) {
+                    const int tile = tile_seq(j, t0, t1, straddle_);
+                    int li = 0;
                     while (li + 1 < count && tile >= op.tile_start[li + 1]) ++li;
                     const CUtensorMap *map = op.maps[li];
                     const int row0 = (tile - op.tile_start[li]) * kTileRows;
@@ -551,6 +830,7 @@ __global__ void __launch_bounds__(kStepThreads, 1) stack_step(const __grid_const
                 }
             }
         }
+        if (a.clustered) cluster_sync_all();
         return;
     }
 
@@ -570,7 +850,8 @@ __global__ void __launch_bounds__(kStepThreads, 1) stack_step(const __grid_const
         const int K2 = (int)(k / 2);
         const int nchunks = (K2 + kChunkBytes - 1) / kChunkBytes;
         int t0, t1;
-        cta_tiles(op, t0, t1);
+        bool straddle_;
+        cta_tiles(op, t0, t1, straddle_);
         unsigned long long tr0 = 0, tr1 = 0, tr2 = 0, tr3 = 0, tr4 = 0, trm = 0;
         unsigned int stalls = 0, nstages = 0;
         if (kTrace) tr0 = globaltimer();
@@ -586,7 +867,7 @@ __global__ void __launch_bounds__(kStepThreads, 1) stack_step(const __grid_const
             hold_set(1u);
             bar_consumers();   // every warp is done reading the previous linear's activations
             if (!(a.flags & 4)) stage_step<kRounds>(kTrace ? &trm : nullptr, op, a16, L, threadIdx.x, t16, !(a.flags & 8), a.spin_ns, a.polls, a.counters,
-                                                         !(a.flags & 128));
+                                                         !(a.flags & 128), t8, a.rec_spin);
             bar_consumers();
             hold_set(0u);
             if (kTrace) tr2 = globaltimer();
@@ -770,4 +1051,5 @@ __global__ void __launch_bounds__(kStepThreads, 1) stack_step(const __grid_const
         }
     }
     hold_set(0u);   // never leave the producer held
+    if (a.clustered) cluster_sync_all();
 }

@@ -72,7 +72,18 @@ struct StackDeps {
     uint32_t *yt[kMaxGroup];      // tagged copies of this op's outputs read later, or null
     int wait_op;                  // barrier: wait until every CTA finished op wait_op, or -1
     int publish;                  // some later op waits on this one
+    // producer-side quantisation: quantised records of this op's outputs read later by a
+    // W4A8 op (6 u64 per 32-group), and the records this op's x comes from
+    unsigned long long *yq[kMaxGroup];
+    const unsigned long long *xq;
 };
+// The step kernel runs as clusters of 2 CTAs (paired tiles, producer-side quantisation):
+// the device co-schedules one cluster per SM pair for the whole grid.
+bool stack_clustered();
+constexpr size_t kStackRecBytes = 48;   // one 32-group record
+// Smallest consumer K that takes producer-side quantised records (MCAPQ_STEP_REC_MINK):
+// below it the consumer quantises the tagged bf16 words itself.
+int64_t stack_rec_min_k();
 // Largest K the step kernel stages (4 rounds of 512 quad threads).
 constexpr int64_t kStepMaxK = 16384;
 // Fill one op (host memory, stack_op_bytes() bytes) for `route` over group g with

@@ -63,9 +63,13 @@ def main():
     buf = np.zeros((1 << 16, 8), np.uint64)
     n = mq.load().mcapq_debug_stream_trace(ctypes.c_void_p(buf.ctypes.data), buf.shape[0])
     rec = buf[:n].astype(np.int64)
+    half = n // 2
+    ep = rec[half:n]          # epilogue records: [op][cta] {last tile start, stores issued}
+    rec = rec[:half]
+    nops_ = half // max(1, int(rec[:, 1].max() >> 48) + 1) if half else 0
     t0 = rec[rec[:, 2] > 0, 2].min()
     print(f"{'op':>3} {'ctas':>4} {'start':>8} {'go':>6} {'stage':>6} {'wfirst':>6} {'compute':>7} {'epi':>6} "
-          f"{'end_med':>8} {'end_max':>8} {'stages':>6} {'stalled':>7} {'load':>6}")
+          f"{'end_med':>8} {'end_max':>8} {'stages':>6} {'stalled':>7} {'load':>6} {'ep_med':>8} {'ep_max':>8}")
     tot = np.zeros(5)
     for op in range(min(args.ops, int(rec[:, 0].max()) + 1)):
         r = rec[(rec[:, 0] == op) & (rec[:, 6] > 0)]
@@ -75,9 +79,13 @@ def main():
                                 r[:, 5] - r[:, 7]], 1), 0) / 1000
         load = np.median((r[:, 1] >> 32) & 0xFFFF) / 1000   # go -> input loaded and checked
         tot += d
+        grid = int(rec[:, 1].max() >> 48) + 1
+        e = ep[op * grid:(op + 1) * grid]
+        e = e[e[:, 1] > 0]
+        ep_s = f"{(np.median(e[:, 1]) - t0) / 1000:8.2f} {(e[:, 1].max() - t0) / 1000:8.2f}" if len(e) else ""
         print(f"{op:3d} {len(r):4d} {(np.median(r[:, 2]) - t0) / 1000:8.2f} {d[0]:6.2f} {d[1]:6.2f} {d[2]:6.2f} "
               f"{d[3]:7.2f} {d[4]:6.2f} {(np.median(r[:, 5]) - t0) / 1000:8.2f} {(r[:, 5].max() - t0) / 1000:8.2f} "
-              f"{np.mean(r[:, 1] & 0xFFFF):6.2f} {np.mean((r[:, 1] >> 16) & 0xFFFF):7.2f} {load:6.2f}")
+              f"{np.mean(r[:, 1] & 0xFFFF):6.2f} {np.mean((r[:, 1] >> 16) & 0xFFFF):7.2f} {load:6.2f} {ep_s}")
     print("sum of medians (go, stage, wfirst, compute, epi):", np.round(tot, 2))
     print("total span us:", (rec[:, 5].max() - t0) / 1000)
 
