@@ -71,6 +71,45 @@ def peaks():
     return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
+def ncu_dram_peak():
+    """ncu's DRAM peak (dram__bytes.sum.peak_sustained x dram__cycles_elapsed.avg.per_second)
+    from the newest committed summary, GB/s, or None (SURVEY 8(d) D.2 denominator (i))."""
+    pdir = os.path.join(ROOT, "profiles")
+    if not os.path.isdir(pdir):
+        return None, None
+    for sub in sorted(os.listdir(pdir), reverse=True):
+        p = os.path.join(pdir, sub, "summary.json")
+        if os.path.exists(p):
+            for cap, e in json.load(open(p)).get("captures", {}).items():
+                if e.get("dram_peak_gbs"):
+                    return float(e["dram_peak_gbs"]), f"profiles/{sub}/summary.json:{cap}"
+    return None, None
+
+
+def read_ceiling(mq, dev, stream, gib=1, reps=10):
+    """Pure-read HBM ceiling in this run (D.2 (iii)): mcapq_debug_read_bw streaming a
+    `gib` GiB buffer (> 8 x L2), median of `reps` CUDA-event-timed reads, GB/s."""
+    buf = torch.empty(gib << 30, dtype=torch.uint8, device=dev)
+    buf.fill_(1)
+    sink = torch.zeros(1, dtype=torch.int64, device=dev)
+    times = []
+    with torch.cuda.stream(stream):
+        mq.debug_read_bw(buf, sink, stream=stream)
+        for _ in range(reps):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            mq.debug_read_bw(buf, sink, stream=stream)
+            e1.record(stream)
+            e1.synchronize()
+            times.append(e0.elapsed_time(e1))
+    del buf
+    return buf_bytes_gbs(gib << 30, statistics.median(times))
+
+
+def buf_bytes_gbs(nbytes, ms):
+    return round(nbytes / (ms * 1e-3) / 1e9, 1)
+
+
 def bf16_peak_tflops():
     """Dense bf16 tensor peak: MEASURED_PEAKS.json bf16_tflops (cuBLAS burst), else 2250."""
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
@@ -202,6 +241,20 @@ def time_graph(st, stream, steps, warmup, dist=None):
     if dist is not None:
         dist.barrier()
     return e0.elapsed_time(e1) / steps
+
+
+def step_percentiles(st, stream, steps):
+    """Per-step times (ms) of `steps` back-to-back graph replays, one CUDA event between
+    consecutive replays on the launching stream: p10 / p50 / p90 (D.4)."""
+    evs = [torch.cuda.Event(enable_timing=True) for _ in range(steps + 1)]
+    evs[0].record(stream)
+    for i in range(steps):
+        st.replay(stream=stream)
+        evs[i + 1].record(stream)
+    evs[-1].synchronize()
+    t = sorted(evs[i].elapsed_time(evs[i + 1]) for i in range(steps))
+    q = lambda f: t[min(len(t) - 1, int(f * len(t)))]
+    return {"p10_ms": round(q(0.10), 5), "p50_ms": round(q(0.50), 5), "p90_ms": round(q(0.90), 5), "steps": steps}
 
 
 def time_dominant_kernel(mq, weights, xs, stream, reps_per_layer=4):
@@ -560,14 +613,44 @@ def oracle_step(routes, prep):
     return total_b / total_t / 1e9, sum(t_route.values())
 
 
-def oracle_baseline(steps=3):
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def oracle_baseline(steps=5, warmup=1):
+    """The oracle on all the process's cores: `warmup` untimed samples, then the median
+    of `steps` timed ones (the same procedure as --impl reference)."""
     routes, prep = oracle_prepare()
+    for _ in range(warmup):
+        oracle_step(routes, prep)
     vals, secs = [], 0.0
     for _ in range(steps):
         v, t = oracle_step(routes, prep)
         vals.append(v)
         secs += t
     return statistics.median(vals), len(os.sched_getaffinity(0)), secs
+
+
+def oracle_baseline_1core(steps=3, warmup=1):
+    """The same sample on ONE core: a child process pinned to one CPU with one OpenMP
+    thread (the oracle's row loop is OpenMP), so the thread count is what it says."""
+    import subprocess
+    cpu = sorted(os.sched_getaffinity(0))[0]
+    env = dict(os.environ, OMP_NUM_THREADS="1")
+    code = ("import os, sys, json; os.sched_setaffinity(0, {%d}); sys.path.insert(0, %r); import bench; "
+            "v, c, t = bench.oracle_baseline(%d, %d); print(json.dumps([v, c, t]))" % (cpu, ROOT, steps, warmup))
+    try:
+        out = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
+        v, c, t = json.loads(out.stdout.strip().splitlines()[-1])
+        return v, c, t
+    except Exception as e:   # the headline line must still print
+        return None, 1, f"{type(e).__name__}: {e}"[:120]
 
 
 def run_reference(args):
@@ -590,6 +673,7 @@ def run_reference(args):
         "vs_baseline": None, "dtype": "s8xu4->s32,f32 (W4A8) | f32 (W4A16)", "data": "synthetic",
         "config": {"workload": WORKLOAD, "m": 1, "layers": 16, "routes": "".join(str(r) for r in routes)},
         "cpu_baseline": {"value": round(v, 4), "unit": "GB/s", "cores": cores, "kind": "oracle",
+                         "cpu_model": cpu_model(),
                          "sample": "per step: layer 0 (W4A8) and layer 15 (W4A16) of the stack run in full by the "
                                    f"C oracle, extrapolated to the 15+1 mask; {secs:.1f} s of CPU work in total"},
         "e2e": {"value": round(v, 4), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -652,6 +736,7 @@ def main():
 
     with ClockSampler(local) as clk:
         ms = time_graph(st, stream, args.steps, args.warmup, dist)
+    pct = step_percentiles(st, stream, args.steps)
     # max over ranks
     t = torch.tensor([ms], device=dev)
     if dist is not None:
@@ -698,6 +783,8 @@ def main():
     # (CUDA events on the launching stream).  Algorithmic bytes per launch = the step's
     # packed weights + every activation read once + every output written once.
     peak, peak_src = peaks()
+    dram_peak, dram_peak_src = ncu_dram_peak()
+    read_ceil = read_ceiling(mq, dev, stream)
     kernels_per_step = st.launches(1)
     step_alg_bytes = wbytes + act_bytes
     achieved = step_alg_bytes / (ms_max * 1e-3) / 1e9
@@ -719,9 +806,14 @@ def main():
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         gbs, cores, secs = oracle_baseline()
+        g1, _, s1 = oracle_baseline_1core()
         cpu = {"value": round(gbs, 4), "unit": "GB/s", "cores": cores, "kind": "oracle",
+               "cpu_model": cpu_model(),
                "sample": "layer 0 (W4A8) + layer 15 (W4A16) of the same stack, each run in full by the C oracle "
-                         f"(3 repeats, {secs:.1f} s), extrapolated to the 15+1 mask"}
+                         f"(1 warm-up + median of 5, {secs:.1f} s timed), extrapolated to the 15+1 mask",
+               "value_1core": None if g1 is None else round(g1, 4),
+               "sample_1core": f"the same sample pinned to one CPU, OMP_NUM_THREADS=1 (1 warm-up + median of 3"
+                               + (f", {s1:.1f} s timed)" if g1 is not None else f"; failed: {s1})")}
 
     if rank == 0:
         line = {
@@ -734,6 +826,7 @@ def main():
                        "weight_bytes_per_step": wbytes, "activation_bytes_per_step": act_bytes,
                        "l2_policy": f"no flush: {wbytes / 1e6:.0f} MB of weights per step > {l2 / 1e6:.0f} MB L2",
                        "parallelism": f"replicas x{world}" if world > 1 else "1 GPU"},
+            "step_ms_percentiles": pct,
             "us_per_layer": round(ms_max * 1000 / L, 3),
             "us_per_linear": round(ms_max * 1000 / (L * len(SLOTS)), 3),
             "routes_endpoints": {"all_w4a8_gbs": round(wbytes / (ms8 * 1e-3) / 1e9, 1),
@@ -746,7 +839,13 @@ def main():
                          "kernel": "stack_step (persistent routed decode step: all 112 linears, one launch)"
                          if kernels_per_step == 1 else "stack (per-linear launches)",
                          "alg_bytes_per_launch": step_alg_bytes, "us_per_launch": round(ms_max * 1000, 3),
-                         "launches_timed": args.steps, "peak_source": peak_src},
+                         "launches_timed": args.steps, "peak_source": peak_src,
+                         "other_denominators": {
+                             "ncu_dram_peak_gbs": dram_peak, "frac_ncu_dram_peak":
+                                 round(achieved / dram_peak, 4) if dram_peak else None,
+                             "ncu_dram_peak_source": dram_peak_src,
+                             "read_ceiling_gbs": read_ceil, "frac_read_ceiling": round(achieved / read_ceil, 4),
+                             "read_ceiling_source": "mcapq_debug_read_bw, 1 GiB streaming LDG.128, this run"}},
             "per_linear_kernel": {"kernel": "stream_linear<DP4A> grouped gate+up (2 x 8192x2048, M=1, fused "
                                             "quantiser), launched alone, rotating 16 layers' weights",
                                   "achieved": round(k_bytes / (k_ms * 1e-3) / 1e9, 1), "unit": "GB/s",

@@ -304,6 +304,16 @@ mcapq_status mcapq_debug_stream_w4a8_dump(const uint8_t *nib, const uint16_t *sc
  */
 size_t mcapq_debug_stream_trace(uint64_t *host_out, size_t max_records);
 
+/*
+ * DIAGNOSTIC (measurement only, never on the hot path): one streaming read of `bytes`
+ * bytes of device memory at `buf` (16-B aligned, >= 16 bytes; the tail below 16 bytes
+ * is skipped), LDG.128 with L1 no-allocate, 4 CTAs x 512 threads per
+ * SM -- the pure-read HBM ceiling SURVEY 8(d) D.2 (iii) reports the GEMV beside.  `sink`
+ * (device, 8 bytes) is written only to keep the loads live.  Stream-ordered; the caller
+ * times it (CUDA events).  MCAPQ_EINVAL on a NULL / misaligned pointer.
+ */
+mcapq_status mcapq_debug_read_bw(const void *buf, size_t bytes, unsigned long long *sink, void *stream);
+
 /* ------------------------------------------------------ dispatch table (a7) */
 /*
  * MCAP profile -> per-layer routes.  Alg. 1 lines 8-13, P:840-846,

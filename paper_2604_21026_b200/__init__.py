@@ -30,7 +30,7 @@ __all__ = [
     "profile_parse", "profile_write_json", "mcap_accumulate", "Stack", "Comm", "linear_colshard", "PackedW4",
     "colshard_assemble", "stream_w4a8_dump", "linear_argmax", "argmax_keys", "argmax_combine",
     "argmax_workspace_bytes", "linear_colshard_argmax",
-    "device_sms", "set_pdl",
+    "device_sms", "set_pdl", "debug_read_bw",
 ]
 
 
@@ -356,6 +356,13 @@ def stream_w4a8_dump(w: PackedW4, x: torch.Tensor, stream=None):
 
 
 # ------------------------------------------------------------------ profile
+def debug_read_bw(buf: torch.Tensor, sink: torch.Tensor, stream=None):
+    """Diagnostic: one streaming read of buf (the pure-read HBM ceiling; mcapq_debug_read_bw)."""
+    _need_cuda(buf, sink)
+    check(load().mcapq_debug_read_bw(_ptr(buf), buf.numel() * buf.element_size(), _ptr(sink), _stream(stream)),
+          "mcapq_debug_read_bw")
+
+
 class Profile:
     """Dispatch table parsed by the library (a7)."""
 

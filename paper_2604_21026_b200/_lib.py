@@ -27,6 +27,7 @@ SIGNATURES = {
     "mcapq_device_sms": (I32, []),
     "mcapq_set_pdl": (I32, [I32]),
     "mcapq_debug_stream_trace": (SZ, [P, SZ]),
+    "mcapq_debug_read_bw": (I32, [P, SZ, P, P]),
     "mcapq_w4_nib_bytes": (SZ, [I64, I64]),
     "mcapq_w4_scale_bytes": (SZ, [I64, I64]),
     "mcapq_pack_w4": (I32, [P, I32, I64, I64, I64, P, P, P, P]),
@@ -101,6 +102,8 @@ def load(path: str | os.PathLike | None = None) -> ctypes.CDLL:
         raise ImportError(f"{p} is missing: run `python -m paper_2604_21026_b200.build` (no fallback path exists)")
     L = ctypes.CDLL(str(p))
     for name, (res, args) in SIGNATURES.items():
+        if name.startswith("mcapq_debug_") and os.environ.get("MCAPQ_LIB") and not hasattr(L, name):
+            continue   # an older build under A/B (MCAPQ_LIB) may predate a diagnostic entry
         f = getattr(L, name)
         f.restype = res
         f.argtypes = args

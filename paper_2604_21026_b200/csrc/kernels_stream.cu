@@ -269,6 +269,9 @@ __device__ __forceinline__ int quant_code(float v, float s, float inv)
     return code < -127 ? -127 : (code > 127 ? 127 : code);
 }
 
+// quant_code out of line (the rare slow path of the fused quantisers)
+__device__ __noinline__ int quant_code_ool(float v, float s, float inv) { return quant_code(v, s, inv); }
+
 // D = A.B + C with an explicit accumulator init (C may repeat registers).
 __device__ __forceinline__ void hmma_c(uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3, uint32_t b0, uint32_t b1,
                                        float c0, float c1, float c2, float c3, float d[4])
@@ -361,7 +364,7 @@ struct Tune {
     // per-SM queue of in-flight weight data that the chain's L2 accesses wait behind
     int smem_kb = 112, max_stages = 12, nocompute = 0, pdl = 0, trace = 0, step_smem_kb = 200, step = 1,
         step_flags = 0, step_spin_ns = 16, step_polls = 1, ctas_per_sm = 0, step_ep_log2 = 1, smem_kb_env = 0,
-        step_hold = 1, step_inflight = 0, step_rec_spin = 64;
+        step_hold = 2, step_rec_spin = 64;
 };
 const Tune &tune()
 {
@@ -383,7 +386,6 @@ const Tune &tune()
         if (const char *e = getenv("MCAPQ_STREAM_CTAS_PER_SM")) v.ctas_per_sm = atoi(e);
         if (const char *e = getenv("MCAPQ_STEP_EP_LOG2")) v.step_ep_log2 = atoi(e);
         if (const char *e = getenv("MCAPQ_STEP_HOLD")) v.step_hold = atoi(e);
-        if (const char *e = getenv("MCAPQ_STEP_INFLIGHT")) v.step_inflight = atoi(e);
         if (const char *e = getenv("MCAPQ_STEP_REC_SPIN")) v.step_rec_spin = atoi(e);
         if (v.step_ep_log2 < 1) v.step_ep_log2 = 1;
         if (v.step_ep_log2 > 3) v.step_ep_log2 = 3;
@@ -840,12 +842,16 @@ bool stack_clustered()
 }
 
 cudaError_t launch_stack_step(const void *ops_dev, int nops, unsigned int *counters_dev, int64_t max_k,
-                              cudaStream_t s)
+                              bool clustered, int route_kinds, cudaStream_t s)
 {
     for (const void *f : {reinterpret_cast<const void *>(stack_step<false, 2>),
                           reinterpret_cast<const void *>(stack_step<true, 2>),
                           reinterpret_cast<const void *>(stack_step<false, 4>),
-                          reinterpret_cast<const void *>(stack_step<true, 4>)}) {
+                          reinterpret_cast<const void *>(stack_step<true, 4>),
+                          reinterpret_cast<const void *>(stack_step<false, 2, 1>),
+                          reinterpret_cast<const void *>(stack_step<false, 2, 2>),
+                          reinterpret_cast<const void *>(stack_step<false, 4, 1>),
+                          reinterpret_cast<const void *>(stack_step<false, 4, 2>)}) {
         cudaError_t e = kernel_smem_attr(f, 227 * 1024);
         if (e != cudaSuccess) return e;
     }
@@ -859,7 +865,6 @@ cudaError_t launch_stack_step(const void *ops_dev, int nops, unsigned int *count
     a.polls = tune().step_polls;
     a.ep_log2 = tune().step_ep_log2;
     a.hold = tune().step_hold;
-    a.inflight = tune().step_inflight;
     a.rec_spin = tune().step_rec_spin;
     // one CTA per SM: activations for the largest K under either route, the rest is ring
     const size_t act = round_up(act_bytes(HMMA1, max_k, 1) > act_bytes(DP4A, max_k, 1) ? act_bytes(HMMA1, max_k, 1)
@@ -891,7 +896,7 @@ cudaError_t launch_stack_step(const void *ops_dev, int nops, unsigned int *count
     cfg.dynamicSmemBytes = smem;
     cfg.stream = s;
     cudaLaunchAttribute attr[1];
-    a.clustered = stack_clustered() ? 1 : 0;
+    a.clustered = (clustered && stack_clustered()) ? 1 : 0;
     if (a.clustered) {
         // clusters of 2 (paired tiles); all CTAs co-resident: one per SM, and the
         // occupancy check found room for every cluster
@@ -905,9 +910,19 @@ cudaError_t launch_stack_step(const void *ops_dev, int nops, unsigned int *count
     }
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    if (max_k <= 8192)
-        return a.trace ? cudaLaunchKernelEx(&cfg, stack_step<true, 2>, a) : cudaLaunchKernelEx(&cfg, stack_step<false, 2>, a);
-    return a.trace ? cudaLaunchKernelEx(&cfg, stack_step<true, 4>, a) : cudaLaunchKernelEx(&cfg, stack_step<false, 4>, a);
+    // route_kinds: bit 0 = some W4A8 linear, bit 1 = some W4A16 linear (a single-route
+    // program takes the instantiation without the other engine)
+    const int kinds = a.trace ? 3 : (route_kinds & 3);
+    if (max_k <= 8192) {
+        if (a.trace) return cudaLaunchKernelEx(&cfg, stack_step<true, 2>, a);
+        if (kinds == 1) return cudaLaunchKernelEx(&cfg, stack_step<false, 2, 1>, a);
+        if (kinds == 2) return cudaLaunchKernelEx(&cfg, stack_step<false, 2, 2>, a);
+        return cudaLaunchKernelEx(&cfg, stack_step<false, 2>, a);
+    }
+    if (a.trace) return cudaLaunchKernelEx(&cfg, stack_step<true, 4>, a);
+    if (kinds == 1) return cudaLaunchKernelEx(&cfg, stack_step<false, 4, 1>, a);
+    if (kinds == 2) return cudaLaunchKernelEx(&cfg, stack_step<false, 4, 2>, a);
+    return cudaLaunchKernelEx(&cfg, stack_step<false, 4>, a);
 }
 
 size_t stream_trace_read(unsigned long long *host_out, size_t max_records)

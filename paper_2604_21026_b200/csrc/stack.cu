@@ -49,6 +49,8 @@ struct mcapq_stack {
     uint32_t *tags = nullptr;           // tagged copies of outputs consumed inside the step
     int nops = 0;
     int64_t max_k = 0;
+    bool has_records = false;   // some op stages producer-quantised records: clustered launch
+    int route_kinds = 3;        // bit 0: some W4A8 op, bit 1: some W4A16 op
 };
 
 using namespace mcapq;
@@ -302,6 +304,7 @@ static mcapq_status build_program(mcapq_stack *st)
     // one allocation: tagged words, then the 16-B aligned records (both zero: tag 0 is
     // never current)
     const size_t tag_bytes = (tag_words * 4 + 15) / 16 * 16;
+    st->has_records = rec_words > 0;
     if (tag_words + rec_words) {
         MCAPQ_CUDA_TRY(cudaMalloc(&st->tags, tag_bytes + rec_words * 8));
         MCAPQ_CUDA_TRY(cudaMemset(st->tags, 0, tag_bytes + rec_words * 8));
@@ -327,6 +330,8 @@ static mcapq_status build_program(mcapq_stack *st)
         if (deps[i].wait_op >= 0) deps[deps[i].wait_op].publish = 2;
     }
 
+    st->route_kinds = 0;
+    for (int i = 0; i < nops; ++i) st->route_kinds |= st->routes[groups[i].first] == MCAPQ_W4A16 ? 2 : 1;
     const size_t ob = stack_op_bytes();
     st->nops = nops;
     MCAPQ_CUDA_TRY(cudaMallocHost(&st->ops_host, ob * nops));
@@ -368,7 +373,8 @@ mcapq_status mcapq_stack_run(mcapq_stack *st, int64_t m, void *stream)
     }
     if (m == 1 && !st->prog_dirty && st->prog_ok) {
         // the whole step in one persistent cooperative kernel
-        cudaError_t e = launch_stack_step(st->ops_dev, st->nops, st->counters, st->max_k, s);
+        cudaError_t e = launch_stack_step(st->ops_dev, st->nops, st->counters, st->max_k, st->has_records,
+                                          st->route_kinds, s);
         MCAPQ_REQUIRE(e == cudaSuccess, MCAPQ_ECUDA, "stack_step launch: %s", cudaGetErrorString(e));
         return MCAPQ_OK;
     }

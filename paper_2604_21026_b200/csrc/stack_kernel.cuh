@@ -69,7 +69,6 @@ struct StackArgs {
     int polls;                   // CTA-wide re-read rounds before waiting on the producer's counter
     int ep_log2;                 // log2 of the tile slots between the consumers and the epilogue warp (1..3)
     int hold;                    // 1: the producer holds ring refills while this CTA stages an input (see `hold`)
-    int inflight;                // > 0: at most this many stages issued by the producer and not yet landed
     int clustered;               // launched as clusters of 2 CTAs: paired ops split their tiles per cluster
     int rec_spin;                // > 0: record consumers spin per thread (back-off cap, ns); 0: counter scheme
 };
@@ -93,6 +92,19 @@ __device__ __forceinline__ uint32_t lds32_volatile(uint32_t addr)
 {
     uint32_t v;
     asm volatile("ld.volatile.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr) : "memory");
+    return v;
+}
+// The refill-hold flag is a lock-free flag between a consumer thread (writer) and the
+// producer thread (poller): atomic accesses on both sides, so it is not a data race
+// (compute-sanitizer racecheck) and every poll sees the latest write.
+__device__ __forceinline__ void hold_write(uint32_t addr, uint32_t v)
+{
+    asm volatile("atom.shared.exch.b32 _, [%0], %1;" ::"r"(addr), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t hold_read(uint32_t addr)
+{
+    uint32_t v;
+    asm volatile("atom.shared.or.b32 %0, [%1], 0;" : "=r"(v) : "r"(addr) : "memory");
     return v;
 }
 __device__ __forceinline__ bool tags_ok(uint4 a, uint32_t t16)
@@ -169,7 +181,7 @@ __device__ __forceinline__ void quant_group_record(uint32_t xb, unsigned long lo
     const float r = __fsub_rn(qa, __fsub_rn(t, 12582912.0f));
     int c = __float_as_int(t) - 0x4B400000;
     // a NaN residual (inv = inf) counts as bad: !(|r| < 0.4999)
-    if (__any_sync(0xffffffffu, !(fabsf(r) < 0.4999f)) && live) c = quant_code(v, s, inv);
+    if (__any_sync(0xffffffffu, !(fabsf(r) < 0.4999f)) && live) c = quant_code_ool(v, s, inv);
     if (!live) c = 0;
     const int sum = __reduce_add_sync(0xffffffffu, c);
     const uint32_t cb = (uint32_t)c & 0xffu;
@@ -529,7 +541,10 @@ __device__ __forceinline__ void store_step(const StackOp &op, int m, int64_t row
 
 // kRounds: staging rounds of 512 quads (2: K <= 8192, 4: K <= 16384) -- fewer rounds,
 // fewer live registers under the 96-register cap of 18 warps per SM
-template <bool kTrace, int kRounds>
+// kRoutes: 3 = a mixed program (both engines), 1 = W4A8 only, 2 = W4A16 only -- a
+// single-route program runs an instantiation without the other engine's code (a
+// smaller kernel: the mixed one regressed untouched W4A16 loops by ~8 % as it grew)
+template <bool kTrace, int kRounds, int kRoutes = 3>
 __global__ void __launch_bounds__(kStepThreads, 1) stack_step(const __grid_constant__ StackArgs a)
 {
     extern __shared__ __align__(16) uint8_t smem_raw[];
@@ -645,18 +660,29 @@ __global__ void __launch_bounds__(kStepThreads, 1) stack_step(const __grid_const
                 }
                 __syncwarp();
             }
-            const bool a16 = op.route == MCAPQ_W4A16;
+            const bool a16 = kRoutes == 2 ? true : (kRoutes == 1 ? false : op.route == MCAPQ_W4A16);
+            // member li of the group and its first tile, advanced incrementally (the
+            // reordered rank-0 range of a straddling pair restarts the walk once)
+            int li = 0, li_start = 0, li_next = op.count > 1 ? op.tile_start[1] : 0x7fffffff;
             for (int j = 0; j < t1 - t0; ++j, ++ts) {
                 const int tile = tile_seq(j, t0, t1, straddle);
-                int li = 0;
-                while (li + 1 < op.count && tile >= op.tile_start[li + 1]) ++li;
+                if (j <= 1 && straddle) {
+                    li = 0;
+                    li_start = 0;
+                    li_next = op.count > 1 ? op.tile_start[1] : 0x7fffffff;
+                }
+                while (tile >= li_next) {
+                    ++li;
+                    li_start = li_next;
+                    li_next = li + 1 < op.count ? op.tile_start[li + 1] : 0x7fffffff;
+                }
                 const uint32_t slot = ts & (EN - 1u);
                 mbar_wait(epf + 8u * slot, (ts >> EL) & 1u);
                 unsigned long long te0 = 0;
                 if (kTrace && lane == 0 && j == t1 - t0 - 1) te0 = globaltimer();
                 const uint32_t sl = red + 1024u * slot;
                 float v = 0.0f;
-                const int tl = tile - op.tile_start[li];
+                const int tl = tile - li_start;
                 if (lane < kTileRows && !(a.flags & 512)) {
                     float x[kConsumerWarps];
 #pragma unroll
@@ -676,12 +702,12 @@ __global__ void __launch_bounds__(kStepThreads, 1) stack_step(const __grid_const
                         v = x[0];
                     }
                 }
-                __syncwarp();
-                if (lane == 0) mbar_arrive(epe + 8u * slot);   // the slot is read: release it
                 if (lane < kTileRows && !(a.flags & 512)) {
                     const int64_t row = (int64_t)tl * kTileRows + lane;
                     if (row < op.n[li] && !(a.flags & 32)) store_step(op, li, row, v, t16);
                 }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(epe + 8u * slot);   // the slot is consumed: release it
                 if (op.yq[li] && !(a.flags & 512)) {
                     // producer-side quantisation of group tl / 2 (rows 32 (tl/2) ..): this
                     // tile's 16 bf16 values (exactly what y holds) in lanes 0..15
@@ -762,8 +788,9 @@ __global__ void __launch_bounds__(kStepThreads, 1) stack_step(const __grid_const
         // ================= producer: the whole step's weights, in op order =================
         if (lane == 0) {
             const uint64_t pol = evict_first_policy();
-            int s = 0, ls = 0, inflight = 0;
-            uint32_t ph = 0, lph = 0;
+            int s = 0;
+            uint32_t ph = 0;
+            const bool noload = (a.flags & 256) != 0;
             auto prefetch_maps = [&](int j) {
                 // TMA descriptors of linear j into the TMA unit's cache before first use
                 if (j >= a.nops) return;
@@ -791,31 +818,28 @@ __global__ void __launch_bounds__(kStepThreads, 1) stack_step(const __grid_const
                     for (int ln = blockIdx.x; ln < xlines; ln += gridDim.x)
                         asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(op.x + 64 * ln) : "memory");
                 }
+                int li = 0, li_start = 0, li_next = count > 1 ? op.tile_start[1] : 0x7fffffff;
                 for (int j = 0; j < t1 - t0; ++j) {
                     const int tile = tile_seq(j, t0, t1, straddle_);
-                    int li = 0;
-                    while (li + 1 < count && tile >= op.tile_start[li + 1]) ++li;
+                    if (j <= 1 && straddle_) {
+                        li = 0;
+                        li_start = 0;
+                        li_next = count > 1 ? op.tile_start[1] : 0x7fffffff;
+                    }
+                    while (tile >= li_next) {
+                        ++li;
+                        li_start = li_next;
+                        li_next = li + 1 < count ? op.tile_start[li + 1] : 0x7fffffff;
+                    }
                     const CUtensorMap *map = op.maps[li];
-                    const int row0 = (tile - op.tile_start[li]) * kTileRows;
+                    const int row0 = (tile - li_start) * kTileRows;
                     for (int ch = 0; ch < nchunks; ++ch) {
                         mbar_wait(empty + 8u * s, ph ^ 1u);
                         if (a.hold)
                             while (lds32_volatile(hold) != 0u) __nanosleep(32);
-                        // in-flight cap: at most a.inflight stages issued and not landed, so
-                        // this SM's weight requests never queue deep in front of the chain's
-                        // latency-critical L2 accesses while the ring still refills continuously
-                        while (a.inflight > 0 && inflight >= a.inflight) {
-                            mbar_wait(full + 8u * ls, lph);
-                            --inflight;
-                            if (++ls == S) {
-                                ls = 0;
-                                lph ^= 1u;
-                            }
-                        }
-                        ++inflight;
                         const uint32_t st = ring + (uint32_t)s * kStageBytes;
                         const uint32_t fb = full + 8u * s;
-                        if (a.flags & 256) {
+                        if (noload) {
                             mbar_arrive(fb);   // debug: no weight traffic (the chain alone, garbage results)
                         } else {
                             mbar_expect_tx(fb, (uint32_t)kStageBytes);
@@ -839,8 +863,18 @@ __global__ void __launch_bounds__(kStepThreads, 1) stack_step(const __grid_const
     asm volatile("" : "+r"(kNib2), "+r"(kMagic));
     int s = 0;
     uint32_t ph = 0, goph = 0, ts = 0;
+    // hold modes: 1 always, 2 only while a tagged-bf16 input is staged (not records), 3 only
+    // for W4A16 inputs -- decided per linear from the linear about to be staged
+    bool hold_on = false;
+    auto hold_for = [&](int j) {
+        if (j >= a.nops || a.hold == 0) return false;
+        const StackOp &nx = ops[j];
+        if (a.hold == 2) return nx.xt != nullptr;
+        if (a.hold == 3) return nx.route == MCAPQ_W4A16;
+        return true;
+    };
     auto hold_set = [&](uint32_t v) {
-        if (a.hold && threadIdx.x == 0) sts32(hold, v);
+        if (a.hold && threadIdx.x == 0 && (v == 0u || hold_on)) hold_write(hold, v);
     };
     for (int i = 0; i < a.nops; ++i) {
         const StackOp &op = ops[i];
@@ -862,14 +896,16 @@ __global__ void __launch_bounds__(kStepThreads, 1) stack_step(const __grid_const
                 goph ^= 1u;
             }
             if (kTrace) tr1 = globaltimer();
-            const bool a16 = route == MCAPQ_W4A16;
+            const bool a16 = kRoutes == 2 ? true : (kRoutes == 1 ? false : route == MCAPQ_W4A16);
             const ActSmem L = act_layout(a16, act, k, 1);
+            hold_on = hold_for(i);
             hold_set(1u);
             bar_consumers();   // every warp is done reading the previous linear's activations
             if (!(a.flags & 4)) stage_step<kRounds>(kTrace ? &trm : nullptr, op, a16, L, threadIdx.x, t16, !(a.flags & 8), a.spin_ns, a.polls, a.counters,
                                                          !(a.flags & 128), t8, a.rec_spin);
             bar_consumers();
             hold_set(0u);
+            hold_on = hold_for(i + 1);   // the in-loop set below is for the next linear's staging
             if (kTrace) tr2 = globaltimer();
 
             if (!a16) {
@@ -998,6 +1034,7 @@ __global__ void __launch_bounds__(kStepThreads, 1) stack_step(const __grid_const
                 }
             } else {
                 // ---- W4A16, HMMA1 engine (warp w owns blocks 4w..4w+3 for all 16 rows)
+
                 for (int tile = t0; tile < t1; ++tile, ++ts) {
                     float acc[4] = {0.f, 0.f, 0.f, 0.f};
                     for (int ch = 0; ch < nchunks; ++ch) {

@@ -94,9 +94,11 @@ bool stack_fill_op(void *host_op, int route, const StreamGroup &g, const uint16_
                    CUtensorMap *host_maps, const CUtensorMap *dev_maps);
 // Launch the step: ops_dev = nops filled ops in device memory; counters_dev = nops + 2
 // uint32 (zeroed once at allocation; the kernel's last CTA resets them and advances
-// the epoch at [nops + 1]); max_k = the largest K of the program.
+// the epoch at [nops + 1]); max_k = the largest K of the program; clustered = the
+// program uses producer-quantised records (clusters of 2, requires stack_clustered());
+// route_kinds = bit 0 some W4A8 op, bit 1 some W4A16 op.
 cudaError_t launch_stack_step(const void *ops_dev, int nops, unsigned int *counters_dev, int64_t max_k,
-                              cudaStream_t s);
+                              bool clustered, int route_kinds, cudaStream_t s);
 
 // Encode the {nib, scale} tensor-map pair of a packed weight for the stream / step
 // kernels (host only; false if the driver entry point is missing or encoding fails).

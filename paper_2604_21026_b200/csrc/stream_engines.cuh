@@ -222,22 +222,26 @@ __device__ __forceinline__ bool quant_words_fast(const uint32_t *w, float inv, u
     return worst < 0.4999f && inv < __int_as_float(0x7f800000);
 }
 
-// Slow path of quant_words_fast (a group with an element near a half-integer): every
-// code by quant_code (IEEE division), packed four per word.
+// Slow path of quant_words_fast (a group with an element near a half-integer): four
+// codes by quant_code (IEEE division), packed.  Out of line and register-only (scalar
+// arguments, a scalar result): the rare path costs no instruction-cache space in the
+// callers and no local memory.
+__device__ __noinline__ uint32_t quant4_ieee(uint32_t w0, uint32_t w1, float s, float inv)
+{
+    uint32_t p = 0;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        const uint32_t b = (j >> 1) ? w1 : w0;
+        const float v = __uint_as_float((j & 1) ? (b & 0xffff0000u) : (b << 16));
+        p |= ((uint32_t)quant_code(v, s, inv) & 0xffu) << (8 * j);
+    }
+    return p;
+}
 template <int NW>
 __device__ __forceinline__ void quant_words_ieee(const uint32_t *w, float s, float inv, uint32_t *out)
 {
 #pragma unroll
-    for (int o = 0; o < NW / 2; ++o) {
-        uint32_t p = 0;
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            const uint32_t b = w[2 * o + (j >> 1)];
-            const float v = __uint_as_float((j & 1) ? (b & 0xffff0000u) : (b << 16));
-            p |= ((uint32_t)quant_code(v, s, inv) & 0xffu) << (8 * j);
-        }
-        out[o] = p;
-    }
+    for (int o = 0; o < NW / 2; ++o) out[o] = quant4_ieee(w[2 * o], w[2 * o + 1], s, inv);
 }
 
 // Codes of NW packed bf16 words of a group whose abs-max bits are m (reduced over the

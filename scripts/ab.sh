@@ -10,7 +10,7 @@ if [ "${TESTS:-1}" = "1" ]; then
   timeout 600 python -m pytest tests -m gpu -x -q -k "${TESTK:-step or stack}" > $O/pytest.txt 2>&1; echo "rc $?" >> $O/pytest.txt
 fi
 IFS=';' read -ra CS <<< "$CASES"
-for rep in 1 2; do
+for rep in $(seq 1 ${REPS:-2}); do
 for lib in $LIBS; do
   for r in $ROUTES; do
     for c in "${CS[@]}"; do

@@ -9,6 +9,7 @@ python __graft_entry__.py > $OUT/build.log 2>&1
 timeout 1200 python -m pytest tests -m gpu -x -q > $OUT/pytest_gpu.log 2>&1; echo "pytest exit $?" >> $OUT/pytest_gpu.log
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $OUT/smoke.log 2>&1; echo "smoke exit $?" >> $OUT/smoke.log
 timeout 900 python bench.py > $OUT/bench.json 2> $OUT/bench.err; echo "bench exit $?" >> $OUT/bench.err
+if [ "${ONLY_NCU:-0}" = "1" ]; then :; fi
 timeout 400 python scripts/kbench.py --cases o_1b,qkv_1b,gateup_1b,down_1b,gate_8b,down_8b,lmhead_8b,up_3b_m16,q_3b_m64,lmhead_8b_m64 > $OUT/kbench.jsonl 2>&1
 timeout 300 python scripts/kbench.py --cases up_3b_m16,up_3b_m64,q_3b_m64,lmhead_8b_m16,lmhead_8b_m64 --routes 2 >> $OUT/kbench.jsonl 2>&1
 if [ "${NCU:-1}" = "1" ]; then
@@ -18,6 +19,11 @@ if [ "${NCU:-1}" = "1" ]; then
   # the headline step kernel (whole 16-layer step in one launch)
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:stack_step -s 3 -c 1 \
      -o $OUT/prof_step python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-extras > $OUT/ncu_step.log 2>&1
+  # the 8B MLP stack step (records path: clusters of 2, producer-side quantisation), both routes
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:stack_step -s 3 -c 1 \
+     -o $OUT/prof_step_mlp8b python scripts/step_probe.py --mlp8b --routes 0 > $OUT/ncu_step_mlp8b.log 2>&1
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:stack_step -s 3 -c 1 \
+     -o $OUT/prof_step_mlp8b_a16 python scripts/step_probe.py --mlp8b --routes 1 > $OUT/ncu_step_mlp8b_a16.log 2>&1
   # the dominant per-linear kernel: W4A8 grouped gate+up (bench's roofline kernel)
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:stream_linear -s 8 -c 1 \
      -o $OUT/prof_w4a8 python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-extras > $OUT/ncu_w4a8.log 2>&1

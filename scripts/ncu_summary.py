@@ -22,7 +22,8 @@ RAW = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum"
        "smsp__warps_issue_stalled_long_scoreboard_per_warp_active.pct",
        "sm__pipe_tensor_subpipe_hmma_cycles_active.avg.pct_of_peak_sustained_active",
        "sm__pipe_tensor_subpipe_imma_cycles_active.avg.pct_of_peak_sustained_active",
-       "sm__inst_executed_pipe_uniform.avg.pct_of_peak_sustained_active"]
+       "sm__inst_executed_pipe_uniform.avg.pct_of_peak_sustained_active",
+       "dram__bytes.sum.peak_sustained", "dram__cycles_elapsed.avg.per_second"]
 
 
 def raw_metrics(rep):
@@ -85,6 +86,13 @@ def main():
             wr = to_bytes(d["dram__bytes_write.sum"]) if "dram__bytes_write.sum" in d else None
             entry = {"kernel": d["kernel"][:120], "duration_ns": dur, "dram_read_bytes": rd, "dram_write_bytes": wr,
                      "dram_GBps": (rd + wr) / dur if dur and rd is not None else None}
+            if "dram__bytes.sum.peak_sustained" in d and "dram__cycles_elapsed.avg.per_second" in d:
+                # ncu's DRAM peak: bytes per DRAM cycle x DRAM clock
+                v, u = d["dram__bytes.sum.peak_sustained"]
+                bpc = float(v.replace(",", "")) * {"byte/cycle": 1, "Kbyte/cycle": 1e3, "Mbyte/cycle": 1e6}.get(u, 1)
+                v, u = d["dram__cycles_elapsed.avg.per_second"]
+                hz = float(v.replace(",", "")) * {"hz": 1, "Khz": 1e3, "Mhz": 1e6, "Ghz": 1e9}.get(u, 1)
+                entry["dram_peak_gbs"] = round(bpc * hz / 1e9, 1)
             for k in RAW[3:]:
                 if k in d:
                     entry[k] = d[k][0]

@@ -27,6 +27,7 @@ def main():
     ap.add_argument("--independent", action="store_true")
     ap.add_argument("--ops", type=int, default=64)
     ap.add_argument("--mlp8b", action="store_true", help="the 8-layer Llama-3.1-8B MLP stack instead")
+    ap.add_argument("--no-epilogue", action="store_true", help="a build without the epilogue records (A/B)")
     args = ap.parse_args()
     assert os.environ.get("MCAPQ_STREAM_TRACE") == "1"
     dev = torch.device("cuda:0")
@@ -63,7 +64,7 @@ def main():
     buf = np.zeros((1 << 16, 8), np.uint64)
     n = mq.load().mcapq_debug_stream_trace(ctypes.c_void_p(buf.ctypes.data), buf.shape[0])
     rec = buf[:n].astype(np.int64)
-    half = n // 2
+    half = n if args.no_epilogue else n // 2
     ep = rec[half:n]          # epilogue records: [op][cta] {last tile start, stores issued}
     rec = rec[:half]
     nops_ = half // max(1, int(rec[:, 1].max() >> 48) + 1) if half else 0

@@ -153,3 +153,45 @@ def test_colshard_assemble_f32_ragged_m(mq):
     src = torch.randn(P, m, per, device=DEV)
     y = mq.colshard_assemble(src, P)
     assert torch.equal(y, src.permute(1, 0, 2).reshape(m, P * per))
+
+
+# ---------------------------------------------------------------- producer-side quantisation records
+@pytest.mark.parametrize("route_down", [0])
+def test_step_records_edge_groups(mq, orc, route_down):
+    """The producer-quantised records (step kernel, a W4A8 consumer with K >= 4096): the
+    up linear's output is made to contain all-zero 32-row groups (amax = 0: s = +0,
+    codes 0), groups with one x100 outlier row, and groups whose two 16-row halves come
+    from the two CTAs of a cluster; down (K = 8192) reads the records.  Each linear
+    against the oracle on the input it actually read, and down bit-identical to the
+    per-linear path (which quantises the same bf16 words itself)."""
+    n_up, k = 8192, 2048
+    w_up = si.weight(n_up, k, 2600)
+    g = torch.arange(n_up) // 32
+    w_up[(g % 7) == 3] = 0.0                         # whole groups of zero rows -> y = 0
+    w_up[(torch.arange(n_up) % 224) == 17] *= 100.0   # one x100 outlier row in some groups
+    w_down = si.weight(2048, n_up, 2601)
+    x = si.activation(1, k, 2602).to(DEV)
+    y_up = torch.empty(1, n_up, dtype=torch.bfloat16, device=DEV)
+    y_down = torch.empty(1, 2048, dtype=torch.bfloat16, device=DEV)
+    pw_up, pw_down = mq.pack_w4(w_up.to(DEV)), mq.pack_w4(w_down.to(DEV))
+    st = mq.Stack([route_down], max_m=1)
+    st.set(0, 0, 0, pw_up, x, y_up)
+    st.set(0, 1, 1, pw_down, y_up, y_down)
+    st.run(1)
+    torch.cuda.synchronize()
+    assert st.launches(1) == 1
+    assert (y_up.view(-1)[(g % 7 == 3).to(DEV)] == 0).all()
+    nib, sc = orc.pack_w4(_f32(w_down))
+    _assert_close(y_down, _oracle_y64(orc, route_down, nib, sc, y_up), 2e-3)
+    ref = mq.linear(route_down, pw_down, y_up.clone(), out_dtype=torch.bfloat16)
+    assert torch.equal(ref, y_down)
+    # replays: records carry the new epoch's tag every launch
+    first = y_down.clone()
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        st.capture(1, stream=s)
+        for _ in range(3):
+            y_down.zero_()
+            st.replay(stream=s)
+            s.synchronize()
+            assert torch.equal(first, y_down)
