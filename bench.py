@@ -337,8 +337,10 @@ def time_sharded(mq, dev, stream, dist, world, rank):
     (M = 1, 64) and MLP gate / down column-sharded over the job's ranks.  Per layer and
     route: T(1) = the unsharded linear on one GPU (no collective), T(P) = the sharded
     linear + NCCL all-gather into the replicated y (mcapq_linear_colshard), t_local = the
-    rank's shard alone, comm = T(P) - t_local, E(P) = T(1) / (P T(P)); for the lm_head
-    also greedy decode (local argmax + P x M key gather, mcapq_linear_colshard_argmax).
+    rank's shard alone, comm = T(P) - t_local, E(P) = T(1) / (P T(P)); at M = 1 also the
+    fused epilogue (NVLink stores into NCCL symmetric-window replicas + one LSA barrier:
+    fused_TP_us, fused_comm_us, fused_E); for the lm_head also greedy decode (local argmax +
+    P x M key gather, mcapq_linear_colshard_argmax).
     Every time is a CUDA graph of repeated calls over rotating weight copies (>= 4 x L2
     together), CUDA events, max over ranks."""
     comm = mq.Comm() if world > 1 else None
@@ -371,6 +373,19 @@ def time_sharded(mq, dev, stream, dist, world, rank):
                                 for c in shard_c], stream, reps, dist)
                 row.update({"t_local_us": round(tl, 3), "TP_us": round(tp, 3), "comm_us": round(tp - tl, 3),
                             "E": round(t1 / (world * tp), 3), "gbs_total": round(wbytes / tp / 1e3, 1)})
+                if m == 1:
+                    # a8 fused epilogue: NVLink stores into every rank's window replica + one LSA
+                    # barrier instead of the all-gather (mcapq_linear_colshard fused_epilogue=1)
+                    try:
+                        yw = comm.window(n)
+                        tf = _graph_us([lambda c=c: mq.linear_colshard(comm, route, c, n, x, out=yw, ws=wsc,
+                                                                       stream=stream, fused=True) for c in shard_c],
+                                       stream, reps, dist)
+                        comm.free_window(yw)
+                        row.update({"fused_TP_us": round(tf, 3), "fused_comm_us": round(tf - tl, 3),
+                                    "fused_E": round(t1 / (world * tf), 3)})
+                    except Exception as e:   # the headline line must still print
+                        row["fused_error"] = f"{type(e).__name__}: {e}"[:160]
                 if slot == "lm_head":
                     wsa = torch.empty(max(256, mq.argmax_workspace_bytes(route, m, per, k, world)),
                                       dtype=torch.uint8, device=dev)

@@ -445,7 +445,36 @@ int mcapq_comm_rank(const mcapq_comm *c);
 size_t mcapq_colshard_workspace_bytes(int route, int64_t m, int64_t n_full, int64_t k, int world);
 mcapq_status mcapq_linear_colshard(const mcapq_comm *c, int route, const uint8_t *nib_shard,
                                    const uint16_t *scale_shard, int64_t n_full, int64_t k, const uint16_t *x,
-                                   int64_t m, void *y_full, int ydt, void *ws, size_t ws_bytes, void *stream);
+                                   int64_t m, void *y_full, int ydt, void *ws, size_t ws_bytes, int fused_epilogue,
+                                   void *stream);
+/*
+ * fused_epilogue (SURVEY 8(e) "Collective: fused"; a8): with fused_epilogue != 0, m == 1
+ * and a stream-path K (k % 256 == 0, k >= 2048), y_full must lie in a symmetric window from
+ * mcapq_comm_window_alloc: the GEMV epilogue stores each of this rank's rows into EVERY
+ * rank's replica of y_full directly over NVLink (NCCL symmetric window, LSA load/store
+ * pointers; P stores per element), then one NCCL LSA barrier kernel orders them -- no
+ * all-gather kernel, no separate copy.  Otherwise (fused_epilogue == 0, m > 1, or another
+ * K) the NCCL all-gather path above runs.  Errors: MCAPQ_EINVAL if fused and y_full is not
+ * in this communicator's window.
+ *
+ * mcapq_comm_window_alloc: COLLECTIVE over the communicator (every rank calls it with the
+ * same bytes, in the same order): ncclMemAlloc + ncclCommWindowRegister(symmetric), and on
+ * first use an ncclDevComm with one LSA barrier; *y_full = this rank's replica (device,
+ * library-owned, 4 KiB-aligned size).  MCAPQ_EUNSUP when the ranks do not share one NVLink
+ * (LSA) domain of <= 8 GPUs.  mcapq_comm_window_free: collective; frees it (synchronises
+ * the device).  Not graph-capturable; the fused colshard call itself is.
+ */
+mcapq_status mcapq_comm_window_alloc(mcapq_comm *c, size_t bytes, void **y_full);
+mcapq_status mcapq_comm_window_free(mcapq_comm *c, void *y_full);
+/*
+ * TEST ENTRY (a8 fused epilogue on one GPU): the routed linear (m = 1, stream-path K)
+ * writing its n rows at y and, for every p < npeers, at y + peer_delta_host[p] bytes --
+ * the per-peer stores of the fused epilogue with P emulated replicas in one allocation.
+ * 1 <= npeers <= 8; peer_delta_host is host memory.
+ */
+mcapq_status mcapq_debug_linear_peers(int route, const uint8_t *nib, const uint16_t *scale, int64_t n, int64_t k,
+                                      const uint16_t *x, void *y, int ydt, const int64_t *peer_delta_host, int npeers,
+                                      void *stream);
 mcapq_status mcapq_colshard_assemble(const void *rank_major, void *y_full, int64_t m, int64_t n_full, int world,
                                      int ydt, void *stream);
 /*

@@ -30,7 +30,7 @@ __all__ = [
     "profile_parse", "profile_write_json", "mcap_accumulate", "Stack", "Comm", "linear_colshard", "PackedW4",
     "colshard_assemble", "stream_w4a8_dump", "linear_argmax", "argmax_keys", "argmax_combine",
     "argmax_workspace_bytes", "linear_colshard_argmax",
-    "device_sms", "set_pdl", "debug_read_bw",
+    "device_sms", "set_pdl", "debug_read_bw", "debug_linear_peers",
 ]
 
 
@@ -523,6 +523,30 @@ class Comm:
     def workspace_bytes(self, route, m, n_full, k):
         return load().mcapq_colshard_workspace_bytes(route, m, n_full, k, self.world)
 
+    def window(self, n_full: int, dtype=torch.bfloat16) -> torch.Tensor:
+        """COLLECTIVE: a [1, n_full] y_full replica in an NCCL symmetric window
+        (mcapq_comm_window_alloc) for linear_colshard(..., fused=True); library-owned,
+        released by free_window() or with the communicator."""
+        es = torch.tensor([], dtype=dtype).element_size()
+        ptr = ctypes.c_void_p()
+        check(load().mcapq_comm_window_alloc(self._h, n_full * es, ctypes.byref(ptr)), "mcapq_comm_window_alloc")
+
+        class _Raw:   # a device pointer as a CUDA array (int16/int32 words, viewed as dtype below)
+            __cuda_array_interface__ = {"shape": (1, n_full), "typestr": "<i2" if es == 2 else "<i4",
+                                        "data": (ptr.value, False), "version": 3}
+        t = torch.as_tensor(_Raw(), device="cuda").view(dtype)
+        self._windows = getattr(self, "_windows", []) + [(ptr.value, t)]
+        return t
+
+    def free_window(self, t: torch.Tensor):
+        """COLLECTIVE: release a window from window()."""
+        for i, (p, tt) in enumerate(getattr(self, "_windows", [])):
+            if tt.data_ptr() == t.data_ptr():
+                check(load().mcapq_comm_window_free(self._h, ctypes.c_void_p(p)), "mcapq_comm_window_free")
+                del self._windows[i]
+                return
+        raise ValueError("not a window of this communicator")
+
 
 def colshard_assemble(rank_major: torch.Tensor, world: int, out=None, stream=None) -> torch.Tensor:
     """a8 assembly: rank-major [P, M, N/P] -> y_full [M, N] (mcapq_colshard_assemble)."""
@@ -551,13 +575,26 @@ def linear_colshard_argmax(comm: Comm, route: int, w_shard: PackedW4, n_full: in
 
 
 def linear_colshard(comm: Comm, route: int, w_shard: PackedW4, n_full: int, x: torch.Tensor,
-                    out_dtype=torch.bfloat16, out=None, ws=None, stream=None):
-    """a8: column-sharded routed linear + NCCL all-gather into y_full [M, n_full]."""
+                    out_dtype=torch.bfloat16, out=None, ws=None, stream=None, fused: bool = False):
+    """a8: column-sharded routed linear + NCCL all-gather into y_full [M, n_full].
+    fused=True (M = 1): `out` must be a window tensor from Comm.window(); the GEMV epilogue
+    stores straight into every rank's replica over NVLink, then one LSA barrier."""
     x2 = _act(x, w_shard.k)
     m = x2.shape[0]
     y = _out(m, n_full, out_dtype, x.device, out)
     ws = ws if ws is not None else _scratch(comm.workspace_bytes(route, m, n_full, w_shard.k), x.device, stream)
     check(load().mcapq_linear_colshard(comm._h, route, _ptr(w_shard.nib), _ptr(w_shard.scale), n_full, w_shard.k,
-                                       _ptr(x2), m, _ptr(y), _dt(y.dtype), _ptr(ws), ws.numel(), _stream(stream)),
+                                       _ptr(x2), m, _ptr(y), _dt(y.dtype), _ptr(ws), ws.numel(), int(bool(fused)),
+                                       _stream(stream)),
           "mcapq_linear_colshard")
     return y
+
+
+def debug_linear_peers(route: int, w: PackedW4, x: torch.Tensor, y: torch.Tensor, peer_delta, stream=None):
+    """Test entry: the fused epilogue's per-peer stores on one GPU (mcapq_debug_linear_peers):
+    y (a view into one buffer) receives the rows, and so does every y + peer_delta[p] bytes."""
+    x2 = _act(x, w.k)
+    d = (ctypes.c_int64 * len(peer_delta))(*[int(v) for v in peer_delta])
+    check(load().mcapq_debug_linear_peers(route, _ptr(w.nib), _ptr(w.scale), w.n, w.k, _ptr(x2), _ptr(y), _dt(y.dtype),
+                                          ctypes.cast(d, ctypes.c_void_p), len(peer_delta), _stream(stream)),
+          "mcapq_debug_linear_peers")

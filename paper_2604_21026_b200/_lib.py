@@ -28,6 +28,7 @@ SIGNATURES = {
     "mcapq_set_pdl": (I32, [I32]),
     "mcapq_debug_stream_trace": (SZ, [P, SZ]),
     "mcapq_debug_read_bw": (I32, [P, SZ, P, P]),
+    "mcapq_debug_linear_peers": (I32, [I32, P, P, I64, I64, P, P, I32, P, I32, P]),
     "mcapq_w4_nib_bytes": (SZ, [I64, I64]),
     "mcapq_w4_scale_bytes": (SZ, [I64, I64]),
     "mcapq_pack_w4": (I32, [P, I32, I64, I64, I64, P, P, P, P]),
@@ -76,7 +77,9 @@ SIGNATURES = {
     "mcapq_comm_world": (I32, [P]),
     "mcapq_comm_rank": (I32, [P]),
     "mcapq_colshard_workspace_bytes": (SZ, [I32, I64, I64, I64, I32]),
-    "mcapq_linear_colshard": (I32, [P, I32, P, P, I64, I64, P, I64, P, I32, P, SZ, P]),
+    "mcapq_linear_colshard": (I32, [P, I32, P, P, I64, I64, P, I64, P, I32, P, SZ, I32, P]),
+    "mcapq_comm_window_alloc": (I32, [P, SZ, P]),
+    "mcapq_comm_window_free": (I32, [P, P]),
     "mcapq_colshard_assemble": (I32, [P, P, I64, I64, I32, I32, P]),
     "mcapq_linear_colshard_argmax": (I32, [P, I32, P, P, I64, I64, P, I64, P, P, P, SZ, P]),
     "mcapq_comm_destroy": (None, [P]),

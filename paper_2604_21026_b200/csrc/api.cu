@@ -138,6 +138,24 @@ size_t mcapq_debug_stream_trace(uint64_t *host_out, size_t max_records)
     return stream_trace_read(reinterpret_cast<unsigned long long *>(host_out), max_records);
 }
 
+mcapq_status mcapq_debug_linear_peers(int route, const uint8_t *nib, const uint16_t *scale, int64_t n, int64_t k,
+                                      const uint16_t *x, void *y, int ydt, const int64_t *peer_delta_host, int npeers,
+                                      void *stream)
+{
+    clear_error();
+    CHECK_SHAPE(n, k, 1);
+    mcapq_status st = check_weight(nib, scale, n, k);
+    if (st != MCAPQ_OK) return st;
+    CHECK_PTR(x, "x");
+    CHECK_PTR(y, "y");
+    CHECK_YDT(ydt);
+    MCAPQ_REQUIRE(peer_delta_host && npeers >= 1 && npeers <= kMaxPeers, MCAPQ_EINVAL, "bad peers");
+    MCAPQ_REQUIRE(route == MCAPQ_W4A8 || route == MCAPQ_W4A16, MCAPQ_EINVAL, "bad route");
+    MCAPQ_REQUIRE(stream_supported(k) && aligned16(scale), MCAPQ_EUNSUP, "stream-path K only (k %% 256 == 0, >= 2048)");
+    LAUNCH_TRY(launch_linear_peers(route, nib, scale, n, k, x, y, ydt, peer_delta_host, npeers, as_stream(stream)));
+    return MCAPQ_OK;
+}
+
 size_t mcapq_w4_nib_bytes(int64_t n, int64_t k) { return (n > 0 && k > 0) ? (size_t)(n * (k / 2)) : 0; }
 size_t mcapq_w4_scale_bytes(int64_t n, int64_t k) { return (n > 0 && k > 0) ? (size_t)(n * (k / 32) * 2) : 0; }
 

@@ -13,12 +13,29 @@
 //            kernel writes y_full[m][r N/P + j] (mcapq_colshard_assemble, also a test
 //            entry: P-way shard emulation on one GPU).
 #include <nccl.h>
+#include <nccl_device.h>
+
+#include <vector>
 
 #include "internal.h"
+#include "stream.h"
+
+// A symmetric NCCL window holding one y_full replica per rank (a8 fused epilogue): the
+// byte offsets from this rank's replica to every LSA peer's (NVLink load/store mapping).
+struct McapqWindow {
+    void *ptr = nullptr;
+    size_t bytes = 0;
+    ncclWindow_t win = nullptr;
+    int npeers = 0;
+    int64_t delta[mcapq::kMaxPeers] = {};
+};
 
 struct mcapq_comm {
     ncclComm_t comm = nullptr;
     int world = 1, rank = 0;
+    bool dev_ok = false;        // ncclDevComm with one LSA barrier, created with the first window
+    ncclDevComm dev = {};
+    std::vector<McapqWindow> wins;
 };
 
 using namespace mcapq;
@@ -43,6 +60,23 @@ __global__ void permute_rank_major(const uint8_t *__restrict__ src, uint8_t *__r
 }
 
 size_t align256(size_t b) { return (b + 255) & ~(size_t)255; }
+
+// byte offsets from this rank's replica to each LSA peer's (ncclGetLsaPointer is device-side)
+__global__ void lsa_peer_deltas(ncclWindow_t w, int npeers, int64_t *out)
+{
+    const int p = threadIdx.x;
+    if (p < npeers)
+        out[p] = reinterpret_cast<const char *>(ncclGetLsaPointer(w, 0, p)) -
+                 reinterpret_cast<const char *>(ncclGetLocalPointer(w, 0));
+}
+
+// every LSA peer arrives, then waits: orders all peers' NVLink stores into the replicas
+// (issued by the preceding kernel on each rank's stream) before anyone reads y_full
+__global__ void lsa_barrier_kernel(ncclDevComm dev)
+{
+    ncclLsaBarrierSession<ncclCoopCta> bar(ncclCoopCta(), dev, ncclTeamTagLsa(), 0);
+    bar.sync(ncclCoopCta(), cuda::memory_order_acq_rel);
+}
 
 }  // namespace
 
@@ -119,7 +153,8 @@ mcapq_status mcapq_colshard_assemble(const void *rank_major, void *y_full, int64
 
 mcapq_status mcapq_linear_colshard(const mcapq_comm *c, int route, const uint8_t *nib_shard,
                                    const uint16_t *scale_shard, int64_t n_full, int64_t k, const uint16_t *x,
-                                   int64_t m, void *y_full, int ydt, void *ws, size_t ws_bytes, void *stream)
+                                   int64_t m, void *y_full, int ydt, void *ws, size_t ws_bytes, int fused_epilogue,
+                                   void *stream)
 {
     clear_error();
     MCAPQ_REQUIRE(c && c->comm, MCAPQ_EINVAL, "communicator is NULL");
@@ -132,6 +167,23 @@ mcapq_status mcapq_linear_colshard(const mcapq_comm *c, int route, const uint8_t
     const int64_t per = n_full / c->world;
     MCAPQ_REQUIRE(per % 8 == 0, MCAPQ_EINVAL, "N/P=%lld must be a multiple of 8", (long long)per);
     const int es = ydt == MCAPQ_F32 ? 4 : 2;
+    if (fused_epilogue && m == 1 && stream_supported(k) && aligned16(scale_shard)) {
+        // a8 fused: the GEMV epilogue stores each of this rank's rows into every LSA
+        // peer's replica of y_full (NVLink stores), then one LSA barrier -- no all-gather
+        const McapqWindow *w = nullptr;
+        for (const auto &v : c->wins)
+            if (reinterpret_cast<uint8_t *>(y_full) >= reinterpret_cast<uint8_t *>(v.ptr) &&
+                reinterpret_cast<uint8_t *>(y_full) + (size_t)n_full * es <= reinterpret_cast<uint8_t *>(v.ptr) + v.bytes)
+                w = &v;
+        MCAPQ_REQUIRE(w, MCAPQ_EINVAL, "fused_epilogue: y_full is not in a window from mcapq_comm_window_alloc");
+        uint8_t *mine = reinterpret_cast<uint8_t *>(y_full) + (size_t)c->rank * (size_t)per * es;
+        cudaStream_t s = as_stream(stream);
+        cudaError_t e = launch_linear_peers(route, nib_shard, scale_shard, per, k, x, mine, ydt, w->delta, w->npeers, s);
+        MCAPQ_REQUIRE(e == cudaSuccess, MCAPQ_ECUDA, "fused colshard launch: %s", cudaGetErrorString(e));
+        lsa_barrier_kernel<<<1, 32, 0, s>>>(c->dev);
+        MCAPQ_CUDA_TRY(cudaGetLastError());
+        return MCAPQ_OK;
+    }
     uint8_t *p = reinterpret_cast<uint8_t *>(ws) + 256;
     uint8_t *gathered = nullptr;
     if (m > 1) {
@@ -177,10 +229,67 @@ mcapq_status mcapq_linear_colshard_argmax(const mcapq_comm *c, int route, const 
     return mcapq_argmax_combine(keys, c->world, m, idx, val, stream);
 }
 
+mcapq_status mcapq_comm_window_alloc(mcapq_comm *c, size_t bytes, void **y_full)
+{
+    clear_error();
+    MCAPQ_REQUIRE(c && c->comm && y_full && bytes > 0, MCAPQ_EINVAL, "bad window_alloc arguments");
+    McapqWindow w;
+    w.bytes = (bytes + NCCL_WIN_REQUIRED_ALIGNMENT - 1) / NCCL_WIN_REQUIRED_ALIGNMENT * NCCL_WIN_REQUIRED_ALIGNMENT;
+    NCCL_TRY(ncclMemAlloc(&w.ptr, w.bytes));
+    ncclResult_t r = ncclCommWindowRegister(c->comm, w.ptr, w.bytes, &w.win, NCCL_WIN_COLL_SYMMETRIC);
+    if (r != ncclSuccess) {
+        ncclMemFree(w.ptr);
+        set_error("ncclCommWindowRegister: %s", ncclGetErrorString(r));
+        return MCAPQ_ENCCL;
+    }
+    if (!c->dev_ok) {
+        ncclDevCommRequirements reqs = {};
+        reqs.lsaBarrierCount = 1;
+        NCCL_TRY(ncclDevCommCreate(c->comm, &reqs, &c->dev));
+        c->dev_ok = true;
+    }
+    w.npeers = c->dev.lsaSize < kMaxPeers ? c->dev.lsaSize : kMaxPeers;
+    MCAPQ_REQUIRE(c->dev.lsaSize == c->world && c->world <= kMaxPeers, MCAPQ_EUNSUP,
+                  "fused epilogue needs every rank in one NVLink (LSA) domain of <= %d GPUs (lsa %d, world %d)",
+                  kMaxPeers, c->dev.lsaSize, c->world);
+    int64_t *d = nullptr;
+    MCAPQ_CUDA_TRY(cudaMalloc(&d, sizeof(int64_t) * kMaxPeers));
+    lsa_peer_deltas<<<1, 32>>>(w.win, w.npeers, d);
+    cudaError_t e = cudaMemcpy(w.delta, d, sizeof(int64_t) * w.npeers, cudaMemcpyDeviceToHost);
+    cudaFree(d);
+    MCAPQ_CUDA_TRY(e);
+    c->wins.push_back(w);
+    *y_full = w.ptr;
+    return MCAPQ_OK;
+}
+
+mcapq_status mcapq_comm_window_free(mcapq_comm *c, void *y_full)
+{
+    clear_error();
+    MCAPQ_REQUIRE(c && c->comm, MCAPQ_EINVAL, "communicator is NULL");
+    for (size_t i = 0; i < c->wins.size(); ++i)
+        if (c->wins[i].ptr == y_full) {
+            MCAPQ_CUDA_TRY(cudaDeviceSynchronize());
+            NCCL_TRY(ncclCommWindowDeregister(c->comm, c->wins[i].win));
+            NCCL_TRY(ncclMemFree(c->wins[i].ptr));
+            c->wins.erase(c->wins.begin() + (long)i);
+            return MCAPQ_OK;
+        }
+    MCAPQ_REQUIRE(false, MCAPQ_EINVAL, "not a window of this communicator");
+}
+
 void mcapq_comm_destroy(mcapq_comm *c)
 {
     if (!c) return;
-    if (c->comm) ncclCommDestroy(c->comm);
+    if (c->comm) {
+        cudaDeviceSynchronize();
+        for (auto &w : c->wins) {
+            ncclCommWindowDeregister(c->comm, w.win);
+            ncclMemFree(w.ptr);
+        }
+        if (c->dev_ok) ncclDevCommDestroy(c->comm, &c->dev);
+        ncclCommDestroy(c->comm);
+    }
     delete c;
 }
 

@@ -1104,6 +1104,8 @@ cudaError_t launch_stream_group(int route, const StreamGroup &g, const uint16_t 
     a.x = x;
     a.ldx = ldx;
     a.ydt = ydt;
+    a.npeers = (m == 1 && g.npeers > 0) ? (g.npeers < kMaxPeers ? g.npeers : kMaxPeers) : 0;
+    for (int p = 0; p < a.npeers; ++p) a.peer_delta[p] = g.peer_delta[p];
     // grid: one CTA per SM leaves room for the next linear's CTA under PDL (hides the
     // ramp of back-to-back linears); a long linear (>= 16 tiles per SM) instead runs two
     // CTAs per SM -- twice the consumer warps per SM, and its ramp is amortised anyway
@@ -1134,6 +1136,23 @@ cudaError_t launch_stream_group(int route, const StreamGroup &g, const uint16_t 
         pdl = true;
     }
     return cudaSuccess;
+}
+
+cudaError_t launch_linear_peers(int route, const uint8_t *nib, const uint16_t *scale, int64_t n, int64_t k,
+                                const uint16_t *x, void *y, int ydt, const int64_t *delta, int npeers, cudaStream_t s)
+{
+    if (npeers < 1 || npeers > kMaxPeers) return cudaErrorInvalidValue;
+    StreamGroup g = {};
+    g.count = 1;
+    g.k = k;
+    g.nib[0] = nib;
+    g.scale[0] = scale;
+    g.n[0] = n;
+    g.y[0] = y;
+    g.ldy[0] = n;
+    g.npeers = npeers;
+    for (int p = 0; p < npeers; ++p) g.peer_delta[p] = delta[p];
+    return launch_stream_group(route, g, x, 1, k, ydt, s, false);
 }
 
 }  // namespace mcapq

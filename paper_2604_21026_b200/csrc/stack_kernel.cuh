@@ -661,100 +661,118 @@ __global__ void __launch_bounds__(kStepThreads, 1) stack_step(const __grid_const
                 __syncwarp();
             }
             const bool a16 = kRoutes == 2 ? true : (kRoutes == 1 ? false : op.route == MCAPQ_W4A16);
-            // member li of the group and its first tile, advanced incrementally (the
-            // reordered rank-0 range of a straddling pair restarts the walk once)
-            int li = 0, li_start = 0, li_next = op.count > 1 ? op.tile_start[1] : 0x7fffffff;
-            for (int j = 0; j < t1 - t0; ++j, ++ts) {
-                const int tile = tile_seq(j, t0, t1, straddle);
-                if (j <= 1 && straddle) {
-                    li = 0;
-                    li_start = 0;
-                    li_next = op.count > 1 ? op.tile_start[1] : 0x7fffffff;
-                }
-                while (tile >= li_next) {
-                    ++li;
-                    li_start = li_next;
-                    li_next = li + 1 < op.count ? op.tile_start[li + 1] : 0x7fffffff;
-                }
-                const uint32_t slot = ts & (EN - 1u);
-                mbar_wait(epf + 8u * slot, (ts >> EL) & 1u);
-                unsigned long long te0 = 0;
-                if (kTrace && lane == 0 && j == t1 - t0 - 1) te0 = globaltimer();
-                const uint32_t sl = red + 1024u * slot;
-                float v = 0.0f;
-                const int tl = tile - li_start;
-                if (lane < kTileRows && !(a.flags & 512)) {
-                    float x[kConsumerWarps];
-#pragma unroll
-                    for (int w = 0; w < kConsumerWarps; ++w) x[w] = __uint_as_float(lds32(sl + 64u * w + 4u * lane));
-                    if (a16) {
-                        // HMMA1 partials: the stream kernel's linear order over the warps
-                        v = x[0];
-#pragma unroll
-                        for (int w = 1; w < kConsumerWarps; ++w) v += x[w];
-                    } else {
-                        // row-lane DP4A: warp w holds level 1 of stream_linear's butterfly
-                        // (lanes w, w + 16); levels 2..5 pair w with w + 8, + 4, + 2, + 1
-#pragma unroll
-                        for (int h = kConsumerWarps / 2; h > 0; h >>= 1)
-#pragma unroll
-                            for (int w = 0; w < h; ++w) x[w] += x[w + h];
-                        v = x[0];
+            // the tile loop in two instantiations: ops whose outputs feed records carry the
+            // producer-side quantiser; the others keep the plain loop (the record code in a
+            // shared loop slowed W4A16 tiles by ~3.5 % although it never ran for them)
+            auto ep_tiles = [&](auto rec_c) {
+                constexpr bool kRec = decltype(rec_c)::value;
+                // member li of the group and its first tile, advanced incrementally (the
+                // reordered rank-0 range of a straddling pair restarts the walk once)
+                int li = 0, li_start = 0, li_next = op.count > 1 ? op.tile_start[1] : 0x7fffffff;
+                for (int j = 0; j < t1 - t0; ++j, ++ts) {
+                    const int tile = tile_seq(j, t0, t1, straddle);
+                    if (j <= 1 && straddle) {
+                        li = 0;
+                        li_start = 0;
+                        li_next = op.count > 1 ? op.tile_start[1] : 0x7fffffff;
                     }
-                }
-                if (lane < kTileRows && !(a.flags & 512)) {
-                    const int64_t row = (int64_t)tl * kTileRows + lane;
-                    if (row < op.n[li] && !(a.flags & 32)) store_step(op, li, row, v, t16);
-                }
-                __syncwarp();
-                if (lane == 0) mbar_arrive(epe + 8u * slot);   // the slot is consumed: release it
-                if (op.yq[li] && !(a.flags & 512)) {
-                    // producer-side quantisation of group tl / 2 (rows 32 (tl/2) ..): this
-                    // tile's 16 bf16 values (exactly what y holds) in lanes 0..15
-                    const uint32_t b = lane < kTileRows ? (uint32_t)dev::float_to_bf16_bits(v) : 0u;
-                    if ((tl & 1) == 0) {
-                        if (straddle && tile == t1 - 1) {
-                            // first half of the group the peer (rank 1) completes: push the 16
-                            // values into its exchange slot (st.async + complete_tx)
-                            const uint32_t xs = xsend & 1u;
-                            if (lane == 0) mbar_wait_cluster(xempty + 8u * xs, ((xsend >> 1) & 1u) ^ 1u);
-                            __syncwarp();
-                            const uint32_t lo = __shfl_sync(0xffffffffu, b, (2 * lane) & 31);
-                            const uint32_t hi = __shfl_sync(0xffffffffu, b, (2 * lane + 1) & 31);
-                            if (lane < 8)
-                                st_async_u32(mapa_peer(xbuf + 32u * xs + 4u * lane, 1u), lo | (hi << 16),
-                                             mapa_peer(xfull + 8u * xs, 1u));
-                            ++xsend;
+                    while (tile >= li_next) {
+                        ++li;
+                        li_start = li_next;
+                        li_next = li + 1 < op.count ? op.tile_start[li + 1] : 0x7fffffff;
+                    }
+                    const uint32_t slot = ts & (EN - 1u);
+                    mbar_wait(epf + 8u * slot, (ts >> EL) & 1u);
+                    unsigned long long te0 = 0;
+                    if (kTrace && lane == 0 && j == t1 - t0 - 1) te0 = globaltimer();
+                    const uint32_t sl = red + 1024u * slot;
+                    float v = 0.0f;
+                    const int tl = tile - li_start;
+                    if (lane < kTileRows && !(a.flags & 512)) {
+                        float x[kConsumerWarps];
+    #pragma unroll
+                        for (int w = 0; w < kConsumerWarps; ++w) x[w] = __uint_as_float(lds32(sl + 64u * w + 4u * lane));
+                        if (a16) {
+                            // HMMA1 partials: the stream kernel's linear order over the warps
+                            v = x[0];
+    #pragma unroll
+                            for (int w = 1; w < kConsumerWarps; ++w) v += x[w];
                         } else {
-                            held = b;
-                        }
-                    } else {
-                        uint32_t first = held;
-                        if (straddle && tile == t0) {
-                            // second half here, first half from the peer (rank 0)
-                            const uint32_t xs = xrecv & 1u;
-                            if (lane == 0) mbar_expect_tx(xfull + 8u * xs, 32u);
-                            mbar_wait(xfull + 8u * xs, (xrecv >> 1) & 1u);
-                            first = lane < kTileRows ? lds16(xbuf + 32u * xs + 2u * lane) : 0u;
-                        }
-                        const uint32_t second = __shfl_sync(0xffffffffu, b, lane & 15);
-                        quant_group_record(lane < kTileRows ? first : second, op.yq[li] + (size_t)(tl >> 1) * kRecWords,
-                                           t8, lane);
-                        if (straddle && tile == t0) {
-                            // the exchange slot is free again: every lane consumed its value
-                            // (the record is built from it), so a relaxed arrive suffices
-                            __syncwarp();
-                            if (lane == 0) mbar_arrive_remote_relaxed(mapa_peer(xempty + 8u * (xrecv & 1u), 0u));
-                            ++xrecv;
+                            // row-lane DP4A: warp w holds level 1 of stream_linear's butterfly
+                            // (lanes w, w + 16); levels 2..5 pair w with w + 8, + 4, + 2, + 1
+    #pragma unroll
+                            for (int h = kConsumerWarps / 2; h > 0; h >>= 1)
+    #pragma unroll
+                                for (int w = 0; w < h; ++w) x[w] += x[w + h];
+                            v = x[0];
                         }
                     }
+                    if (lane < kTileRows && !(a.flags & 512)) {
+                        const int64_t row = (int64_t)tl * kTileRows + lane;
+                        if (row < op.n[li] && !(a.flags & 32)) store_step(op, li, row, v, t16);
+                    }
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(epe + 8u * slot);   // the slot is consumed: release it
+                    if (kRec && op.yq[li] && !(a.flags & 512)) {
+                        // producer-side quantisation of group tl / 2 (rows 32 (tl/2) ..): this
+                        // tile's 16 bf16 values (exactly what y holds) in lanes 0..15
+                        const uint32_t b = lane < kTileRows ? (uint32_t)dev::float_to_bf16_bits(v) : 0u;
+                        if ((tl & 1) == 0) {
+                            if (straddle && tile == t1 - 1) {
+                                // first half of the group the peer (rank 1) completes: push the 16
+                                // values into its exchange slot (st.async + complete_tx)
+                                const uint32_t xs = xsend & 1u;
+                                if (lane == 0) mbar_wait_cluster(xempty + 8u * xs, ((xsend >> 1) & 1u) ^ 1u);
+                                __syncwarp();
+                                const uint32_t lo = __shfl_sync(0xffffffffu, b, (2 * lane) & 31);
+                                const uint32_t hi = __shfl_sync(0xffffffffu, b, (2 * lane + 1) & 31);
+                                if (lane < 8)
+                                    st_async_u32(mapa_peer(xbuf + 32u * xs + 4u * lane, 1u), lo | (hi << 16),
+                                                 mapa_peer(xfull + 8u * xs, 1u));
+                                ++xsend;
+                            } else {
+                                held = b;
+                            }
+                        } else {
+                            uint32_t first = held;
+                            if (straddle && tile == t0) {
+                                // second half here, first half from the peer (rank 0)
+                                const uint32_t xs = xrecv & 1u;
+                                if (lane == 0) mbar_expect_tx(xfull + 8u * xs, 32u);
+                                mbar_wait(xfull + 8u * xs, (xrecv >> 1) & 1u);
+                                first = lane < kTileRows ? lds16(xbuf + 32u * xs + 2u * lane) : 0u;
+                            }
+                            const uint32_t second = __shfl_sync(0xffffffffu, b, lane & 15);
+                            quant_group_record(lane < kTileRows ? first : second, op.yq[li] + (size_t)(tl >> 1) * kRecWords,
+                                               t8, lane);
+                            if (straddle && tile == t0) {
+                                // the exchange slot is free again: every lane consumed its value
+                                // (the record is built from it), so a relaxed arrive suffices
+                                __syncwarp();
+                                if (lane == 0) mbar_arrive_remote_relaxed(mapa_peer(xempty + 8u * (xrecv & 1u), 0u));
+                                ++xrecv;
+                            }
+                        }
+                    }
+                    if (kTrace && lane == 0 && j == t1 - t0 - 1) {
+                        // debug: the op's last tile in this epilogue (start, stores issued)
+                        unsigned long long *r = a.trace + 8ull * ((unsigned long long)(a.nops + i) * gridDim.x + blockIdx.x);
+                        r[0] = te0;
+                        r[1] = globaltimer();
+                    }
                 }
-                if (kTrace && lane == 0 && j == t1 - t0 - 1) {
-                    // debug: the op's last tile in this epilogue (start, stores issued)
-                    unsigned long long *r = a.trace + 8ull * ((unsigned long long)(a.nops + i) * gridDim.x + blockIdx.x);
-                    r[0] = te0;
-                    r[1] = globaltimer();
-                }
+            };
+            // (a W4A16-only program has no W4A8 consumer, hence no records)
+            bool rec_op = false;
+            for (int m = 0; m < op.count; ++m) rec_op = rec_op || op.yq[m] != nullptr;
+            if constexpr (kRoutes == 2) rec_op = false;
+            if constexpr (kRoutes == 2) {
+                ep_tiles(std::false_type{});
+            } else {
+                if (rec_op)
+                    ep_tiles(std::true_type{});
+                else
+                    ep_tiles(std::false_type{});
             }
             // publish: 2 = release (a barrier dependency reads through this counter),
             // 1 = relaxed (dataflow consumers only take it as a hint to re-read their tags;
@@ -818,6 +836,30 @@ __global__ void __launch_bounds__(kStepThreads, 1) stack_step(const __grid_const
                     for (int ln = blockIdx.x; ln < xlines; ln += gridDim.x)
                         asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(op.x + 64 * ln) : "memory");
                 }
+#ifdef MCAPQ_ABL_PROD
+                int li = 0;
+                for (int tile = t0; tile < t1; ++tile) {
+                    while (li + 1 < count && tile >= op.tile_start[li + 1]) ++li;
+                    const CUtensorMap *map = op.maps[li];
+                    const int row0 = (tile - op.tile_start[li]) * kTileRows;
+                    for (int ch = 0; ch < nchunks; ++ch) {
+                        mbar_wait(empty + 8u * s, ph ^ 1u);
+                        if (a.hold)
+                            while (lds32_volatile(hold) != 0u) __nanosleep(32);
+                        const uint32_t st = ring + (uint32_t)s * kStageBytes;
+                        const uint32_t fb = full + 8u * s;
+                        mbar_expect_tx(fb, (uint32_t)kStageBytes);
+                        tma_3d(st, map, 0, row0, ch * 8, fb, pol);
+                        tma_2d(st + 8 * kBox, map + 1, ch * kChunkBlocks, row0, fb, pol);
+                        if (++s == S) {
+                            s = 0;
+                            ph ^= 1u;
+                        }
+                    }
+                }
+                (void)noload;
+                (void)straddle_;
+#else
                 int li = 0, li_start = 0, li_next = count > 1 ? op.tile_start[1] : 0x7fffffff;
                 for (int j = 0; j < t1 - t0; ++j) {
                     const int tile = tile_seq(j, t0, t1, straddle_);
@@ -852,6 +894,7 @@ __global__ void __launch_bounds__(kStepThreads, 1) stack_step(const __grid_const
                         }
                     }
                 }
+#endif
             }
         }
         if (a.clustered) cluster_sync_all();

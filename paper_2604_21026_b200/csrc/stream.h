@@ -7,6 +7,7 @@
 namespace mcapq {
 
 constexpr int kMaxGroup = 4;   // linears sharing one input per launch (q/k/v, gate/up)
+constexpr int kMaxPeers = 8;   // a8 fused column shard: one NVSwitch node
 
 // Host description of a group of linears that share the same input x.
 struct StreamGroup {
@@ -17,6 +18,11 @@ struct StreamGroup {
     int64_t n[kMaxGroup];
     void *y[kMaxGroup];
     int64_t ldy[kMaxGroup];
+    // a8 fused epilogue (M = 1): every output element is also stored at byte offset
+    // peer_delta[p] from its local address, p < npeers (the LSA peers' replicas of y_full,
+    // NVLink stores); npeers = 0: local stores only
+    int64_t peer_delta[kMaxPeers];
+    int npeers;
 };
 
 // Kernel parameters.  The TMA descriptors travel IN the parameter block
@@ -52,6 +58,8 @@ struct StreamArgs {
     // the launch is atomicMax-ed into *amax_key (zeroed by the launcher first)
     unsigned long long *amax_key;
     int64_t amax_off;
+    int64_t peer_delta[kMaxPeers];   // see StreamGroup
+    int npeers;
 };
 
 // Debug timeline (MCAPQ_STREAM_TRACE=1): per CTA {launch, block, t_start, t_wait,
@@ -142,5 +150,10 @@ cudaError_t launch_linear_group(int route, const StreamGroup &g, const uint16_t 
                                 void *ws, cudaStream_t s, bool pdl);
 cudaError_t launch_stream_group(int route, const StreamGroup &g, const uint16_t *x, int64_t m, int64_t ldx,
                                 int ydt, cudaStream_t s, bool pdl);
+// a8 fused epilogue: one routed linear (M = 1, stream path: K % 256 == 0, K >= 2048) whose
+// epilogue stores every output element at y + row and at the npeers byte offsets delta[p]
+// from it (the LSA peers' replicas of y_full; the local one is delta 0)
+cudaError_t launch_linear_peers(int route, const uint8_t *nib, const uint16_t *scale, int64_t n, int64_t k,
+                                const uint16_t *x, void *y, int ydt, const int64_t *delta, int npeers, cudaStream_t s);
 
 }  // namespace mcapq

@@ -545,15 +545,27 @@ __device__ __forceinline__ float argmax_key_value(unsigned long long key)
 }
 
 // ---------------------------------------------------------------- tile epilogues
+// One output element: the local store, or (a8 fused epilogue) one store per LSA peer at
+// its byte offset from the local address -- the local replica is one of them (delta 0).
+__device__ __forceinline__ void store_out_peers(void *y, int ydt, int64_t idx, float v, const int64_t *delta,
+                                                int npeers)
+{
+    if (npeers == 0) {
+        dev::store_out(y, ydt, idx, v);
+        return;
+    }
+    for (int p = 0; p < npeers; ++p) dev::store_out(reinterpret_cast<uint8_t *>(y) + delta[p], ydt, idx, v);
+}
+
 // DP4A: fixed xor butterfly; lane 0 of warp w stores row row0 + w.
 __device__ __forceinline__ void epilogue_dp4a(float acc, int64_t row0, int64_t n, void *y, int ydt, int64_t off, int warp,
-                                              int lane)
+                                              int lane, const int64_t *delta = nullptr, int npeers = 0)
 {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
     if (lane == 0) {
         const int64_t row = row0 + warp;
-        if (row < n) dev::store_out(y, ydt, off + row, acc);
+        if (row < n) store_out_peers(y, ydt, off + row, acc, delta, npeers);
     }
 }
 
@@ -575,7 +587,8 @@ __device__ __forceinline__ void epilogue_dp4a_amax(float acc, int64_t row0, int6
 // best != nullptr: greedy-decode mode (token 0's rows folded into a running argmax key).
 __device__ __forceinline__ void epilogue_mma(const float acc[4], uint32_t red, int64_t row0, int64_t n, void *y,
                                              int ydt, int64_t ldy, int64_t tok0, int ntok, int warp, int lane,
-                                             unsigned long long *best = nullptr, int64_t amax_off = 0)
+                                             unsigned long long *best = nullptr, int64_t amax_off = 0,
+                                             const int64_t *delta = nullptr, int npeers = 0)
 {
     const int gid = lane >> 2, t = lane & 3;
     const uint32_t rw = red + 512u * warp;
@@ -598,7 +611,7 @@ __device__ __forceinline__ void epilogue_mma(const float acc[4], uint32_t red, i
                 *best = key > *best ? key : *best;
             }
         } else if (row < n && tk < ntok) {
-            dev::store_out(y, ydt, (tok0 + tk) * ldy + row, sum);
+            store_out_peers(y, ydt, (tok0 + tk) * ldy + row, sum, delta, npeers);
         }
     }
     bar_consumers();

@@ -135,10 +135,11 @@ __global__ void __launch_bounds__(kThreads, 2) stream_linear(const __grid_consta
             if (a.amax_key)
                 epilogue_dp4a_amax(acc[0], row0, a.n[li], a.amax_off, warp, lane, best);
             else
-                epilogue_dp4a(acc[0], row0, a.n[li], a.y[li], a.ydt, a.tok0 * a.ldy[li], warp, lane);
+                epilogue_dp4a(acc[0], row0, a.n[li], a.y[li], a.ydt, a.tok0 * a.ldy[li], warp, lane, a.peer_delta,
+                              a.npeers);
         } else {
             epilogue_mma(acc, red, row0, a.n[li], a.y[li], a.ydt, a.ldy[li], a.tok0, ntok, warp, lane,
-                         a.amax_key ? &best : nullptr, a.amax_off);
+                         a.amax_key ? &best : nullptr, a.amax_off, a.peer_delta, a.npeers);
         }
     }
     if (a.amax_key) {

@@ -39,4 +39,12 @@ if [ "${NCU:-1}" = "1" ]; then
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:tc05 -s 2 -c 1 \
      -o $OUT/prof_tc05 python scripts/kbench.py --cases lmhead_8b_m64 --routes 2 --reps 2 > $OUT/ncu_tc05.log 2>&1
 fi
+# summarise on the box (ncu -i needs no GPU) and keep only what fits the 64 MiB return:
+# the summaries, the source-level hot spots of the step kernels, and the 1B step report
+python scripts/ncu_summary.py $OUT $OUT/sum > $OUT/sum.log 2>&1
+for r in prof_step prof_step_mlp8b prof_step_mlp8b_a16 prof_w4a16; do
+  [ -f $OUT/$r.ncu-rep ] && python scripts/ncu_source.py $OUT/$r.ncu-rep 40 > $OUT/sum/${r}_source.txt 2>&1
+  [ -f $OUT/$r.ncu-rep ] && python scripts/ncu_stalls.py $OUT/$r.ncu-rep > $OUT/sum/${r}_stalls.txt 2>&1
+done
+for f in $OUT/*.ncu-rep; do [ "$(basename $f)" = "prof_step.ncu-rep" ] || rm -f $f; done
 echo done > $OUT/DONE

@@ -195,3 +195,34 @@ def test_step_records_edge_groups(mq, orc, route_down):
             st.replay(stream=s)
             s.synchronize()
             assert torch.equal(first, y_down)
+
+
+# ---------------------------------------------------------------- a8 fused epilogue (NVLink stores)
+@pytest.mark.parametrize("P", [1, 2, 4, 8])
+@pytest.mark.parametrize("route", [0, 1])
+def test_fused_colshard_peer_stores_emulated(mq, orc, P, route):
+    """The fused column-shard epilogue on one GPU: P emulated replicas of y_full in one
+    buffer; 'rank' r runs its N/P rows with mcapq_debug_linear_peers, storing every row
+    into all P replicas (the per-peer stores the fused path issues over NVLink).  Every
+    replica must equal the unsharded linear bit-for-bit and the oracle's sharded linear."""
+    n, k = 2048, 2048
+    w = si.weight(n, k, 2700 + P)
+    x = si.activation(1, k, 2710 + P).to(DEV)
+    pw = mq.pack_w4(w.to(DEV))
+    per = n // P
+    reps = torch.full((P, n), float("nan"), dtype=torch.bfloat16, device=DEV)
+    es = 2
+    for r in range(P):
+        shard = pw.shard(P, r)
+        y_local = reps[r, r * per:(r + 1) * per]
+        deltas = [(p - r) * n * es for p in range(P)]     # replica p's row block r, from replica r's
+        mq.debug_linear_peers(route, shard, x, y_local, deltas)
+    torch.cuda.synchronize()
+    ref = mq.linear(route, pw, x, out_dtype=torch.bfloat16)
+    for p in range(P):
+        assert torch.equal(reps[p:p + 1], ref), f"replica {p}"
+    nib, sc = orc.pack_w4(_f32(w))
+    y64 = (orc.w4a8_from_x(nib, sc, _f32(x)) if route == 0 else orc.w4a16(nib, sc, _f32(x)))[1]
+    y32c = orc.colshard_linear(route, nib, sc, _f32(x), P)
+    assert np.array_equal(y32c, (orc.w4a8_from_x(nib, sc, _f32(x)) if route == 0 else orc.w4a16(nib, sc, _f32(x)))[0])
+    _assert_close(reps[0:1], y64, 2e-3)

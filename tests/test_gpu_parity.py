@@ -675,6 +675,48 @@ def test_colshard_nccl_world1(mq):
         dist.destroy_process_group()
 
 
+def test_colshard_fused_nccl_world1(mq):
+    """a8 fused epilogue through a real NCCL symmetric window on this box's one GPU:
+    mcapq_comm_window_alloc (ncclMemAlloc + symmetric registration + an ncclDevComm with an
+    LSA barrier), the GEMV epilogue storing into every LSA peer's replica, the LSA barrier
+    kernel: y_full equals the plain linear bit-for-bit, for both routes; replays from a
+    captured graph give the same bits."""
+    import socket
+    import torch.distributed as dist
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", world_size=1, rank=0,
+                            device_id=torch.device(DEV))
+    try:
+        comm = mq.Comm()
+        n, k = 4096, 2048
+        pw = mq.pack_w4(si.weight(n, k, 1721).to(DEV))
+        x = si.activation(1, k, 1722).to(DEV)
+        y = comm.window(n)
+        for route in (0, 1):
+            y.zero_()
+            mq.linear_colshard(comm, route, pw.shard(1, 0), n, x, out=y, fused=True)
+            torch.cuda.synchronize()
+            ref = mq.linear(route, pw, x, out_dtype=torch.bfloat16)
+            assert torch.equal(y, ref)
+            st = torch.cuda.Stream()
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.stream(st):
+                ws = torch.empty(max(256, comm.workspace_bytes(route, 1, n, k)), dtype=torch.uint8, device=DEV)
+                with torch.cuda.graph(g, stream=st):
+                    mq.linear_colshard(comm, route, pw.shard(1, 0), n, x, out=y, ws=ws, stream=st, fused=True)
+            y.zero_()
+            g.replay()
+            torch.cuda.synchronize()
+            assert torch.equal(y, ref)
+        comm.free_window(y)
+        del comm
+    finally:
+        dist.destroy_process_group()
+
+
 def test_step_kernel_k14336_chain(mq, orc):
     """The 8B MLP chain through the persistent step (K = 14336 input: 4 staging rounds per
     thread; both routes), each linear against the oracle on the input it actually read."""
