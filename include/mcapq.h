@@ -489,6 +489,41 @@ mcapq_status mcapq_linear_colshard_argmax(const mcapq_comm *c, int route, const 
                                           const uint16_t *scale_shard, int64_t n_full, int64_t k, const uint16_t *x,
                                           int64_t m, int64_t *idx, float *val, void *ws, size_t ws_bytes,
                                           void *stream);
+/*
+ * NEXT-2 row-parallel (K-sharded) linear -- the Megatron partner of the column shard
+ * ("row-parallel o/down with reduce-scatter or all-reduce instead of
+ * gathering activations").  Rank r owns the K-slice [r K/P, (r+1) K/P) of the packed
+ * weight (all n rows: nib_shard [n][k_shard/2], scale_shard [n][k_shard/32]) and of x
+ * (x_shard [m][k_shard], row stride ldx elements) -- e.g. the output rows a column-sharded
+ * up / q projection produced locally.  k_shard % 32 == 0, so every Q4_0 block and every
+ * per-token int8 quantisation group lies in one rank: the codes and the
+ * per-group int32 dot products are exactly the unsharded linear's; only the fp32
+ * scale-and-accumulate over groups is split into P partial sums y_r[m][n]
+ * (fp32), which the call sums over the ranks into y [m][n] (ydt bf16 or fp32, row stride
+ * n) on every rank.  The sum order differs from the unsharded call: y equals it within
+ * the north-star tolerance, not bit-for-bit.
+ *   fused_epilogue == 0: y_r into ws (fp32; into y itself when ydt is fp32), NCCL sum
+ *     all-reduce in place, conversion to ydt.  ws >= mcapq_rowshard_workspace_bytes().
+ *   fused_epilogue != 0 (m == 1, stream-path k_shard): ws must be a window from
+ *     mcapq_comm_window_alloc of >= P * n * 4 bytes ([P][n] fp32 slots).  LSA barrier
+ *     (no peer still reads its slots), the GEMV epilogue stores y_r into slot r of EVERY
+ *     rank's window over NVLink, LSA barrier, then every rank sums the P slots in rank
+ *     order (mcapq_rowshard_reduce): one NVLink all-reduce, identical y on all ranks.
+ * Errors: MCAPQ_EINVAL (k_shard not whole groups, NULL/misaligned buffers, fused ws not a
+ * window), MCAPQ_EUNSUP (fused with m > 1 or a non-stream k_shard), MCAPQ_ENOSPACE.
+ *
+ * mcapq_rowshard_reduce: y[i][j] = sum_{r = 0 .. world-1} partials[r][i][j] in rank order
+ * (fp32), written as ydt -- the fused path's reduction, the non-fused path's conversion
+ * (world = 1), and a test entry (P shards computed by mcapq_linear on one GPU).
+ * partials: device [world][m][n] fp32; y: device [m][n]; no overlap.
+ */
+size_t mcapq_rowshard_workspace_bytes(int route, int64_t m, int64_t n, int64_t k_shard, int world);
+mcapq_status mcapq_linear_rowshard(const mcapq_comm *c, int route, const uint8_t *nib_shard,
+                                   const uint16_t *scale_shard, int64_t n, int64_t k_shard, const uint16_t *x_shard,
+                                   int64_t m, int64_t ldx, void *y, int ydt, void *ws, size_t ws_bytes,
+                                   int fused_epilogue, void *stream);
+mcapq_status mcapq_rowshard_reduce(const float *partials, int world, int64_t m, int64_t n, void *y, int ydt,
+                                   void *stream);
 void mcapq_comm_destroy(mcapq_comm *c);
 
 #ifdef __cplusplus

@@ -359,6 +359,37 @@ def colshard_linear(route: int, nib, scale, x, world: int):
 
 
 # --------------------------------------------------------------------------
+# NEXT-2: row-parallel (K-sharded) linear, the Megatron partner of the column shard
+# (SURVEY 8(f) NEXT-2).  Rank r owns the K-slice [r K/P, (r+1) K/P) of W and x; K/P is
+# a whole number of 32-groups, so every Q4_0 block and every per-token
+# quantisation group lies in one rank.  Each rank's partial is the
+# routed linear on its slice; the all-reduce is their sum.
+# --------------------------------------------------------------------------
+def rowshard_cols(k: int, world: int, rank: int):
+    if k % world or (k // world) % 32:
+        raise OracleError("rowshard: K/P must be a whole number of 32-groups")
+    per = k // world
+    return rank * per, (rank + 1) * per
+
+
+def rowshard_linear(route: int, nib, scale, x, world: int):
+    """-> (y32 [m, n]: the fp32 partials summed in rank order, y64 [m, n]: the fp64
+    partials summed).  x: [m, k] values (bf16-representable)."""
+    x = _f32(x)
+    if x.ndim == 1:
+        x = x[None, :]
+    k = nib.shape[1] * 2
+    y32 = y64 = None
+    for r in range(world):
+        a, b = rowshard_cols(k, world, r)
+        nb, sb, xs = nib[:, a // 2:b // 2], scale[:, a // 32:b // 32], x[:, a:b]
+        p32, p64 = w4a8_from_x(nb, sb, xs) if route == W4A8 else w4a16(nb, sb, xs)
+        y32 = p32.copy() if y32 is None else (y32 + p32).astype(np.float32)
+        y64 = p64.copy() if y64 is None else y64 + p64
+    return y32, y64
+
+
+# --------------------------------------------------------------------------
 # NEXT-2: greedy decode (P:2661-2662 "decode uses greedy (argmax) sampling")
 def argmax_first(y):
     """Per row of y: the index of the largest value, the FIRST such index on ties

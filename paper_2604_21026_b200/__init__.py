@@ -29,7 +29,7 @@ __all__ = [
     "linear", "linear_group", "linear_host", "w4a8_group_dots", "workspace_bytes", "host_workspace_bytes", "Profile",
     "profile_parse", "profile_write_json", "mcap_accumulate", "Stack", "Comm", "linear_colshard", "PackedW4",
     "colshard_assemble", "stream_w4a8_dump", "linear_argmax", "argmax_keys", "argmax_combine",
-    "argmax_workspace_bytes", "linear_colshard_argmax",
+    "argmax_workspace_bytes", "linear_colshard_argmax", "linear_rowshard", "rowshard_reduce",
     "device_sms", "set_pdl", "debug_read_bw", "debug_linear_peers",
 ]
 
@@ -94,6 +94,16 @@ class PackedW4:
     def shard(self, world: int, rank: int) -> "PackedW4":
         per = self.n // world
         return PackedW4(self.nib[rank * per:(rank + 1) * per], self.scale[rank * per:(rank + 1) * per])
+
+    def kshard(self, world: int, rank: int) -> "PackedW4":
+        """NEXT-2 row-parallel shard: the K-slice [r K/P, (r+1) K/P) of every row (whole
+        Q4_0 blocks: K/P % 32 == 0), copied to its own contiguous [N, K/(2P)] planes."""
+        kp = self.k // world
+        if self.k % world or kp % 32:
+            raise McapqError(1, "binding", f"K={self.k} does not split into {world} whole-group slices")
+        a = rank * kp
+        return PackedW4(self.nib[:, a // 2:(a + kp) // 2].contiguous(),
+                        self.scale[:, a // 32:(a + kp) // 32].contiguous())
 
     @property
     def nbytes(self) -> int:
@@ -523,16 +533,22 @@ class Comm:
     def workspace_bytes(self, route, m, n_full, k):
         return load().mcapq_colshard_workspace_bytes(route, m, n_full, k, self.world)
 
-    def window(self, n_full: int, dtype=torch.bfloat16) -> torch.Tensor:
-        """COLLECTIVE: a [1, n_full] y_full replica in an NCCL symmetric window
-        (mcapq_comm_window_alloc) for linear_colshard(..., fused=True); library-owned,
-        released by free_window() or with the communicator."""
+    def rowshard_workspace_bytes(self, route, m, n, k_shard):
+        return load().mcapq_rowshard_workspace_bytes(route, m, n, k_shard, self.world)
+
+    def window(self, n_full: int, dtype=torch.bfloat16, rows: int = 1) -> torch.Tensor:
+        """COLLECTIVE: a [rows, n_full] buffer in an NCCL symmetric window
+        (mcapq_comm_window_alloc): a y_full replica for linear_colshard(..., fused=True)
+        (rows = 1), or the [P, n] fp32 partial slots of linear_rowshard(..., fused=True)
+        (rows = P, dtype fp32); library-owned, released by free_window() or with the
+        communicator."""
         es = torch.tensor([], dtype=dtype).element_size()
         ptr = ctypes.c_void_p()
-        check(load().mcapq_comm_window_alloc(self._h, n_full * es, ctypes.byref(ptr)), "mcapq_comm_window_alloc")
+        check(load().mcapq_comm_window_alloc(self._h, rows * n_full * es, ctypes.byref(ptr)),
+              "mcapq_comm_window_alloc")
 
         class _Raw:   # a device pointer as a CUDA array (int16/int32 words, viewed as dtype below)
-            __cuda_array_interface__ = {"shape": (1, n_full), "typestr": "<i2" if es == 2 else "<i4",
+            __cuda_array_interface__ = {"shape": (rows, n_full), "typestr": "<i2" if es == 2 else "<i4",
                                         "data": (ptr.value, False), "version": 3}
         t = torch.as_tensor(_Raw(), device="cuda").view(dtype)
         self._windows = getattr(self, "_windows", []) + [(ptr.value, t)]
@@ -587,6 +603,40 @@ def linear_colshard(comm: Comm, route: int, w_shard: PackedW4, n_full: int, x: t
                                        _ptr(x2), m, _ptr(y), _dt(y.dtype), _ptr(ws), ws.numel(), int(bool(fused)),
                                        _stream(stream)),
           "mcapq_linear_colshard")
+    return y
+
+
+def linear_rowshard(comm: Comm, route: int, w_shard: PackedW4, x_shard: torch.Tensor, out_dtype=torch.bfloat16,
+                    out=None, ws=None, stream=None, fused: bool = False):
+    """NEXT-2: row-parallel (K-sharded) routed linear (mcapq_linear_rowshard): this rank's
+    partial over its K-slice, summed over the ranks into y [M, n] on every rank (NCCL
+    all-reduce; fused=True, M = 1: NVLink stores into every rank's window slots + LSA
+    barriers + a rank-order sum -- `ws` must then be Comm.window(n, torch.float32, rows=P))."""
+    x2 = _act(x_shard, w_shard.k)
+    m = x2.shape[0]
+    y = _out(m, w_shard.n, out_dtype, x_shard.device, out)
+    if fused:
+        assert ws is not None, "fused rowshard needs ws = Comm.window(n, torch.float32, rows=P)"
+        wsb = ws.numel() * ws.element_size()
+    else:
+        ws = ws if ws is not None else _scratch(comm.rowshard_workspace_bytes(route, m, w_shard.n, w_shard.k),
+                                                x_shard.device, stream)
+        wsb = ws.numel() * ws.element_size()
+    check(load().mcapq_linear_rowshard(comm._h, route, _ptr(w_shard.nib), _ptr(w_shard.scale), w_shard.n, w_shard.k,
+                                       _ptr(x2), m, x2.stride(0), _ptr(y), _dt(y.dtype), _ptr(ws), wsb,
+                                       int(bool(fused)), _stream(stream)), "mcapq_linear_rowshard")
+    return y
+
+
+def rowshard_reduce(partials: torch.Tensor, out_dtype=torch.bfloat16, out=None, stream=None) -> torch.Tensor:
+    """NEXT-2 reduction / test entry: [P, M, N] fp32 partials -> y [M, N] = rank-order sum
+    (mcapq_rowshard_reduce)."""
+    _need_cuda(partials)
+    assert partials.dtype == torch.float32 and partials.is_contiguous() and partials.dim() == 3
+    P, m, n = partials.shape
+    y = _out(m, n, out_dtype, partials.device, out)
+    check(load().mcapq_rowshard_reduce(_ptr(partials), P, m, n, _ptr(y), _dt(y.dtype), _stream(stream)),
+          "mcapq_rowshard_reduce")
     return y
 
 

@@ -82,6 +82,9 @@ SIGNATURES = {
     "mcapq_comm_window_free": (I32, [P, P]),
     "mcapq_colshard_assemble": (I32, [P, P, I64, I64, I32, I32, P]),
     "mcapq_linear_colshard_argmax": (I32, [P, I32, P, P, I64, I64, P, I64, P, P, P, SZ, P]),
+    "mcapq_rowshard_workspace_bytes": (SZ, [I32, I64, I64, I64, I32]),
+    "mcapq_linear_rowshard": (I32, [P, I32, P, P, I64, I64, P, I64, I64, P, I32, P, SZ, I32, P]),
+    "mcapq_rowshard_reduce": (I32, [P, I32, I64, I64, P, I32, P]),
     "mcapq_comm_destroy": (None, [P]),
 }
 

@@ -78,6 +78,32 @@ __global__ void lsa_barrier_kernel(ncclDevComm dev)
     bar.sync(ncclCoopCta(), cuda::memory_order_acq_rel);
 }
 
+// NEXT-2 row-parallel reduction: y[i][j] = sum over r = 0 .. P-1 (rank order, fp32) of
+// partials[r][i][j]; every rank sums the same slots in the same order, so y is identical
+// on all ranks (the fused all-reduce), and P = 1 is the fp32 -> ydt conversion
+__global__ void rowshard_sum(const float *__restrict__ partials, int world, int64_t total, void *__restrict__ y,
+                             int ydt)
+{
+    for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+         idx += (int64_t)gridDim.x * blockDim.x) {
+        float v = partials[idx];
+        for (int r = 1; r < world; ++r) v += partials[(int64_t)r * total + idx];
+        if (ydt == MCAPQ_F32)
+            reinterpret_cast<float *>(y)[idx] = v;
+        else
+            reinterpret_cast<uint16_t *>(y)[idx] = dev::float_to_bf16_bits(v);
+    }
+}
+
+const McapqWindow *find_window(const mcapq_comm *c, const void *p, size_t bytes)
+{
+    for (const auto &v : c->wins)
+        if (reinterpret_cast<const uint8_t *>(p) >= reinterpret_cast<const uint8_t *>(v.ptr) &&
+            reinterpret_cast<const uint8_t *>(p) + bytes <= reinterpret_cast<const uint8_t *>(v.ptr) + v.bytes)
+            return &v;
+    return nullptr;
+}
+
 }  // namespace
 
 #define NCCL_TRY(expr)                                                                                        \
@@ -227,6 +253,81 @@ mcapq_status mcapq_linear_colshard_argmax(const mcapq_comm *c, int route, const 
     if (st != MCAPQ_OK) return st;
     NCCL_TRY(ncclAllGather(keys + (size_t)c->rank * m, keys, (size_t)m, ncclUint64, c->comm, as_stream(stream)));
     return mcapq_argmax_combine(keys, c->world, m, idx, val, stream);
+}
+
+// ---- NEXT-2: row-parallel (K-sharded) linear, the Megatron partner of the column shard
+size_t mcapq_rowshard_workspace_bytes(int route, int64_t m, int64_t n, int64_t k_shard, int world)
+{
+    if (world < 1 || m < 1 || n < 1 || k_shard < 32 || k_shard % 32) return 0;
+    size_t b = 256 + align256((size_t)(m * n) * 4);   // this rank's fp32 partial (all-reduced in place)
+    if (route == MCAPQ_W4A8) b += a8_workspace_bytes(m, k_shard);
+    return b;
+}
+
+mcapq_status mcapq_rowshard_reduce(const float *partials, int world, int64_t m, int64_t n, void *y, int ydt,
+                                   void *stream)
+{
+    clear_error();
+    MCAPQ_REQUIRE(partials && y && world >= 1 && m >= 1 && n >= 1, MCAPQ_EINVAL, "bad rowshard_reduce arguments");
+    MCAPQ_REQUIRE(ydt == MCAPQ_BF16 || ydt == MCAPQ_F32, MCAPQ_EDTYPE, "bad ydt");
+    const int64_t total = m * n;
+    const int grid = (int)((total + 255) / 256 < 4096 ? (total + 255) / 256 : 4096);
+    rowshard_sum<<<grid, 256, 0, as_stream(stream)>>>(partials, world, total, y, ydt);
+    MCAPQ_CUDA_TRY(cudaGetLastError());
+    return MCAPQ_OK;
+}
+
+mcapq_status mcapq_linear_rowshard(const mcapq_comm *c, int route, const uint8_t *nib_shard,
+                                   const uint16_t *scale_shard, int64_t n, int64_t k_shard, const uint16_t *x_shard,
+                                   int64_t m, int64_t ldx, void *y, int ydt, void *ws, size_t ws_bytes,
+                                   int fused_epilogue, void *stream)
+{
+    clear_error();
+    MCAPQ_REQUIRE(c && c->comm, MCAPQ_EINVAL, "communicator is NULL");
+    MCAPQ_REQUIRE(ydt == MCAPQ_BF16 || ydt == MCAPQ_F32, MCAPQ_EDTYPE, "bad ydt");
+    MCAPQ_REQUIRE(route == MCAPQ_W4A8 || route == MCAPQ_W4A16, MCAPQ_EINVAL, "bad route");
+    MCAPQ_REQUIRE(k_shard >= 32 && k_shard % 32 == 0, MCAPQ_EINVAL,
+                  "K/P=%lld must be whole 32-groups (the W4A8 quantiser stays rank-local)", (long long)k_shard);
+    MCAPQ_REQUIRE(m >= 1 && n >= 1 && ldx >= k_shard && x_shard && y && aligned16(y), MCAPQ_EINVAL,
+                  "bad rowshard arguments");
+    MCAPQ_REQUIRE(ws && aligned16(ws), MCAPQ_EINVAL, "NULL/misaligned ws");
+    cudaStream_t s = as_stream(stream);
+    if (fused_epilogue) {
+        // fused all-reduce over NVLink: ws is a window from mcapq_comm_window_alloc holding
+        // [P][m][n] fp32 slots.  The GEMV epilogue stores this rank's partial into slot
+        // `rank` of every LSA peer's window; after the LSA barrier every rank sums the P
+        // slots in rank order (rowshard_sum) -- identical y everywhere, no NCCL collective.
+        // A barrier first: no peer is still reading its slots from the previous call.
+        MCAPQ_REQUIRE(m == 1 && stream_supported(k_shard) && aligned16(scale_shard), MCAPQ_EUNSUP,
+                      "fused rowshard: M = 1 and a stream-path K/P (K %% 256 == 0, >= 2048)");
+        const size_t slot = (size_t)n * 4;
+        const McapqWindow *w = find_window(c, ws, slot * (size_t)c->world);
+        MCAPQ_REQUIRE(w, MCAPQ_EINVAL, "fused_epilogue: ws is not a window from mcapq_comm_window_alloc");
+        MCAPQ_REQUIRE(ws_bytes >= slot * (size_t)c->world, MCAPQ_ENOSPACE, "window too small for P x N fp32");
+        lsa_barrier_kernel<<<1, 32, 0, s>>>(c->dev);
+        MCAPQ_CUDA_TRY(cudaGetLastError());
+        uint8_t *mine = reinterpret_cast<uint8_t *>(ws) + (size_t)c->rank * slot;
+        cudaError_t e = launch_linear_peers(route, nib_shard, scale_shard, n, k_shard, x_shard, mine, MCAPQ_F32,
+                                            w->delta, w->npeers, s);
+        MCAPQ_REQUIRE(e == cudaSuccess, MCAPQ_ECUDA, "fused rowshard launch: %s", cudaGetErrorString(e));
+        lsa_barrier_kernel<<<1, 32, 0, s>>>(c->dev);
+        MCAPQ_CUDA_TRY(cudaGetLastError());
+        return mcapq_rowshard_reduce(reinterpret_cast<const float *>(ws), c->world, 1, n, y, ydt, stream);
+    }
+    MCAPQ_REQUIRE(ws_bytes >= mcapq_rowshard_workspace_bytes(route, m, n, k_shard, c->world), MCAPQ_ENOSPACE,
+                  "workspace too small");
+    // this rank's fp32 partial over its K-slice (its groups: codes and int32 dots exactly
+    // those of the unsharded linear), then an in-place NCCL sum all-reduce
+    float *part = ydt == MCAPQ_F32 ? reinterpret_cast<float *>(y)
+                                   : reinterpret_cast<float *>(reinterpret_cast<uint8_t *>(ws) + 256);
+    uint8_t *rest = reinterpret_cast<uint8_t *>(ws) + 256 + align256((size_t)(m * n) * 4);
+    const size_t rest_bytes = ws_bytes - (size_t)(rest - reinterpret_cast<uint8_t *>(ws));
+    mcapq_status st = mcapq_linear(route, nib_shard, scale_shard, n, k_shard, x_shard, m, ldx, part, MCAPQ_F32, n,
+                                   rest, rest_bytes, stream);
+    if (st != MCAPQ_OK) return st;
+    NCCL_TRY(ncclAllReduce(part, part, (size_t)(m * n), ncclFloat32, ncclSum, c->comm, s));
+    if (ydt == MCAPQ_F32) return MCAPQ_OK;
+    return mcapq_rowshard_reduce(part, 1, m, n, y, ydt, stream);
 }
 
 mcapq_status mcapq_comm_window_alloc(mcapq_comm *c, size_t bytes, void **y_full)

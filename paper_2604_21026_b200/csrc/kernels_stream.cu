@@ -50,6 +50,9 @@ constexpr int kBox = 128 * kTileRows;              // one {128 B x 16 rows} TMA 
 constexpr int kStageBytes = 8 * kBox + kBox;       // 8 nibble boxes + 1 scale box (18 KiB)
 constexpr int kRedBytes = kConsumerWarps * kTileRows * 8 * 4;
 constexpr int kMaxStages = 16;
+constexpr int kHmma1Blocks = 1;                   // min CTAs per SM of stream_linear<HMMA1> (launch bounds)
+constexpr int kRedSlots = 4;                      // HMMA1 lean path: tile slots of 1 KiB in the reduction area
+static_assert(kRedSlots * 1024 <= kRedBytes, "HMMA1 tile slots fit the reduction area");
 constexpr int kBarBytes = 512;                     // mbarriers: full[S] + empty[S] + done + go <= 16*16 + 16
 
 // HMMA1: W4A16 with a single token (only MMA column 0 is computed);  NONE: bandwidth probe
@@ -1014,7 +1017,9 @@ cudaError_t launch_argmax_fused(int route, const uint8_t *nib, const uint16_t *s
     a.ydt = MCAPQ_F32;
     a.amax_key = key;
     a.amax_off = row_off;
-    const int per_sm = tune().ctas_per_sm ? tune().ctas_per_sm : (a.tile_start[1] >= 16 * device_sms() ? 2 : 1);
+    const bool one_cta = route == MCAPQ_W4A16 && kHmma1Blocks == 1;
+    const int per_sm = tune().ctas_per_sm ? tune().ctas_per_sm
+                                          : (one_cta ? 1 : (a.tile_start[1] >= 16 * device_sms() ? 2 : 1));
     a.smem_kb = (!tune().smem_kb_env && per_sm == 1 && k >= 8192) ? 130 : 0;
     const bool pdl = tune().pdl || api_pdl();
     return route == MCAPQ_W4A16 ? launch_one<HMMA1>(a, s, pdl, device_sms() * per_sm)
@@ -1110,7 +1115,11 @@ cudaError_t launch_stream_group(int route, const StreamGroup &g, const uint16_t 
     // ramp of back-to-back linears); a long linear (>= 16 tiles per SM) instead runs two
     // CTAs per SM -- twice the consumer warps per SM, and its ramp is amortised anyway
     // (8B lm_head: 6.08 -> 6.47 TB/s).  MCAPQ_STREAM_CTAS_PER_SM forces 1 or 2.
-    const int per_sm = tune().ctas_per_sm ? tune().ctas_per_sm : (tiles >= 16 * device_sms() ? 2 : 1);
+    // (the W4A16 M = 1 engine runs one CTA per SM: its lean loop keeps its lane offsets in
+    // registers -- 86 of them -- instead of re-deriving them under the 56-register cap of
+    // two CTAs per SM: 8B lm_head 80.9 -> 66.3 us, gate 13.4 -> 10.5 us)
+    const bool one_cta = route == MCAPQ_W4A16 && m == 1 && kHmma1Blocks == 1;
+    const int per_sm = tune().ctas_per_sm ? tune().ctas_per_sm : (one_cta ? 1 : (tiles >= 16 * device_sms() ? 2 : 1));
     const int sms = device_sms() * per_sm;
     // shared-memory plan: ~112 KB (two CTAs per SM: the next linear's CTA co-resides under
     // PDL); a wide input (K >= 8192: a 9-15 KB activation area) at one CTA per SM takes

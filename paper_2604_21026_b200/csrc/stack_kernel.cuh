@@ -1077,6 +1077,11 @@ __global__ void __launch_bounds__(kStepThreads, 1) stack_step(const __grid_const
                 }
             } else {
                 // ---- W4A16, HMMA1 engine (warp w owns blocks 4w..4w+3 for all 16 rows)
+                // every chunk full (K % 2048 == 0): chunk_hmma1 with the lane offsets computed
+                // once per linear (bit-identical to chunk_mma<HMMA1>) -- W4A16-only programs
+                // (in the mixed kernel the extra live registers spill in the W4A8 staging)
+                const bool full_chunks = kRoutes == 2 && (K2 & (kChunkBytes - 1)) == 0;
+                const Hmma1Lane H = hmma1_lane(L, warp, lane);
 
                 for (int tile = t0; tile < t1; ++tile, ++ts) {
                     float acc[4] = {0.f, 0.f, 0.f, 0.f};
@@ -1092,7 +1097,9 @@ __global__ void __launch_bounds__(kStepThreads, 1) stack_step(const __grid_const
                         if (tile == t1 - 1 && ch == nchunks - 1) hold_set(1u);   // the linear's last stage is resident
                         if (kTrace && tile == t0 && ch == 0) tr3 = globaltimer();
                         const uint32_t st = ring + (uint32_t)s * kStageBytes;
-                        if (!(a.flags & 1))
+                        if (full_chunks && !(a.flags & 1))
+                            chunk_hmma1(st, 4096u * (uint32_t)ch, 2048u * (uint32_t)ch, H, kNib2, kMagic, acc[0], acc[2]);
+                        else if (!(a.flags & 1))
                             chunk_mma<HMMA1>(st, nblk, blk0, (uint32_t)K2, L, G, 1, warp, lane, kNib2, kMagic, acc);
                         __syncwarp();
                         if (lane == 0) mbar_arrive(empty + 8u * s);

@@ -526,6 +526,60 @@ __device__ __forceinline__ void chunk_mma(uint32_t st, int nblk, int blk0, uint3
     }
 }
 
+// HMMA1 on a full chunk with the lane's loop-invariant shared-memory offsets computed once
+// per kernel (the generic chunk_mma re-derives them every stage under the 60-register cap
+// of two CTAs per SM).  Same loads, MMAs and fmaf order as chunk_mma<HMMA1>: bit-identical.
+struct Hmma1Lane {
+    uint32_t oa, ob;   // ldmatrix offsets in a stage: blocks bq + mhalf, bq + 2 + mhalf
+    uint32_t sa, sb;   // scale offsets in a stage: rows gid / gid + 8, blocks bq .. bq + 3
+    uint32_t xo;       // x of block bq, this lane's 16 B (token 0, lanes gid == 0)
+    uint32_t co;       // corr of block bq
+    bool xon;
+};
+__device__ __forceinline__ Hmma1Lane hmma1_lane(const ActSmem &L, int warp, int lane)
+{
+    const int gid = lane >> 2, t = lane & 3;
+    const int mrow = (lane & 7) + ((lane >> 3) & 1) * 8, mhalf = lane >> 4;
+    const int bq = 4 * warp;
+    Hmma1Lane H;
+    H.oa = nib_off(mrow, bq + mhalf);
+    H.ob = nib_off(mrow, bq + 2 + mhalf);
+    H.sa = scale_off(gid, bq);
+    H.sb = scale_off(gid + 8, bq);
+    H.xo = L.act + 64u * (uint32_t)bq + 16u * (uint32_t)t;
+    H.co = L.corr + 32u * (uint32_t)bq;
+    H.xon = gid == 0;
+    return H;
+}
+// xo / co: the chunk's offsets (64 B of x and 32 B of corr per block of the chunk)
+__device__ __forceinline__ void chunk_hmma1(uint32_t st, uint32_t xo, uint32_t co, const Hmma1Lane &H, uint32_t kNib2,
+                                            uint32_t kMagic, float &acc0, float &acc2)
+{
+    uint32_t wv[8];
+    ldmatrix_x4(st + H.oa, wv[0], wv[1], wv[2], wv[3]);
+    ldmatrix_x4(st + H.ob, wv[4], wv[5], wv[6], wv[7]);
+    const uint2 sa = lds64(st + H.sa);
+    const uint2 sbb = lds64(st + H.sb);
+    const float dA[4] = {h2f((uint16_t)(sa.x & 0xffff)), h2f((uint16_t)(sa.x >> 16)), h2f((uint16_t)(sa.y & 0xffff)),
+                         h2f((uint16_t)(sa.y >> 16))};
+    const float dB[4] = {h2f((uint16_t)(sbb.x & 0xffff)), h2f((uint16_t)(sbb.x >> 16)),
+                         h2f((uint16_t)(sbb.y & 0xffff)), h2f((uint16_t)(sbb.y >> 16))};
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        uint4 bx = make_uint4(0, 0, 0, 0);
+        if (H.xon) bx = lds128(H.xo + xo + 64u * j);
+        uint32_t pa[4], pb[4];
+        magic_bf16(wv[2 * j], kNib2, kMagic, pa);
+        magic_bf16(wv[2 * j + 1], kNib2, kMagic, pb);
+        float c[4];
+        hmma_c(pa[0], pb[0], pa[2], pb[2], bx.x, bx.y, 0.f, 0.f, 0.f, 0.f, c);
+        hmma(pa[1], pb[1], pa[3], pb[3], bx.z, bx.w, c);
+        const float crx = __uint_as_float(lds32(H.co + co + 32u * j));
+        acc0 = fmaf(dA[j], c[0] + crx, acc0);
+        acc2 = fmaf(dB[j], c[2] + crx, acc2);
+    }
+}
+
 // ---------------------------------------------------------------- argmax keys (NEXT-2)
 // A 64-bit key whose unsigned order is "larger fp32 value first, then smaller index":
 // high word = the IEEE bits mapped to an unsigned total order (-0 folded onto +0, so

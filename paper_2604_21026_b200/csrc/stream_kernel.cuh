@@ -5,10 +5,13 @@
 //   ring [S x 18 KiB] | full[S] empty[S] | activations | reduction
 #pragma once
 
-// 2 CTAs per SM (<= 60 registers, <= ~113 KB smem): under PDL the next linear's CTA
-// becomes resident beside this one and starts its weight stream early.
+// 2 CTAs per SM (<= 56 registers, <= ~113 KB smem): under PDL the next linear's CTA
+// becomes resident beside this one and starts its weight stream early.  The W4A16 M = 1
+// engine (HMMA1) instead runs one CTA per SM with up to 112 registers (kHmma1Blocks, see
+// the launchers): its dequantise-MMA loop is instruction-bound, and at 56 registers it
+// re-derived its lane offsets every stage.
 template <int E>
-__global__ void __launch_bounds__(kThreads, 2) stream_linear(const __grid_constant__ StreamArgs a)
+__global__ void __launch_bounds__(kThreads, E == HMMA1 ? kHmma1Blocks : 2) stream_linear(const __grid_constant__ StreamArgs a)
 {
     extern __shared__ __align__(16) uint8_t smem_raw[];
     const uint32_t sb = (smem_addr(smem_raw) + 1023u) & ~1023u;
@@ -30,11 +33,20 @@ __global__ void __launch_bounds__(kThreads, 2) stream_linear(const __grid_consta
     const int t1 = (int)(((int64_t)T * (blockIdx.x + 1)) / gridDim.x);
 
     const uint32_t amax_slot = full + 480u;                      // greedy-decode mode: the CTA's best key
+    // HMMA1 lean path: kRedSlots tile slots of 16 warps x 16 rows fp32 partials in `red`,
+    // an arrival counter per slot (the 16th warp to arrive reduces the tile) and a
+    // "slot consumed" mbarrier per slot (count 1: the reducing warp)
+    const uint32_t rcnt = full + 256u, repe = full + 288u;
     if (threadIdx.x == 0) {
         for (int s = 0; s < S; ++s) {
             mbar_init(full + 8u * s, 1);
             mbar_init(empty + 8u * s, kConsumerWarps);
         }
+        if constexpr (E == HMMA1)
+            for (int j = 0; j < kRedSlots; ++j) {
+                sts32(rcnt + 4u * j, 0u);
+                mbar_init(repe + 8u * j, 1);
+            }
         asm volatile("st.shared.u64 [%0], %1;" ::"r"(amax_slot), "l"(0ull) : "memory");
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -104,6 +116,72 @@ __global__ void __launch_bounds__(kThreads, 2) stream_linear(const __grid_consta
     uint32_t ph = 0;
     int li = 0;
     unsigned long long best = 0ull;   // greedy-decode mode: this thread's running argmax key
+    if constexpr (E == HMMA1) {
+        if ((K2 & (kChunkBytes - 1)) == 0 && !a.trace) {
+            // ---- lean W4A16 M = 1 loop (every chunk full: K % 2048 == 0).  No per-stage
+            // predicates; the tile's cross-warp reduction is handed to whichever warp
+            // arrives last at the tile's slot (no CTA-wide barrier per tile: the other
+            // warps go straight on to the next tile's stages).  Same chunk_mma arithmetic
+            // and the same fixed reduction order (warp 0 + warp 1 + .. + warp 15) as
+            // epilogue_mma, so the outputs are bit-identical to the generic path.
+            uint32_t st = ring + (uint32_t)s * kStageBytes;
+            uint32_t ts = 0;
+            const Hmma1Lane H = hmma1_lane(L, warp, lane);
+            for (int tile = t0; tile < t1; ++tile, ++ts) {
+                while (li + 1 < a.count && tile >= a.tile_start[li + 1]) ++li;
+                float acc[4] = {0.f, 0.f, 0.f, 0.f};
+                for (int ch = 0; ch < nchunks; ++ch) {
+                    mbar_wait(full + 8u * s, ph);
+                    chunk_hmma1(st, 4096u * (uint32_t)ch, 2048u * (uint32_t)ch, H, kNib2, kMagic, acc[0], acc[2]);
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(empty + 8u * s);
+                    if (++s == S) {
+                        s = 0;
+                        ph ^= 1u;
+                        st = ring;
+                    } else {
+                        st += (uint32_t)kStageBytes;
+                    }
+                }
+                const uint32_t slot = ts & (uint32_t)(kRedSlots - 1);
+                if (ts >= (uint32_t)kRedSlots) mbar_wait(repe + 8u * slot, ((ts / kRedSlots) - 1u) & 1u);
+                const uint32_t sl = red + 1024u * slot;
+                // lanes t == 0 hold rows gid (acc[0]) and gid + 8 (acc[2]) of the token
+                if ((lane & 3) == 0) {
+                    sts32(sl + 64u * warp + 4u * (lane >> 2), __float_as_uint(acc[0]));
+                    sts32(sl + 64u * warp + 4u * ((lane >> 2) + 8), __float_as_uint(acc[2]));
+                }
+                __syncwarp();
+                uint32_t old = 0;
+                if (lane == 0)
+                    asm volatile("atom.acq_rel.cta.shared::cta.add.u32 %0, [%1], 1;"
+                                 : "=r"(old)
+                                 : "r"(rcnt + 4u * slot)
+                                 : "memory");
+                old = __shfl_sync(0xffffffffu, old, 0);
+                if ((old & (uint32_t)(kConsumerWarps - 1)) == (uint32_t)(kConsumerWarps - 1)) {
+                    __syncwarp();   // lane 0's acquire orders the whole warp's reads
+                    if (lane < kTileRows) {
+                        float v = __uint_as_float(lds32(sl + 4u * lane));
+#pragma unroll
+                        for (int w = 1; w < kConsumerWarps; ++w) v += __uint_as_float(lds32(sl + 64u * w + 4u * lane));
+                        const int64_t row = (int64_t)(tile - a.tile_start[li]) * kTileRows + lane;
+                        if (row < a.n[li]) {
+                            if (a.amax_key) {
+                                const unsigned long long key = argmax_key(v, a.amax_off + row);
+                                best = key > best ? key : best;
+                            } else {
+                                store_out_peers(a.y[li], a.ydt, a.tok0 * a.ldy[li] + row, v, a.peer_delta, a.npeers);
+                            }
+                        }
+                    }
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(repe + 8u * slot);   // the slot is consumed
+                }
+            }
+            goto consumers_done;
+        }
+    }
     for (int tile = t0; tile < t1; ++tile) {
         while (li + 1 < a.count && tile >= a.tile_start[li + 1]) ++li;
         float acc[4] = {0.f, 0.f, 0.f, 0.f};
@@ -142,6 +220,7 @@ __global__ void __launch_bounds__(kThreads, 2) stream_linear(const __grid_consta
                          a.amax_key ? &best : nullptr, a.amax_off, a.peer_delta, a.npeers);
         }
     }
+consumers_done:
     if (a.amax_key) {
         // greedy decode: CTA maximum in shared memory, then one global atomic per CTA
         if (best) asm volatile("atom.shared.max.u64 %0, [%1], %2;" : "=l"(best) : "r"(amax_slot), "l"(best) : "memory");

@@ -226,3 +226,80 @@ def test_fused_colshard_peer_stores_emulated(mq, orc, P, route):
     y32c = orc.colshard_linear(route, nib, sc, _f32(x), P)
     assert np.array_equal(y32c, (orc.w4a8_from_x(nib, sc, _f32(x)) if route == 0 else orc.w4a16(nib, sc, _f32(x)))[0])
     _assert_close(reps[0:1], y64, 2e-3)
+
+
+# ---------------------------------------------------------------- NEXT-2: P-way row shards on one GPU
+@pytest.mark.parametrize("P", [2, 4, 8])
+@pytest.mark.parametrize("m", [1, 4, 64])
+@pytest.mark.parametrize("route", [0, 1])
+def test_rowshard_emulated_vs_oracle(mq, orc, P, m, route):
+    """Row-parallel (K-sharded) linear emulated P ways: rank r's routed linear on its
+    K-slice (PackedW4.kshard, x[:, r K/P ..]) into slot r of [P, M, N] fp32 partials (what
+    each rank computes before the all-reduce / the fused path's slot stores), then
+    mcapq_rowshard_reduce (the rank-order sum every rank runs): equal to the oracle's
+    sharded linear within the north-star tolerance, each partial equal to the unsharded
+    oracle's partial over the same groups, and the reduce an exact fp32 rank-order sum."""
+    n, k = 2048, 16384 if P == 8 else 8192
+    w = si.weight(n, k, 2800 + P)
+    x = si.activation(m, k, 2801 + m)
+    pw, nib, sc = _pack_both(mq, orc, w)
+    xd = x.to(DEV)
+    kp = k // P
+    parts = torch.empty(P, m, n, dtype=torch.float32, device=DEV)
+    for r in range(P):
+        mq.linear(route, pw.kshard(P, r), xd[:, r * kp:(r + 1) * kp].contiguous(), out=parts[r])
+    y = mq.rowshard_reduce(parts, out_dtype=torch.float32)
+    yb = mq.rowshard_reduce(parts, out_dtype=torch.bfloat16)
+    torch.cuda.synchronize()
+    _, y64 = orc.rowshard_linear(route, nib, sc, _f32(x), P)
+    _assert_close(y, y64, 1e-3)
+    _assert_close(yb, y64, 2e-3)
+    ref = parts[0].clone()
+    for r in range(1, P):
+        ref += parts[r]
+    assert torch.equal(y, ref)
+    for r in (0, P - 1):
+        a = r * kp
+        p64 = _oracle_y64(orc, route, nib[:, a // 2:(a + kp) // 2], sc[:, a // 32:(a + kp) // 32], x[:, a:a + kp])
+        _assert_close(parts[r], p64, 1e-3)
+
+
+@pytest.mark.parametrize("P", [2, 4, 8])
+@pytest.mark.parametrize("route", [0, 1])
+def test_fused_rowshard_peer_stores_emulated(mq, orc, P, route):
+    """The fused row-shard all-reduce on one GPU: P emulated windows of [P][N] fp32 slots
+    in one buffer; 'rank' r's GEMV (mcapq_debug_linear_peers) stores its K-slice partial
+    into slot r of EVERY window (the per-peer NVLink stores), then each window's rank-order
+    sum (mcapq_rowshard_reduce): every rank's y identical, equal to the oracle's sharded
+    linear."""
+    n, k = 2048, 2048 * P
+    w = si.weight(n, k, 2900 + P)
+    x = si.activation(1, k, 2910 + P)
+    pw, nib, sc = _pack_both(mq, orc, w)
+    xd = x.to(DEV)
+    kp = k // P
+    wins = torch.full((P, P, n), float("nan"), dtype=torch.float32, device=DEV)   # [window p][slot r][n]
+    for r in range(P):
+        y_local = wins[r, r]
+        deltas = [(p - r) * P * n * 4 for p in range(P)]     # window p's slot r, from window r's slot r
+        mq.debug_linear_peers(route, pw.kshard(P, r), xd[:, r * kp:(r + 1) * kp].contiguous(), y_local.view(1, n),
+                              deltas)
+    ys = [mq.rowshard_reduce(wins[p].view(P, 1, n), out_dtype=torch.bfloat16) for p in range(P)]
+    torch.cuda.synchronize()
+    for p in range(1, P):
+        assert torch.equal(ys[p], ys[0]), f"rank {p}"
+    _, y64 = orc.rowshard_linear(route, nib, sc, _f32(x), P)
+    _assert_close(ys[0], y64, 2e-3)
+
+
+def test_rowshard_reduce_ragged(mq):
+    P, m, n = 3, 5, 37
+    src = torch.randn(P, m, n, device=DEV)
+    y = mq.rowshard_reduce(src, out_dtype=torch.float32)
+    assert torch.equal(y, src[0] + src[1] + src[2])
+
+
+def test_rowshard_rejects_partial_groups(mq):
+    pw = mq.pack_w4(si.weight(64, 96, 2950).to(DEV))
+    with pytest.raises(mq.McapqError):
+        pw.kshard(2, 0)

@@ -717,6 +717,54 @@ def test_colshard_fused_nccl_world1(mq):
         dist.destroy_process_group()
 
 
+def test_rowshard_nccl_world1(mq, orc):
+    """NEXT-2 through NCCL on this box's one GPU: mcapq_linear_rowshard (local K-slice
+    partial, ncclAllReduce in place, conversion) for M = 1 / 16 and both routes, and the
+    fused path through a real symmetric window (LSA barrier, epilogue stores into the
+    window slots, LSA barrier, rank-order sum), eager and graph-replayed: at P = 1 both
+    equal the plain linear (the sum of one partial is the partial)."""
+    import socket
+    import torch.distributed as dist
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", world_size=1, rank=0,
+                            device_id=torch.device(DEV))
+    try:
+        comm = mq.Comm()
+        n, k = 2048, 4096
+        pw = mq.pack_w4(si.weight(n, k, 1731).to(DEV))
+        for m in (1, 16):
+            x = si.activation(m, k, 1732 + m).to(DEV)
+            for route in (0, 1):
+                for dt in (torch.float32, torch.bfloat16):
+                    y = mq.linear_rowshard(comm, route, pw.kshard(1, 0), x, out_dtype=dt)
+                    torch.cuda.synchronize()
+                    assert torch.equal(y, mq.linear(route, pw, x, out_dtype=dt))
+        win = comm.window(n, torch.float32, rows=1)
+        x = si.activation(1, k, 1740).to(DEV)
+        for route in (0, 1):
+            ref = mq.linear(route, pw, x, out_dtype=torch.bfloat16)
+            y = mq.linear_rowshard(comm, route, pw.kshard(1, 0), x, ws=win, fused=True)
+            torch.cuda.synchronize()
+            assert torch.equal(y, ref)
+            st = torch.cuda.Stream()
+            g = torch.cuda.CUDAGraph()
+            y2 = torch.empty_like(ref)
+            with torch.cuda.stream(st):
+                with torch.cuda.graph(g, stream=st):
+                    mq.linear_rowshard(comm, route, pw.kshard(1, 0), x, out=y2, ws=win, stream=st, fused=True)
+            y2.zero_()
+            g.replay()
+            torch.cuda.synchronize()
+            assert torch.equal(y2, ref)
+        comm.free_window(win)
+        del comm
+    finally:
+        dist.destroy_process_group()
+
+
 def test_step_kernel_k14336_chain(mq, orc):
     """The 8B MLP chain through the persistent step (K = 14336 input: 4 staging rounds per
     thread; both routes), each linear against the oracle on the input it actually read."""

@@ -1,8 +1,10 @@
-"""World-size-2 `gloo` tests (CPU) of the multi-GPU host logic (row a8):
+"""World-size-2 `gloo` tests (CPU) of the multi-GPU host logic (rows a8 and NEXT-2):
 the NCCL unique-id bootstrap over a torch process group, the rank-major row
 partition (reading A22) and the all-gather reassembly.  Each rank computes its
 shard with the oracle; the gathered result must equal the unsharded one
-bit-for-bit, for M = 1 (in-place gather order) and M > 1 (rank-major + permute)."""
+bit-for-bit, for M = 1 (in-place gather order) and M > 1 (rank-major + permute).  The
+row-parallel (K-sharded) partition: each rank's K-slice partial, summed by an
+all-reduce, equals the oracle's sharded sum and the unsharded linear."""
 import os
 import socket
 
@@ -60,6 +62,28 @@ def _worker(rank, world, port, q):
                 y = gathered.permute(1, 0, 2).reshape(m, n).numpy()
                 full = oracle.colshard_linear(route, nib, sc, x, 1)
                 assert np.array_equal(y, full)
+        # 3. NEXT-2 row-parallel: this rank's K-slice (PackedW4.kshard) partial, then the sum
+        # all-reduce; equal to the oracle's rank-order sharded sum and, within fp32
+        # rounding, to the unsharded linear
+        k2 = 512
+        w2 = si.weight(n, k2, 9).float().numpy()
+        nib2, sc2 = oracle.pack_w4(w2)
+        pw2 = mq.PackedW4(torch.from_numpy(nib2), torch.from_numpy(sc2.view(np.int16)))
+        ks = pw2.kshard(world, rank)
+        a, b = oracle.rowshard_cols(k2, world, rank)
+        assert ks.k == b - a and torch.equal(ks.nib, pw2.nib[:, a // 2:b // 2])
+        for m in (1, 3):
+            x = si.activation(m, k2, 10 + m).float().numpy()
+            for route in (oracle.W4A8, oracle.W4A16):
+                fn = oracle.w4a8_from_x if route == oracle.W4A8 else oracle.w4a16
+                p32, p64 = fn(ks.nib.numpy(), ks.scale.numpy().view(np.uint16), x[:, a:b])
+                t = torch.from_numpy(np.ascontiguousarray(p64))
+                dist.all_reduce(t)
+                _, u64 = fn(nib2, sc2, x)
+                _, r64 = oracle.rowshard_linear(route, nib2, sc2, x, world)
+                scale = np.maximum(np.abs(u64), np.sqrt(np.mean(u64 ** 2)))
+                assert np.max(np.abs(t.numpy() - r64) / scale) < 1e-12
+                assert np.max(np.abs(t.numpy() - u64) / scale) < 1e-12
         q.put((rank, "ok"))
     except Exception as e:  # noqa: BLE001
         q.put((rank, repr(e)))
