@@ -332,7 +332,7 @@ def _copies(pw, l2):
 SHARDED = (("lm_head", 1, 20), ("lm_head", 64, 4), ("gate", 1, 64), ("down", 1, 64))
 
 
-def time_sharded(mq, dev, stream, dist, world, rank):
+def time_sharded(mq, dev, stream, dist, world, rank, force_comm=False, slots=None):
     """Rows a8 / NEXT-2 at P = world: the Llama-3.1-8B lm_head
     (M = 1, 64) and MLP gate / down column-sharded over the job's ranks.  Per layer and
     route: T(1) = the unsharded linear on one GPU (no collective), T(P) = the sharded
@@ -343,10 +343,10 @@ def time_sharded(mq, dev, stream, dist, world, rank):
     P x M key gather, mcapq_linear_colshard_argmax).
     Every time is a CUDA graph of repeated calls over rotating weight copies (>= 4 x L2
     together), CUDA events, max over ranks."""
-    comm = mq.Comm() if world > 1 else None
+    comm = mq.Comm() if world > 1 or force_comm else None   # force_comm: the P = 1 path check
     l2 = torch.cuda.get_device_properties(dev).L2_cache_size
     rows = []
-    for slot, m, reps in SHARDED:
+    for slot, m, reps in (slots or SHARDED):
         n, k = si.linear_shape("llama-3.1-8b", slot)
         per = n // world
         w = si.weight(n, k, si.seed_for(5 if slot == "lm_head" else 4, 0, slot))
@@ -355,7 +355,7 @@ def time_sharded(mq, dev, stream, dist, world, rank):
         pw = pw_full.shard(world, rank) if world > 1 else pw_full
         x = si.activation(m, k, si.seed_for(5 if slot == "lm_head" else 4, 0, slot, True)).to(dev)
         wbytes = n * k // 2 + n * (k // 32) * 2
-        full_c, shard_c = _copies(pw_full, l2), (_copies(pw, l2) if world > 1 else None)
+        full_c, shard_c = _copies(pw_full, l2), (_copies(pw, l2) if comm is not None else None)
         for route, name in ((0, "w4a8"), (1, "w4a16")):
             y = torch.empty(m, n, dtype=torch.bfloat16, device=dev)
             yl = torch.empty(m, per, dtype=torch.bfloat16, device=dev)
@@ -386,6 +386,30 @@ def time_sharded(mq, dev, stream, dist, world, rank):
                                     "fused_E": round(t1 / (world * tf), 3)})
                     except Exception as e:   # the headline line must still print
                         row["fused_error"] = f"{type(e).__name__}: {e}"[:160]
+                if slot == "down" and k % (32 * world) == 0:
+                    # NEXT-2 Megatron pairing: down row-parallel (K-sharded, the partner of a
+                    # column-sharded up) -- this rank's K-slice partial + NCCL sum all-reduce
+                    # (mcapq_linear_rowshard), and at M = 1 the fused NVLink slot stores + LSA
+                    # barriers + rank-order sum
+                    try:
+                        kp = k // world
+                        ks_c = _copies(pw_full.kshard(world, rank), l2)
+                        xs = x[:, rank * kp:(rank + 1) * kp].contiguous()
+                        wsr = torch.empty(max(256, comm.rowshard_workspace_bytes(route, m, n, kp)), dtype=torch.uint8,
+                                          device=dev)
+                        tr = _graph_us([lambda c=c: mq.linear_rowshard(comm, route, c, xs, out=y, ws=wsr,
+                                                                       stream=stream) for c in ks_c], stream, reps, dist)
+                        row.update({"rowpar_TP_us": round(tr, 3), "rowpar_E": round(t1 / (world * tr), 3)})
+                        if m == 1 and kp % 256 == 0 and kp >= 2048:
+                            win = comm.window(n, torch.float32, rows=world)
+                            trf = _graph_us([lambda c=c: mq.linear_rowshard(comm, route, c, xs, out=y, ws=win,
+                                                                            stream=stream, fused=True) for c in ks_c],
+                                            stream, reps, dist)
+                            comm.free_window(win)
+                            row.update({"rowpar_fused_TP_us": round(trf, 3), "rowpar_fused_E": round(t1 / (world * trf), 3)})
+                        del ks_c
+                    except Exception as e:   # the headline line must still print
+                        row["rowpar_error"] = f"{type(e).__name__}: {e}"[:160]
                 if slot == "lm_head":
                     wsa = torch.empty(max(256, mq.argmax_workspace_bytes(route, m, per, k, world)),
                                       dtype=torch.uint8, device=dev)
@@ -402,7 +426,8 @@ def time_sharded(mq, dev, stream, dist, world, rank):
     del comm
     return {"timing": "CUDA graph of repeated calls over rotating weight copies (>= 4 x L2), CUDA events, max "
                       "over ranks; T(1) unsharded on one GPU, "
-                      "T(P) sharded + NCCL all-gather (E = T(1) / (P T(P)))", "rows": rows}
+                      "T(P) sharded + NCCL all-gather (E = T(1) / (P T(P))); down also row-parallel "
+                      "(rowpar_*: K-sharded + all-reduce, NEXT-2)", "rows": rows}
 
 
 def time_mlp8b_stack(mq, dev, stream, layers=8, steps=20):

@@ -7,9 +7,11 @@
 //
 // = "dequantise to 16-bit, then a dense GEMM" (the paper's prefill path);
 // oracle: oracle_w4a16_bf16deq.  The exact per-block-scale semantics (mcapq_w4a16) needs
-// one TMEM read-back per Q4_0 block, and TMEM reads at ~64 B/clk/SM make that 8 * MP
-// cycles per 128-row block: 5x the HBM time at MP = 64 (measured 231 us for the 8B
-// lm_head) -- that path stays on mma.sync (gemm_w4); this one reads TMEM once per tile.
+// one TMEM read-back per Q4_0 block (a first tcgen05 version measured 231 us for the 8B
+// lm_head at M = 64) -- that path stays on mma.sync (gemm_w4); this one reads TMEM once
+// per tile.  (TMEM itself reads ~400 B/clk/SM here, scripts/probes/tmem_ld.cu: the per-block
+// MMA -> commit -> read-back chain, not TMEM bandwidth, is what such kernels pay; see
+// tc05_w4a8 below.)
 //
 // CTA = 128 weight rows (UMMA_M = 128) x MP tokens (UMMA_N = MP), K in slices of 256.
 // Warp roles (448 threads):
@@ -496,6 +498,435 @@ __global__ void __launch_bounds__(192, 1) tc05_prefill(const __grid_constant__ P
             if (++bf == 2) {
                 bf = 0;
                 phb ^= 1u;
+            }
+        }
+    }
+    fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tbase), "r"(kCols) : "memory");
+    }
+}
+
+// ============================================================================ a5 on tcgen05
+// tc05_w4a8<MP>: batched W4A8 decode (row a5, M >= 9) on the 5th-generation tensor cores,
+// tcgen05.mma kind::i8 (s8 x s8 -> s32 in TMEM), the paper's exact semantics:
+//     y[t][n] = sum_g d[n][g] * s[t][g] * D[t][n][g],   D = sum_{k in g} (c - 8) q  (int32)
+// (oracle_w4a8).  Q4_0 scales one 32-K block at a time, so each
+// block's int32 product is its own MMA (M = 128 rows, N = MP tokens, K = 32 = one block)
+// into its own TMEM accumulator, read back once (tcgen05.ld) and scale-accumulated in
+// fp32 registers by the epilogue warps -- the per-block read-back the mma.sync path
+// (gemm_w4) does in registers.  Measured TMEM read rate on this B200: ~400 B/clk/SM
+// (scripts/probes/tmem_ld.cu), i.e. 128 x 64 x 4 B per block in ~80 clk.
+//
+// CTA = 128 weight rows x MP tokens, K in slices of 256 (8 blocks), 256 + 8 MP threads:
+//   warp 0      TMA: nibble box {128 B, 128 rows} SW128, scale box {8 fp16, 128 rows}, the
+//               slice's int8 q as 2 SW128 atoms [2][MP][128 B] (quant_a8 workspace; rows
+//               past M zero), s as [MP][8] fp32.
+//   warp 1      TMEM (8 x MP columns: 8 block accumulators in flight) + the MMA issuer
+//               (one kind::i8 MMA per block, fresh accumulator, commit per block).
+//   warps 2-5   unpack: thread = weight row r: the slice's 8 blocks of nibbles -> s8 (c - 8)
+//               bytes in the canonical K-major SW128 layout (two 128-K atoms of the A ring).
+//   warps 6..   epilogue (MP / 4 warps): warp = (TMEM lane quarter, 16-token group): per slice it copies s
+//               transposed ([8][MP], LDS.128-friendly) and releases the stage; per block
+//               one tcgen05.ld of its 32 rows x 16 tokens (the next block's load in
+//               flight under this block's math), acc[t] = fma(d, s[t] * float(D[t]), acc[t])
+//               on the f32x2 pipe; after the tile's last slice it stores its rows.
+namespace tc05 {
+// epilogue warps: 4 lane quarters x MP / 16 token groups of 16 (each thread: one row x 16 tokens)
+// x kA8Sets: at MP <= 32 two sets split each slice's two atoms (partial sums added at the
+// tile's end) -- a lone epilogue warp per SMSP cannot keep up with the weight stream
+template <int MP> constexpr int kA8Unpack = MP == 64 ? 4 : 8;   // unpack warps (a multiple of 4)
+template <int MP> constexpr int kA8Sets = MP == 16 ? 2 : 1;
+template <int MP> constexpr int kA8Epi = MP / 4 * kA8Sets<MP>;
+template <int MP> constexpr int kA8Threads = (2 + kA8Unpack<MP> + kA8Epi<MP>) * 32;
+// A ring (128-K atoms of 128 rows x 128 B s8, even) and block accumulators in TMEM (all
+// 512 columns: one block's MMA -> commit -> epilogue round trip is long, so as many blocks
+// as TMEM holds stay in flight)
+template <int MP> constexpr int kA8NA = 4;
+template <int MP> constexpr int kA8NB = (512 / MP) > 32 ? 32 : (512 / MP);   // a multiple of 4
+template <int MP> constexpr int kA8NE = MP == 64 ? 3 : 4;   // E-ring slices (epilogue operands)
+constexpr uint32_t kA8AtomBytes = 128u * 128u;
+// kind::i8: D s32 (2 << 4), A s8 (1 << 7), B s8 (1 << 10), both K-major, N = MP, M = 128
+template <int MP>
+__device__ __forceinline__ constexpr uint32_t idesc_i8()
+{
+    return (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(MP >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+}
+// issued by the whole (converged) warp: one elected lane executes the MMA / commit, so the
+// warp-uniform descriptors live in uniform registers (no per-MMA R2UR chain)
+__device__ __forceinline__ void mma_i8_elect(uint32_t dtmem, uint64_t adesc, uint64_t bdesc, uint32_t id)
+{
+    asm volatile(
+        "{\n\t.reg .pred p, e;\n\tsetp.ne.b32 p, 0, 0;\n\telect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(dtmem),
+        "l"(adesc), "l"(bdesc), "r"(id)
+        : "memory");
+}
+// the four blocks of one 128-K atom: descriptors advanced 32 B (2 units) per block, the
+// accumulators MP columns apart, issued in one block of PTX by one elected lane
+template <int MP>
+__device__ __forceinline__ void mma4_i8_elect(uint32_t dq, uint64_t ad, uint64_t bd, uint32_t id)
+{
+    asm volatile(
+        "{\n\t.reg .pred p, e;\n\t.reg .b64 a1, a2, a3, b1, b2, b3;\n\t.reg .b32 d1, d2, d3;\n\t"
+        "setp.ne.b32 p, 0, 0;\n\t"
+        "add.s64 a1, %1, 2;\n\tadd.s64 a2, %1, 4;\n\tadd.s64 a3, %1, 6;\n\t"
+        "add.s64 b1, %2, 2;\n\tadd.s64 b2, %2, 4;\n\tadd.s64 b3, %2, 6;\n\t"
+        "add.u32 d1, %0, %4;\n\tadd.u32 d2, %0, %5;\n\tadd.u32 d3, %0, %6;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::i8 [d1], a1, b1, %3, p;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::i8 [d2], a2, b2, %3, p;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::i8 [d3], a3, b3, %3, p;\n\t}" ::"r"(dq),
+        "l"(ad), "l"(bd), "r"(id), "n"(MP), "n"(2 * MP), "n"(3 * MP)
+        : "memory");
+}
+__device__ __forceinline__ void commit_elect(uint32_t bar)
+{
+    asm volatile(
+        "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(bar)
+        : "memory");
+}
+// four nibble codes c (bytes of v4 & 0x0F0F0F0F) -> four s8 (c - 8): c ^ 8 is c - 8 for
+// c >= 8 and c + 8 (bit 3 set) for c < 8, where the byte needs 0xF0 ORed in (sign)
+__device__ __forceinline__ uint32_t s8_codes(uint32_t v4)
+{
+    const uint32_t v = (v4 & 0x0F0F0F0Fu) ^ 0x08080808u;
+    return v | ((v & 0x08080808u) * 30u);   // 0x08 * 30 = 0xF0 per byte, no carries
+}
+template <int X>
+__device__ __forceinline__ void tmem_ld_x(uint32_t taddr, uint32_t *r)
+{
+    if constexpr (X == 4) {
+        asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"
+                     : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+                     : "r"(taddr)
+                     : "memory");
+    } else if constexpr (X == 8) {
+        asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                     : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+                       "=r"(r[7])
+                     : "r"(taddr)
+                     : "memory");
+    } else {
+        static_assert(X == 16, "x4 / x8 / x16");
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+            : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+              "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+            : "r"(taddr)
+            : "memory");
+    }
+}
+template <int MP>
+__device__ __forceinline__ void bar_epi() { asm volatile("bar.sync 2, %0;" ::"n"(kA8Epi<MP> * 32) : "memory"); }
+}  // namespace tc05
+
+template <int MP>
+__global__ void __launch_bounds__(tc05::kA8Threads<MP>, 1) tc05_w4a8(const __grid_constant__ GemmArgs a)
+{
+    using namespace tc05;
+    constexpr int TOK = 16;                       // tokens per epilogue thread
+    constexpr int kA8Epi = tc05::kA8Epi<MP>, kSets = tc05::kA8Sets<MP>;
+    constexpr int NA = kA8NA<MP>, NB = kA8NB<MP>, NE = kA8NE<MP>;
+    extern __shared__ __align__(16) uint8_t smem_raw[];
+    const uint32_t sb = (smem_addr(smem_raw) + 1023u) & ~1023u;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int S = a.stages;
+    const int G8 = (int)(a.k / 256);
+    const uint32_t stage_bytes = a.stage_bytes;
+    const uint32_t q_off = kNibBytes + kScBytes;           // 18 KiB: 1024-aligned for SW128
+    const uint32_t s_off = q_off + (uint32_t)MP * 256u;
+    const uint32_t ring = sb;
+    const uint32_t aring = sb + (uint32_t)S * stage_bytes;
+    // E ring (NE slices): each slice's row scales [128][8] fp16 and s transposed [8][MP]
+    // fp32, copied out of the stage by the unpack warps so the stage is recycled as soon as
+    // the MMAs and the unpack are done with it (the epilogue runs slices behind)
+    constexpr uint32_t kEBytes = 128u * 16u + 8u * (uint32_t)MP * 4u;
+    const uint32_t ering = aring + (uint32_t)NA * kA8AtomBytes;
+    const uint32_t xch = ering + (uint32_t)NE * kEBytes;      // [128][MP] fp32: set 1's partials (kSets == 2)
+    const uint32_t bars = xch + (kSets == 2 ? 128u * (uint32_t)MP * 4u : 0u);
+    const uint32_t efull = bars, eempty = bars + 8u * NE;
+    const uint32_t sfull = eempty + 8u * NE, sempty = sfull + 8u * S;
+    const uint32_t afull = sempty + 8u * S, aempty = afull + 8u * NA;
+    constexpr int NQ = NB / 4;                    // accumulator quads: one per 128-K atom (4 blocks)
+    const uint32_t dfull = aempty + 8u * NA, dempty = dfull + 8u * NQ;
+    const uint32_t tslot = dempty + 8u * NQ;
+    constexpr uint32_t kCols = (NB * MP) < 32 ? 32 : (NB * MP);   // 128 / 256 / 512
+
+    const int T = a.row_tiles;
+    const int t0 = (int)(((uint32_t)T * blockIdx.x) / gridDim.x);
+    const int t1 = (int)(((uint32_t)T * (blockIdx.x + 1)) / gridDim.x);
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < S; ++s) {
+            mbar_init(sfull + 8u * s, 1);
+            mbar_init(sempty + 8u * s, 1 + kA8Unpack<MP>);   // MMA commit + unpack warps
+        }
+        for (int e = 0; e < NE; ++e) {
+            mbar_init(efull + 8u * e, 4);   // the unpack warps of rows' first half
+            mbar_init(eempty + 8u * e, kA8Epi);
+        }
+        for (int s = 0; s < NA; ++s) {
+            mbar_init(afull + 8u * s, 4);   // the 4 unpack warps writing the atom
+            mbar_init(aempty + 8u * s, 1);
+        }
+        for (int s = 0; s < NQ; ++s) {
+            mbar_init(dfull + 8u * s, 1);
+            mbar_init(dempty + 8u * s, kA8Epi / kSets);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(tslot), "r"(kCols)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    dev::griddep_launch();
+    fence_before();
+    __syncthreads();
+    fence_after();
+    const uint32_t tbase = lds32(tslot);
+    dev::griddep_wait();
+
+    if (warp == 0) {
+        // ================= TMA producer =================
+        if (lane == 0) {
+            const uint64_t pol = evict_first_policy();
+            int s = 0;
+            uint32_t ph = 0;
+            const uint32_t tx = kNibBytes + kScBytes + (uint32_t)MP * 256u + (uint32_t)MP * 32u;
+            for (int rt = t0; rt < t1; ++rt) {
+                const int row0 = rt * 128;
+                for (int sl = 0; sl < G8; ++sl) {
+                    mbar_wait(sempty + 8u * s, ph ^ 1u);
+                    const uint32_t st = ring + (uint32_t)s * stage_bytes;
+                    const uint32_t fb = sfull + 8u * s;
+                    mbar_expect_tx(fb, tx);
+                    tma_2d(st, a.maps, sl * 128, row0, fb, pol);
+                    tma_2d(st + kNibBytes, a.maps + 1, sl * 8, row0, fb, pol);
+                    tma_3d(st + q_off, a.amaps, 0, (int)a.tok0, sl * 2, fb, 0);
+                    tma_2d(st + s_off, a.amaps + 1, sl * 8, (int)a.tok0, fb, 0);
+                    if (++s == S) {
+                        s = 0;
+                        ph ^= 1u;
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ================= MMA issuer: one kind::i8 MMA per Q4_0 block =================
+        // per 128-K atom: one wait for its A, one for a free accumulator quad, four MMAs on
+        // descriptors advanced 32 B (2 units of 16 B) per block, one commit for the quad --
+        // the issue loop's serial latency bounds the kernel, so it is kept short and runs on the
+        // whole warp (uniform registers; the MMAs and commits by one elected lane)
+        {
+            constexpr uint32_t id = idesc_i8<MP>();
+            int s = 0, sa = 0, qb = 0;
+            uint32_t ph = 0, pha = 0, phq = 0;
+            for (int rt = t0; rt < t1; ++rt) {
+                for (int sl = 0; sl < G8; ++sl) {
+                    mbar_wait(sfull + 8u * s, ph);
+                    const uint32_t qs = ring + (uint32_t)s * stage_bytes + q_off;
+#pragma unroll
+                    for (int at = 0; at < 2; ++at) {
+                        mbar_wait(afull + 8u * sa, pha);
+                        mbar_wait(dempty + 8u * qb, phq ^ 1u);   // the epilogue drained this quad
+                        fence_after();
+                        const uint64_t ad = smem_desc(aring + (uint32_t)sa * kA8AtomBytes);
+                        const uint64_t bd = smem_desc(qs + (uint32_t)at * (uint32_t)MP * 128u);
+                        const uint32_t dq = tbase + (uint32_t)(qb * 4 * MP);
+                        mma4_i8_elect<MP>(dq, ad, bd, id);
+                        commit_elect(dfull + 8u * qb);
+                        commit_elect(aempty + 8u * sa);
+                        if (++qb == NQ) {
+                            qb = 0;
+                            phq ^= 1u;
+                        }
+                        if (++sa == NA) {
+                            sa = 0;
+                            pha ^= 1u;
+                        }
+                    }
+                    commit_elect(sempty + 8u * s);
+                    if (++s == S) {
+                        s = 0;
+                        ph ^= 1u;
+                    }
+                }
+            }
+        }
+    } else if (warp < 2 + kA8Unpack<MP>) {
+        // ================= unpack: thread = (row r, atom half hb) =================
+        // A = 16 (c - 8) as s8: the code in the byte's high nibble with the sign bit flipped
+        // (one LOP3 for a high nibble, SHF + LOP3 for a low one); D' = 16 D exactly
+        // (|D'| <= 2^19), the 1/16 goes into the copied s (exact)
+        constexpr int kHalves = kA8Unpack<MP> / 4;      // 2: each half-CTA of rows' threads owns one atom
+        const int tu = threadIdx.x - 64;
+        const int r = tu & 127, hb0 = kHalves == 2 ? (tu >> 7) : 0;
+        const uint32_t sw = (uint32_t)(r & 7);
+        int s = 0, sa = 0, e = 0;
+        uint32_t ph = 0, pha = 0, phe = 0;
+        for (int rt = t0; rt < t1; ++rt) {
+            for (int sl = 0; sl < G8; ++sl) {
+                mbar_wait(sfull + 8u * s, ph);
+                const uint32_t st = ring + (uint32_t)s * stage_bytes;
+                uint4 w[8 / kHalves];
+#pragma unroll
+                for (int j = 0; j < 8 / kHalves; ++j)
+                    w[j] = lds128(st + (uint32_t)r * 128u + (((uint32_t)(j + 4 * hb0) ^ sw) << 4));
+                if (hb0 == 0) {
+                    // the slice's epilogue operands into E-ring slot e: row r's 8 scales, and
+                    // s / 16 [MP][8] -> [8][MP] (MP / 16 elements per thread)
+                    mbar_wait(eempty + 8u * e, phe ^ 1u);
+                    const uint32_t eb = ering + (uint32_t)e * kEBytes;
+                    sts128(eb + (uint32_t)r * 16u, lds128(st + kNibBytes + (uint32_t)r * 16u));
+#pragma unroll
+                    for (int i = 0; i < MP / 16; ++i) {
+                        const int idx = r + 128 * i;   // [t][g] index in the stage
+                        const float sv = __uint_as_float(lds32(st + s_off + 4u * (uint32_t)idx)) * 0.0625f;
+                        sts32(eb + 2048u + 4u * (uint32_t)((idx & 7) * MP + (idx >> 3)), __float_as_uint(sv));
+                    }
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(efull + 8u * e);
+                }
+                if (++e == NE) {
+                    e = 0;
+                    phe ^= 1u;
+                }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(sempty + 8u * s);   // nibbles, scales and s read
+#pragma unroll
+                for (int h = 0; h < 2 / kHalves; ++h) {
+                    const int hb = hb0 + h;
+                    mbar_wait(aempty + 8u * (sa + hb), pha ^ 1u);
+                    const uint32_t ar = aring + (uint32_t)(sa + hb) * kA8AtomBytes + (uint32_t)r * 128u;
+#pragma unroll
+                    for (int jj = 0; jj < 4; ++jj) {
+                        // block jj of the atom: K bytes 32 jj .. + 31 = chunks 2 jj (c0..c15), 2 jj + 1 (c16..c31)
+                        const uint4 v = w[4 * h + jj];
+                        const uint32_t c0 = 2u * (uint32_t)jj;
+                        if (a.wt & 1) {   // debug (MCAPQ_TC05_DBG=1): raw words, no conversion
+                            sts128(ar + ((c0 ^ sw) << 4), v);
+                            sts128(ar + (((c0 + 1) ^ sw) << 4), v);
+                            continue;
+                        }
+                        const uint32_t M = 0xF0F0F0F0u, X = 0x80808080u;
+                        sts128(ar + ((c0 ^ sw) << 4),
+                               make_uint4(((v.x << 4) & M) ^ X, ((v.y << 4) & M) ^ X, ((v.z << 4) & M) ^ X, ((v.w << 4) & M) ^ X));
+                        sts128(ar + (((c0 + 1) ^ sw) << 4), make_uint4((v.x & M) ^ X, (v.y & M) ^ X, (v.z & M) ^ X, (v.w & M) ^ X));
+                    }
+                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(afull + 8u * (sa + hb));
+                }
+                sa += 2;
+                if (sa == NA) {
+                    sa = 0;
+                    pha ^= 1u;
+                }
+                if (++s == S) {
+                    s = 0;
+                    ph ^= 1u;
+                }
+            }
+        }
+    } else {
+        // ================= epilogue: per block TMEM -> fp32 scale-accumulate =================
+        const int ew = warp - 2 - kA8Unpack<MP>;             // 0 .. kA8Epi - 1
+        const int quarter = warp & 3;                    // TMEM lane quarter = warp % 4 (hardware rule)
+        const int set = kSets == 2 ? ew / (kA8Epi / 2) : 0;   // the atoms (quads) this warp drains
+        const int tq = (ew % (kA8Epi / kSets)) >> 2;     // 16-token group
+        const int r = quarter * 32 + lane;
+        const uint32_t tl = tbase + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(tq * TOK);
+        int e = 0, qb = set;
+        uint32_t phe = 0, phq = 0;
+        for (int rt = t0; rt < t1; ++rt) {
+            f2_t acc[TOK / 2];
+#pragma unroll
+            for (int t = 0; t < TOK / 2; ++t) acc[t] = 0ull;
+            for (int sl = 0; sl < G8; ++sl) {
+                mbar_wait(efull + 8u * e, phe);
+                const uint32_t eb = ering + (uint32_t)e * kEBytes;
+                const uint4 scw = lds128(eb + (uint32_t)r * 16u);   // the row's 8 block scales (fp16)
+                const uint32_t sTb = eb + 2048u;                   // s [8][MP]
+                const uint32_t sc[4] = {scw.x, scw.y, scw.z, scw.w};
+                uint32_t Da[TOK], Db[TOK];
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {   // the slice's two atoms = two accumulator quads
+                    if (kSets == 2 && h != set) continue;   // the other set's atom
+                    mbar_wait(dfull + 8u * qb, phq);
+                    fence_after();
+                    const uint32_t tq0 = tl + (uint32_t)(qb * 4 * MP);
+                    tmem_ld_x<TOK>(tq0, Da);
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        const int g = 4 * h + j;
+                        uint32_t *Dc = (j & 1) ? Db : Da;
+                        uint32_t *Dn = (j & 1) ? Da : Db;
+                        tmem_wait_ld();   // block g's D is in registers
+                        if (j < 3) {
+                            tmem_ld_x<TOK>(tq0 + (uint32_t)((j + 1) * MP), Dn);   // in flight under block g's math
+                        } else {
+                            fence_before();
+                            __syncwarp();
+                            if (lane == 0) mbar_arrive(dempty + 8u * qb);   // the quad is drained
+                            qb += kSets;   // a set drains every kSets-th quad (NQ is even)
+                            if (qb >= NQ) {
+                                qb -= NQ;
+                                phq ^= 1u;
+                            }
+                        }
+                        if (a.wt & 2) continue;   // debug (MCAPQ_TC05_DBG=2): no epilogue math
+                        const float d = h2f((uint16_t)((g & 1) ? (sc[g >> 1] >> 16) : (sc[g >> 1] & 0xffffu)));
+                        const f2_t d2 = f2_pack(d, d);
+                        const uint32_t srow = sTb + (uint32_t)(g * MP + tq * TOK) * 4u;
+#pragma unroll
+                        for (int t = 0; t < TOK; t += 4) {
+                            const uint4 sv = lds128(srow + 4u * (uint32_t)t);
+                            const f2_t s01 = f2_pack_bits(sv.x, sv.y), s23 = f2_pack_bits(sv.z, sv.w);
+                            const f2_t D01 = f2_pack(__int2float_rn((int)Dc[t]), __int2float_rn((int)Dc[t + 1]));
+                            const f2_t D23 = f2_pack(__int2float_rn((int)Dc[t + 2]), __int2float_rn((int)Dc[t + 3]));
+                            acc[t / 2] = f2_fma(d2, f2_mul(s01, D01), acc[t / 2]);
+                            acc[t / 2 + 1] = f2_fma(d2, f2_mul(s23, D23), acc[t / 2 + 1]);
+                        }
+                    }
+                }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(eempty + 8u * e);   // this warp is done with the slice's operands
+                if (++e == NE) {
+                    e = 0;
+                    phe ^= 1u;
+                }
+            }
+            if constexpr (kSets == 2) {
+                // set 1 hands its partial sums (its atoms' blocks) to set 0 through shared memory
+                const uint32_t xr = xch + ((uint32_t)r * MP + (uint32_t)(tq * TOK)) * 4u;
+                if (set == 1)
+#pragma unroll
+                    for (int t = 0; t < TOK; t += 2) asm volatile("st.shared.v2.u32 [%0], {%1,%2};" ::"r"(xr + 4u * t),
+                                                               "r"((uint32_t)acc[t / 2]), "r"((uint32_t)(acc[t / 2] >> 32)) : "memory");
+                bar_epi<MP>();
+                if (set == 1) continue;
+#pragma unroll
+                for (int t = 0; t < TOK; t += 2) {
+                    uint32_t lo, hi;
+                    asm volatile("ld.shared.v2.u32 {%0,%1}, [%2];" : "=r"(lo), "=r"(hi) : "r"(xr + 4u * t) : "memory");
+                    acc[t / 2] = f2_add(acc[t / 2], f2_pack_bits(lo, hi));
+                }
+            }
+            const int64_t row = (int64_t)rt * 128 + r;
+            if (row < a.n) {
+#pragma unroll
+                for (int t = 0; t < TOK; t += 2) {
+                    const float2 v = f2_unpack(acc[t / 2]);
+                    const int tt = tq * TOK + t;
+                    if (tt < a.ntok) dev::store_out(a.y, a.ydt, (a.tok0 + tt) * a.ldy + row, v.x);
+                    if (tt + 1 < a.ntok) dev::store_out(a.y, a.ydt, (a.tok0 + tt + 1) * a.ldy + row, v.y);
+                }
             }
         }
     }
