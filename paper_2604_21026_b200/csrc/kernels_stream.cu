@@ -943,6 +943,7 @@ cudaError_t launch_stack_step(const void *ops_dev, int nops, unsigned int *count
     const size_t prog = round_up(sizeof(StackOp) * (size_t)nops, 128);
     int S = (int)(((long)budget - 1024 - (long)kBarBytes - (long)prog - (long)act - kRedBytes) / kStageBytes);
     S = S < 2 ? 2 : (S > kMaxStages ? kMaxStages : S);
+    S = S > 13 ? 13 : S;   // the step's barrier area: 16 S + 288 bytes <= kBarBytes
     a.stages = S;
     a.ops_off = S * kStageBytes + kBarBytes;
     a.act_off = (int)(a.ops_off + prog);

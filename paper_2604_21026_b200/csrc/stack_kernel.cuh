@@ -169,7 +169,11 @@ __device__ __forceinline__ bool rec_ok(unsigned long long w, uint32_t t8) { retu
 // group) and store its record: codes, s = fl(amax / 127) and 8 sum q,
 // bit-identical to quant_a8_kernel (same fast path and IEEE fallback as a8_*_store).
 // All 32 lanes call it.
-__device__ __forceinline__ void quant_group_record(uint32_t xb, unsigned long long *rec, uint32_t t8, int lane)
+// scr: 48 B of this warp's shared scratch (6 x u64, 8-aligned): the record is assembled
+// there byte by byte (lane j's code at byte 7 (j / 7) + j % 7 of the payload stream) and
+// read back as six tagged words
+__device__ __forceinline__ void quant_group_record(uint32_t xb, unsigned long long *rec, uint32_t t8, int lane,
+                                                   uint32_t scr)
 {
     const uint32_t m = __reduce_max_sync(0xffffffffu, xb & 0x7fffu);
     const float s = div127_rn(__uint_as_float(m << 16));
@@ -187,19 +191,26 @@ __device__ __forceinline__ void quant_group_record(uint32_t xb, unsigned long lo
     const uint32_t cb = (uint32_t)c & 0xffu;
     const uint32_t sbits = __float_as_uint(live ? s : 0.0f);
     const uint32_t sq16 = (uint32_t)(8 * sum) & 0xffffu;
-    unsigned long long word = (unsigned long long)t8 << 56;
-#pragma unroll
-    for (int k = 0; k < 7; ++k) {
-        const int idx = 7 * lane + k;
-        const uint32_t code = __shfl_sync(0xffffffffu, cb, idx & 31);
-        uint32_t byte;
-        if (idx < 32) byte = code;
-        else if (idx < 36) byte = (sbits >> (8 * (idx - 32))) & 0xffu;
-        else if (idx < 38) byte = (sq16 >> (8 * (idx - 36))) & 0xffu;
-        else byte = 0u;
-        word |= (unsigned long long)byte << (8 * k);
+    // payload stream: codes 0..31, s (4 bytes LE), 8 sum q (2 bytes LE), 4 zero bytes; stream
+    // byte i sits in word i / 7, byte i % 7; byte 7 of every word is the tag
+    if (lane < kRecWords)
+        asm volatile("st.shared.u64 [%0], %1;" ::"r"(scr + 8u * (uint32_t)lane), "l"((unsigned long long)t8 << 56)
+                     : "memory");
+    __syncwarp();
+    auto put = [&](int i, uint32_t byte) {
+        asm volatile("st.shared.u8 [%0], %1;" ::"r"(scr + 8u * (uint32_t)(i / 7) + (uint32_t)(i % 7)), "r"(byte)
+                     : "memory");
+    };
+    put(lane, cb);
+    if (lane < 4) put(32 + lane, (sbits >> (8 * lane)) & 0xffu);
+    else if (lane < 6) put(32 + lane, (sq16 >> (8 * (lane - 4))) & 0xffu);
+    __syncwarp();
+    if (lane < kRecWords) {
+        unsigned long long word;
+        asm volatile("ld.shared.u64 %0, [%1];" : "=l"(word) : "r"(scr + 8u * (uint32_t)lane) : "memory");
+        asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(rec + lane), "l"(word) : "memory");
     }
-    if (lane < kRecWords) asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(rec + lane), "l"(word) : "memory");
+    __syncwarp();   // the scratch is free again for the next record
 }
 
 // A record's payload into the engine's activation layout: q_lo (codes 0..15), q_hi
@@ -573,6 +584,7 @@ __global__ void __launch_bounds__(kStepThreads, 1) stack_step(const __grid_const
     // CTA-pair exchange of a group's first 16 rows when its two tiles sit on the two CTAs
     // of a cluster: xfull[2] (st.async complete_tx), xempty[2] (the reader's release), xbuf[2][32 B]
     const uint32_t xfull = go + 144u, xempty = go + 160u, xbuf = go + 176u;
+    const uint32_t rscr = go + 240u;   // the epilogue warp's 48-B record scratch (quant_group_record)
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < S; ++s) {
@@ -744,7 +756,7 @@ __global__ void __launch_bounds__(kStepThreads, 1) stack_step(const __grid_const
                             }
                             const uint32_t second = __shfl_sync(0xffffffffu, b, lane & 15);
                             quant_group_record(lane < kTileRows ? first : second, op.yq[li] + (size_t)(tl >> 1) * kRecWords,
-                                               t8, lane);
+                                               t8, lane, rscr);
                             if (straddle && tile == t0) {
                                 // the exchange slot is free again: every lane consumed its value
                                 // (the record is built from it), so a relaxed arrive suffices
