@@ -337,10 +337,13 @@ void mcapq_profile_free(mcapq_profile *p);
 
 /*
  * NEXT-3: the MCAP profile artifact from raw per-layer scores s_i (Alg. 1 line 10,
- * P:547-549): writes {"format_version":1,"num_layers":L,"prompt_count":k,"epsilon":1e-09,
- * "raw_scores":[...],"tau":tau} (NUL-terminated) into buf (host, cap bytes); *len = length
- * without the NUL.  mcapq_profile_parse of it min-max normalises (lines 11-15) and routes
- * (line 16).  MCAPQ_ENOSPACE if cap < *len + 1; MCAPQ_EINVAL for NULL / non-finite input.
+ * P:547-549): writes {"epsilon":1e-09,"format_version":1,"num_layers":L,"prompt_count":k,
+ * "raw_scores":[...],"tau":tau} (NUL-terminated; keys sorted, every double in its shortest
+ * round-trip form, so writing what mcapq_profile_parse read back gives the same bytes) into
+ * buf (host, cap bytes); *len = length without the NUL.  mcapq_profile_parse of it min-max
+ * normalises (lines 11-15) and routes (line 16); parse rejects epsilon <= 0 and negative raw
+ * scores (sums of norms).  MCAPQ_ENOSPACE if cap < *len + 1; MCAPQ_EINVAL for NULL,
+ * non-finite or negative input.
  */
 mcapq_status mcapq_profile_write_json(const double *raw_scores_host, int layers, int prompts, double tau, char *buf,
                                       size_t cap, size_t *len);

@@ -6,6 +6,7 @@
 // profile artifact is the paper's compact per-architecture JSON;
 // its schema is not printed, so the accepted keys are the DESIGN.md reading A14
 // (SPEC.md S:109-111 ImportanceProfile fields + "scores" alias).
+#include <charconv>
 #include <cerrno>
 #include <cmath>
 #include <cstdlib>
@@ -211,6 +212,9 @@ mcapq_status mcapq_profile_parse(const char *json, size_t len, double tau_overri
     MCAPQ_REQUIRE(ok, MCAPQ_EPARSE, "profile: %s", ps.err.c_str());
     (void)have_tau;
 
+    MCAPQ_REQUIRE(std::isfinite(eps) && eps > 0.0, MCAPQ_EPARSE, "profile: epsilon %g must be finite and > 0", eps);
+    for (double v : raw)   // MCAP scores are sums of L2 norms (Alg. 1 lines 5-10): never negative
+        MCAPQ_REQUIRE(std::isfinite(v) && v >= 0.0, MCAPQ_EPARSE, "profile: raw score %g must be finite and >= 0", v);
     if (!have_scores) {
         MCAPQ_REQUIRE(have_raw && !raw.empty(), MCAPQ_EPARSE, "profile: no scores / normalized_scores / raw_scores");
         // Alg. 1 lines 8-12
@@ -267,7 +271,15 @@ void mcapq_profile_free(mcapq_profile *p) { delete p; }
 
 // The profile artifact from raw per-layer scores (Alg. 1 line 10 output, e.g. accumulated by
 // mcapq_mcap_accumulate): the same JSON form mcapq_profile_parse reads ("raw_scores" are
-// min-max normalised there, Alg. 1 lines 11-15).  %.17g keeps every double exact.
+// min-max normalised there, Alg. 1 lines 11-15).  Keys in sorted order, every double in
+// its shortest round-trip form (std::to_chars), so serialise -> parse -> serialise is
+// byte-identical.
+static std::string shortest(double v)
+{
+    char b[64];
+    const auto r = std::to_chars(b, b + sizeof(b), v);
+    return std::string(b, r.ptr);
+}
 mcapq_status mcapq_profile_write_json(const double *raw_scores_host, int layers, int prompts, double tau, char *buf,
                                       size_t cap, size_t *len)
 {
@@ -275,16 +287,15 @@ mcapq_status mcapq_profile_write_json(const double *raw_scores_host, int layers,
     MCAPQ_REQUIRE(raw_scores_host && buf && len, MCAPQ_EINVAL, "NULL argument");
     MCAPQ_REQUIRE(layers >= 1 && prompts >= 1, MCAPQ_EINVAL, "layers=%d prompts=%d", layers, prompts);
     MCAPQ_REQUIRE(std::isfinite(tau), MCAPQ_EINVAL, "tau is not finite");
-    std::string s = "{\"format_version\":1,\"num_layers\":" + std::to_string(layers) +
-                    ",\"prompt_count\":" + std::to_string(prompts) + ",\"epsilon\":1e-09,\"raw_scores\":[";
-    char num[64];
+    std::string s = "{\"epsilon\":1e-09,\"format_version\":1,\"num_layers\":" + std::to_string(layers) +
+                    ",\"prompt_count\":" + std::to_string(prompts) + ",\"raw_scores\":[";
     for (int i = 0; i < layers; ++i) {
-        MCAPQ_REQUIRE(std::isfinite(raw_scores_host[i]), MCAPQ_EINVAL, "raw score %d is not finite", i);
-        snprintf(num, sizeof(num), "%s%.17g", i ? "," : "", raw_scores_host[i]);
-        s += num;
+        MCAPQ_REQUIRE(std::isfinite(raw_scores_host[i]) && raw_scores_host[i] >= 0.0, MCAPQ_EINVAL,
+                      "raw score %d must be finite and >= 0", i);
+        if (i) s += ",";
+        s += shortest(raw_scores_host[i]);
     }
-    snprintf(num, sizeof(num), "],\"tau\":%.17g}", tau);
-    s += num;
+    s += "],\"tau\":" + shortest(tau) + "}";
     *len = s.size();
     MCAPQ_REQUIRE(cap >= s.size() + 1, MCAPQ_ENOSPACE, "buffer %zu < %zu bytes", cap, s.size() + 1);
     memcpy(buf, s.c_str(), s.size() + 1);

@@ -132,6 +132,8 @@ def test_profile_raw_scores_and_degenerate(L, orc):
     ("{\"scores\": [0.1, 0.2], \"num_layers\": 3}", 4), ("{\"scores\": [0.1,", 4),
     ("{\"scores\": [0.1, 0.2]} x", 4), ("{\"scores\": [0.5], \"tau\": -1}", 3),
     ("{\"scores\": [\"a\"]}", 4),
+    ("{\"raw_scores\": [1.0, 2.0], \"epsilon\": 0}", 4), ("{\"raw_scores\": [1.0, 2.0], \"epsilon\": -1e-9}", 4),
+    ("{\"raw_scores\": [1.0, -2.0]}", 4),
 ])
 def test_profile_errors(L, bad, code):
     assert _routes(L, bad)[0] == code
@@ -140,3 +142,29 @@ def test_profile_errors(L, bad, code):
 def test_profile_ignores_unknown_keys(L):
     text = json.dumps({"arch": "x", "nested": {"a": [1, {"b": None}], "t": True}, "scores": [0.2, 0.9], "tau": 0.5})
     assert _routes(L, text)[1] == [0, 1]
+
+
+def _write(L, raw, prompts, tau):
+    buf = ctypes.create_string_buffer(1 << 16)
+    n = ctypes.c_size_t()
+    arr = (ctypes.c_double * len(raw))(*raw)
+    st = L.mcapq_profile_write_json(ctypes.cast(arr, ctypes.c_void_p), len(raw), prompts, tau, buf, len(buf),
+                                    ctypes.byref(n))
+    return st, buf.value.decode()
+
+
+def test_profile_writer_canonical_round_trip(L):
+    """The artifact mcapq_profile_write_json emits is canonical: keys sorted, every double in
+    its shortest round-trip form -- so parse(text) reproduces the raw scores exactly and
+    writing them again gives the same bytes (serialise -> load -> serialise identity)."""
+    raw = [85.14, 117.62, 61.0, 0.1 + 0.2, 1e-300, 142.0, 3.0000000000000004, 0.0]
+    st, text = _write(L, raw, 12, 0.7)
+    assert st == 0
+    obj = json.loads(text)
+    assert list(obj) == sorted(obj)
+    assert obj["raw_scores"] == raw and obj["tau"] == 0.7
+    assert text == json.dumps(obj, separators=(",", ":"))           # Python's repr is also shortest round-trip
+    st2, text2 = _write(L, obj["raw_scores"], obj["prompt_count"], obj["tau"])
+    assert st2 == 0 and text2 == text
+    assert _routes(L, text)[0] == 0
+    assert _write(L, [1.0, -1.0], 1, 0.7)[0] == 1                    # negative raw scores are rejected
