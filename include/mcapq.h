@@ -137,9 +137,12 @@ mcapq_status mcapq_quant_a8(const uint16_t *x, int64_t m, int64_t k, int64_t ldx
  * tokens (row strides k, k/32, k/32).  y: out [m][ldy] of dtype ydt.
  * m == 1 runs the batch-1 GEMV (dp4a), m > 1 the int8 tensor-core kernel; for
  * m >= 9 with K % 256 == 0 (and sx, sq 16-byte aligned) the batched kernel
- * streams each weight once per 64 tokens (rows a5, IMMA m16n8k32 per block).
- * The fp32 summation order depends on K only (never on N, M or the grid), so a
- * column shard of the weight gives bit-identical rows (A22).
+ * streams each weight once per 64 tokens (rows a5: mma.sync IMMA m16n8k32 per
+ * block; for m > 32 with at least one 128-row tile per SM, tcgen05 kind::i8 with
+ * the per-block D read back from TMEM).  Within one kernel the fp32 summation
+ * order depends on K only (never on N, M or the grid), so a column shard of the
+ * weight gives bit-identical rows (A22) whenever shard and whole run the same
+ * kernel; the two batched kernels differ by fp32 rounding (within reading T).
  */
 mcapq_status mcapq_w4a8(const uint8_t *nib, const uint16_t *scale, int64_t n, int64_t k, const int8_t *q,
                         const float *sx, const int32_t *sq, int64_t m, void *y, int ydt, int64_t ldy,
