@@ -1185,15 +1185,19 @@ cudaError_t launch_stream_group(int route, const StreamGroup &g, const uint16_t 
     // (the W4A16 M = 1 engine runs one CTA per SM: its lean loop keeps its lane offsets in
     // registers -- 86 of them -- instead of re-deriving them under the 56-register cap of
     // two CTAs per SM: 8B lm_head 80.9 -> 66.3 us, gate 13.4 -> 10.5 us)
+    // (a mid-size grouped linear, 10-16 tiles per SM -- the 8B gate+up -- also runs two CTAs per
+    // SM, at 96 KB each: 14.5 -> 13.3 us; a single 8B gate at 6 tiles per SM stays at one)
     const bool one_cta = route == MCAPQ_W4A16 && m == 1 && kHmma1Blocks == 1;
-    const int per_sm = tune().ctas_per_sm ? tune().ctas_per_sm : (one_cta ? 1 : (tiles >= 16 * device_sms() ? 2 : 1));
+    const bool mid = tiles >= 10 * device_sms() && tiles < 16 * device_sms();
+    const int per_sm = tune().ctas_per_sm ? tune().ctas_per_sm
+                                          : (one_cta ? 1 : (tiles >= 16 * device_sms() || mid ? 2 : 1));
     const int sms = device_sms() * per_sm;
     // shared-memory plan: ~112 KB (two CTAs per SM: the next linear's CTA co-resides under
     // PDL); a wide input (K >= 8192: a 9-15 KB activation area) at one CTA per SM takes
     // 130 KB instead -- two more ring stages beat the PDL overlap there (1B down 6.2 ->
     // 4.8 us, 8B down 11.3 -> 10.6 us; 8B gate at K = 4096 stays faster at 112 KB).
     // MCAPQ_STREAM_SMEM_KB overrides both.
-    a.smem_kb = (!tune().smem_kb_env && per_sm == 1 && g.k >= 8192) ? 130 : 0;
+    a.smem_kb = tune().smem_kb_env ? 0 : (per_sm == 1 && g.k >= 8192 ? 130 : (per_sm == 2 && mid ? 96 : 0));
     const int tp = stream_tokens_per_pass(route, g.k);
     pdl = pdl || tune().pdl || api_pdl();
     for (int64_t tok0 = 0; tok0 < m; tok0 += tp) {
