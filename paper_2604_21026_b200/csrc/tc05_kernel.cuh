@@ -63,6 +63,31 @@ __device__ __forceinline__ void commit(uint32_t bar)
 {
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar) : "memory");
 }
+// The four K16 steps of one 64-K atom (descriptors 32 B = 2 units apart), issued by one
+// elected lane of the converged warp (warp-uniform operands, no per-MMA R2UR chain); the
+// first step accumulates iff acc0 != 0.
+__device__ __forceinline__ void mma4_bf16_elect(uint32_t d, uint64_t ad, uint64_t bd, uint32_t id, uint32_t acc0)
+{
+    asm volatile(
+        "{\n\t.reg .pred p, q, e;\n\t.reg .b64 a1, a2, a3, b1, b2, b3;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\tsetp.eq.b32 q, 0, 0;\n\t"
+        "add.s64 a1, %1, 2;\n\tadd.s64 a2, %1, 4;\n\tadd.s64 a3, %1, 6;\n\t"
+        "add.s64 b1, %2, 2;\n\tadd.s64 b2, %2, 4;\n\tadd.s64 b3, %2, 6;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a1, b1, %3, q;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a2, b2, %3, q;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a3, b3, %3, q;\n\t}" ::"r"(d),
+        "l"(ad), "l"(bd), "r"(id), "r"(acc0)
+        : "memory");
+}
+__device__ __forceinline__ void commit_elect16(uint32_t bar)
+{
+    asm volatile(
+        "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(bar)
+        : "memory");
+}
 // 32 lanes x 16 columns of fp32 from TMEM (lane quarter of the calling warp)
 __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float *v)
 {
@@ -192,7 +217,8 @@ __global__ void __launch_bounds__(tc05::kThreads, 1) tc05_w4a16(const __grid_con
         }
     } else if (warp == 1) {
         // ================= MMA issuer: D[buf] = sum over K of W^ . X^T =================
-        if (lane == 0) {
+        // the whole warp runs the loop (warp-uniform descriptors); one elected lane issues
+        {
             constexpr uint32_t id = idesc<MP>();
             int s = 0, sa = 0, bf = 0;
             uint32_t ph = 0, pha = 0, phb = 0;
@@ -204,28 +230,27 @@ __global__ void __launch_bounds__(tc05::kThreads, 1) tc05_w4a16(const __grid_con
                     mbar_wait(sfull + 8u * s, ph);
                     fence_after();
                     const uint32_t xs = ring + (uint32_t)s * stage_bytes + kNibBytes + kScBytes;
+#pragma unroll
                     for (int at = 0; at < 4; ++at) {
                         mbar_wait(afull + 8u * sa, pha);
                         fence_after();
                         const uint32_t aa = aring + (uint32_t)sa * kAtomBytes;
                         const uint32_t xa = xs + (uint32_t)at * (uint32_t)MP * 128u;
-#pragma unroll
-                        for (int kk = 0; kk < 4; ++kk)   // K16 steps of the atom: 32 B apart
-                            mma_bf16(d, smem_desc(aa + 32u * kk), smem_desc(xa + 32u * kk), id,
-                                     (sl | at | kk) != 0 ? 1u : 0u);
-                        commit(aempty + 8u * sa);
+                        // K16 steps of the atom: 32 B apart
+                        mma4_bf16_elect(d, smem_desc(aa), smem_desc(xa), id, (sl | at) != 0 ? 1u : 0u);
+                        commit_elect16(aempty + 8u * sa);
                         if (++sa == kNA) {
                             sa = 0;
                             pha ^= 1u;
                         }
                     }
-                    commit(sempty + 8u * s);
+                    commit_elect16(sempty + 8u * s);
                     if (++s == S) {
                         s = 0;
                         ph ^= 1u;
                     }
                 }
-                commit(dfull + 8u * bf);
+                commit_elect16(dfull + 8u * bf);
                 if (++bf == kNB) {
                     bf = 0;
                     phb ^= 1u;
