@@ -558,6 +558,11 @@ def time_single_linears(mq, dev, stream):
                     if route == 2:   # useful bf16 FLOP/s against the measured dense bf16 peak
                         row[f"{name_}_tensor_frac"] = round(2 * m * n * k / (us * 1e-6) / 1e12 / bf16_peak_tflops(), 4)
         row["w4a8_over_w4a16"] = round(row["w4a16_us"] / row["w4a8_us"], 3)
+        if m > 1:   # which batched W4A8 kernel ran (launch_gemm's dispatch, DESIGN 6.4 / 6.4b)
+            mode = os.environ.get("MCAPQ_GEMM_A8_TC05", "1")
+            tc = m >= 9 and (mode == "2" or (mode == "1" and m > 32 and (n + 127) // 128 >= mq.device_sms()))
+            row["w4a8_kernel"] = ("tc05_w4a8 (tcgen05 kind::i8, TMEM read-back per block)" if tc
+                                  else ("stream_linear<IMMA>" if m <= 8 else "gemm_w4<A8> (mma.sync IMMA)"))
         out.append(row)
         del ws, pw0s
         torch.cuda.empty_cache()
