@@ -33,7 +33,9 @@
 // Determinism: the chunking and the block->lane/warp maps depend on K only and
 // all reductions have a fixed order, so an output row is bit-identical whatever
 // N, the group, the grid or the column shard (reading A22).
+#include <cmath>
 #include <cstdlib>
+#include <vector>
 
 #include "internal.h"
 #include "stream.h"
@@ -871,6 +873,63 @@ bool stack_fill_op(void *host_op, int route, const StreamGroup &g, const uint16_
     return true;
 }
 
+// Every CTA's tile range per op of a step program: [nops][grid] {t0, t1 | straddle << 31}.
+// Paired ops of a clustered launch (producer-side records): 32-row pairs split over the
+// clusters -- by weight: a pair of a member whose epilogue also builds records weighs
+// 1 + rec_r 2048 / K (the record work is fixed per group, the tile's compute grows with
+// K; rec_r = 0.6, MCAPQ_STEP_REC_R), the others 1 -- and each cluster's range in halves over its two CTAs, so a
+// quantisation group lies in one CTA or, at most once per op, straddles the pair (the
+// straddle flag: rank 0's last tile is its first half, rank 1's first tile its second).
+// Otherwise contiguous balanced ranges.
+void stack_partition(const void *ops_host, int nops, int grid, bool clustered, double rec_r, int2 *out)
+{
+    const StackOp *ops = reinterpret_cast<const StackOp *>(ops_host);
+    for (int i = 0; i < nops; ++i) {
+        const StackOp &op = ops[i];
+        const int T = op.tile_start[op.count];
+        if (clustered && op.paired) {
+            const int C = grid / 2;
+            const double wr = 1.0 + rec_r * (2048.0 / (double)op.k);
+            std::vector<double> wm(op.count);
+            double W = 0.0;
+            for (int m = 0; m < op.count; ++m) {
+                wm[m] = op.yq[m] ? wr : 1.0;
+                W += (double)((op.tile_start[m + 1] - op.tile_start[m]) >> 1) * wm[m];
+            }
+            auto pair_at = [&](int c) {
+                if (c >= C) return T >> 1;
+                double t = W * c / C;
+                int base = 0;
+                for (int m = 0; m < op.count; ++m) {
+                    const int np_m = (op.tile_start[m + 1] - op.tile_start[m]) >> 1;
+                    if (t < np_m * wm[m]) return base + (int)std::floor(t / wm[m] + 1e-9);
+                    t -= np_m * wm[m];
+                    base += np_m;
+                }
+                return base;
+            };
+            for (int b = 0; b < grid; ++b) {
+                const int c = b >> 1, r = b & 1;
+                const int p0 = pair_at(c), p1 = pair_at(c + 1), np = p1 - p0;
+                const int t0 = 2 * p0 + (r ? np : 0), t1 = r ? 2 * p1 : 2 * p0 + np;
+                out[(size_t)i * grid + b] = make_int2(t0, t1 | ((np & 1) ? (int)0x80000000u : 0));
+            }
+        } else {
+            for (int b = 0; b < grid; ++b)
+                out[(size_t)i * grid + b] = make_int2((int)(((int64_t)T * b) / grid), (int)(((int64_t)T * (b + 1)) / grid));
+        }
+    }
+}
+
+double stack_rec_r()
+{
+    static const double v = [] {
+        const char *e = getenv("MCAPQ_STEP_REC_R");
+        return e ? atof(e) : 0.6;
+    }();
+    return v;
+}
+
 int64_t stack_rec_min_k()
 {
     static const int64_t v = [] {
@@ -910,8 +969,8 @@ bool stack_clustered()
     return v != 0;
 }
 
-cudaError_t launch_stack_step(const void *ops_dev, int nops, unsigned int *counters_dev, int64_t max_k,
-                              bool clustered, int route_kinds, cudaStream_t s)
+cudaError_t launch_stack_step(const void *ops_dev, const void *part_dev, int nops, unsigned int *counters_dev,
+                              int64_t max_k, bool clustered, int route_kinds, cudaStream_t s)
 {
     for (const void *f : {reinterpret_cast<const void *>(stack_step<false, 2>),
                           reinterpret_cast<const void *>(stack_step<true, 2>),
@@ -940,12 +999,15 @@ cudaError_t launch_stack_step(const void *ops_dev, int nops, unsigned int *count
                                                                                            : act_bytes(DP4A, max_k, 1),
                                 128);
     const size_t budget = (size_t)tune().step_smem_kb * 1024;
-    const size_t prog = round_up(sizeof(StackOp) * (size_t)nops, 128);
+    const size_t prog_ops = round_up(sizeof(StackOp) * (size_t)nops, 16);
+    const size_t prog = round_up(prog_ops + sizeof(int2) * (size_t)nops, 128);   // ops + this CTA's ranges
     int S = (int)(((long)budget - 1024 - (long)kBarBytes - (long)prog - (long)act - kRedBytes) / kStageBytes);
     S = S < 2 ? 2 : (S > kMaxStages ? kMaxStages : S);
     S = S > 13 ? 13 : S;   // the step's barrier area: 16 S + 288 bytes <= kBarBytes
     a.stages = S;
     a.ops_off = S * kStageBytes + kBarBytes;
+    a.part_off = (int)(a.ops_off + prog_ops);
+    a.part = reinterpret_cast<const int2 *>(part_dev);
     a.act_off = (int)(a.ops_off + prog);
     a.red_off = (int)(a.act_off + act);
     const size_t smem = 1024 + (size_t)a.red_off + kRedBytes;

@@ -46,6 +46,7 @@ struct mcapq_stack {
     void *ops_dev = nullptr, *ops_host = nullptr;
     unsigned int *counters = nullptr;   // [nops] + exit count + epoch
     CUtensorMap *descs = nullptr;       // [nops][kMaxGroup][2] TMA descriptors the ops point at
+    int2 *part = nullptr;               // [nops][grid] tile ranges per CTA (stack_partition)
     uint32_t *tags = nullptr;           // tagged copies of outputs consumed inside the step
     int nops = 0;
     int64_t max_k = 0;
@@ -63,6 +64,8 @@ static void free_program(mcapq_stack *st)
     if (st->tags) cudaFree(st->tags);
     if (st->descs) cudaFree(st->descs);
     st->descs = nullptr;
+    if (st->part) cudaFree(st->part);
+    st->part = nullptr;
     st->ops_dev = st->ops_host = nullptr;
     st->counters = nullptr;
     st->tags = nullptr;
@@ -352,6 +355,14 @@ static mcapq_status build_program(mcapq_stack *st)
     }
     MCAPQ_CUDA_TRY(cudaMemcpy(st->descs, hmaps.data(), nmaps * sizeof(CUtensorMap), cudaMemcpyHostToDevice));
     MCAPQ_CUDA_TRY(cudaMemcpy(st->ops_dev, st->ops_host, ob * nops, cudaMemcpyHostToDevice));
+    // every CTA's tile range per op, for the grid and cluster shape launch_stack_step uses
+    {
+        const int grid = device_sms();
+        std::vector<int2> part((size_t)nops * grid);
+        stack_partition(st->ops_host, nops, grid, st->has_records && stack_clustered(), stack_rec_r(), part.data());
+        MCAPQ_CUDA_TRY(cudaMalloc(&st->part, part.size() * sizeof(int2)));
+        MCAPQ_CUDA_TRY(cudaMemcpy(st->part, part.data(), part.size() * sizeof(int2), cudaMemcpyHostToDevice));
+    }
     st->prog_ok = true;
     return MCAPQ_OK;
 }
@@ -373,7 +384,7 @@ mcapq_status mcapq_stack_run(mcapq_stack *st, int64_t m, void *stream)
     }
     if (m == 1 && !st->prog_dirty && st->prog_ok) {
         // the whole step in one persistent cooperative kernel
-        cudaError_t e = launch_stack_step(st->ops_dev, st->nops, st->counters, st->max_k, st->has_records,
+        cudaError_t e = launch_stack_step(st->ops_dev, st->part, st->nops, st->counters, st->max_k, st->has_records,
                                           st->route_kinds, s);
         MCAPQ_REQUIRE(e == cudaSuccess, MCAPQ_ECUDA, "stack_step launch: %s", cudaGetErrorString(e));
         return MCAPQ_OK;

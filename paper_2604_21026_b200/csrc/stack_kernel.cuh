@@ -71,6 +71,10 @@ struct StackArgs {
     int hold;                    // 1: the producer holds ring refills while this CTA stages an input (see `hold`)
     int clustered;               // launched as clusters of 2 CTAs: paired ops split their tiles per cluster
     int rec_spin;                // > 0: record consumers spin per thread (back-off cap, ns); 0: counter scheme
+    // [nops][gridDim] {t0, t1 | straddle << 31}: every CTA's tile range per op, computed on the
+    // host with the program (stack_partition) -- no partition arithmetic in the kernel
+    const int2 *part;
+    int part_off;                // shared-memory offset of this CTA's column of `part`
 };
 
 __device__ __forceinline__ unsigned int ld_acquire_gpu(const unsigned int *p)
@@ -612,6 +616,8 @@ __global__ void __launch_bounds__(kStepThreads, 1) stack_step(const __grid_const
         const int n16 = (int)(sizeof(StackOp) * a.nops / 16);
         for (int i = threadIdx.x; i < n16; i += blockDim.x) dst[i] = src[i];
     }
+    int2 *part_s = reinterpret_cast<int2 *>(smem_raw + (sb - smem_addr(smem_raw)) + a.part_off);
+    for (int i = threadIdx.x; i < a.nops; i += blockDim.x) part_s[i] = a.part[(size_t)i * gridDim.x + blockIdx.x];
     __syncthreads();
     if (a.clustered) cluster_sync_all();   // the peer's exchange barriers are initialised
 
@@ -620,22 +626,12 @@ __global__ void __launch_bounds__(kStepThreads, 1) stack_step(const __grid_const
     // CTAs, so a quantisation group (two tiles) lies in one CTA or, at most once per op,
     // straddles the cluster's two CTAs (`straddle`: rank 0's last tile is its first
     // half, rank 1's first tile its second half).  Otherwise contiguous balanced ranges.
-    auto cta_tiles = [&](const StackOp &op, int &t0, int &t1, bool &straddle) {
-        const int T = op.tile_start[op.count];
-        straddle = false;
-        if (a.clustered && op.paired) {
-            const uint32_t C = gridDim.x >> 1, c = blockIdx.x >> 1, r = blockIdx.x & 1u;
-            const int P = T >> 1;
-            const int p0 = (int)(((uint32_t)P * c) / C), p1 = (int)(((uint32_t)P * (c + 1)) / C);
-            const int np = p1 - p0;
-            t0 = 2 * p0 + (r ? np : 0);
-            t1 = r ? 2 * p1 : 2 * p0 + np;
-            straddle = (np & 1) != 0;
-            return;
-        }
-        // 32-bit: T * gridDim < 2^32 (T <= 2^20 tiles, checked by the program builder)
-        t0 = (int)(((uint32_t)T * blockIdx.x) / gridDim.x);
-        t1 = (int)(((uint32_t)T * (blockIdx.x + 1)) / gridDim.x);
+    // (the ranges come from the host's partition table, see StackArgs::part / stack_partition)
+    auto cta_tiles = [&](int i, int &t0, int &t1, bool &straddle) {
+        const int2 v = part_s[i];
+        t0 = v.x;
+        t1 = v.y & 0x7fffffff;
+        straddle = v.y < 0;
     };
     // The order a CTA works through its tiles (the producer's stages, the epilogue's
     // slots; the consumers just follow the ring): rank 0 of a straddling pair takes the
@@ -661,7 +657,7 @@ __global__ void __launch_bounds__(kStepThreads, 1) stack_step(const __grid_const
             const StackOp &op = ops[i];
             int t0, t1;
             bool straddle;
-            cta_tiles(op, t0, t1, straddle);
+            cta_tiles(i, t0, t1, straddle);
             if (op.wait_op >= 0 && t1 > t0) {
                 if (lane == 0) {
                     if (!nowait)
@@ -841,7 +837,7 @@ __global__ void __launch_bounds__(kStepThreads, 1) stack_step(const __grid_const
                 const int nchunks = (K2 + kChunkBytes - 1) / kChunkBytes;
                 int t0, t1;
                 bool straddle_;
-                cta_tiles(op, t0, t1, straddle_);
+                cta_tiles(i, t0, t1, straddle_);
                 if (!op.xt && !op.xq) {
                     // a step input: warm it in L2 (evict_last) while the weights stream
                     const int xlines = (int)((op.k * 2 + 127) / 128);
@@ -940,7 +936,7 @@ __global__ void __launch_bounds__(kStepThreads, 1) stack_step(const __grid_const
         const int nchunks = (K2 + kChunkBytes - 1) / kChunkBytes;
         int t0, t1;
         bool straddle_;
-        cta_tiles(op, t0, t1, straddle_);
+        cta_tiles(i, t0, t1, straddle_);
         unsigned long long tr0 = 0, tr1 = 0, tr2 = 0, tr3 = 0, tr4 = 0, trm = 0;
         unsigned int stalls = 0, nstages = 0;
         if (kTrace) tr0 = globaltimer();

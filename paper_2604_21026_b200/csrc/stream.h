@@ -105,8 +105,11 @@ bool stack_fill_op(void *host_op, int route, const StreamGroup &g, const uint16_
 // the epoch at [nops + 1]); max_k = the largest K of the program; clustered = the
 // program uses producer-quantised records (clusters of 2, requires stack_clustered());
 // route_kinds = bit 0 some W4A8 op, bit 1 some W4A16 op.
-cudaError_t launch_stack_step(const void *ops_dev, int nops, unsigned int *counters_dev, int64_t max_k,
-                              bool clustered, int route_kinds, cudaStream_t s);
+cudaError_t launch_stack_step(const void *ops_dev, const void *part_dev, int nops, unsigned int *counters_dev,
+                              int64_t max_k, bool clustered, int route_kinds, cudaStream_t s);
+// [nops][grid] int2 tile ranges of a step program (host; see kernels_stream.cu)
+void stack_partition(const void *ops_host, int nops, int grid, bool clustered, double rec_r, int2 *out);
+double stack_rec_r();
 
 // Encode the {nib, scale} tensor-map pair of a packed weight for the stream / step
 // kernels (host only; false if the driver entry point is missing or encoding fails).
