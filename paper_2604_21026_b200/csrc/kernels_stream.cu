@@ -875,12 +875,12 @@ bool stack_fill_op(void *host_op, int route, const StreamGroup &g, const uint16_
 
 // Every CTA's tile range per op of a step program: [nops][grid] {t0, t1 | straddle << 31}.
 // Paired ops of a clustered launch (producer-side records): 32-row pairs split over the
-// clusters -- by weight: a pair of a member whose epilogue also builds records weighs
-// 1 + rec_r 2048 / K (the record work is fixed per group, the tile's compute grows with
-// K; rec_r = 0.6, MCAPQ_STEP_REC_R), the others 1 -- and each cluster's range in halves over its two CTAs, so a
-// quantisation group lies in one CTA or, at most once per op, straddles the pair (the
-// straddle flag: rank 0's last tile is its first half, rank 1's first tile its second).
-// Otherwise contiguous balanced ranges.
+// clusters by weight -- a pair of a member whose epilogue also builds records weighs
+// 1 + rec_r 2048 / K (the record work is fixed per group while a tile's compute grows
+// with K; rec_r = 0.6, MCAPQ_STEP_REC_R), the others 1 -- and each cluster's range in
+// halves over its two CTAs, so a quantisation group lies in one CTA or, at most once per
+// op, straddles the pair (the straddle flag: rank 0's last tile is its first half, rank
+// 1's first tile its second).  Otherwise contiguous balanced ranges.
 void stack_partition(const void *ops_host, int nops, int grid, bool clustered, double rec_r, int2 *out)
 {
     const StackOp *ops = reinterpret_cast<const StackOp *>(ops_host);
