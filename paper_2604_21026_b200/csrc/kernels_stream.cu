@@ -877,7 +877,7 @@ bool stack_fill_op(void *host_op, int route, const StreamGroup &g, const uint16_
 // Paired ops of a clustered launch (producer-side records): 32-row pairs split over the
 // clusters by weight -- a pair of a member whose epilogue also builds records weighs
 // 1 + rec_r 2048 / K (the record work is fixed per group while a tile's compute grows
-// with K; rec_r = 0.6, MCAPQ_STEP_REC_R), the others 1 -- and each cluster's range in
+// with K; rec_r = 0.75, MCAPQ_STEP_REC_R), the others 1 -- and each cluster's range in
 // halves over its two CTAs, so a quantisation group lies in one CTA or, at most once per
 // op, straddles the pair (the straddle flag: rank 0's last tile is its first half, rank
 // 1's first tile its second).  Otherwise contiguous balanced ranges.
@@ -925,7 +925,7 @@ double stack_rec_r()
 {
     static const double v = [] {
         const char *e = getenv("MCAPQ_STEP_REC_R");
-        return e ? atof(e) : 0.6;
+        return e ? atof(e) : 0.75;
     }();
     return v;
 }
