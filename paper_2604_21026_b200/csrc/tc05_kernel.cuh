@@ -81,7 +81,7 @@ __device__ __forceinline__ void mma4_bf16_elect(uint32_t d, uint64_t ad, uint64_
         "l"(ad), "l"(bd), "r"(id), "r"(acc0)
         : "memory");
 }
-__device__ __forceinline__ void commit_elect16(uint32_t bar)
+__device__ __forceinline__ void commit_elect(uint32_t bar)
 {
     asm volatile(
         "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
@@ -238,19 +238,19 @@ __global__ void __launch_bounds__(tc05::kThreads, 1) tc05_w4a16(const __grid_con
                         const uint32_t xa = xs + (uint32_t)at * (uint32_t)MP * 128u;
                         // K16 steps of the atom: 32 B apart
                         mma4_bf16_elect(d, smem_desc(aa), smem_desc(xa), id, (sl | at) != 0 ? 1u : 0u);
-                        commit_elect16(aempty + 8u * sa);
+                        commit_elect(aempty + 8u * sa);
                         if (++sa == kNA) {
                             sa = 0;
                             pha ^= 1u;
                         }
                     }
-                    commit_elect16(sempty + 8u * s);
+                    commit_elect(sempty + 8u * s);
                     if (++s == S) {
                         s = 0;
                         ph ^= 1u;
                     }
                 }
-                commit_elect16(dfull + 8u * bf);
+                commit_elect(dfull + 8u * bf);
                 if (++bf == kNB) {
                     bf = 0;
                     phb ^= 1u;
@@ -579,16 +579,6 @@ __device__ __forceinline__ constexpr uint32_t idesc_i8()
 {
     return (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(MP >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
 }
-// issued by the whole (converged) warp: one elected lane executes the MMA / commit, so the
-// warp-uniform descriptors live in uniform registers (no per-MMA R2UR chain)
-__device__ __forceinline__ void mma_i8_elect(uint32_t dtmem, uint64_t adesc, uint64_t bdesc, uint32_t id)
-{
-    asm volatile(
-        "{\n\t.reg .pred p, e;\n\tsetp.ne.b32 p, 0, 0;\n\telect.sync _|e, 0xffffffff;\n\t"
-        "@e tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(dtmem),
-        "l"(adesc), "l"(bdesc), "r"(id)
-        : "memory");
-}
 // the four blocks of one 128-K atom: descriptors advanced 32 B (2 units) per block, the
 // accumulators MP columns apart, issued in one block of PTX by one elected lane
 template <int MP>
@@ -607,20 +597,6 @@ __device__ __forceinline__ void mma4_i8_elect(uint32_t dq, uint64_t ad, uint64_t
         "@e tcgen05.mma.cta_group::1.kind::i8 [d3], a3, b3, %3, p;\n\t}" ::"r"(dq),
         "l"(ad), "l"(bd), "r"(id), "n"(MP), "n"(2 * MP), "n"(3 * MP)
         : "memory");
-}
-__device__ __forceinline__ void commit_elect(uint32_t bar)
-{
-    asm volatile(
-        "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
-        "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(bar)
-        : "memory");
-}
-// four nibble codes c (bytes of v4 & 0x0F0F0F0F) -> four s8 (c - 8): c ^ 8 is c - 8 for
-// c >= 8 and c + 8 (bit 3 set) for c < 8, where the byte needs 0xF0 ORed in (sign)
-__device__ __forceinline__ uint32_t s8_codes(uint32_t v4)
-{
-    const uint32_t v = (v4 & 0x0F0F0F0Fu) ^ 0x08080808u;
-    return v | ((v & 0x08080808u) * 30u);   // 0x08 * 30 = 0xF0 per byte, no carries
 }
 template <int X>
 __device__ __forceinline__ void tmem_ld_x(uint32_t taddr, uint32_t *r)
