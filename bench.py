@@ -563,6 +563,10 @@ def time_single_linears(mq, dev, stream):
             tc = m >= 9 and (mode == "2" or (mode == "1" and m > 32 and (n + 127) // 128 >= mq.device_sms()))
             row["w4a8_kernel"] = ("tc05_w4a8 (tcgen05 kind::i8, TMEM read-back per block)" if tc
                                   else ("stream_linear<IMMA>" if m <= 8 else "gemm_w4<A8> (mma.sync IMMA)"))
+            mode16 = os.environ.get("MCAPQ_GEMM_A16_TC05", "1")
+            tc16 = m >= 9 and (mode16 == "2" or (mode16 == "1" and (n + 127) // 128 >= mq.device_sms()))
+            row["w4a16_kernel"] = ("tc05_w4a16x (tcgen05 kind::f16, exact per-block read-back)" if tc16
+                                   else ("stream_linear<HMMA>" if m <= 8 else "gemm_w4<A16> (mma.sync HMMA)"))
         out.append(row)
         del ws, pw0s
         torch.cuda.empty_cache()

@@ -170,7 +170,9 @@ mcapq_status mcapq_w4a8_x(const uint8_t *nib, const uint16_t *scale, int64_t n, 
  * Each term is exact in fp32; the inner per-group sums run on bf16 tensor cores
  * (c - 8 is exact in bf16) with fp32 accumulation, the scale d is applied per
  * group in fp32.  x: [m][ldx] bf16.  y: out [m][ldy].  m >= 9 with K % 256 == 0
- * runs the batched kernel (row a6: one weight pass per 64 tokens, HMMA on c - 8).
+ * runs the batched kernel (row a6: one weight pass per 64 tokens; mma.sync HMMA on
+ * c - 8, or -- with at least one 128-row tile per SM -- tcgen05 kind::f16 with one
+ * TMEM accumulator per Q4_0 block, the same semantics within reading T).
  */
 mcapq_status mcapq_w4a16(const uint8_t *nib, const uint16_t *scale, int64_t n, int64_t k, const uint16_t *x,
                          int64_t m, int64_t ldx, void *y, int ydt, int64_t ldy, void *stream);

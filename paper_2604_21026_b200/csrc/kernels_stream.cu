@@ -369,7 +369,7 @@ struct Tune {
     // per-SM queue of in-flight weight data that the chain's L2 accesses wait behind
     int smem_kb = 112, max_stages = 12, nocompute = 0, pdl = 0, trace = 0, step_smem_kb = 200, step = 1,
         step_flags = 0, step_spin_ns = 16, step_polls = 1, ctas_per_sm = 0, step_ep_log2 = 1, smem_kb_env = 0,
-        step_hold = 2, step_rec_spin = 64, a8_tc05 = 1;
+        step_hold = 2, step_rec_spin = 64, a8_tc05 = 1, a16_tc05 = 1;
 };
 const Tune &tune()
 {
@@ -393,6 +393,7 @@ const Tune &tune()
         if (const char *e = getenv("MCAPQ_STEP_HOLD")) v.step_hold = atoi(e);
         if (const char *e = getenv("MCAPQ_STEP_REC_SPIN")) v.step_rec_spin = atoi(e);
         if (const char *e = getenv("MCAPQ_GEMM_A8_TC05")) v.a8_tc05 = atoi(e);
+        if (const char *e = getenv("MCAPQ_GEMM_A16_TC05")) v.a16_tc05 = atoi(e);
         if (v.step_ep_log2 < 1) v.step_ep_log2 = 1;
         if (v.step_ep_log2 > 3) v.step_ep_log2 = 3;
         if (v.ctas_per_sm < 0 || v.ctas_per_sm > 2) v.ctas_per_sm = 0;
@@ -730,6 +731,58 @@ cudaError_t launch_tc05_a8(const uint8_t *nib, const uint16_t *scale, int64_t n,
     return cudaSuccess;
 }
 
+namespace {
+template <int MP>
+cudaError_t launch_tc05_a16x_mp(GemmArgs &a, size_t smem, int grid, cudaStream_t s, bool pdl)
+{
+    cudaError_t e = kernel_smem_attr(reinterpret_cast<const void *>(tc05_w4a16x<MP>), 227 * 1024);
+    if (e != cudaSuccess) return e;
+    return launch_pdl(tc05_w4a16x<MP>, dim3(grid), dim3(tc05::kXThreads<MP>), smem, s, pdl, a);
+}
+}  // namespace
+
+// tc05_w4a16x (exact W4A16 on tcgen05, one accumulator per Q4_0 block): 128-row CTA tiles,
+// passes of <= 64 tokens; K % 256 == 0.
+cudaError_t launch_tc05_a16x(const uint8_t *nib, const uint16_t *scale, int64_t n, int64_t k, const uint16_t *x,
+                             int64_t ldx, int64_t m, void *y, int ydt, int64_t ldy, cudaStream_t s, bool pdl)
+{
+    const int sms = device_sms();
+    for (int64_t tok0 = 0; tok0 < m; tok0 += 64) {
+        const int ntok = (int)((m - tok0) < 64 ? (m - tok0) : 64);
+        const int mp = ntok <= 16 ? 16 : (ntok <= 32 ? 32 : 64);
+        GemmArgs a;
+        memset(&a, 0, sizeof(a));
+        if (!encode_gemm_maps(&a.maps[0], &a.maps[1], nib, scale, n, k, 128) ||
+            !encode_gemm_act_maps(a.amaps, false, x, nullptr, nullptr, m, k, ldx, mp))
+            return cudaErrorInvalidValue;
+        a.y = y;
+        a.ldy = ldy;
+        a.n = n;
+        a.k = k;
+        a.ydt = ydt;
+        a.tok0 = tok0;
+        a.ntok = ntok;
+        a.mp = mp;
+        a.bn = 128;
+        a.row_tiles = (int)((n + 127) / 128);
+        a.stage_bytes = tc05::kNibBytes + tc05::kScBytes + (uint32_t)mp * 512u;
+        const size_t fixed = 1024 + (size_t)tc05::kNA * tc05::kAtomBytes + (size_t)tc05::kXNE * 2048 +
+                             (mp == 16 ? 128 * (size_t)mp * 4 : 0) + 1024;
+        int S = (int)((227 * 1024 - fixed) / a.stage_bytes);
+        S = S > 8 ? 8 : S;
+        if (S < 2) return cudaErrorInvalidValue;
+        a.stages = S;
+        const size_t smem = fixed + (size_t)S * a.stage_bytes;
+        const int grid = a.row_tiles < sms ? a.row_tiles : sms;
+        cudaError_t e = mp == 16 ? launch_tc05_a16x_mp<16>(a, smem, grid, s, pdl)
+                                 : (mp == 32 ? launch_tc05_a16x_mp<32>(a, smem, grid, s, pdl)
+                                             : launch_tc05_a16x_mp<64>(a, smem, grid, s, pdl));
+        if (e != cudaSuccess) return e;
+        pdl = true;
+    }
+    return cudaSuccess;
+}
+
 cudaError_t launch_gemm(int route, const uint8_t *nib, const uint16_t *scale, int64_t n, int64_t k, const uint16_t *x,
                         int64_t ldx, const int8_t *q, const float *sx, const int32_t *sq, int64_t m, void *y, int ydt,
                         int64_t ldy, cudaStream_t s, bool pdl)
@@ -743,6 +796,11 @@ cudaError_t launch_gemm(int route, const uint8_t *nib, const uint16_t *scale, in
     // (default), 2 always.
     if (a8 && (tune().a8_tc05 == 2 || (tune().a8_tc05 == 1 && m > 32 && (n + 127) / 128 >= device_sms())))
         return launch_tc05_a8(nib, scale, n, k, q, sx, sq, m, y, ydt, ldy, s, pdl);
+    // exact W4A16 on tcgen05 (tc05_w4a16x) over at least one 128-row tile per SM: the 8B
+    // lm_head M = 64 250 -> 140 us, M = 16 135 -> 112 us (narrower linears stay on mma.sync:
+    // the 3B q / up at 24 / 64 tiles).  MCAPQ_GEMM_A16_TC05: 0 never, 1 auto, 2 always.
+    if (!a8 && (tune().a16_tc05 == 2 || (tune().a16_tc05 == 1 && (n + 127) / 128 >= device_sms())))
+        return launch_tc05_a16x(nib, scale, n, k, x, ldx, m, y, ydt, ldy, s, pdl);
     const int sms = device_sms();
     for (int64_t tok0 = 0; tok0 < m; tok0 += 64) {
         const int ntok = (int)((m - tok0) < 64 ? (m - tok0) : 64);

@@ -938,3 +938,338 @@ __global__ void __launch_bounds__(tc05::kA8Threads<MP>, 1) tc05_w4a8(const __gri
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tbase), "r"(kCols) : "memory");
     }
 }
+
+// ============================================================================ a6 exact on tcgen05
+// tc05_w4a16x<MP>: batched W4A16 with the EXACT per-block semantics of mcapq_w4a16 (reading
+// A13: y = sum_g d_g sum_{k in g} (c - 8) x_k, fp32 accumulate; oracle_w4a16) on tcgen05: the
+// dequantise warps write the exact bf16 codes (c - 8) (one bf16x2 FMA per pair from the
+// 128 + c magic), one kind::f16 accumulator per Q4_0 block (two K16 MMAs: D = sum (c - 8) x,
+// exact products, fp32 sums), and the epilogue warps read each block's D once and fold it
+// into acc += d * D on the f32x2 pipe (0.5 instructions per output element -- a quarter of
+// the W4A8 read-back's work: the accumulator is already fp32 and there is no per-token
+// scale).  The operand pipeline is tc05_w4a16's (TMA nibble / scale / x boxes, 64-K A atoms),
+// the accumulator management tc05_w4a8's (quads of 4 block accumulators, warp-wide elected
+// MMA issue, epilogue warps of 16 tokens, an E ring for the row scales).
+namespace tc05 {
+template <int MP> constexpr int kXSets = MP == 16 ? 2 : 1;
+template <int MP> constexpr int kXEpi = MP / 4 * kXSets<MP>;
+template <int MP> constexpr int kXThreads = (2 + kDqWarps + kXEpi<MP>) * 32;
+constexpr int kXNE = 4;                           // E-ring slices (row scales)
+// exact codes: bf16x2 (128 + c) -> (c - 8), one FMA (exact)
+__device__ __forceinline__ uint32_t cm8_pair(uint32_t m)
+{
+    const uint32_t one = 0x3F803F80u, m136 = 0xC308C308u;
+    uint32_t r;
+    asm("fma.rn.bf16x2 %0, %1, %2, %3;" : "=r"(r) : "r"(m), "r"(one), "r"(m136));
+    return r;
+}
+__device__ __forceinline__ void cm4(uint32_t w, uint32_t &lo01, uint32_t &lo23, uint32_t &hi01, uint32_t &hi23)
+{
+    const uint32_t l = w & 0x0F0F0F0Fu, h = (w >> 4) & 0x0F0F0F0Fu;
+    lo01 = cm8_pair(__byte_perm(l, 0x43u, 0x4140));
+    lo23 = cm8_pair(__byte_perm(l, 0x43u, 0x4342));
+    hi01 = cm8_pair(__byte_perm(h, 0x43u, 0x4140));
+    hi23 = cm8_pair(__byte_perm(h, 0x43u, 0x4342));
+}
+// one 64-K atom = two Q4_0 blocks: K16 steps 0, 1 into accumulator d0 (block 0), 2, 3 into d1
+__device__ __forceinline__ void mma4_bf16_2acc_elect(uint32_t d0, uint32_t d1, uint64_t ad, uint64_t bd, uint32_t id)
+{
+    asm volatile(
+        "{\n\t.reg .pred p, q, e;\n\t.reg .b64 a1, a2, a3, b1, b2, b3;\n\t"
+        "setp.ne.b32 p, 0, 0;\n\tsetp.eq.b32 q, 0, 0;\n\t"
+        "add.s64 a1, %2, 2;\n\tadd.s64 a2, %2, 4;\n\tadd.s64 a3, %2, 6;\n\t"
+        "add.s64 b1, %3, 2;\n\tadd.s64 b2, %3, 4;\n\tadd.s64 b3, %3, 6;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %2, %3, %4, p;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a1, b1, %4, q;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%1], a2, b2, %4, p;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%1], a3, b3, %4, q;\n\t}" ::"r"(d0),
+        "r"(d1), "l"(ad), "l"(bd), "r"(id)
+        : "memory");
+}
+}  // namespace tc05
+
+template <int MP>
+__global__ void __launch_bounds__(tc05::kXThreads<MP>, 1) tc05_w4a16x(const __grid_constant__ GemmArgs a)
+{
+    using namespace tc05;
+    constexpr int TOK = 16;
+    constexpr int kEpi = kXEpi<MP>, kSets = kXSets<MP>;
+    constexpr int NB = (512 / MP) > 32 ? 32 : (512 / MP);   // block accumulators (a multiple of 4)
+    constexpr int NQ = NB / 4;
+    extern __shared__ __align__(16) uint8_t smem_raw[];
+    const uint32_t sb = (smem_addr(smem_raw) + 1023u) & ~1023u;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int S = a.stages;
+    const int G8 = (int)(a.k / 256);
+    const uint32_t stage_bytes = a.stage_bytes;
+    const uint32_t ring = sb;
+    const uint32_t aring = sb + (uint32_t)S * stage_bytes;
+    const uint32_t ering = aring + (uint32_t)kNA * kAtomBytes;          // [kXNE][128 rows][8 fp16]
+    const uint32_t xch = ering + (uint32_t)kXNE * 2048u;                // [128][MP] fp32 (kSets == 2)
+    const uint32_t bars = xch + (kSets == 2 ? 128u * (uint32_t)MP * 4u : 0u);
+    const uint32_t sfull = bars, sempty = bars + 8u * S;
+    const uint32_t afull = sempty + 8u * S, aempty = afull + 8u * kNA;
+    const uint32_t dfull = aempty + 8u * kNA, dempty = dfull + 8u * NQ;
+    const uint32_t efull = dempty + 8u * NQ, eempty = efull + 8u * kXNE;
+    const uint32_t tslot = eempty + 8u * kXNE;
+    constexpr uint32_t kCols = (NB * MP) < 32 ? 32 : (NB * MP);
+
+    const int T = a.row_tiles;
+    const int t0 = (int)(((uint32_t)T * blockIdx.x) / gridDim.x);
+    const int t1 = (int)(((uint32_t)T * (blockIdx.x + 1)) / gridDim.x);
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < S; ++s) {
+            mbar_init(sfull + 8u * s, 1);
+            mbar_init(sempty + 8u * s, 1 + kDqWarps);   // MMA commit (x read) + the dequantise warps
+        }
+        for (int s = 0; s < kNA; ++s) {
+            mbar_init(afull + 8u * s, kDqWarps);
+            mbar_init(aempty + 8u * s, 1);
+        }
+        for (int s = 0; s < NQ; ++s) {
+            mbar_init(dfull + 8u * s, 1);
+            mbar_init(dempty + 8u * s, kEpi / kSets);
+        }
+        for (int e = 0; e < kXNE; ++e) {
+            mbar_init(efull + 8u * e, 4);   // the dequantise warps of half bb = 0
+            mbar_init(eempty + 8u * e, kEpi);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(tslot), "r"(kCols)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    dev::griddep_launch();
+    fence_before();
+    __syncthreads();
+    fence_after();
+    const uint32_t tbase = lds32(tslot);
+    dev::griddep_wait();
+
+    if (warp == 0) {
+        // ================= TMA producer (tc05_w4a16's boxes) =================
+        if (lane == 0) {
+            const uint64_t pol = evict_first_policy();
+            int s = 0;
+            uint32_t ph = 0;
+            const uint32_t tx = kNibBytes + kScBytes + (uint32_t)MP * 512u;
+            for (int rt = t0; rt < t1; ++rt) {
+                const int row0 = rt * 128;
+                for (int sl = 0; sl < G8; ++sl) {
+                    mbar_wait(sempty + 8u * s, ph ^ 1u);
+                    const uint32_t st = ring + (uint32_t)s * stage_bytes;
+                    const uint32_t fb = sfull + 8u * s;
+                    mbar_expect_tx(fb, tx);
+                    tma_2d(st, a.maps, sl * 128, row0, fb, pol);
+                    tma_2d(st + kNibBytes, a.maps + 1, sl * 8, row0, fb, pol);
+                    tma_3d(st + kNibBytes + kScBytes, a.amaps, 0, (int)a.tok0, sl * 4, fb, 0);
+                    if (++s == S) {
+                        s = 0;
+                        ph ^= 1u;
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ================= MMA issuer: per atom two blocks, one accumulator each =================
+        {
+            constexpr uint32_t id = idesc<MP>();
+            int s = 0, sa = 0, qb = 0;
+            uint32_t ph = 0, pha = 0, phq = 0;
+            for (int rt = t0; rt < t1; ++rt) {
+                for (int sl = 0; sl < G8; ++sl) {
+                    mbar_wait(sfull + 8u * s, ph);
+                    const uint32_t xs = ring + (uint32_t)s * stage_bytes + kNibBytes + kScBytes;
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {   // two quads (4 blocks = 2 atoms) per slice
+                        mbar_wait(dempty + 8u * qb, phq ^ 1u);
+                        fence_after();
+                        const uint32_t dq = tbase + (uint32_t)(qb * 4 * MP);
+#pragma unroll
+                        for (int j = 0; j < 2; ++j) {
+                            const int at = 2 * h + j;
+                            mbar_wait(afull + 8u * sa, pha);
+                            fence_after();
+                            mma4_bf16_2acc_elect(dq + (uint32_t)(2 * j * MP), dq + (uint32_t)((2 * j + 1) * MP),
+                                                 smem_desc(aring + (uint32_t)sa * kAtomBytes),
+                                                 smem_desc(xs + (uint32_t)at * (uint32_t)MP * 128u), id);
+                            commit_elect(aempty + 8u * sa);
+                            if (++sa == kNA) {
+                                sa = 0;
+                                pha ^= 1u;
+                            }
+                        }
+                        commit_elect(dfull + 8u * qb);
+                        if (++qb == NQ) {
+                            qb = 0;
+                            phq ^= 1u;
+                        }
+                    }
+                    commit_elect(sempty + 8u * s);
+                    if (++s == S) {
+                        s = 0;
+                        ph ^= 1u;
+                    }
+                }
+            }
+        }
+    } else if (warp < 2 + kDqWarps) {
+        // ================= dequantise to exact codes: thread = (row r, block bb of each atom) =================
+        const int tq = threadIdx.x - 64;
+        const int r = tq & 127, bb = tq >> 7;
+        const uint32_t sw = (uint32_t)(r & 7);
+        int s = 0, sa = 0, e = 0;
+        uint32_t ph = 0, pha = 0, phe = 0;
+        for (int rt = t0; rt < t1; ++rt) {
+            for (int sl = 0; sl < G8; ++sl) {
+                mbar_wait(sfull + 8u * s, ph);
+                const uint32_t st = ring + (uint32_t)s * stage_bytes;
+                if (bb == 0) {
+                    // the slice's row scales into E-ring slot e for the epilogue
+                    mbar_wait(eempty + 8u * e, phe ^ 1u);
+                    sts128(ering + (uint32_t)e * 2048u + (uint32_t)r * 16u, lds128(st + kNibBytes + (uint32_t)r * 16u));
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(efull + 8u * e);
+                }
+                if (++e == kXNE) {
+                    e = 0;
+                    phe ^= 1u;
+                }
+                for (int ap = 0; ap < 4; ap += 2) {
+#pragma unroll
+                    for (int j = 0; j < 2; ++j) {
+                        const int at = ap + j;
+                        const int blk = 2 * at + bb;
+                        const uint4 w = lds128(st + (uint32_t)r * 128u + (((uint32_t)blk ^ sw) << 4));
+                        uint32_t lo[8], hi[8];
+                        cm4(w.x, lo[0], lo[1], hi[0], hi[1]);
+                        cm4(w.y, lo[2], lo[3], hi[2], hi[3]);
+                        cm4(w.z, lo[4], lo[5], hi[4], hi[5]);
+                        cm4(w.w, lo[6], lo[7], hi[6], hi[7]);
+                        mbar_wait(aempty + 8u * (sa + j), pha ^ 1u);
+                        const uint32_t ar = aring + (uint32_t)(sa + j) * kAtomBytes + (uint32_t)r * 128u;
+                        const uint32_t c0 = 4u * (uint32_t)bb;
+                        asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(ar + (((c0 + 0) ^ sw) << 4)),
+                                     "r"(lo[0]), "r"(lo[1]), "r"(lo[2]), "r"(lo[3]) : "memory");
+                        asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(ar + (((c0 + 1) ^ sw) << 4)),
+                                     "r"(lo[4]), "r"(lo[5]), "r"(lo[6]), "r"(lo[7]) : "memory");
+                        asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(ar + (((c0 + 2) ^ sw) << 4)),
+                                     "r"(hi[0]), "r"(hi[1]), "r"(hi[2]), "r"(hi[3]) : "memory");
+                        asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(ar + (((c0 + 3) ^ sw) << 4)),
+                                     "r"(hi[4]), "r"(hi[5]), "r"(hi[6]), "r"(hi[7]) : "memory");
+                    }
+                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                    __syncwarp();
+                    if (lane == 0) {
+                        mbar_arrive(afull + 8u * sa);
+                        mbar_arrive(afull + 8u * (sa + 1));
+                    }
+                    sa += 2;
+                    if (sa == kNA) {
+                        sa = 0;
+                        pha ^= 1u;
+                    }
+                }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(sempty + 8u * s);
+                if (++s == S) {
+                    s = 0;
+                    ph ^= 1u;
+                }
+            }
+        }
+    } else {
+        // ================= epilogue: per block TMEM -> acc += d * D =================
+        const int ew = warp - 2 - kDqWarps;
+        const int quarter = warp & 3;
+        const int set = kSets == 2 ? ew / (kEpi / 2) : 0;
+        const int tq = (ew % (kEpi / kSets)) >> 2;
+        const int r = quarter * 32 + lane;
+        const uint32_t tl = tbase + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(tq * TOK);
+        int e = 0, qb = set;
+        uint32_t phe = 0, phq = 0;
+        for (int rt = t0; rt < t1; ++rt) {
+            f2_t acc[TOK / 2];
+#pragma unroll
+            for (int t = 0; t < TOK / 2; ++t) acc[t] = 0ull;
+            for (int sl = 0; sl < G8; ++sl) {
+                mbar_wait(efull + 8u * e, phe);
+                const uint4 scw = lds128(ering + (uint32_t)e * 2048u + (uint32_t)r * 16u);
+                const uint32_t sc[4] = {scw.x, scw.y, scw.z, scw.w};
+                uint32_t Da[TOK], Db[TOK];
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    if (kSets == 2 && h != set) continue;
+                    mbar_wait(dfull + 8u * qb, phq);
+                    fence_after();
+                    const uint32_t tq0 = tl + (uint32_t)(qb * 4 * MP);
+                    tmem_ld_x<TOK>(tq0, Da);
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        const int g = 4 * h + j;
+                        uint32_t *Dc = (j & 1) ? Db : Da;
+                        uint32_t *Dn = (j & 1) ? Da : Db;
+                        tmem_wait_ld();
+                        if (j < 3) {
+                            tmem_ld_x<TOK>(tq0 + (uint32_t)((j + 1) * MP), Dn);
+                        } else {
+                            fence_before();
+                            __syncwarp();
+                            if (lane == 0) mbar_arrive(dempty + 8u * qb);
+                            qb += kSets;
+                            if (qb >= NQ) {
+                                qb -= NQ;
+                                phq ^= 1u;
+                            }
+                        }
+                        const float d = h2f((uint16_t)((g & 1) ? (sc[g >> 1] >> 16) : (sc[g >> 1] & 0xffffu)));
+                        const f2_t d2 = f2_pack(d, d);
+#pragma unroll
+                        for (int t = 0; t < TOK; t += 2) acc[t / 2] = f2_fma(d2, f2_pack_bits(Dc[t], Dc[t + 1]), acc[t / 2]);
+                    }
+                }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(eempty + 8u * e);
+                if (++e == kXNE) {
+                    e = 0;
+                    phe ^= 1u;
+                }
+            }
+            if constexpr (kSets == 2) {
+                const uint32_t xr = xch + ((uint32_t)r * MP + (uint32_t)(tq * TOK)) * 4u;
+                if (set == 1)
+#pragma unroll
+                    for (int t = 0; t < TOK; t += 2) asm volatile("st.shared.v2.u32 [%0], {%1,%2};" ::"r"(xr + 4u * t),
+                                                               "r"((uint32_t)acc[t / 2]), "r"((uint32_t)(acc[t / 2] >> 32)) : "memory");
+                asm volatile("bar.sync 2, %0;" ::"n"(kEpi * 32) : "memory");
+                if (set == 1) continue;
+#pragma unroll
+                for (int t = 0; t < TOK; t += 2) {
+                    uint32_t lo, hi;
+                    asm volatile("ld.shared.v2.u32 {%0,%1}, [%2];" : "=r"(lo), "=r"(hi) : "r"(xr + 4u * t) : "memory");
+                    acc[t / 2] = f2_add(acc[t / 2], f2_pack_bits(lo, hi));
+                }
+            }
+            const int64_t row = (int64_t)rt * 128 + r;
+            if (row < a.n) {
+#pragma unroll
+                for (int t = 0; t < TOK; t += 2) {
+                    const float2 v = f2_unpack(acc[t / 2]);
+                    const int tt = tq * TOK + t;
+                    if (tt < a.ntok) dev::store_out(a.y, a.ydt, (a.tok0 + tt) * a.ldy + row, v.x);
+                    if (tt + 1 < a.ntok) dev::store_out(a.y, a.ydt, (a.tok0 + tt + 1) * a.ldy + row, v.y);
+                }
+            }
+        }
+    }
+    fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tbase), "r"(kCols) : "memory");
+    }
+}
