@@ -41,6 +41,7 @@ struct GemmArgs {
     int row_tiles;
     int stages;
     uint32_t nib_bytes, sc_off, act_off, ss_off, sq_off, stage_bytes;   // per-stage layout
+    int na;                    // tc05_w4a16x: A-atom ring slots (even)
 };
 
 // IMMA m16n8k32 with an explicit int32 accumulator init (C may repeat registers)

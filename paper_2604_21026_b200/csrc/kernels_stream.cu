@@ -732,12 +732,12 @@ cudaError_t launch_tc05_a8(const uint8_t *nib, const uint16_t *scale, int64_t n,
 }
 
 namespace {
-template <int MP>
+template <int MP, bool TS>
 cudaError_t launch_tc05_a16x_mp(GemmArgs &a, size_t smem, int grid, cudaStream_t s, bool pdl)
 {
-    cudaError_t e = kernel_smem_attr(reinterpret_cast<const void *>(tc05_w4a16x<MP>), 227 * 1024);
+    cudaError_t e = kernel_smem_attr(reinterpret_cast<const void *>(tc05_w4a16x<MP, TS>), 227 * 1024);
     if (e != cudaSuccess) return e;
-    return launch_pdl(tc05_w4a16x<MP>, dim3(grid), dim3(tc05::kXThreads<MP>), smem, s, pdl, a);
+    return launch_pdl(tc05_w4a16x<MP, TS>, dim3(grid), dim3(tc05::kXThreads<MP>), smem, s, pdl, a);
 }
 }  // namespace
 
@@ -765,18 +765,32 @@ cudaError_t launch_tc05_a16x(const uint8_t *nib, const uint16_t *scale, int64_t 
         a.mp = mp;
         a.bn = 128;
         a.row_tiles = (int)((n + 127) / 128);
+        static const int dbg = getenv("MCAPQ_TC05_DBG") ? atoi(getenv("MCAPQ_TC05_DBG")) : 0;
+        a.wt = dbg;   // debug flags (timing experiments only; outputs wrong when set)
         a.stage_bytes = tc05::kNibBytes + tc05::kScBytes + (uint32_t)mp * 512u;
-        const size_t fixed = 1024 + (size_t)tc05::kNA * tc05::kAtomBytes + (size_t)tc05::kXNE * 2048 +
+        static const int na_env = getenv("MCAPQ_TC05_NA") ? atoi(getenv("MCAPQ_TC05_NA")) : 0;
+        a.na = na_env >= 2 ? (na_env & ~1) : 4;   // A-atom ring slots (smem-A kernel; even)
+        // A operand from tensor memory (tcgen05.st by the dequantise warps, no shared-memory
+        // atoms): 8B lm_head M = 16 141 -> 128 us; at MP = 64 the 512 columns leave one
+        // accumulator quad and the smem-A kernel is faster (177 vs 185 us).
+        // MCAPQ_TC05_TS: 0 never, 1 always, default MP <= 32.
+        static const int ts_env = getenv("MCAPQ_TC05_TS") ? atoi(getenv("MCAPQ_TC05_TS")) : -1;
+        const bool ts = ts_env < 0 ? mp <= 32 : ts_env != 0;
+        const size_t fixed = 1024 + (ts ? 0 : (size_t)a.na * tc05::kAtomBytes) + (size_t)tc05::kXNE * 2048 +
                              (mp == 16 ? 128 * (size_t)mp * 4 : 0) + 1024;
         int S = (int)((227 * 1024 - fixed) / a.stage_bytes);
-        S = S > 8 ? 8 : S;
+        static const int scap = getenv("MCAPQ_TC05_STAGES") ? atoi(getenv("MCAPQ_TC05_STAGES")) : 8;
+        S = S > scap ? scap : S;
         if (S < 2) return cudaErrorInvalidValue;
         a.stages = S;
         const size_t smem = fixed + (size_t)S * a.stage_bytes;
         const int grid = a.row_tiles < sms ? a.row_tiles : sms;
-        cudaError_t e = mp == 16 ? launch_tc05_a16x_mp<16>(a, smem, grid, s, pdl)
-                                 : (mp == 32 ? launch_tc05_a16x_mp<32>(a, smem, grid, s, pdl)
-                                             : launch_tc05_a16x_mp<64>(a, smem, grid, s, pdl));
+        cudaError_t e = ts ? (mp == 16 ? launch_tc05_a16x_mp<16, true>(a, smem, grid, s, pdl)
+                                       : (mp == 32 ? launch_tc05_a16x_mp<32, true>(a, smem, grid, s, pdl)
+                                                   : launch_tc05_a16x_mp<64, true>(a, smem, grid, s, pdl)))
+                           : (mp == 16 ? launch_tc05_a16x_mp<16, false>(a, smem, grid, s, pdl)
+                                       : (mp == 32 ? launch_tc05_a16x_mp<32, false>(a, smem, grid, s, pdl)
+                                                   : launch_tc05_a16x_mp<64, false>(a, smem, grid, s, pdl)));
         if (e != cudaSuccess) return e;
         pdl = true;
     }

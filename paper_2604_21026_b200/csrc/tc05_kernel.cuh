@@ -987,33 +987,62 @@ __device__ __forceinline__ void mma4_bf16_2acc_elect(uint32_t d0, uint32_t d1, u
         "r"(d1), "l"(ad), "l"(bd), "r"(id)
         : "memory");
 }
+// the same two blocks with A read from tensor memory (ta = the atom's first column: row =
+// TMEM lane, K pairs packed bf16x2 per 32-bit column, 8 columns per K16 step)
+__device__ __forceinline__ void mma4_bf16_2acc_ts_elect(uint32_t d0, uint32_t d1, uint32_t ta, uint64_t bd, uint32_t id)
+{
+    asm volatile(
+        "{\n\t.reg .pred p, q, e;\n\t.reg .b32 a1, a2, a3;\n\t.reg .b64 b1, b2, b3;\n\t"
+        "setp.ne.b32 p, 0, 0;\n\tsetp.eq.b32 q, 0, 0;\n\t"
+        "add.u32 a1, %2, 8;\n\tadd.u32 a2, %2, 16;\n\tadd.u32 a3, %2, 24;\n\t"
+        "add.s64 b1, %3, 2;\n\tadd.s64 b2, %3, 4;\n\tadd.s64 b3, %3, 6;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%2], %3, %4, p;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a1], b1, %4, q;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%1], [a2], b2, %4, p;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%1], [a3], b3, %4, q;\n\t}" ::"r"(d0),
+        "r"(d1), "r"(ta), "l"(bd), "r"(id)
+        : "memory");
+}
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&lo)[8], const uint32_t (&hi)[8])
+{
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(
+                     taddr),
+                 "r"(lo[0]), "r"(lo[1]), "r"(lo[2]), "r"(lo[3]), "r"(lo[4]), "r"(lo[5]), "r"(lo[6]), "r"(lo[7]), "r"(hi[0]),
+                 "r"(hi[1]), "r"(hi[2]), "r"(hi[3]), "r"(hi[4]), "r"(hi[5]), "r"(hi[6]), "r"(hi[7])
+                 : "memory");
+}
+// A from TMEM: accumulator blocks and A atoms share the 512 columns
+template <int MP> constexpr int kXTsNB = MP == 16 ? 16 : (MP == 32 ? 8 : 4);
+constexpr int kXTsNA = 8;   // A atoms in TMEM (32 columns each)
 }  // namespace tc05
 
-template <int MP>
+template <int MP, bool TS>
 __global__ void __launch_bounds__(tc05::kXThreads<MP>, 1) tc05_w4a16x(const __grid_constant__ GemmArgs a)
 {
     using namespace tc05;
     constexpr int TOK = 16;
     constexpr int kEpi = kXEpi<MP>, kSets = kXSets<MP>;
-    constexpr int NB = (512 / MP) > 32 ? 32 : (512 / MP);   // block accumulators (a multiple of 4)
+    constexpr int NB = TS ? kXTsNB<MP> : ((512 / MP) > 32 ? 32 : (512 / MP));   // block accumulators (x4)
     constexpr int NQ = NB / 4;
     extern __shared__ __align__(16) uint8_t smem_raw[];
     const uint32_t sb = (smem_addr(smem_raw) + 1023u) & ~1023u;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int S = a.stages;
+    const int NA = TS ? kXTsNA : a.na;
     const int G8 = (int)(a.k / 256);
     const uint32_t stage_bytes = a.stage_bytes;
     const uint32_t ring = sb;
     const uint32_t aring = sb + (uint32_t)S * stage_bytes;
-    const uint32_t ering = aring + (uint32_t)kNA * kAtomBytes;          // [kXNE][128 rows][8 fp16]
+    const uint32_t ering = aring + (TS ? 0u : (uint32_t)NA * kAtomBytes);          // [kXNE][128 rows][8 fp16]
     const uint32_t xch = ering + (uint32_t)kXNE * 2048u;                // [128][MP] fp32 (kSets == 2)
     const uint32_t bars = xch + (kSets == 2 ? 128u * (uint32_t)MP * 4u : 0u);
     const uint32_t sfull = bars, sempty = bars + 8u * S;
-    const uint32_t afull = sempty + 8u * S, aempty = afull + 8u * kNA;
-    const uint32_t dfull = aempty + 8u * kNA, dempty = dfull + 8u * NQ;
+    const uint32_t afull = sempty + 8u * S, aempty = afull + 8u * NA;
+    const uint32_t dfull = aempty + 8u * NA, dempty = dfull + 8u * NQ;
     const uint32_t efull = dempty + 8u * NQ, eempty = efull + 8u * kXNE;
     const uint32_t tslot = eempty + 8u * kXNE;
-    constexpr uint32_t kCols = (NB * MP) < 32 ? 32 : (NB * MP);
+    constexpr uint32_t kCols = TS ? 512u : ((NB * MP) < 32 ? 32 : (NB * MP));
 
     const int T = a.row_tiles;
     const int t0 = (int)(((uint32_t)T * blockIdx.x) / gridDim.x);
@@ -1024,7 +1053,7 @@ __global__ void __launch_bounds__(tc05::kXThreads<MP>, 1) tc05_w4a16x(const __gr
             mbar_init(sfull + 8u * s, 1);
             mbar_init(sempty + 8u * s, 1 + kDqWarps);   // MMA commit (x read) + the dequantise warps
         }
-        for (int s = 0; s < kNA; ++s) {
+        for (int s = 0; s < NA; ++s) {
             mbar_init(afull + 8u * s, kDqWarps);
             mbar_init(aempty + 8u * s, 1);
         }
@@ -1048,6 +1077,7 @@ __global__ void __launch_bounds__(tc05::kXThreads<MP>, 1) tc05_w4a16x(const __gr
     __syncthreads();
     fence_after();
     const uint32_t tbase = lds32(tslot);
+    const uint32_t ta0 = tbase + (uint32_t)(NB * MP);   // TS: the A-atom ring's first column
     dev::griddep_wait();
 
     if (warp == 0) {
@@ -1084,6 +1114,14 @@ __global__ void __launch_bounds__(tc05::kXThreads<MP>, 1) tc05_w4a16x(const __gr
                 for (int sl = 0; sl < G8; ++sl) {
                     mbar_wait(sfull + 8u * s, ph);
                     const uint32_t xs = ring + (uint32_t)s * stage_bytes + kNibBytes + kScBytes;
+                    if (a.wt & 16) {   // debug (MCAPQ_TC05_DBG=16): the TMA stream alone
+                        commit_elect(sempty + 8u * s);
+                        if (++s == S) {
+                            s = 0;
+                            ph ^= 1u;
+                        }
+                        continue;
+                    }
 #pragma unroll
                     for (int h = 0; h < 2; ++h) {   // two quads (4 blocks = 2 atoms) per slice
                         mbar_wait(dempty + 8u * qb, phq ^ 1u);
@@ -1094,11 +1132,16 @@ __global__ void __launch_bounds__(tc05::kXThreads<MP>, 1) tc05_w4a16x(const __gr
                             const int at = 2 * h + j;
                             mbar_wait(afull + 8u * sa, pha);
                             fence_after();
-                            mma4_bf16_2acc_elect(dq + (uint32_t)(2 * j * MP), dq + (uint32_t)((2 * j + 1) * MP),
-                                                 smem_desc(aring + (uint32_t)sa * kAtomBytes),
-                                                 smem_desc(xs + (uint32_t)at * (uint32_t)MP * 128u), id);
-                            commit_elect(aempty + 8u * sa);
-                            if (++sa == kNA) {
+                            if constexpr (TS)
+                                mma4_bf16_2acc_ts_elect(dq + (uint32_t)(2 * j * MP), dq + (uint32_t)((2 * j + 1) * MP),
+                                                        ta0 + (uint32_t)sa * 32u,
+                                                        smem_desc(xs + (uint32_t)at * (uint32_t)MP * 128u), id);
+                            else if (!(a.wt & 8))   // debug (MCAPQ_TC05_DBG=8): no MMAs, commits only
+                                mma4_bf16_2acc_elect(dq + (uint32_t)(2 * j * MP), dq + (uint32_t)((2 * j + 1) * MP),
+                                                     smem_desc(aring + (uint32_t)sa * kAtomBytes),
+                                                     smem_desc(xs + (uint32_t)at * (uint32_t)MP * 128u), id);
+                            if (!(a.wt & 128)) commit_elect(aempty + 8u * sa);   // debug 128: atoms unprotected
+                            if (++sa == NA) {
                                 sa = 0;
                                 pha ^= 1u;
                             }
@@ -1120,7 +1163,8 @@ __global__ void __launch_bounds__(tc05::kXThreads<MP>, 1) tc05_w4a16x(const __gr
     } else if (warp < 2 + kDqWarps) {
         // ================= dequantise to exact codes: thread = (row r, block bb of each atom) =================
         const int tq = threadIdx.x - 64;
-        const int r = tq & 127, bb = tq >> 7;
+        // TS: a warp reaches only its TMEM lane quarter (warp % 4), so row = 32 (warp % 4) + lane
+        const int r = TS ? (((warp & 3) << 5) | lane) : (tq & 127), bb = TS ? ((warp - 2) >> 2) : (tq >> 7);
         const uint32_t sw = (uint32_t)(r & 7);
         int s = 0, sa = 0, e = 0;
         uint32_t ph = 0, pha = 0, phe = 0;
@@ -1128,7 +1172,16 @@ __global__ void __launch_bounds__(tc05::kXThreads<MP>, 1) tc05_w4a16x(const __gr
             for (int sl = 0; sl < G8; ++sl) {
                 mbar_wait(sfull + 8u * s, ph);
                 const uint32_t st = ring + (uint32_t)s * stage_bytes;
-                if (bb == 0) {
+                if (a.wt & 16) {   // debug: the TMA stream alone
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(sempty + 8u * s);
+                    if (++s == S) {
+                        s = 0;
+                        ph ^= 1u;
+                    }
+                    continue;
+                }
+                if (bb == 0 && !(a.wt & 64)) {   // debug 64: no E ring
                     // the slice's row scales into E-ring slot e for the epilogue
                     mbar_wait(eempty + 8u * e, phe ^ 1u);
                     sts128(ering + (uint32_t)e * 2048u + (uint32_t)r * 16u, lds128(st + kNibBytes + (uint32_t)r * 16u));
@@ -1146,11 +1199,22 @@ __global__ void __launch_bounds__(tc05::kXThreads<MP>, 1) tc05_w4a16x(const __gr
                         const int blk = 2 * at + bb;
                         const uint4 w = lds128(st + (uint32_t)r * 128u + (((uint32_t)blk ^ sw) << 4));
                         uint32_t lo[8], hi[8];
-                        cm4(w.x, lo[0], lo[1], hi[0], hi[1]);
-                        cm4(w.y, lo[2], lo[3], hi[2], hi[3]);
-                        cm4(w.z, lo[4], lo[5], hi[4], hi[5]);
-                        cm4(w.w, lo[6], lo[7], hi[6], hi[7]);
-                        mbar_wait(aempty + 8u * (sa + j), pha ^ 1u);
+                        if (a.wt & 1) {   // debug (MCAPQ_TC05_DBG=1): raw words, no conversion
+                            lo[0] = lo[2] = lo[4] = lo[6] = hi[0] = hi[2] = hi[4] = hi[6] = w.x;
+                            lo[1] = lo[3] = lo[5] = lo[7] = hi[1] = hi[3] = hi[5] = hi[7] = w.y;
+                        } else {
+                            cm4(w.x, lo[0], lo[1], hi[0], hi[1]);
+                            cm4(w.y, lo[2], lo[3], hi[2], hi[3]);
+                            cm4(w.z, lo[4], lo[5], hi[4], hi[5]);
+                            cm4(w.w, lo[6], lo[7], hi[6], hi[7]);
+                        }
+                        if (!(a.wt & 128)) mbar_wait(aempty + 8u * (sa + j), pha ^ 1u);
+                        if constexpr (TS) {
+                            fence_after();
+                            tmem_st16(ta0 + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)(sa + j) * 32u + 16u * (uint32_t)bb,
+                                      lo, hi);
+                            continue;
+                        }
                         const uint32_t ar = aring + (uint32_t)(sa + j) * kAtomBytes + (uint32_t)r * 128u;
                         const uint32_t c0 = 4u * (uint32_t)bb;
                         asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(ar + (((c0 + 0) ^ sw) << 4)),
@@ -1162,14 +1226,19 @@ __global__ void __launch_bounds__(tc05::kXThreads<MP>, 1) tc05_w4a16x(const __gr
                         asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(ar + (((c0 + 3) ^ sw) << 4)),
                                      "r"(hi[4]), "r"(hi[5]), "r"(hi[6]), "r"(hi[7]) : "memory");
                     }
-                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                    if constexpr (TS) {
+                        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+                        fence_before();
+                    } else if (!(a.wt & 32)) {   // debug 32: no proxy fence
+                        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                    }
                     __syncwarp();
                     if (lane == 0) {
                         mbar_arrive(afull + 8u * sa);
                         mbar_arrive(afull + 8u * (sa + 1));
                     }
                     sa += 2;
-                    if (sa == kNA) {
+                    if (sa == NA) {
                         sa = 0;
                         pha ^= 1u;
                     }
@@ -1192,12 +1261,12 @@ __global__ void __launch_bounds__(tc05::kXThreads<MP>, 1) tc05_w4a16x(const __gr
         const uint32_t tl = tbase + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(tq * TOK);
         int e = 0, qb = set;
         uint32_t phe = 0, phq = 0;
-        for (int rt = t0; rt < t1; ++rt) {
+        for (int rt = t0; rt < t1 && !(a.wt & 16); ++rt) {
             f2_t acc[TOK / 2];
 #pragma unroll
             for (int t = 0; t < TOK / 2; ++t) acc[t] = 0ull;
             for (int sl = 0; sl < G8; ++sl) {
-                mbar_wait(efull + 8u * e, phe);
+                if (!(a.wt & 64)) mbar_wait(efull + 8u * e, phe);
                 const uint4 scw = lds128(ering + (uint32_t)e * 2048u + (uint32_t)r * 16u);
                 const uint32_t sc[4] = {scw.x, scw.y, scw.z, scw.w};
                 uint32_t Da[TOK], Db[TOK];
@@ -1207,6 +1276,16 @@ __global__ void __launch_bounds__(tc05::kXThreads<MP>, 1) tc05_w4a16x(const __gr
                     mbar_wait(dfull + 8u * qb, phq);
                     fence_after();
                     const uint32_t tq0 = tl + (uint32_t)(qb * 4 * MP);
+                    if (a.wt & 4) {   // debug (MCAPQ_TC05_DBG=4): no TMEM read-back, no math
+                        __syncwarp();
+                        if (lane == 0) mbar_arrive(dempty + 8u * qb);
+                        qb += kSets;
+                        if (qb >= NQ) {
+                            qb -= NQ;
+                            phq ^= 1u;
+                        }
+                        continue;
+                    }
                     tmem_ld_x<TOK>(tq0, Da);
 #pragma unroll
                     for (int j = 0; j < 4; ++j) {
@@ -1226,6 +1305,7 @@ __global__ void __launch_bounds__(tc05::kXThreads<MP>, 1) tc05_w4a16x(const __gr
                                 phq ^= 1u;
                             }
                         }
+                        if (a.wt & 2) continue;   // debug (MCAPQ_TC05_DBG=2): no epilogue math
                         const float d = h2f((uint16_t)((g & 1) ? (sc[g >> 1] >> 16) : (sc[g >> 1] & 0xffffu)));
                         const f2_t d2 = f2_pack(d, d);
 #pragma unroll
