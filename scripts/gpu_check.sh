@@ -38,6 +38,11 @@ if [ "${NCU:-1}" = "1" ]; then
      -o $OUT/prof_gemm_a8 python scripts/kbench.py --cases lmhead_8b_m16 --routes 0 --reps 2 > $OUT/ncu_gemm_a8.log 2>&1
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:gemm_w4 -s 2 -c 1 \
      -o $OUT/prof_gemm_a16 python scripts/kbench.py --cases lmhead_8b_m64 --routes 1 --reps 2 > $OUT/ncu_gemm_a16.log 2>&1
+  # exact batched W4A16 on tcgen05 (tc05_w4a16x: A from TMEM at M = 16, from smem at M = 64)
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:tc05_w4a16x -s 2 -c 1 \
+     -o $OUT/prof_tc05x_m16 python scripts/kbench.py --cases lmhead_8b_m16 --routes 1 --reps 2 > $OUT/ncu_tc05x_m16.log 2>&1
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:tc05_w4a16x -s 2 -c 1 \
+     -o $OUT/prof_tc05x_m64 python scripts/kbench.py --cases lmhead_8b_m64 --routes 1 --reps 2 > $OUT/ncu_tc05x_m64.log 2>&1
   # batched W4A16 with bf16-dequantised weights on tcgen05 (8B lm_head, M = 64)
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:tc05 -s 2 -c 1 \
      -o $OUT/prof_tc05 python scripts/kbench.py --cases lmhead_8b_m64 --routes 2 --reps 2 > $OUT/ncu_tc05.log 2>&1
@@ -45,7 +50,7 @@ fi
 # summarise on the box (ncu -i needs no GPU) and keep only what fits the 64 MiB return:
 # the summaries, the source-level hot spots of the step kernels, and the 1B step report
 python scripts/ncu_summary.py $OUT $OUT/sum > $OUT/sum.log 2>&1
-for r in prof_step prof_step_mlp8b prof_step_mlp8b_a16 prof_w4a16 prof_tc05_a8; do
+for r in prof_step prof_step_mlp8b prof_step_mlp8b_a16 prof_w4a16 prof_tc05_a8 prof_tc05x_m16 prof_tc05x_m64; do
   [ -f $OUT/$r.ncu-rep ] && python scripts/ncu_source.py $OUT/$r.ncu-rep 40 > $OUT/sum/${r}_source.txt 2>&1
   [ -f $OUT/$r.ncu-rep ] && python scripts/ncu_stalls.py $OUT/$r.ncu-rep > $OUT/sum/${r}_stalls.txt 2>&1
 done
