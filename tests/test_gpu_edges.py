@@ -303,3 +303,21 @@ def test_rowshard_rejects_partial_groups(mq):
     pw = mq.pack_w4(si.weight(64, 96, 2950).to(DEV))
     with pytest.raises(mq.McapqError):
         pw.kshard(2, 0)
+
+
+# ---------------------------------------------------------------- wide batched linears (tcgen05 dispatch)
+@pytest.mark.parametrize("m", [9, 70])
+def test_wide_batched_default_dispatch_ragged(mq, orc, m):
+    """At least one 128-row tile per SM sends batched decode to the tcgen05 kernels by default
+    (kernels_stream.cu launch_gemm): W4A16 -> tc05_w4a16x (A operand in TMEM for passes of
+    <= 32 tokens, in shared memory at 64), W4A8 -> tc05_w4a8 for passes of > 32 tokens.  N is
+    148 tiles + a ragged 77 rows, M = 9 is one ragged 16-token pass, M = 70 a full 64-token
+    pass plus a 6-token one (tok0 = 64).  Whole output against the oracle (reading T)."""
+    n, k = 148 * 128 + 77, 512
+    w = si.weight(n, k, 4100 + m)
+    x = si.activation(m, k, 4101 + m)
+    pw, nib, sc = _pack_both(mq, orc, w)
+    xd = x.to(DEV)
+    for route in (0, 1):
+        y = mq.linear(route, pw, xd, out_dtype=torch.float32)
+        _assert_close(y, _oracle_y64(orc, route, nib, sc, x), 1e-3)

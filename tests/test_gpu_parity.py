@@ -420,7 +420,8 @@ def test_linear_host_e2e(mq, orc):
 
 # ---------------------------------------------------------------- full-size configs, sampled rows
 FULL = [("llama-3.1-8b", "gate", 1), ("llama-3.1-8b", "down", 1), ("llama-3.1-8b", "lm_head", 1),
-        ("llama-3.1-8b", "lm_head", 64), ("llama-3.2-3b", "up", 16), ("llama-3.2-3b", "q", 64)]
+        ("llama-3.1-8b", "lm_head", 16), ("llama-3.1-8b", "lm_head", 24), ("llama-3.1-8b", "lm_head", 64),
+        ("llama-3.2-3b", "up", 16), ("llama-3.2-3b", "q", 64)]
 
 
 @pytest.mark.parametrize("model,slot,m", FULL)
