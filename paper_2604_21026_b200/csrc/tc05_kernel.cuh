@@ -1132,11 +1132,13 @@ __global__ void __launch_bounds__(tc05::kXThreads<MP>, 1) tc05_w4a16x(const __gr
                             const int at = 2 * h + j;
                             mbar_wait(afull + 8u * sa, pha);
                             fence_after();
-                            if constexpr (TS)
+                            if (a.wt & 8) {
+                                // debug (MCAPQ_TC05_DBG=8): no MMAs, commits only
+                            } else if constexpr (TS)
                                 mma4_bf16_2acc_ts_elect(dq + (uint32_t)(2 * j * MP), dq + (uint32_t)((2 * j + 1) * MP),
                                                         ta0 + (uint32_t)sa * 32u,
                                                         smem_desc(xs + (uint32_t)at * (uint32_t)MP * 128u), id);
-                            else if (!(a.wt & 8))   // debug (MCAPQ_TC05_DBG=8): no MMAs, commits only
+                            else
                                 mma4_bf16_2acc_elect(dq + (uint32_t)(2 * j * MP), dq + (uint32_t)((2 * j + 1) * MP),
                                                      smem_desc(aring + (uint32_t)sa * kAtomBytes),
                                                      smem_desc(xs + (uint32_t)at * (uint32_t)MP * 128u), id);

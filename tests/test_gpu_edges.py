@@ -311,9 +311,9 @@ def test_wide_batched_default_dispatch_ragged(mq, orc, m):
     """At least one 128-row tile per SM sends batched decode to the tcgen05 kernels by default
     (kernels_stream.cu launch_gemm): W4A16 -> tc05_w4a16x (A operand in TMEM for passes of
     <= 32 tokens, in shared memory at 64), W4A8 -> tc05_w4a8 for passes of > 32 tokens.  N is
-    148 tiles + a ragged 77 rows, M = 9 is one ragged 16-token pass, M = 70 a full 64-token
+    148 tiles + a ragged 72 rows, M = 9 is one ragged 16-token pass, M = 70 a full 64-token
     pass plus a 6-token one (tok0 = 64).  Whole output against the oracle (reading T)."""
-    n, k = 148 * 128 + 77, 512
+    n, k = 148 * 128 + 72, 512             # ragged against the 128-row tile, ldy % 8 == 0
     w = si.weight(n, k, 4100 + m)
     x = si.activation(m, k, 4101 + m)
     pw, nib, sc = _pack_both(mq, orc, w)
