@@ -737,7 +737,7 @@ cudaError_t launch_tc05_a16x_mp(GemmArgs &a, size_t smem, int grid, cudaStream_t
 {
     cudaError_t e = kernel_smem_attr(reinterpret_cast<const void *>(tc05_w4a16x<MP, TS>), 227 * 1024);
     if (e != cudaSuccess) return e;
-    return launch_pdl(tc05_w4a16x<MP, TS>, dim3(grid), dim3(tc05::kXThreads<MP>), smem, s, pdl, a);
+    return launch_pdl(tc05_w4a16x<MP, TS>, dim3(grid), dim3(tc05::kXThreads<MP, TS>), smem, s, pdl, a);
 }
 }  // namespace
 
@@ -769,7 +769,7 @@ cudaError_t launch_tc05_a16x(const uint8_t *nib, const uint16_t *scale, int64_t 
         a.wt = dbg;   // debug flags (timing experiments only; outputs wrong when set)
         a.stage_bytes = tc05::kNibBytes + tc05::kScBytes + (uint32_t)mp * 512u;
         static const int na_env = getenv("MCAPQ_TC05_NA") ? atoi(getenv("MCAPQ_TC05_NA")) : 0;
-        a.na = na_env >= 2 ? (na_env & ~1) : 4;   // A-atom ring slots (smem-A kernel; even)
+        a.na = na_env >= 4 ? (na_env & ~3) : 4;   // A-atom ring slots (smem-A kernel; a multiple of 4)
         // A operand from tensor memory (tcgen05.st by the dequantise warps, no shared-memory
         // atoms): 8B lm_head M = 16 141 -> 128 us; at MP = 64 the 512 columns leave one
         // accumulator quad and the smem-A kernel is faster (177 vs 185 us).

@@ -953,7 +953,6 @@ __global__ void __launch_bounds__(tc05::kA8Threads<MP>, 1) tc05_w4a8(const __gri
 namespace tc05 {
 template <int MP> constexpr int kXSets = MP == 16 ? 2 : 1;
 template <int MP> constexpr int kXEpi = MP / 4 * kXSets<MP>;
-template <int MP> constexpr int kXThreads = (2 + kDqWarps + kXEpi<MP>) * 32;
 constexpr int kXNE = 4;                           // E-ring slices (row scales)
 // exact codes: bf16x2 (128 + c) -> (c - 8), one FMA (exact)
 __device__ __forceinline__ uint32_t cm8_pair(uint32_t m)
@@ -1015,15 +1014,21 @@ __device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&lo)[8
 // A from TMEM: accumulator blocks and A atoms share the 512 columns
 template <int MP> constexpr int kXTsNB = MP == 16 ? 16 : (MP == 32 ? 8 : 4);
 constexpr int kXTsNA = 8;   // A atoms in TMEM (32 columns each)
+template <int MP, bool TS> constexpr int kXNB = TS ? kXTsNB<MP> : ((512 / MP) > 32 ? 32 : (512 / MP));
+// MMA issuers: two warps (one per accumulator quad of a slice, i.e. atoms 0-1 and 2-3) when the
+// quad ring has an even length, so each warp's quads and A slots stay disjoint; else one
+template <int MP, bool TS> constexpr int kXMW = (kXNB<MP, TS> / 4) % 2 == 0 ? 2 : 1;
+template <int MP, bool TS> constexpr int kXThreads = (1 + kXMW<MP, TS> + kDqWarps + kXEpi<MP>) * 32;
 }  // namespace tc05
 
 template <int MP, bool TS>
-__global__ void __launch_bounds__(tc05::kXThreads<MP>, 1) tc05_w4a16x(const __grid_constant__ GemmArgs a)
+__global__ void __launch_bounds__(tc05::kXThreads<MP, TS>, 1) tc05_w4a16x(const __grid_constant__ GemmArgs a)
 {
     using namespace tc05;
     constexpr int TOK = 16;
     constexpr int kEpi = kXEpi<MP>, kSets = kXSets<MP>;
-    constexpr int NB = TS ? kXTsNB<MP> : ((512 / MP) > 32 ? 32 : (512 / MP));   // block accumulators (x4)
+    constexpr int NB = kXNB<MP, TS>;   // block accumulators (a multiple of 4)
+    constexpr int kMW = kXMW<MP, TS>, kW0 = 1 + kMW;   // MMA warps 1 .. kMW, dequantise warps from kW0
     constexpr int NQ = NB / 4;
     extern __shared__ __align__(16) uint8_t smem_raw[];
     const uint32_t sb = (smem_addr(smem_raw) + 1023u) & ~1023u;
@@ -1051,7 +1056,7 @@ __global__ void __launch_bounds__(tc05::kXThreads<MP>, 1) tc05_w4a16x(const __gr
     if (threadIdx.x == 0) {
         for (int s = 0; s < S; ++s) {
             mbar_init(sfull + 8u * s, 1);
-            mbar_init(sempty + 8u * s, 1 + kDqWarps);   // MMA commit (x read) + the dequantise warps
+            mbar_init(sempty + 8u * s, kMW + kDqWarps);   // MMA commits (x read) + the dequantise warps
         }
         for (int s = 0; s < NA; ++s) {
             mbar_init(afull + 8u * s, kDqWarps);
@@ -1104,8 +1109,12 @@ __global__ void __launch_bounds__(tc05::kXThreads<MP>, 1) tc05_w4a16x(const __gr
                 }
             }
         }
-    } else if (warp == 1) {
-        // ================= MMA issuer: per atom two blocks, one accumulator each =================
+    } else if (warp <= kMW) {
+        // ================= MMA issuers: per atom two blocks, one accumulator each =================
+        // with two issuers, warp 1 takes quad h = 0 (atoms 0, 1) of every slice and warp 2 quad
+        // h = 1 (atoms 2, 3): both walk the same ring counters and skip the other's share, so the
+        // two serial wait -> issue -> commit chains overlap
+        const int mw = warp - 1;
         {
             constexpr uint32_t id = idesc<MP>();
             int s = 0, sa = 0, qb = 0;
@@ -1124,6 +1133,18 @@ __global__ void __launch_bounds__(tc05::kXThreads<MP>, 1) tc05_w4a16x(const __gr
                     }
 #pragma unroll
                     for (int h = 0; h < 2; ++h) {   // two quads (4 blocks = 2 atoms) per slice
+                        if (kMW == 2 && h != mw) {   // the other issuer's quad and atoms
+                            sa += 2;
+                            if (sa == NA) {
+                                sa = 0;
+                                pha ^= 1u;
+                            }
+                            if (++qb == NQ) {
+                                qb = 0;
+                                phq ^= 1u;
+                            }
+                            continue;
+                        }
                         mbar_wait(dempty + 8u * qb, phq ^ 1u);
                         fence_after();
                         const uint32_t dq = tbase + (uint32_t)(qb * 4 * MP);
@@ -1162,11 +1183,11 @@ __global__ void __launch_bounds__(tc05::kXThreads<MP>, 1) tc05_w4a16x(const __gr
                 }
             }
         }
-    } else if (warp < 2 + kDqWarps) {
+    } else if (warp < kW0 + kDqWarps) {
         // ================= dequantise to exact codes: thread = (row r, block bb of each atom) =================
-        const int tq = threadIdx.x - 64;
+        const int tq = threadIdx.x - 32 * kW0;
         // TS: a warp reaches only its TMEM lane quarter (warp % 4), so row = 32 (warp % 4) + lane
-        const int r = TS ? (((warp & 3) << 5) | lane) : (tq & 127), bb = TS ? ((warp - 2) >> 2) : (tq >> 7);
+        const int r = TS ? (((warp & 3) << 5) | lane) : (tq & 127), bb = TS ? ((warp - kW0) >> 2) : (tq >> 7);
         const uint32_t sw = (uint32_t)(r & 7);
         int s = 0, sa = 0, e = 0;
         uint32_t ph = 0, pha = 0, phe = 0;
@@ -1255,7 +1276,7 @@ __global__ void __launch_bounds__(tc05::kXThreads<MP>, 1) tc05_w4a16x(const __gr
         }
     } else {
         // ================= epilogue: per block TMEM -> acc += d * D =================
-        const int ew = warp - 2 - kDqWarps;
+        const int ew = warp - kW0 - kDqWarps;
         const int quarter = warp & 3;
         const int set = kSets == 2 ? ew / (kEpi / 2) : 0;
         const int tq = (ew % (kEpi / kSets)) >> 2;
