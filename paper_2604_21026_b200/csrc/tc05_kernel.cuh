@@ -1012,8 +1012,8 @@ __device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&lo)[8
                  : "memory");
 }
 // A from TMEM: accumulator blocks and A atoms share the 512 columns
-template <int MP> constexpr int kXTsNB = MP == 16 ? 16 : (MP == 32 ? 8 : 4);
-constexpr int kXTsNA = 8;   // A atoms in TMEM (32 columns each)
+template <int MP> constexpr int kXTsNB = MP == 16 ? 24 : (MP == 32 ? 8 : 4);
+template <int MP> constexpr int kXTsNA = MP == 16 ? 4 : 8;   // A atoms in TMEM (32 columns each)
 template <int MP, bool TS> constexpr int kXNB = TS ? kXTsNB<MP> : ((512 / MP) > 32 ? 32 : (512 / MP));
 // MMA issuers: two warps (one per accumulator quad of a slice, i.e. atoms 0-1 and 2-3) when the
 // quad ring has an even length, so each warp's quads and A slots stay disjoint; else one
@@ -1034,7 +1034,7 @@ __global__ void __launch_bounds__(tc05::kXThreads<MP, TS>, 1) tc05_w4a16x(const 
     const uint32_t sb = (smem_addr(smem_raw) + 1023u) & ~1023u;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int S = a.stages;
-    const int NA = TS ? kXTsNA : a.na;
+    const int NA = TS ? kXTsNA<MP> : a.na;
     const int G8 = (int)(a.k / 256);
     const uint32_t stage_bytes = a.stage_bytes;
     const uint32_t ring = sb;
