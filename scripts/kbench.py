@@ -34,6 +34,7 @@ CASES = {
     "q_3b_m64": ([(3072, 3072)], 64),
     "lmhead_8b_m64": ([(128256, 4096)], 64),
     "lmhead_8b_m16": ([(128256, 4096)], 16),
+    "lmhead_8b_m32": ([(128256, 4096)], 32),
     "up_3b_m64": ([(8192, 3072)], 64),
 }
 
